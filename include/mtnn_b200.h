@@ -1,0 +1,145 @@
+/*
+ * mtnn_b200.h — C-ABI of the B200-native MTNN hot path (arXiv 1702.03192).
+ *
+ * This is the drop-in boundary. The reference binds its kernels through the
+ * `_impl` module protocol: a module exposing nine functions that is chosen once
+ * at import by `_backend.BACKEND` and looked up by attribute at call time
+ *   - /root/reference/pkg/src/mtnn/kernels/__init__.py:24-27  (kernel API binds _impl)
+ *   - /root/reference/pkg/src/mtnn/selector.py:25-28          (selector binds _impl)
+ *   - protocol signatures: kernels/_numba_impl.py:103-222, kernels/_numpy_impl.py:18-67
+ * Every entry point below replaces one protocol function (or the selector step
+ * that calls it); the comment on each names the reference interface it replaces.
+ *
+ * Conventions (mirroring the reference protocol):
+ *   - matrices are dense, row-major (C-contiguous) float32; A is m x k, B is n x k,
+ *     B^T is k x n, C is m x n; inputs are never written.
+ *   - "device" entry points take device pointers and a cudaStream_t passed as
+ *     void* (NULL = legacy default stream); they are asynchronous on that stream.
+ *   - "_host" entry points take HOST pointers, copy in, compute, copy out and
+ *     return synchronously — the reference's numpy-in/numpy-out semantics.
+ *   - return value: 0 on success, else one of the MTNN_E* codes; the message
+ *     is in mtnn_last_error() (thread-local). The Python shim maps
+ *     MTNN_EINVAL -> ValueError, MTNN_ENOMEM -> MemoryError, others -> RuntimeError,
+ *     matching the reference's error taxonomy (kernels/__init__.py:70-158).
+ *   - no CPU fallback exists: a missing/unsupported GPU is an error.
+ */
+#ifndef MTNN_B200_H
+#define MTNN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MTNN_ABI_VERSION 1
+
+/* status codes */
+#define MTNN_OK 0
+#define MTNN_EINVAL 22  /* bad argument            -> ValueError   */
+#define MTNN_ENOMEM 12  /* allocation / budget     -> MemoryError  */
+#define MTNN_ECUDA 5    /* CUDA runtime failure    -> RuntimeError */
+#define MTNN_ENOTSUP 95 /* no sm_100 device / unsupported variant   */
+
+/* GEMM variant selector (within one path; the NT-vs-TNN choice is the model's). */
+#define MTNN_VARIANT_AUTO 0     /* heuristic: tensor-core 3xTF32 when eligible, else FFMA */
+#define MTNN_VARIANT_TC3XTF32 1 /* tcgen05 kind::tf32, 3-term split, TMEM accumulator      */
+#define MTNN_VARIANT_FFMA 2     /* SIMT FP32 FFMA (exact-order fp32, any shape)            */
+
+/* dispatcher choices (reference selector.py:43-51) */
+#define MTNN_CHOICE_NT 0
+#define MTNN_CHOICE_TNN 1
+#define MTNN_REASON_PREDICTED 0
+#define MTNN_REASON_MEMORY_FALLBACK 1
+
+typedef struct mtnn_model mtnn_model;
+
+/* ---- library ---------------------------------------------------------- */
+int mtnn_abi_version(void);
+const char* mtnn_last_error(void);
+/* 1 if a compute-capability-10.x device is usable, else 0 (never errors). */
+int mtnn_device_available(void);
+/* Free device memory in bytes (cudaMemGetInfo), cached for 1 s.
+ * Replaces selector.py:76-79 / :158-169 (psutil available memory, 1 s cache). */
+int mtnn_device_free_bytes(int64_t* out);
+/* The five platform features (gm GiB, sm count, cc MHz, mbw bits, l2c KB) of the
+ * current device. Replaces platform.py:113-139 probe_platform detection. */
+int mtnn_device_features(double out5[5]);
+
+/* ---- device-resident kernels ----------------------------------------- */
+/* C = A x B^T directly. Replaces _impl.gemm_nt / gemm_nt_parallel
+ * (_numba_impl.py:139-166; caller kernels/__init__.py:105-116). */
+int mtnn_gemm_nt(const float* A, const float* B, float* C, int64_t m, int64_t n,
+                 int64_t k, int variant, void* stream);
+/* C = A x BT with BT k x n. Replaces _impl.gemm_nn / gemm_nn_parallel
+ * (_numba_impl.py:103-136; caller kernels/__init__.py:89-102). */
+int mtnn_gemm_nn(const float* A, const float* BT, float* C, int64_t m, int64_t n,
+                 int64_t k, int variant, void* stream);
+/* Out-of-place transpose: BT[j,i] = B[i,j], B rows x cols. Bit-exact copy.
+ * Replaces _impl.transpose_oop (_numba_impl.py:169-182; caller kernels/__init__.py:119-124). */
+int mtnn_transpose(const float* B, float* BT, int64_t rows, int64_t cols, void* stream);
+/* TNN: allocate B^T (4*n*k bytes, stream-ordered), transpose, NN, release — all
+ * inside the call. mem_budget >= 0 caps the buffer and fails with MTNN_ENOMEM
+ * before allocating (kernels/__init__.py:150-155); -1 = no cap.
+ * Replaces _impl.gemm_tnn / gemm_tnn_parallel (_numba_impl.py:185-194). */
+int mtnn_gemm_tnn(const float* A, const float* B, float* C, int64_t m, int64_t n,
+                  int64_t k, int variant, int64_t mem_budget, void* stream);
+
+/* ---- host-buffer (drop-in) variants: synchronous, numpy semantics ------ */
+int mtnn_gemm_nt_host(const float* A, const float* B, float* C, int64_t m, int64_t n,
+                      int64_t k, int variant);
+int mtnn_gemm_nn_host(const float* A, const float* BT, float* C, int64_t m, int64_t n,
+                      int64_t k, int variant);
+int mtnn_transpose_host(const float* B, float* BT, int64_t rows, int64_t cols);
+int mtnn_gemm_tnn_host(const float* A, const float* B, float* C, int64_t m, int64_t n,
+                       int64_t k, int variant, int64_t mem_budget);
+
+/* ---- packed-tree walkers (host, float64) -------------------------------
+ * Same flat layout as selector._pack_trees (selector.py:82-123): arrays of shape
+ * (n_trees, width), feat = -1 marks a leaf, pre-order, root at 0. Routing
+ * x[f] < t -> left else right; raw = base; raw += eta * leaf, tree order.
+ * Replace _impl.walk_trees / walk_trees_mnk (_numba_impl.py:197-222). */
+double mtnn_walk_trees(const int64_t* feat, const double* thresh, const int64_t* left,
+                       const int64_t* right, const double* leaf, int64_t n_trees,
+                       int64_t width, const double* x, double base_score, double eta);
+double mtnn_walk_trees_mnk(const int64_t* feat, const double* thresh,
+                           const int64_t* left, const int64_t* right,
+                           const double* leaf, int64_t n_trees, int64_t width,
+                           const double* prefix5, double m, double n, double k,
+                           double base_score, double eta);
+
+/* ---- model handle (immutable, thread-safe) ----------------------------- */
+/* Parse the reference's model JSON v1 (gbdt.py:388-455). Errors -> MTNN_EINVAL. */
+int mtnn_model_load_json(const char* text, size_t len, mtnn_model** out);
+/* Build a model from packed arrays (the Dispatcher's one-time pack, selector.py:151). */
+int mtnn_model_from_packed(const int64_t* feat, const double* thresh, const int64_t* left,
+                           const int64_t* right, const double* leaf, int64_t n_trees,
+                           int64_t width, double base_score, double eta,
+                           int64_t n_features, mtnn_model** out);
+void mtnn_model_free(mtnn_model* model);
+int64_t mtnn_model_n_features(const mtnn_model* model);
+int64_t mtnn_model_n_trees(const mtnn_model* model);
+/* Raw score of one feature vector (gbdt.predict_raw, gbdt.py:242-254; finite check,
+ * arity check -> MTNN_EINVAL). */
+int mtnn_model_raw(const mtnn_model* model, const double* x, int64_t nx, double* raw);
+/* Algorithm 2's decision (selector.py:181-190): 4*n*k > free_bytes -> NT with
+ * reason MEMORY_FALLBACK and raw = NaN; else raw >= 0 -> NT, raw < 0 -> TNN.
+ * free_bytes < 0 -> query the device (mtnn_device_free_bytes). */
+int mtnn_select(const mtnn_model* model, const double prefix5[5], int64_t m, int64_t n,
+                int64_t k, int64_t free_bytes, double* raw_out, int* choice_out,
+                int* reason_out);
+/* Dispatcher.gemm (selector.py:192-221): select, run TNN or NT; a TNN
+ * allocation failure is retried as NT (choice_out reports what ran). */
+int mtnn_dispatch_gemm(const mtnn_model* model, const double prefix5[5], const float* A,
+                       const float* B, float* C, int64_t m, int64_t n, int64_t k,
+                       int64_t free_bytes, int variant, void* stream, int* choice_out);
+int mtnn_dispatch_gemm_host(const mtnn_model* model, const double prefix5[5],
+                            const float* A, const float* B, float* C, int64_t m,
+                            int64_t n, int64_t k, int64_t free_bytes, int variant,
+                            int* choice_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MTNN_B200_H */

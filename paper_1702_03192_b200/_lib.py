@@ -1,0 +1,112 @@
+"""ctypes binding of libmtnn_b200.so (the C-ABI in include/mtnn_b200.h).
+
+The library is the only compute path: if it is missing this module raises on
+import (there is no CPU fallback), and calls that need a GPU fail with the
+library's own error message when none is present.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int64, c_size_t, c_void_p
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libmtnn_b200.so"
+
+OK = 0
+EINVAL = 22
+ENOMEM = 12
+ECUDA = 5
+ENOTSUP = 95
+
+VARIANT_AUTO = 0
+VARIANT_TC3XTF32 = 1
+VARIANT_FFMA = 2
+VARIANTS = {"auto": VARIANT_AUTO, "tc3xtf32": VARIANT_TC3XTF32, "ffma": VARIANT_FFMA}
+
+CHOICE_NT = 0
+CHOICE_TNN = 1
+REASON_PREDICTED = 0
+REASON_MEMORY_FALLBACK = 1
+
+_F = POINTER(ctypes.c_float)
+_I64P = POINTER(c_int64)
+_DP = POINTER(c_double)
+
+
+class MtnnError(RuntimeError):
+    """A CUDA/runtime failure reported by libmtnn_b200."""
+
+
+def _load():
+    path = os.environ.get("MTNN_B200_LIB", str(LIB_PATH))
+    if not Path(path).exists():
+        raise ImportError(
+            f"libmtnn_b200.so not found at {path}; build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback for the B200 backend)"
+        )
+    lib = ctypes.CDLL(path)
+    sig = {
+        "mtnn_abi_version": (c_int, []),
+        "mtnn_last_error": (c_char_p, []),
+        "mtnn_device_available": (c_int, []),
+        "mtnn_device_free_bytes": (c_int, [_I64P]),
+        "mtnn_device_features": (c_int, [_DP]),
+        "mtnn_gemm_nt": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p]),
+        "mtnn_gemm_nn": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p]),
+        "mtnn_transpose": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p]),
+        "mtnn_gemm_tnn": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_int64, c_void_p]),
+        "mtnn_gemm_nt_host": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int]),
+        "mtnn_gemm_nn_host": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int]),
+        "mtnn_transpose_host": (c_int, [c_void_p, c_void_p, c_int64, c_int64]),
+        "mtnn_gemm_tnn_host": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_int64]),
+        "mtnn_walk_trees": (c_double, [_I64P, _DP, _I64P, _I64P, _DP, c_int64, c_int64, _DP, c_double, c_double]),
+        "mtnn_walk_trees_mnk": (c_double, [_I64P, _DP, _I64P, _I64P, _DP, c_int64, c_int64, _DP,
+                                           c_double, c_double, c_double, c_double, c_double]),
+        "mtnn_model_load_json": (c_int, [c_char_p, c_size_t, POINTER(c_void_p)]),
+        "mtnn_model_from_packed": (c_int, [_I64P, _DP, _I64P, _I64P, _DP, c_int64, c_int64,
+                                           c_double, c_double, c_int64, POINTER(c_void_p)]),
+        "mtnn_model_free": (None, [c_void_p]),
+        "mtnn_model_n_features": (c_int64, [c_void_p]),
+        "mtnn_model_n_trees": (c_int64, [c_void_p]),
+        "mtnn_model_raw": (c_int, [c_void_p, _DP, c_int64, _DP]),
+        "mtnn_select": (c_int, [c_void_p, _DP, c_int64, c_int64, c_int64, c_int64, _DP,
+                                POINTER(c_int), POINTER(c_int)]),
+        "mtnn_dispatch_gemm": (c_int, [c_void_p, _DP, c_void_p, c_void_p, c_void_p, c_int64, c_int64,
+                                       c_int64, c_int64, c_int, c_void_p, POINTER(c_int)]),
+        "mtnn_dispatch_gemm_host": (c_int, [c_void_p, _DP, c_void_p, c_void_p, c_void_p, c_int64,
+                                            c_int64, c_int64, c_int64, c_int, POINTER(c_int)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.mtnn_abi_version() != 1:
+        raise ImportError(f"libmtnn_b200 ABI version {lib.mtnn_abi_version()} != 1")
+    return lib
+
+
+lib = _load()
+
+
+def last_error() -> str:
+    msg = lib.mtnn_last_error()
+    return msg.decode("utf-8", "replace") if msg else ""
+
+
+def check(rc: int) -> None:
+    """Map a C-ABI status to the reference's exception taxonomy."""
+    if rc == OK:
+        return
+    msg = last_error()
+    if rc == EINVAL:
+        raise ValueError(msg)
+    if rc == ENOMEM:
+        raise MemoryError(msg)
+    raise MtnnError(msg or f"libmtnn_b200 error {rc}")
+
+
+def exported_symbols() -> list[str]:
+    return [n for n in dir(lib) if n.startswith("mtnn_")]

@@ -1,0 +1,63 @@
+// Shared host-side helpers for the MTNN B200 library: error state, status codes,
+// CUDA checks. Everything here is host code; device code lives in the .cu files.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/mtnn_b200.h"
+
+namespace mtnn {
+
+// Thread-local last error message (mtnn_last_error).
+void set_error(const std::string& msg);
+const std::string& last_error();
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+
+#define MTNN_CUDA_TRY(expr)                                                        \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess) {                                                       \
+      (void)cudaGetLastError();                                                    \
+      if (_e == cudaErrorMemoryAllocation)                                         \
+        return ::mtnn::fail(MTNN_ENOMEM, "%s: %s", #expr, cudaGetErrorString(_e)); \
+      return ::mtnn::fail(MTNN_ECUDA, "%s: %s", #expr, cudaGetErrorString(_e));    \
+    }                                                                              \
+  } while (0)
+
+#define MTNN_TRY(expr)         \
+  do {                         \
+    int _rc = (expr);          \
+    if (_rc != MTNN_OK) return _rc; \
+  } while (0)
+
+// Per-device facts cached at first use.
+struct DeviceInfo {
+  int device = -1;
+  int sm_count = 0;
+  int cc_major = 0, cc_minor = 0;
+  int max_smem_optin = 0;
+  int l2_bytes = 0;
+  int clock_khz = 0;
+  int bus_width = 0;
+  size_t total_mem = 0;
+};
+// Returns MTNN_ENOTSUP when no sm_100-class device is current.
+int device_info(const DeviceInfo** out);
+
+// Kernel launchers (implemented in the .cu files). All asynchronous on `s`.
+int launch_transpose(const float* in, float* out, int64_t rows, int64_t cols,
+                     cudaStream_t s);
+int launch_gemm_ffma(const float* A, const float* B, float* C, int64_t m, int64_t n,
+                     int64_t k, bool b_is_nk, cudaStream_t s);
+// Tensor-core 3xTF32 GEMM. b_is_nk: B stored n x k (NT); else B^T stored k x n (NN).
+// Returns MTNN_ENOTSUP when the shape/alignment is ineligible.
+int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t n,
+                   int64_t k, bool b_is_nk, cudaStream_t s);
+bool tc_eligible(const float* A, const float* B, const float* C, int64_t m, int64_t n,
+                 int64_t k, bool b_is_nk);
+
+}  // namespace mtnn

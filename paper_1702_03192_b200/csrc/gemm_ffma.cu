@@ -1,0 +1,206 @@
+// SIMT FP32 GEMM (FFMA) — the "exact-order" variant of both MTNN paths.
+//
+// Reference semantics: kernels/_numba_impl.py:139-152 (gemm_nt: C[i,j] = sum_p
+// A[i,p] B[j,p], fp32 accumulator) and :31-117 (gemm_nn over B^T, blocked 128,
+// fp32). Both accumulate in float32; so does this kernel (one FFMA chain per
+// output, k ascending within a split), which keeps the reference's bit-exact
+// identity KATs exact (test_kernels.py:32-40, 87-89): every product against an
+// identity matrix is exact and the chain adds only zeros around it.
+//
+// Used for: shapes the tensor-core path cannot take (TMA needs 16-byte row
+// strides), small problems where launch latency dominates, and as the explicit
+// MTNN_VARIANT_FFMA. B200 notes: 128x128x8 CTA tile, 256 threads, 8x8 register
+// micro-tile (two 4-wide halves 64 apart so LDS.128 reads are conflict-free),
+// register-staged double buffering of the next k-slice, optional split-K with a
+// deterministic second-pass reduction for few-tile / long-k shapes so the grid
+// reaches the 148 SMs.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "common.h"
+#include "workspace.h"
+
+namespace mtnn {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 8;
+
+// B_NK: B stored n x k (NT). Else B^T stored k x n (NN).
+template <bool B_NK>
+__global__ void __launch_bounds__(256)
+sgemm_kernel(const float* __restrict__ A, const float* __restrict__ B,
+             float* __restrict__ C, int64_t m, int64_t n, int64_t k, int64_t k_chunk,
+             int64_t split_stride) {
+  __shared__ __align__(16) float As[2][BK][BM];
+  __shared__ __align__(16) float Bs[2][BK][BN];
+
+  const int tid = threadIdx.x;
+  const int64_t bm0 = (int64_t)blockIdx.y * BM;
+  const int64_t bn0 = (int64_t)blockIdx.x * BN;
+  const int64_t kbeg = (int64_t)blockIdx.z * k_chunk;
+  const int64_t kend = min(k, kbeg + k_chunk);
+
+  // global->register load mapping
+  const int a_row = tid >> 1, a_k = (tid & 1) * 4;  // A: 128 rows x 8 k
+  const int bt_k = tid >> 5, bt_c = (tid & 31) * 4;  // B^T: 8 k x 128 cols
+
+  float ra[4], rb[4];
+  auto load_tile = [&](int64_t k0) {
+    {
+      const int64_t r = bm0 + a_row;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t kk = k0 + a_k + j;
+        ra[j] = (r < m && kk < kend) ? __ldg(A + r * k + kk) : 0.f;
+      }
+    }
+    if (B_NK) {
+      const int64_t r = bn0 + a_row;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t kk = k0 + a_k + j;
+        rb[j] = (r < n && kk < kend) ? __ldg(B + r * k + kk) : 0.f;
+      }
+    } else {
+      const int64_t kk = k0 + bt_k;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t c = bn0 + bt_c + j;
+        rb[j] = (kk < kend && c < n) ? __ldg(B + kk * n + c) : 0.f;
+      }
+    }
+  };
+  auto store_tile = [&](int buf) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) As[buf][a_k + j][a_row] = ra[j];
+    if (B_NK) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) Bs[buf][a_k + j][a_row] = rb[j];
+    } else {
+      *reinterpret_cast<float4*>(&Bs[buf][bt_k][bt_c]) =
+          make_float4(rb[0], rb[1], rb[2], rb[3]);
+    }
+  };
+
+  const int tx = tid & 15, ty = tid >> 4;
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+  int buf = 0;
+  if (kbeg < kend) {
+    load_tile(kbeg);
+    store_tile(0);
+  }
+  __syncthreads();
+  for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
+    const bool has_next = k0 + BK < kend;
+    if (has_next) load_tile(k0 + BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[8], b[8];
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 + tx * 4]);
+      a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+      a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
+      b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    if (has_next) {
+      store_tile(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+
+  float* out = C + (int64_t)blockIdx.z * split_stride;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t r = bm0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    if (r >= m) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t c = bn0 + h * 64 + tx * 4;
+      float* dst = out + r * n + c;
+      if (c + 3 < n && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        *reinterpret_cast<float4*>(dst) = make_float4(
+            acc[i][h * 4 + 0], acc[i][h * 4 + 1], acc[i][h * 4 + 2], acc[i][h * 4 + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (c + j < n) dst[j] = acc[i][h * 4 + j];
+      }
+    }
+  }
+}
+
+}  // namespace
+
+// Deterministic split-K reduction: C[i] = sum_s part[s][i], s ascending.
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, float* __restrict__ C,
+                                     int64_t count, int splits) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    float s = part[i];
+    for (int z = 1; z < splits; ++z) s += part[(int64_t)z * count + i];
+    C[i] = s;
+  }
+}
+
+int launch_splitk_reduce(const float* part, float* C, int64_t count, int splits,
+                         cudaStream_t s) {
+  const DeviceInfo* di = nullptr;
+  MTNN_TRY(device_info(&di));
+  int64_t blocks = (count + 255) / 256;
+  blocks = std::min<int64_t>(blocks, (int64_t)di->sm_count * 8);
+  splitk_reduce_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(part, C, count,
+                                                                            splits);
+  MTNN_CUDA_TRY(cudaGetLastError());
+  return MTNN_OK;
+}
+
+int launch_gemm_ffma(const float* A, const float* B, float* C, int64_t m, int64_t n,
+                     int64_t k, bool b_is_nk, cudaStream_t s) {
+  if (m <= 0 || n <= 0) return MTNN_OK;
+  const DeviceInfo* di = nullptr;
+  MTNN_TRY(device_info(&di));
+  const int64_t tiles_m = (m + BM - 1) / BM, tiles_n = (n + BN - 1) / BN;
+  if (tiles_m > 65535) return fail(MTNN_EINVAL, "ffma gemm: m=%lld too large", (long long)m);
+  // Split K when the tile grid cannot fill the chip and k is long enough.
+  int splits = 1;
+  const int64_t tiles = tiles_m * tiles_n;
+  if (tiles < di->sm_count && k >= 512) {
+    splits = (int)std::min<int64_t>((2 * di->sm_count + tiles - 1) / tiles, k / 256);
+    splits = std::max(1, std::min(splits, 64));
+  }
+  int64_t k_chunk = (k + splits - 1) / splits;
+  k_chunk = (k_chunk + BK - 1) / BK * BK;
+  splits = (int)((k + k_chunk - 1) / std::max<int64_t>(k_chunk, 1));
+  if (k <= 0) { splits = 1; k_chunk = 0; }
+  float* out = C;
+  ScratchBuffer part;
+  if (splits > 1) {
+    MTNN_TRY(part.alloc((size_t)splits * m * n * sizeof(float), s));
+    out = static_cast<float*>(part.ptr);
+  }
+  dim3 grid((unsigned)tiles_n, (unsigned)tiles_m, (unsigned)splits);
+  if (b_is_nk)
+    sgemm_kernel<true><<<grid, 256, 0, s>>>(A, B, out, m, n, k, k_chunk, m * n);
+  else
+    sgemm_kernel<false><<<grid, 256, 0, s>>>(A, B, out, m, n, k, k_chunk, m * n);
+  MTNN_CUDA_TRY(cudaGetLastError());
+  if (splits > 1) MTNN_TRY(launch_splitk_reduce(out, C, m * n, splits, s));
+  return MTNN_OK;
+}
+
+}  // namespace mtnn

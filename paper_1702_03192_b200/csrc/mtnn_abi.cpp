@@ -1,0 +1,350 @@
+// C-ABI entry points of libmtnn_b200.so (declared in include/mtnn_b200.h).
+//
+// Host orchestration for the MTNN hot path: argument validation, variant choice,
+// TNN's stream-ordered B^T buffer, the host-buffer (numpy-semantics) variants and
+// the dispatcher (Algorithm 2; reference selector.py:192-221).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <chrono>
+#include <mutex>
+#include <string>
+
+#include "common.h"
+#include "model.h"
+#include "workspace.h"
+
+namespace mtnn {
+
+static thread_local std::string t_last_error;
+
+void set_error(const std::string& msg) { t_last_error = msg; }
+const std::string& last_error() { return t_last_error; }
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  set_error(buf);
+  return code;
+}
+
+static constexpr int kMaxDevices = 64;
+static DeviceInfo g_dev[kMaxDevices];
+static std::once_flag g_dev_once[kMaxDevices];
+static int g_dev_rc[kMaxDevices];
+
+int device_info(const DeviceInfo** out) {
+  int dev = -1;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail(MTNN_ENOTSUP, "no CUDA device: %s", cudaGetErrorString(e));
+  }
+  if (dev < 0 || dev >= kMaxDevices) return fail(MTNN_ENOTSUP, "device index %d out of range", dev);
+  std::call_once(g_dev_once[dev], [dev] {
+    DeviceInfo& d = g_dev[dev];
+    d.device = dev;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
+      (void)cudaGetLastError();
+      g_dev_rc[dev] = MTNN_ENOTSUP;
+      return;
+    }
+    d.sm_count = prop.multiProcessorCount;
+    d.cc_major = prop.major;
+    d.cc_minor = prop.minor;
+    d.max_smem_optin = (int)prop.sharedMemPerBlockOptin;
+    d.l2_bytes = prop.l2CacheSize;
+    d.total_mem = prop.totalGlobalMem;
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrClockRate, dev) == cudaSuccess) d.clock_khz = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrGlobalMemoryBusWidth, dev) == cudaSuccess)
+      d.bus_width = v;
+    (void)cudaGetLastError();
+    g_dev_rc[dev] = (d.cc_major == 10) ? MTNN_OK : MTNN_ENOTSUP;
+  });
+  if (g_dev_rc[dev] != MTNN_OK)
+    return fail(MTNN_ENOTSUP,
+                "device %d is not an sm_100-class GPU (compute capability %d.%d); this "
+                "library has no other code path",
+                dev, g_dev[dev].cc_major, g_dev[dev].cc_minor);
+  *out = &g_dev[dev];
+  return MTNN_OK;
+}
+
+int prepare_mempool() {
+  static std::once_flag once[kMaxDevices];
+  int dev = 0;
+  MTNN_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return MTNN_OK;
+  std::call_once(once[dev], [dev] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t threshold = UINT64_MAX;
+      (void)cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    }
+    (void)cudaGetLastError();
+  });
+  return MTNN_OK;
+}
+
+// ---------------------------------------------------------------- validation
+static int check_dims(int64_t m, int64_t n, int64_t k) {
+  if (m < 0 || n < 0 || k < 0)
+    return fail(MTNN_EINVAL, "dimensions must be non-negative, got m=%lld n=%lld k=%lld",
+                (long long)m, (long long)n, (long long)k);
+  return MTNN_OK;
+}
+
+static bool use_tc(int variant, const float* A, const float* B, const float* C, int64_t m,
+                   int64_t n, int64_t k, bool b_is_nk) {
+  if (variant == MTNN_VARIANT_FFMA) return false;
+  const bool ok = tc_eligible(A, B, C, m, n, k, b_is_nk);
+  if (variant == MTNN_VARIANT_TC3XTF32) return true;  // launch reports ineligibility
+  // AUTO: tensor cores once the problem is big enough to amortise the operand
+  // split; tiny problems keep the exact-order FFMA chain (bit-exact identity KATs).
+  return ok && (double)m * (double)n * (double)k >= 4194304.0;
+}
+
+static int gemm_dispatch(const float* A, const float* B, float* C, int64_t m, int64_t n,
+                         int64_t k, int variant, bool b_is_nk, cudaStream_t s) {
+  MTNN_TRY(check_dims(m, n, k));
+  if (variant < 0 || variant > 2) return fail(MTNN_EINVAL, "unknown variant %d", variant);
+  const DeviceInfo* di = nullptr;
+  MTNN_TRY(device_info(&di));
+  if (m == 0 || n == 0) return MTNN_OK;
+  if (k == 0) {
+    MTNN_CUDA_TRY(cudaMemsetAsync(C, 0, (size_t)m * n * sizeof(float), s));
+    return MTNN_OK;
+  }
+  if (use_tc(variant, A, B, C, m, n, k, b_is_nk))
+    return launch_gemm_tc(A, B, C, m, n, k, b_is_nk, s);
+  return launch_gemm_ffma(A, B, C, m, n, k, b_is_nk, s);
+}
+
+static int tnn_device(const float* A, const float* B, float* C, int64_t m, int64_t n,
+                      int64_t k, int variant, int64_t mem_budget, cudaStream_t s) {
+  MTNN_TRY(check_dims(m, n, k));
+  const int64_t needed = 4 * n * k;
+  if (mem_budget >= 0 && needed > mem_budget)
+    return fail(MTNN_ENOMEM, "transpose buffer needs %lld bytes, budget is %lld",
+                (long long)needed, (long long)mem_budget);
+  const DeviceInfo* di = nullptr;
+  MTNN_TRY(device_info(&di));
+  ScratchBuffer bt;  // B^T lives only for the duration of the call
+  MTNN_TRY(bt.alloc((size_t)needed, s));
+  MTNN_TRY(launch_transpose(B, static_cast<float*>(bt.ptr), n, k, s));
+  return gemm_dispatch(A, static_cast<const float*>(bt.ptr), C, m, n, k, variant, false, s);
+}
+
+// ------------------------------------------------------------ host buffers
+struct HostStream {
+  cudaStream_t s = nullptr;
+  int device = -1;
+};
+static thread_local HostStream t_host_stream;
+
+static int host_stream(cudaStream_t* out) {
+  int dev = 0;
+  MTNN_CUDA_TRY(cudaGetDevice(&dev));
+  if (t_host_stream.s == nullptr || t_host_stream.device != dev) {
+    MTNN_CUDA_TRY(cudaStreamCreateWithFlags(&t_host_stream.s, cudaStreamNonBlocking));
+    t_host_stream.device = dev;
+  }
+  *out = t_host_stream.s;
+  return MTNN_OK;
+}
+
+// Copies host inputs in, runs `body` on device buffers, copies C out, syncs.
+template <class Body>
+static int host_call(const float* A, size_t a_elems, const float* B, size_t b_elems, float* C,
+                     size_t c_elems, Body body) {
+  const DeviceInfo* di = nullptr;
+  MTNN_TRY(device_info(&di));
+  cudaStream_t s;
+  MTNN_TRY(host_stream(&s));
+  ScratchBuffer da, db, dc;
+  MTNN_TRY(da.alloc(a_elems * sizeof(float), s));
+  MTNN_TRY(db.alloc(b_elems * sizeof(float), s));
+  MTNN_TRY(dc.alloc(c_elems * sizeof(float), s));
+  if (a_elems) MTNN_CUDA_TRY(cudaMemcpyAsync(da.ptr, A, a_elems * 4, cudaMemcpyHostToDevice, s));
+  if (b_elems) MTNN_CUDA_TRY(cudaMemcpyAsync(db.ptr, B, b_elems * 4, cudaMemcpyHostToDevice, s));
+  int rc = body(static_cast<const float*>(da.ptr), static_cast<const float*>(db.ptr),
+                static_cast<float*>(dc.ptr), s);
+  if (rc == MTNN_OK && c_elems)
+    rc = (cudaMemcpyAsync(C, dc.ptr, c_elems * 4, cudaMemcpyDeviceToHost, s) == cudaSuccess)
+             ? MTNN_OK
+             : fail(MTNN_ECUDA, "D2H copy failed: %s", cudaGetErrorString(cudaGetLastError()));
+  da.release();
+  db.release();
+  dc.release();
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (rc != MTNN_OK) return rc;
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail(MTNN_ECUDA, "stream synchronize: %s", cudaGetErrorString(e));
+  }
+  return MTNN_OK;
+}
+
+// ---------------------------------------------------------------- free memory
+static std::mutex g_free_mu;
+static double g_free_stamp[kMaxDevices];
+static int64_t g_free_value[kMaxDevices];
+
+int device_free_bytes_cached(int64_t* out) {
+  int dev = 0;
+  MTNN_CUDA_TRY(cudaGetDevice(&dev));
+  const double now =
+      std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  std::lock_guard<std::mutex> lk(g_free_mu);
+  if (dev >= 0 && dev < kMaxDevices && g_free_stamp[dev] != 0.0 &&
+      now - g_free_stamp[dev] <= 1.0) {
+    *out = g_free_value[dev];
+    return MTNN_OK;
+  }
+  size_t fr = 0, total = 0;
+  MTNN_CUDA_TRY(cudaMemGetInfo(&fr, &total));
+  if (dev >= 0 && dev < kMaxDevices) {
+    g_free_stamp[dev] = now;
+    g_free_value[dev] = (int64_t)fr;
+  }
+  *out = (int64_t)fr;
+  return MTNN_OK;
+}
+
+}  // namespace mtnn
+
+using namespace mtnn;
+
+extern "C" {
+
+int mtnn_abi_version(void) { return MTNN_ABI_VERSION; }
+
+const char* mtnn_last_error(void) { return t_last_error.c_str(); }
+
+int mtnn_device_available(void) {
+  const DeviceInfo* di = nullptr;
+  return device_info(&di) == MTNN_OK ? 1 : 0;
+}
+
+int mtnn_device_free_bytes(int64_t* out) {
+  if (!out) return fail(MTNN_EINVAL, "null output pointer");
+  return device_free_bytes_cached(out);
+}
+
+int mtnn_device_features(double out5[5]) {
+  if (!out5) return fail(MTNN_EINVAL, "null output pointer");
+  const DeviceInfo* di = nullptr;
+  MTNN_TRY(device_info(&di));
+  out5[0] = (double)di->total_mem / (double)(1ull << 30);  // gm: GiB
+  out5[1] = (double)di->sm_count;                          // sm: compute units
+  out5[2] = (double)di->clock_khz / 1000.0;                // cc: MHz
+  out5[3] = (double)di->bus_width;                         // mbw: bits
+  out5[4] = (double)di->l2_bytes / 1024.0;                 // l2c: KB
+  return MTNN_OK;
+}
+
+int mtnn_gemm_nt(const float* A, const float* B, float* C, int64_t m, int64_t n, int64_t k,
+                 int variant, void* stream) {
+  return gemm_dispatch(A, B, C, m, n, k, variant, true, static_cast<cudaStream_t>(stream));
+}
+
+int mtnn_gemm_nn(const float* A, const float* BT, float* C, int64_t m, int64_t n, int64_t k,
+                 int variant, void* stream) {
+  return gemm_dispatch(A, BT, C, m, n, k, variant, false, static_cast<cudaStream_t>(stream));
+}
+
+int mtnn_transpose(const float* B, float* BT, int64_t rows, int64_t cols, void* stream) {
+  if (rows < 0 || cols < 0) return fail(MTNN_EINVAL, "dimensions must be non-negative");
+  const DeviceInfo* di = nullptr;
+  MTNN_TRY(device_info(&di));
+  return launch_transpose(B, BT, rows, cols, static_cast<cudaStream_t>(stream));
+}
+
+int mtnn_gemm_tnn(const float* A, const float* B, float* C, int64_t m, int64_t n, int64_t k,
+                  int variant, int64_t mem_budget, void* stream) {
+  return tnn_device(A, B, C, m, n, k, variant, mem_budget, static_cast<cudaStream_t>(stream));
+}
+
+int mtnn_gemm_nt_host(const float* A, const float* B, float* C, int64_t m, int64_t n,
+                      int64_t k, int variant) {
+  MTNN_TRY(check_dims(m, n, k));
+  return host_call(A, m * k, B, n * k, C, m * n,
+                   [&](const float* a, const float* b, float* c, cudaStream_t s) {
+                     return gemm_dispatch(a, b, c, m, n, k, variant, true, s);
+                   });
+}
+
+int mtnn_gemm_nn_host(const float* A, const float* BT, float* C, int64_t m, int64_t n,
+                      int64_t k, int variant) {
+  MTNN_TRY(check_dims(m, n, k));
+  return host_call(A, m * k, BT, k * n, C, m * n,
+                   [&](const float* a, const float* b, float* c, cudaStream_t s) {
+                     return gemm_dispatch(a, b, c, m, n, k, variant, false, s);
+                   });
+}
+
+int mtnn_transpose_host(const float* B, float* BT, int64_t rows, int64_t cols) {
+  if (rows < 0 || cols < 0) return fail(MTNN_EINVAL, "dimensions must be non-negative");
+  return host_call(nullptr, 0, B, rows * cols, BT, rows * cols,
+                   [&](const float*, const float* b, float* c, cudaStream_t s) {
+                     return launch_transpose(b, c, rows, cols, s);
+                   });
+}
+
+int mtnn_gemm_tnn_host(const float* A, const float* B, float* C, int64_t m, int64_t n,
+                       int64_t k, int variant, int64_t mem_budget) {
+  MTNN_TRY(check_dims(m, n, k));
+  const int64_t needed = 4 * n * k;
+  if (mem_budget >= 0 && needed > mem_budget)  // before any allocation or copy
+    return fail(MTNN_ENOMEM, "transpose buffer needs %lld bytes, budget is %lld",
+                (long long)needed, (long long)mem_budget);
+  return host_call(A, m * k, B, n * k, C, m * n,
+                   [&](const float* a, const float* b, float* c, cudaStream_t s) {
+                     return tnn_device(a, b, c, m, n, k, variant, -1, s);
+                   });
+}
+
+int mtnn_dispatch_gemm(const mtnn_model* model, const double prefix5[5], const float* A,
+                       const float* B, float* C, int64_t m, int64_t n, int64_t k,
+                       int64_t free_bytes, int variant, void* stream, int* choice_out) {
+  double raw = 0.0;
+  int choice = MTNN_CHOICE_NT, reason = 0;
+  MTNN_TRY(check_dims(m, n, k));
+  MTNN_TRY(mtnn_select(model, prefix5, m, n, k, free_bytes, &raw, &choice, &reason));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (choice == MTNN_CHOICE_TNN) {
+    int rc = tnn_device(A, B, C, m, n, k, variant, -1, s);
+    if (rc == MTNN_OK) {
+      if (choice_out) *choice_out = MTNN_CHOICE_TNN;
+      return MTNN_OK;
+    }
+    if (rc != MTNN_ENOMEM) return rc;
+    // TNN allocation failed: retry as NT (selector.py:216-218)
+    fprintf(stderr, "mtnn: TNN allocation failed for (%lld, %lld, %lld); retrying as NT\n",
+            (long long)m, (long long)n, (long long)k);
+  }
+  if (choice_out) *choice_out = MTNN_CHOICE_NT;
+  return gemm_dispatch(A, B, C, m, n, k, variant, true, s);
+}
+
+int mtnn_dispatch_gemm_host(const mtnn_model* model, const double prefix5[5], const float* A,
+                            const float* B, float* C, int64_t m, int64_t n, int64_t k,
+                            int64_t free_bytes, int variant, int* choice_out) {
+  MTNN_TRY(check_dims(m, n, k));
+  return host_call(A, m * k, B, n * k, C, m * n,
+                   [&](const float* a, const float* b, float* c, cudaStream_t s) {
+                     return mtnn_dispatch_gemm(model, prefix5, a, b, c, m, n, k, free_bytes,
+                                               variant, s, choice_out);
+                   });
+}
+
+}  // extern "C"
