@@ -446,7 +446,7 @@ int mtnn_select(const mtnn_model* model, const double prefix5[5], int64_t m, int
   if (free_bytes < 0) MTNN_TRY(mtnn_device_free_bytes(&free_bytes));
   double raw;
   int choice, reason;
-  if (4 * n * k > free_bytes) {
+  if (4.0 * (double)n * (double)k > (double)free_bytes) {
     raw = NAN;
     choice = MTNN_CHOICE_NT;
     reason = MTNN_REASON_MEMORY_FALLBACK;

@@ -1,0 +1,207 @@
+"""GPU parity of the kernel API against the oracle and the reference's golden
+outputs. Mirrors /root/reference/pkg/tests/test_kernels.py (KATs, bit-exact
+identities, oracle <= 1e-4 on random shapes, transpose involution, cross-kernel
+equivalence, inputs never mutated) and adds the B200 gates: rel-Frobenius
+<= 1e-5 vs float64 for FP32 GEMMs at large shapes, bit-exact transposes of
+raw bit patterns (NaN payloads, -0.0) on every path."""
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import random_matrix, rel_frobenius
+from paper_1702_03192_b200 import kernels
+from paper_1702_03192_b200.kernels import as_matrix, gemm_nn, gemm_nt, gemm_tnn, transpose_oop
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4          # reference tolerance (test_kernels.py:17)
+FP32_GATE = 1e-5    # north_star: rel Frobenius vs float64-accumulated result
+VARIANTS = ("auto", "tc3xtf32", "ffma")
+
+
+def eye(n):
+    return np.eye(n, dtype=np.float32)
+
+
+def tc_ok(m, n, k):
+    return k % 4 == 0 and n % 4 == 0
+
+
+class TestKats:
+    def test_one_by_one(self):
+        assert gemm_nn(as_matrix([[2.0]]), as_matrix([[3.0]]))[0, 0] == 6.0
+
+    def test_dot_product(self):
+        assert gemm_nt(as_matrix([[1.0, 2.0]]), as_matrix([[3.0, 4.0]]))[0, 0] == 11.0
+
+    def test_transpose_definition(self):
+        b = as_matrix([[1.0, 2.0, 3.0], [4.0, 5.0, 6.0]])
+        assert np.array_equal(transpose_oop(b), np.array([[1, 4], [2, 5], [3, 6]], np.float32))
+
+    def test_scalar_tnn(self):
+        assert gemm_tnn(as_matrix([[2.0]]), as_matrix([[-3.0]]))[0, 0] == -6.0
+
+    def test_golden_kats(self, golden_kernels):
+        g = golden_kernels
+        assert np.array_equal(transpose_oop(g["kat_t_in"]), g["kat_t_out"])
+        assert np.array_equal(gemm_nn(g["ident_a"], eye(130), block=64), g["ident_nn"])
+        assert np.array_equal(gemm_nt(g["ident_a"][:3, :3].copy(), eye(3)), g["ident_nt"])
+
+
+class TestIdentities:
+    def test_identity_times_b(self, rng):
+        b = random_matrix(rng, 3, 4)
+        assert np.array_equal(gemm_nn(eye(3), b), b)
+
+    def test_b_identity_bitexact(self, rng):
+        for m, k in ((3, 3), (70, 70), (130, 130)):
+            a = random_matrix(rng, m, k)
+            assert np.array_equal(gemm_nn(a, eye(k), block=64), a)
+            assert np.array_equal(gemm_nt(a, eye(k)), a)
+            assert np.array_equal(gemm_tnn(a, eye(k)), a)
+
+    def test_ffma_identity_bitexact_any_size(self, rng):
+        a = random_matrix(rng, 300, 260)
+        assert np.array_equal(gemm_nt(a, eye(260), variant="ffma"), a)
+
+    def test_tc_identity_close(self, rng):
+        a = random_matrix(rng, 256, 256)
+        assert rel_frobenius(gemm_nt(a, eye(256), variant="tc3xtf32"), a) < 1e-6
+
+
+class TestAgainstGolden:
+    def test_all_golden_shapes_all_variants(self, golden_kernels):
+        g = golden_kernels
+        for i, (m, n, k) in enumerate(g["shapes"]):
+            a, b, f64 = g[f"a{i}"], g[f"b{i}"], g[f"f64_{i}"]
+            bt = np.ascontiguousarray(b.T)
+            assert np.array_equal(transpose_oop(b), g[f"t{i}"])
+            for v in VARIANTS:
+                if v == "tc3xtf32" and not tc_ok(m, n, k):
+                    continue
+                for got in (gemm_nt(a, b, variant=v), gemm_tnn(a, b, variant=v)):
+                    assert rel_frobenius(got, f64) < FP32_GATE
+                    assert rel_frobenius(got, g[f"nt{i}"]) < FP32_GATE
+                if v != "tc3xtf32" or n % 16 == 0:
+                    assert rel_frobenius(gemm_nn(a, bt, variant=v), g[f"nn{i}"]) < FP32_GATE
+
+    def test_bit_patterns(self, golden_kernels):
+        bits = golden_kernels["bits_in"]
+        out = transpose_oop(bits.view(np.float32)).view(np.uint32)
+        assert np.array_equal(out, golden_kernels["bits_out"])
+
+
+class TestRandomAgainstOracle:
+    def test_random_small_shapes(self, rng):
+        for _ in range(50):
+            m, n, k = (int(v) for v in rng.integers(1, 65, size=3))
+            a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+            want = oracle.oracle_nt(a, b)
+            assert rel_frobenius(gemm_nt(a, b), want) < TOL
+            assert rel_frobenius(gemm_tnn(a, b), want) < TOL
+            assert rel_frobenius(gemm_nn(a, np.ascontiguousarray(b.T)), want) < TOL
+
+    def test_exhaustive_small(self, rng):
+        sizes = (1, 2, 3, 5, 8, 17)
+        for m in sizes:
+            for n in sizes:
+                for k in sizes:
+                    a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+                    want = oracle.oracle_nt(a, b)
+                    assert rel_frobenius(gemm_nt(a, b), want) < TOL
+                    assert rel_frobenius(gemm_tnn(a, b), want) < TOL
+                    assert rel_frobenius(gemm_nn(a, transpose_oop(b)), want) < TOL
+
+    def test_acceptance_grid(self, rng):
+        # reference acceptance criterion 1 (test_acceptance.py:68-88) at the FP32 gate
+        for m in (1, 17, 64):
+            for n in (1, 17, 64):
+                for k in (1, 17, 64):
+                    a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+                    want = oracle.oracle_nt(a, b)
+                    assert rel_frobenius(gemm_nt(a, b), want) < FP32_GATE
+                    assert rel_frobenius(gemm_tnn(a, b), want) < FP32_GATE
+
+    @pytest.mark.parametrize("shape", [(128, 128, 128), (256, 512, 128), (200, 300, 100),
+                                       (130, 260, 36), (1000, 1000, 1000), (4097, 1023, 260),
+                                       (512, 10, 4096), (10, 4096, 1024), (1024, 4096, 784)])
+    def test_mid_shapes_every_variant(self, rng, shape):
+        m, n, k = shape
+        a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+        want = oracle.oracle_nt_blas(a, b)
+        bt = np.ascontiguousarray(b.T)
+        for v in VARIANTS:
+            if v == "tc3xtf32" and not tc_ok(m, n, k):
+                continue
+            assert rel_frobenius(gemm_nt(a, b, variant=v), want) < FP32_GATE, v
+            if v != "tc3xtf32" or n % 16 == 0:
+                assert rel_frobenius(gemm_nn(a, bt, variant=v), want) < FP32_GATE, v
+                assert rel_frobenius(gemm_tnn(a, b, variant=v), want) < FP32_GATE, v
+
+
+class TestTranspose:
+    def test_involution_bitexact(self, rng):
+        for _ in range(20):
+            r, c = (int(v) for v in rng.integers(1, 300, size=2))
+            b = random_matrix(rng, r, c)
+            assert np.array_equal(transpose_oop(transpose_oop(b)), b)
+
+    @pytest.mark.parametrize("shape", [(1, 1), (2, 3), (37, 65), (128, 128), (1000, 1000),
+                                       (3000, 5000), (16384, 128), (128, 16384), (4097, 1023),
+                                       (8191, 8193), (64, 4), (4, 64)])
+    def test_random_bits_bitexact(self, rng, shape):
+        b = oracle.random_bits(rng, *shape)
+        out = transpose_oop(b)
+        assert out.shape == shape[::-1]
+        assert np.array_equal(out.view(np.uint32), b.view(np.uint32).T)
+
+    def test_fresh_buffer(self, rng):
+        b = random_matrix(rng, 4, 4)
+        out = transpose_oop(b)
+        assert out.base is None or out.base is not b
+
+
+class TestCrossKernel:
+    def test_inputs_never_mutated(self, rng):
+        a, b = random_matrix(rng, 40, 30), random_matrix(rng, 20, 30)
+        a0, b0 = a.copy(), b.copy()
+        gemm_nt(a, b); gemm_tnn(a, b); transpose_oop(b); gemm_nn(a, transpose_oop(b))
+        assert np.array_equal(a, a0) and np.array_equal(b, b0)
+
+    def test_result_dtype_and_layout(self, rng):
+        c = gemm_nn(random_matrix(rng, 5, 7), random_matrix(rng, 7, 2))
+        assert c.dtype == np.float32 and c.flags.c_contiguous
+
+    def test_mem_budget(self, rng):
+        a, b = random_matrix(rng, 8, 8), random_matrix(rng, 8, 8)
+        with pytest.raises(MemoryError, match="budget"):
+            gemm_tnn(a, b, mem_budget=16)
+        gemm_tnn(a, b, mem_budget=10**9)
+
+    def test_threads_argument_is_accepted(self, rng):
+        a, b = random_matrix(rng, 80, 60), random_matrix(rng, 70, 60)
+        assert rel_frobenius(gemm_nt(a, b, threads=2), gemm_nt(a, b)) < 1e-6
+
+
+class TestDeviceTensors:
+    def test_device_paths_match_host_paths(self, rng):
+        import torch
+
+        a, b = random_matrix(rng, 300, 200), random_matrix(rng, 256, 200)
+        ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+        want = oracle.oracle_nt_blas(a, b)
+        for v in VARIANTS:
+            assert rel_frobenius(gemm_nt(ta, tb, variant=v).cpu().numpy(), want) < FP32_GATE
+            assert rel_frobenius(gemm_tnn(ta, tb, variant=v).cpu().numpy(), want) < FP32_GATE
+            tbt = transpose_oop(tb)
+            assert torch.equal(tbt, tb.t().contiguous())
+            assert rel_frobenius(gemm_nn(ta, tbt, variant=v).cpu().numpy(), want) < FP32_GATE
+
+    def test_device_transpose_bits(self, rng):
+        import torch
+
+        b = oracle.random_bits(rng, 1000, 4000)
+        tb = torch.from_numpy(b.view(np.int32)).cuda().view(torch.float32)
+        out = transpose_oop(tb).view(torch.int32).cpu().numpy().view(np.uint32)
+        assert np.array_equal(out, b.view(np.uint32).T)
