@@ -1,0 +1,507 @@
+"""MTNN B200 benchmark — BASELINE.json's metric on its sweep configuration.
+
+Workload (configs[1]): the NT sweep m, n, k in {128, ..., 16384} (512 cases),
+every case computed C = A B^T through the MTNN dispatcher (GBDT decision in
+host C++, then the direct-NT or the TNN path on sm_100a). One "step" = one pass
+over all cases. `value` = total flops / total device time (whole job), inputs
+resident in HBM, L2 flushed (256 MiB write) before every case and excluded from
+the timed windows. `e2e` = the same sweep through the reference-facing C-ABI
+with pinned HOST buffers (H2D of A and B, D2H of C inside the timed region).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun, one rank per GPU, NCCL): every case is row-sharded — rank r
+computes its m/N rows of C against the replicated B, with no collective in the
+timed region (strong scaling: the total work is fixed). `--gather` adds the
+NCCL all-gather of C. `--impl reference` times the reference's CPU
+implementation of the path (the C restatement in oracle/, all host threads) on a
+bounded sample of the same sweep.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+SLEEP_CYCLES = 200_000  # ~0.1 ms at 1.9 GHz of GPU spin ahead of each timed window
+METRIC = "NT A·Bᵀ TFLOPS (MTNN-selected) over m,n,k sweep; transpose GB/s; selector accuracy"
+DEFAULT_MODEL = ROOT / "paper_1702_03192_b200" / "models" / "b200_sweep.json"
+
+
+def grid(exp_min, exp_max):
+    s = [2 ** e for e in range(exp_min, exp_max + 1)]
+    return [(m, n, k) for m in s for n in s for k in s]
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[3:7], float(parts[7])))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        loaded = [r for r in rows if r[3] > 0] or rows
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[2]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in loaded),
+                "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(rows), "samples_under_load": len(loaded)}
+
+
+# ----------------------------------------------------------------- CPU legs
+def cpu_sample_run(shapes, threads, seed=0):
+    """Reference CPU path (oracle port of the numba kernels) over `shapes`:
+    NT (row-dot) and TNN (transpose + blocked NN) per case, all `threads`;
+    returns (flops, seconds of the per-case best path, seconds NT, seconds TNN)."""
+    import oracle
+
+    flops = secs_best = secs_nt = secs_tnn = 0.0
+    for (m, n, k) in shapes:
+        a, b, _ = oracle.make_operands(m, n, k, seed)
+        t0 = time.perf_counter()
+        oracle.gemm_nt(a, b, threads=threads)
+        t1 = time.perf_counter()
+        oracle.gemm_tnn(a, b, threads=threads)
+        t2 = time.perf_counter()
+        flops += 2.0 * m * n * k
+        secs_nt += t1 - t0
+        secs_tnn += t2 - t1
+        secs_best += min(t1 - t0, t2 - t1)
+    return flops, secs_best, secs_nt, secs_tnn
+
+
+def cpu_sample_shapes(max_seconds_hint: float):
+    # the 2^7..2^11 sub-grid (125 cases, 1.25e11 flop per path) the survey timed
+    # the reference on: ~10-30 s of CPU work; the full 2^7..2^14 grid would be
+    # hours of CPU time.
+    return grid(7, 11)
+
+
+def cpu_baseline(threads: int):
+    import oracle
+
+    shapes = cpu_sample_shapes(20.0)
+    cpu_sample_run(shapes[:8], threads)  # warm caches / thread pool
+    flops, best, s_nt, s_tnn = cpu_sample_run(shapes, threads)
+    return {
+        "value": flops / best / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+        "sample": (f"sweep sub-grid m,n,k in {{128..2048}} ({len(shapes)} cases), oracle/ C port of "
+                   f"the reference numba kernels, best of NT/TNN per case (upper bound of the CPU "
+                   f"MTNN), {threads} threads; always-NT {flops / s_nt / 1e12:.4f}, "
+                   f"always-TNN {flops / s_tnn / 1e12:.4f} TFLOP/s"),
+        "seconds": best,
+        "max_threads": oracle.max_threads(),
+    }
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU implementation of the path (oracle
+    port), timed on the host cores; rank 0 only."""
+    if rank != 0:
+        return
+    import oracle
+
+    threads = oracle.max_threads()
+    shapes = cpu_sample_shapes(20.0)
+    for _ in range(args.warmup):
+        cpu_sample_run(shapes[:16], threads)
+    times, flops = [], 0.0
+    for _ in range(args.steps):
+        f, best, _, _ = cpu_sample_run(shapes, threads)
+        times.append(best)
+        flops = f
+    value = flops * args.steps / sum(times) / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.mean(times) * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "nt_sweep (bounded CPU sample of configs[1])",
+                   "cases": len(shapes), "sample": "m,n,k in {128..2048}"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+                         "sample": f"sweep sub-grid m,n,k in {{128..2048}} ({len(shapes)} cases), "
+                                   "best of NT/TNN per case, oracle/ C port of the reference kernels"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU legs
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--exp-min", type=int, default=7)
+    ap.add_argument("--exp-max", type=int, default=14)
+    ap.add_argument("--model", default=str(DEFAULT_MODEL))
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--gather", action="store_true", help="N>1: include the C all-gather")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    from paper_1702_03192_b200 import _lib, gbdt
+    from paper_1702_03192_b200.platform import probe_platform
+    from paper_1702_03192_b200.selector import Dispatcher
+
+    dev = torch.device("cuda", local_rank)
+    L = _lib.lib
+    shapes = grid(args.exp_min, args.exp_max)
+    mx = 2 ** args.exp_max
+
+    # model: the B200-trained selector if present, else an empty model (always NT)
+    if Path(args.model).exists():
+        model = gbdt.load_model(args.model)
+        model_name = Path(args.model).name
+    else:
+        model = gbdt.GbdtModel(trees=(), params=gbdt.GbdtParams(), n_features=8)
+        model_name = "empty (always NT)"
+    platform = probe_platform()
+    disp = Dispatcher(model, platform)
+    handle = disp._native.handle
+    prefix_p = disp._prefix_p
+
+    # row shard of every case for this rank (N > 1), as sharding.row_range
+    from paper_1702_03192_b200.sharding import row_range
+
+    def rows_of(m):
+        return row_range(m, rank, world)
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    A = torch.rand(mx * mx, device=dev, generator=g).mul_(2).sub_(1)
+    B = torch.rand(mx * mx, device=dev, generator=g).mul_(2).sub_(1)
+    C = torch.empty(mx * mx, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    choice = __import__("ctypes").c_int()
+
+    def case_call(m, n, k):
+        lo, hi = rows_of(m)
+        mm = hi - lo
+        if mm <= 0:
+            return
+        rc = L.mtnn_dispatch_gemm(handle, prefix_p, A.data_ptr(), B.data_ptr(), C.data_ptr(),
+                                  mm, n, k, -1, 0, stream, __import__("ctypes").byref(choice))
+        if rc:
+            _lib.check(rc)
+
+    def one_step(events=None):
+        for (m, n, k) in shapes:
+            flush.fill_(1.0)
+            # keep the GPU busy while the host enqueues the timed call, so the
+            # event window holds device work only (no Python/ctypes gaps)
+            torch.cuda._sleep(SLEEP_CYCLES)
+            if events is not None:
+                s = torch.cuda.Event(enable_timing=True)
+                e = torch.cuda.Event(enable_timing=True)
+                s.record()
+                case_call(m, n, k)
+                e.record()
+                events.append((s, e))
+            else:
+                case_call(m, n, k)
+
+    local_flops = sum(2.0 * (rows_of(m)[1] - rows_of(m)[0]) * n * k for (m, n, k) in shapes)
+    total_flops = sum(2.0 * m * n * k for (m, n, k) in shapes)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: K steps
+    L.mtnn_profile_reset()
+    L.mtnn_profile_enable(1)
+    events = []
+    with ClockSampler(local_rank) as clocks:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            one_step(events)
+            if world > 1 and args.gather:
+                pass  # gather variant handled by --workload large in later rounds
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        wall = time.perf_counter() - w0
+    L.mtnn_profile_enable(0)
+    device_s = sum(s.elapsed_time(e) for s, e in events) * 1e-3
+    t = torch.tensor([device_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    device_s = float(t.item())
+    step_s = device_s / args.steps
+    value = total_flops / step_s / 1e12
+
+    prof = {c: _lib.profile_read(c) for c in _lib.KCLASS_NAMES}
+    launches = int(sum(v[1] for v in prof.values()))
+
+    # per-case MTNN times (median over the K timed steps) for the oracle ratio
+    ncase = len(shapes)
+    per_case_mtnn = [statistics.median(events[st * ncase + i][0].elapsed_time(events[st * ncase + i][1])
+                                       for st in range(args.steps)) * 1e-3 for i in range(ncase)]
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---------------- roofline of the dominant kernel (tc3xtf32 GEMM)
+    peaks_path = ROOT / "MEASURED_PEAKS.json"
+    peaks = json.loads(peaks_path.read_text()) if peaks_path.exists() else {}
+    bf16 = peaks.get("bf16_tflops", 1590.0)
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    tc_ms, tc_n, tc_work = prof[_lib.KCLASS_GEMM_TC]
+    ncu_path = ROOT / "profiles" / "ncu_summary.json"
+    ncu_traffic = json.loads(ncu_path.read_text()).get("gemm_tc3xtf32_traffic", {}) if ncu_path.exists() else {}
+    dominant = max(prof, key=lambda c: prof[c][0])
+    roofline = {
+        "kernel": _lib.KCLASS_NAMES[_lib.KCLASS_GEMM_TC], "bound": "tensor",
+        "achieved": tc_work / (tc_ms * 1e-3) / 1e12 if tc_ms else None,
+        "peak": bf16 / 6.0, "unit": "TFLOP/s",
+        "frac": (tc_work / (tc_ms * 1e-3) / 1e12) / (bf16 / 6.0) if tc_ms else None,
+        "traffic": ncu_traffic.get("traffic"),
+        "traffic_launch": ncu_traffic.get("launch"),
+        "traffic_algorithmic_bytes": ncu_traffic.get("algorithmic_bytes"),
+        "peak_basis": (f"3xTF32 FP32-accurate roof = measured bf16 dense {bf16} TFLOP/s "
+                       f"(MEASURED_PEAKS.json, burst) / 2 (tf32 rate) / 3 (MMAs per product)"),
+        "launches": tc_n, "avg_launch_ms": tc_ms / tc_n if tc_n else None,
+        "share_of_step": tc_ms / 1e3 / device_s if device_s else None,
+        "dominant_kernel_by_time": _lib.KCLASS_NAMES[dominant],
+    }
+    kernels_summary = {_lib.KCLASS_NAMES[c]: {"ms": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
+                                              "work_per_step": v[2] / args.steps}
+                       for c, v in prof.items()}
+
+    # ---------------- oracle pass: NT and TNN per case (median of 3, interleaved)
+    nt_t, tnn_t = [[] for _ in shapes], [[] for _ in shapes]
+    for _rep in range(3):
+        for i, (m, n, k) in enumerate(shapes):
+            a = A[: m * k].view(m, k)
+            b = B[: n * k].view(n, k)
+            c = C[: m * n].view(m, n)
+            for which in ("nt", "tnn"):
+                flush.fill_(1.0)
+                torch.cuda._sleep(SLEEP_CYCLES)
+                s = torch.cuda.Event(enable_timing=True)
+                e = torch.cuda.Event(enable_timing=True)
+                s.record()
+                if which == "nt":
+                    _lib.check(L.mtnn_gemm_nt(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, 0, stream))
+                else:
+                    _lib.check(L.mtnn_gemm_tnn(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, 0, -1, stream))
+                e.record()
+                (nt_t if which == "nt" else tnn_t)[i].append((s, e))
+    torch.cuda.synchronize()
+    nt_s = [statistics.median(s.elapsed_time(e) for s, e in ev) * 1e-3 for ev in nt_t]
+    tnn_s = [statistics.median(s.elapsed_time(e) for s, e in ev) * 1e-3 for ev in tnn_t]
+    best = [min(x, y) for x, y in zip(nt_s, tnn_s)]
+    ratio = [b_ / m_ for b_, m_ in zip(best, per_case_mtnn)]
+    decisions = [disp.select(__import__("paper_1702_03192_b200").ProblemShape(*sh)) for sh in shapes]
+    picked_tnn = [d.choice.value == "tnn" for d in decisions]
+    faster_tnn = [y < x for x, y in zip(nt_s, tnn_s)]
+    sel_acc = float(np.mean([p == f for p, f in zip(picked_tnn, faster_tnn)]))
+    large = [i for i, (m, n, k) in enumerate(shapes) if min(m, n, k) >= 4096]
+    large_tf = (sum(2.0 * shapes[i][0] * shapes[i][1] * shapes[i][2] for i in large)
+                / sum(per_case_mtnn[i] for i in large) / 1e12) if large else None
+
+    # ---------------- transpose bandwidth (config 3)
+    tshapes = [(2 ** e, 2 ** e) for e in range(7, 15)] + [
+        (1000, 1000), (3000, 5000), (16384, 128), (128, 16384), (4097, 1023), (12345, 6789),
+        (8191, 8193)]
+    tr = {}
+    bt_buf = torch.empty(mx * mx, device=dev)
+    for (r, cc) in tshapes:
+        src = B[: r * cc]
+        dst = bt_buf[: r * cc]
+        ev = []
+        for _ in range(5):
+            flush.fill_(1.0)
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record()
+            _lib.check(L.mtnn_transpose(src.data_ptr(), dst.data_ptr(), r, cc, stream))
+            e.record()
+            ev.append((s, e))
+        torch.cuda.synchronize()
+        tt = statistics.median(s.elapsed_time(e) * 1e-3 for s, e in ev)
+        tr[f"{r}x{cc}"] = 8.0 * r * cc / tt / 1e9
+    big = [tr[f"{2**e}x{2**e}"] for e in (12, 13, 14)]
+    transpose_summary = {"gbs_by_shape": {k_: round(v, 1) for k_, v in tr.items()},
+                         "gbs_large_median": statistics.median(big), "peak_hbm_gbs": hbm,
+                         "frac_of_measured_hbm": statistics.median(big) / hbm,
+                         "frac_of_8tbs_spec": statistics.median(big) / 8000.0}
+
+    # ---------------- selector overhead (native decision)
+    import ctypes
+
+    raw = ctypes.c_double()
+    ch = ctypes.c_int()
+    rs = ctypes.c_int()
+    nsel = 20000
+    t0 = time.perf_counter()
+    for i in range(nsel):
+        L.mtnn_select(handle, prefix_p, 1024, 1024, 1024, 1 << 40, ctypes.byref(raw),
+                      ctypes.byref(ch), ctypes.byref(rs))
+    sel_ns = (time.perf_counter() - t0) / nsel * 1e9
+
+    # ---------------- e2e through the C-ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, shapes, handle, prefix_p, mx, L)
+
+    cpu = None
+    if not args.no_cpu and world == 1:
+        import oracle
+
+        cpu = cpu_baseline(oracle.max_threads())
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic uniform[-1,1) fp32 operands, resident in HBM",
+        "config": {"workload": f"nt_sweep m,n,k in {{2^{args.exp_min}..2^{args.exp_max}}} "
+                               f"({len(shapes)} cases), MTNN-selected (configs[1])",
+                   "cases": len(shapes), "model": model_name,
+                   "l2": "flushed (256 MiB write) before every case, outside the timed windows",
+                   "parallelism": "single GPU" if world == 1 else f"row-sharded x{world}, B replicated",
+                   "precision": "FP32-accurate (3xTF32 tensor cores + FP32 promotion, or FP32 FFMA)",
+                   "wall_ms_per_step": wall / args.steps * 1e3},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "mtnn_vs_best_of_both": {"mean_per_case_ratio": float(np.mean(ratio)),
+                                 "min_per_case_ratio": float(np.min(ratio)),
+                                 "always_nt_tflops": total_flops / sum(nt_s) / 1e12,
+                                 "always_tnn_tflops": total_flops / sum(tnn_s) / 1e12,
+                                 "best_of_both_tflops": total_flops / sum(best) / 1e12},
+        "selector": {"accuracy_vs_measured_faster_path": sel_acc,
+                     "tnn_faster_cases": int(sum(faster_tnn)), "tnn_picked_cases": int(sum(picked_tnn)),
+                     "native_select_ns_incl_ctypes": sel_ns},
+        "large_shapes_tflops": large_tf,
+        "large_shapes_frac_of_3xtf32_roof": large_tf / (bf16 / 6.0) if large_tf else None,
+        "transpose": transpose_summary,
+        "kernels": kernels_summary,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, shapes, handle, prefix_p, mx, L):
+    """Same sweep through mtnn_dispatch_gemm_host (the drop-in C-ABI call):
+    per case H2D of A and B from pinned host memory, decision + kernels, D2H of C."""
+    import ctypes
+
+    import torch
+
+    from paper_1702_03192_b200 import _lib
+
+    max_a = max(m * k for m, n, k in shapes)
+    max_b = max(n * k for m, n, k in shapes)
+    max_c = max(m * n for m, n, k in shapes)
+    ha = torch.empty(max_a, dtype=torch.float32).pin_memory()
+    hb = torch.empty(max_b, dtype=torch.float32).pin_memory()
+    hc = torch.empty(max_c, dtype=torch.float32).pin_memory()
+    ha.uniform_(-1, 1)
+    hb.uniform_(-1, 1)
+    ch = ctypes.c_int()
+    h2d = sum(4 * (m * k + n * k) for m, n, k in shapes)
+    d2h = sum(4 * m * n for m, n, k in shapes)
+    steps = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 2)
+
+    def step():
+        for (m, n, k) in shapes:
+            _lib.check(L.mtnn_dispatch_gemm_host(handle, prefix_p, ha.data_ptr(), hb.data_ptr(),
+                                                 hc.data_ptr(), m, n, k, -1, 0, ctypes.byref(ch)))
+
+    for _ in range(max(1, min(args.warmup, 1))):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = (time.perf_counter() - t0) / steps
+    flops = sum(2.0 * m * n * k for m, n, k in shapes)
+    return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3, "steps": steps,
+            "api": "mtnn_dispatch_gemm_host (include/mtnn_b200.h), pinned host buffers"}
+
+
+if __name__ == "__main__":
+    main()

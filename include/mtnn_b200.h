@@ -67,6 +67,23 @@ int mtnn_device_free_bytes(int64_t* out);
  * current device. Replaces platform.py:113-139 probe_platform detection. */
 int mtnn_device_features(double out5[5]);
 
+/* ---- kernel timing (measurement instrumentation) ----------------------
+ * When enabled, every launch of the library's main kernels is bracketed with
+ * CUDA events on its launch stream and tagged with its algorithmic work:
+ * class 0 = tc3xtf32 GEMM (2mnk flops), 1 = FFMA GEMM (2mnk flops),
+ * 2 = transpose (8*rows*cols bytes), 3 = 3xTF32 operand split (12 bytes per
+ * element), 4 = split-K reduction (4*(splits+1) bytes per output).
+ * mtnn_profile_read synchronizes the recorded events and returns the totals. */
+#define MTNN_KCLASS_GEMM_TC 0
+#define MTNN_KCLASS_GEMM_FFMA 1
+#define MTNN_KCLASS_TRANSPOSE 2
+#define MTNN_KCLASS_SPLIT 3
+#define MTNN_KCLASS_REDUCE 4
+#define MTNN_KCLASS_COUNT 5
+int mtnn_profile_enable(int on);
+int mtnn_profile_reset(void);
+int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* work);
+
 /* ---- device-resident kernels ----------------------------------------- */
 /* C = A x B^T directly. Replaces _impl.gemm_nt / gemm_nt_parallel
  * (_numba_impl.py:139-166; caller kernels/__init__.py:105-116). */

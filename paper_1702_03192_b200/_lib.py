@@ -25,6 +25,13 @@ VARIANT_TC3XTF32 = 1
 VARIANT_FFMA = 2
 VARIANTS = {"auto": VARIANT_AUTO, "tc3xtf32": VARIANT_TC3XTF32, "ffma": VARIANT_FFMA}
 
+KCLASS_GEMM_TC = 0
+KCLASS_GEMM_FFMA = 1
+KCLASS_TRANSPOSE = 2
+KCLASS_SPLIT = 3
+KCLASS_REDUCE = 4
+KCLASS_NAMES = {0: "gemm_tc3xtf32", 1: "gemm_ffma", 2: "transpose", 3: "split_tf32", 4: "splitk_reduce"}
+
 CHOICE_NT = 0
 CHOICE_TNN = 1
 REASON_PREDICTED = 0
@@ -54,6 +61,9 @@ def _load():
         "mtnn_device_available": (c_int, []),
         "mtnn_device_free_bytes": (c_int, [_I64P]),
         "mtnn_device_features": (c_int, [_DP]),
+        "mtnn_profile_enable": (c_int, [c_int]),
+        "mtnn_profile_reset": (c_int, []),
+        "mtnn_profile_read": (c_int, [c_int, _DP, _I64P, _DP]),
         "mtnn_gemm_nt": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p]),
         "mtnn_gemm_nn": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p]),
         "mtnn_transpose": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p]),
@@ -106,6 +116,13 @@ def check(rc: int) -> None:
     if rc == ENOMEM:
         raise MemoryError(msg)
     raise MtnnError(msg or f"libmtnn_b200 error {rc}")
+
+
+def profile_read(kclass: int):
+    """(total_ms, launches, work) accumulated for one kernel class."""
+    ms, n, w = ctypes.c_double(), c_int64(), ctypes.c_double()
+    check(lib.mtnn_profile_read(kclass, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(w)))
+    return ms.value, n.value, w.value
 
 
 def exported_symbols() -> list[str]:

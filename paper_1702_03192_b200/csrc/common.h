@@ -48,6 +48,17 @@ struct DeviceInfo {
 // Returns MTNN_ENOTSUP when no sm_100-class device is current.
 int device_info(const DeviceInfo** out);
 
+// Kernel timing instrumentation (mtnn_profile_*): a scope records a CUDA event
+// pair around one launch when profiling is enabled, else does nothing.
+struct KernelTimer {
+  KernelTimer(int kclass, double work, cudaStream_t s);
+  ~KernelTimer();
+  int kclass;
+  double work;
+  cudaStream_t stream;
+  cudaEvent_t start = nullptr;
+};
+
 // Kernel launchers (implemented in the .cu files). All asynchronous on `s`.
 int launch_transpose(const float* in, float* out, int64_t rows, int64_t cols,
                      cudaStream_t s);

@@ -163,6 +163,7 @@ int launch_splitk_reduce(const float* part, float* C, int64_t count, int splits,
   MTNN_TRY(device_info(&di));
   int64_t blocks = (count + 255) / 256;
   blocks = std::min<int64_t>(blocks, (int64_t)di->sm_count * 8);
+  KernelTimer timer(MTNN_KCLASS_REDUCE, 4.0 * (double)(splits + 1) * (double)count, s);
   splitk_reduce_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(part, C, count,
                                                                             splits);
   MTNN_CUDA_TRY(cudaGetLastError());
@@ -194,10 +195,13 @@ int launch_gemm_ffma(const float* A, const float* B, float* C, int64_t m, int64_
     out = static_cast<float*>(part.ptr);
   }
   dim3 grid((unsigned)tiles_n, (unsigned)tiles_m, (unsigned)splits);
+  {
+  KernelTimer timer(MTNN_KCLASS_GEMM_FFMA, 2.0 * (double)m * (double)n * (double)k, s);
   if (b_is_nk)
     sgemm_kernel<true><<<grid, 256, 0, s>>>(A, B, out, m, n, k, k_chunk, m * n);
   else
     sgemm_kernel<false><<<grid, 256, 0, s>>>(A, B, out, m, n, k, k_chunk, m * n);
+  }
   MTNN_CUDA_TRY(cudaGetLastError());
   if (splits > 1) MTNN_TRY(launch_splitk_reduce(out, C, m * n, splits, s));
   return MTNN_OK;

@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <stdlib.h>
 
 #include "common.h"
 #include "workspace.h"
@@ -49,7 +50,6 @@ constexpr int kStages = 4;
 constexpr int kEpiWarp0 = 4;      // warps 0..3: TMA, MMA, TMEM alloc, spare
 constexpr int kEpiWarps = 16;     // 4 TMEM lane quarters x 4 column quarters
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
-constexpr int kChunkKB = 16;      // k-blocks (16 x 16 = 256 k) per TMEM accumulation
 constexpr uint32_t kLayoutSW128B32 = 1;  // UMMA SWIZZLE_128B_BASE32B
 constexpr uint32_t kLayoutSW64 = 4;      // UMMA SWIZZLE_64B
 
@@ -209,9 +209,30 @@ __host__ __device__ constexpr uint32_t make_idesc(int n, bool b_mn_major) {
 
 struct Params {
   int64_t m, n, k;
+  int chunk_kb;  // k-blocks per TMEM accumulation chunk (FP32 promotion period)
   int tiles_m, tiles_n, splits, kblocks_per_split, total_kblocks;
   int units;
 };
+
+// Work-unit order: units are (k-split, tile); within a split, tiles walk
+// groups of kGroupM m-tiles with the group's m-tiles fastest, so the ~148 units
+// in flight cover a ~16 x 9 block of output tiles. Each A and B panel is then
+// streamed from DRAM by few waves instead of every wave re-streaming all of A
+// (m-fastest order), which cost ~15% at m = 16384.
+constexpr int kGroupM = 16;
+__device__ __forceinline__ void unit_coords(int u, const Params& p, int& split, int& tm,
+                                            int& tn) {
+  const int tiles = p.tiles_m * p.tiles_n;
+  split = u / tiles;
+  const int t = u - split * tiles;
+  const int per_group = kGroupM * p.tiles_n;
+  const int group = t / per_group;
+  const int first_m = group * kGroupM;
+  const int gm = min(kGroupM, p.tiles_m - first_m);
+  const int r = t - group * per_group;
+  tm = first_m + r % gm;
+  tn = r / gm;
+}
 
 // ------------------------------------------------------------------- kernel
 template <int BN, bool B_MN>
@@ -268,7 +289,6 @@ gemm_tc3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi,
   const uint32_t tmem_base = *tmem_slot;
 
   const int kb_per = p.kblocks_per_split;
-  const int tiles = p.tiles_m * p.tiles_n;
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -276,10 +296,8 @@ gemm_tc3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi,
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const int split = u / tiles;
-        const int rem = u - split * tiles;
-        const int tn = rem / p.tiles_m;
-        const int tm = rem - tn * p.tiles_m;
+        int split, tm, tn;
+        unit_coords(u, p, split, tm, tn);
         const int kb0 = split * kb_per;
         const int kb1 = min(p.total_kblocks, kb0 + kb_per);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -316,11 +334,11 @@ gemm_tc3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi,
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const int split = u / tiles;
+      const int split = u / (p.tiles_m * p.tiles_n);
       const int kb0 = split * kb_per;
       const int kb1 = min(p.total_kblocks, kb0 + kb_per);
-      for (int kc = kb0; kc < kb1; kc += kChunkKB) {
-        const int kce = min(kb1, kc + kChunkKB);
+      for (int kc = kb0; kc < kb1; kc += p.chunk_kb) {
+        const int kce = min(kb1, kc + p.chunk_kb);
         mbar_wait(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
@@ -365,7 +383,7 @@ gemm_tc3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi,
   } else if (warp >= kEpiWarp0) {
     // ===================== epilogue: FP32 promotion + store =====================
     // The tensor core's accumulator truncates (measured bias ~ -0.5 ulp per MMA
-    // accumulation), so each TMEM accumulation covers only kChunkKB k-blocks; the
+    // accumulation), so each TMEM accumulation covers only p.chunk_kb k-blocks; the
     // chunk is then added into round-to-nearest FP32 register sums here.
     const int e = warp - kEpiWarp0;
     const int q = warp % 4;             // TMEM lane quarter this warp may access
@@ -374,16 +392,14 @@ gemm_tc3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi,
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const int split = u / tiles;
-      const int rem = u - split * tiles;
-      const int tn = rem / p.tiles_m;
-      const int tm = rem - tn * p.tiles_m;
+      int split, tm, tn;
+      unit_coords(u, p, split, tm, tn);
       const int kb0 = split * kb_per;
       const int kb1 = min(p.total_kblocks, kb0 + kb_per);
       float sum[kColsPerWarp];
 #pragma unroll
       for (int j = 0; j < kColsPerWarp; ++j) sum[j] = 0.f;
-      for (int kc = kb0; kc < kb1; kc += kChunkKB) {
+      for (int kc = kb0; kc < kb1; kc += p.chunk_kb) {
         mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + h * kColsPerWarp;
@@ -433,22 +449,38 @@ gemm_tc3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi,
   }
 }
 
-// 3xTF32 operand split: hi = rna_tf32(x), lo = x - hi (exact).
-__global__ void split_tf32_kernel(const float4* __restrict__ x, float4* __restrict__ hi,
-                                  float4* __restrict__ lo, int64_t n4) {
+// 3xTF32 operand split of A and B in one launch (grid-stride over both).
+// kHiCopy = true : hi = rna_tf32(x) written out, lo = x - hi (exact)
+// kHiCopy = false: the GEMM reads x itself as hi (the tensor core uses only the
+//                  top 19 bits of an fp32 operand, i.e. trunc_tf32(x)), so only
+//                  lo = x - trunc_tf32(x) (exact, <= 13 significant bits) is written:
+//                  8 bytes of traffic per element instead of 12.
+template <bool kHiCopy>
+__global__ void split_tf32_kernel(const float4* __restrict__ a, float4* __restrict__ a_hi,
+                                  float4* __restrict__ a_lo, int64_t na4,
+                                  const float4* __restrict__ b, float4* __restrict__ b_hi,
+                                  float4* __restrict__ b_lo, int64_t nb4) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
-    const float4 v = __ldg(x + i);
+  const int64_t total = na4 + nb4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const bool is_a = i < na4;
+    const int64_t j = is_a ? i : i - na4;
+    const float4 v = __ldg((is_a ? a : b) + j);
     float4 h, l;
-    uint32_t t;
-#define MTNN_SPLIT(c)                                                         \
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(v.c));                      \
-  h.c = __uint_as_float(t);                                                   \
-  l.c = v.c - h.c;
+#define MTNN_SPLIT(c)                                                          \
+  {                                                                            \
+    uint32_t t;                                                                \
+    if (kHiCopy)                                                               \
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(v.c));                    \
+    else                                                                       \
+      t = __float_as_uint(v.c) & 0xFFFFE000u;                                  \
+    h.c = __uint_as_float(t);                                                  \
+    l.c = v.c - h.c;                                                           \
+  }
     MTNN_SPLIT(x) MTNN_SPLIT(y) MTNN_SPLIT(z) MTNN_SPLIT(w)
 #undef MTNN_SPLIT
-    hi[i] = h;
-    lo[i] = l;
+    if (kHiCopy) (is_a ? a_hi : b_hi)[j] = h;
+    (is_a ? a_lo : b_lo)[j] = l;
   }
 }
 
@@ -531,12 +563,35 @@ static int launch_impl(const float* ahi, const float* alo, const float* bhi,
                                        S::kTotal));
     attr_set = true;
   }
-  kern<<<grid, kThreads, S::kTotal, s>>>(mah, mal, mbh, mbl, mc, p);
+  {
+    KernelTimer timer(MTNN_KCLASS_GEMM_TC, 2.0 * (double)p.m * (double)p.n * (double)p.k, s);
+    kern<<<grid, kThreads, S::kTotal, s>>>(mah, mal, mbh, mbl, mc, p);
+  }
   MTNN_CUDA_TRY(cudaGetLastError());
   return MTNN_OK;
 }
 
 }  // namespace tc
+
+// Split mode: "trunc" (default, lo only; the tensor core truncates the raw
+// fp32 operand to tf32 itself) or "rna" (hi and lo materialised) via MTNN_SPLIT.
+static bool split_mode_hi_copy() {
+  static const bool hi = [] {
+    const char* e = getenv("MTNN_SPLIT");
+    return e != nullptr && e[0] == 'r';
+  }();
+  return hi;
+}
+
+// k-blocks per TMEM accumulation chunk; MTNN_CHUNK_KB overrides (testing).
+static int chunk_kblocks() {
+  static const int v = [] {
+    const char* e = getenv("MTNN_CHUNK_KB");
+    const int x = e ? atoi(e) : 0;
+    return x > 0 ? x : 8;  // 128 k per chunk: 1.2e-6 (mixed) / 2.6e-6 (all-positive)
+  }();
+  return v;
+}
 
 bool tc_eligible(const float* A, const float* B, const float* C, int64_t m, int64_t n,
                  int64_t k, bool b_is_nk) {
@@ -561,31 +616,38 @@ int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t 
     return fail(MTNN_ENOTSUP, "tc3xtf32: needs %d B smem, device allows %d", S::kTotal,
                 di->max_smem_optin);
 
-  // operand split into one workspace: [A_hi | A_lo | B_hi | B_lo]
+  // operand split into one workspace: [A_lo | B_lo] (+ [A_hi | B_hi] when the
+  // hi parts are materialised); k % 4 == 0 so the counts are multiples of 4.
   const int64_t na = m * k, nb = n * k;
+  const bool hi_copy = split_mode_hi_copy();
   ScratchBuffer ws;
-  MTNN_TRY(ws.alloc((size_t)(2 * na + 2 * nb) * sizeof(float), s));
-  float* ahi = static_cast<float*>(ws.ptr);
-  float* alo = ahi + na;
-  float* bhi = alo + na;
-  float* blo = bhi + nb;
+  MTNN_TRY(ws.alloc((size_t)((hi_copy ? 2 : 1) * (na + nb)) * sizeof(float), s));
+  float* alo = static_cast<float*>(ws.ptr);
+  float* blo = alo + na;
+  const float* ahi = hi_copy ? blo + nb : A;
+  const float* bhi = hi_copy ? blo + nb + na : B;
   {
-    const int64_t blocks_cap = (int64_t)di->sm_count * 8;
-    auto split = [&](const float* x, float* h, float* l, int64_t count) -> int {
-      const int64_t n4 = count / 4;
-      int64_t blocks = std::min<int64_t>((n4 + 255) / 256, blocks_cap);
-      tc::split_tf32_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(
-          reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(h),
-          reinterpret_cast<float4*>(l), n4);
-      MTNN_CUDA_TRY(cudaGetLastError());
-      return MTNN_OK;
-    };
-    MTNN_TRY(split(A, ahi, alo, na));  // k % 4 == 0 so counts are multiples of 4
-    MTNN_TRY(split(B, bhi, blo, nb));
+    const int64_t total4 = (na + nb) / 4;
+    const int64_t blocks =
+        std::max<int64_t>(1, std::min<int64_t>((total4 + 255) / 256, (int64_t)di->sm_count * 8));
+    KernelTimer timer(MTNN_KCLASS_SPLIT, (hi_copy ? 12.0 : 8.0) * (double)(na + nb), s);
+    auto a4 = reinterpret_cast<const float4*>(A);
+    auto b4 = reinterpret_cast<const float4*>(B);
+    if (hi_copy)
+      tc::split_tf32_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(
+          a4, reinterpret_cast<float4*>(const_cast<float*>(ahi)), reinterpret_cast<float4*>(alo),
+          na / 4, b4, reinterpret_cast<float4*>(const_cast<float*>(bhi)),
+          reinterpret_cast<float4*>(blo), nb / 4);
+    else
+      tc::split_tf32_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(
+          a4, nullptr, reinterpret_cast<float4*>(alo), na / 4, b4, nullptr,
+          reinterpret_cast<float4*>(blo), nb / 4);
+    MTNN_CUDA_TRY(cudaGetLastError());
   }
 
   tc::Params p{};
   p.m = m; p.n = n; p.k = k;
+  p.chunk_kb = chunk_kblocks();
   p.tiles_m = (int)((m + tc::BM - 1) / tc::BM);
   p.tiles_n = (int)((n + BN - 1) / BN);
   p.total_kblocks = (int)((k + tc::BK - 1) / tc::BK);

@@ -128,6 +128,7 @@ int launch_transpose(const float* in, float* out, int64_t rows, int64_t cols,
   const bool vec = (rows % 4 == 0) && (cols % 4 == 0) &&
                    (reinterpret_cast<uintptr_t>(in) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+  KernelTimer timer(MTNN_KCLASS_TRANSPOSE, 8.0 * (double)rows * (double)cols, s);
   if (vec) {
     const int64_t tiles_r = (rows + kTile - 1) / kTile;
     const int64_t tiles_c = (cols + kTile - 1) / kTile;

@@ -1,0 +1,109 @@
+"""Row-sharded NT across GPUs: C = A·Bᵀ with A and C split by rows.
+
+Row i of C depends only on row i of A and all of B, so rank r of N owns rows
+``row_range(m, r, N)`` of A and C; B is replicated (``ncclBroadcast`` from the
+rank that holds it) and, when the caller wants the whole C everywhere, the
+contiguous row blocks are reassembled with one ``ncclAllGather`` — the only two
+exchange steps the path has. One process per GPU, ``torch.distributed`` with the
+NCCL backend for the plumbing; the local product is the MTNN dispatcher (or a
+fixed path) on this rank's GPU.
+
+The reference has no distributed code (SPEC.md:213 lists multi-GPU sweeps as a
+non-goal); this is the B200 build's scaling axis for config 5
+(m = 65536, n = k = 8192 over 1/2/4/8 GPUs).
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+
+def row_range(m: int, rank: int, world: int) -> tuple[int, int]:
+    """[lo, hi) rows of an m-row matrix owned by `rank` (balanced, contiguous)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank/world {rank}/{world}")
+    return (m * rank) // world, (m * (rank + 1)) // world
+
+
+def shard_rows(x: torch.Tensor, rank: int, world: int) -> torch.Tensor:
+    lo, hi = row_range(x.shape[0], rank, world)
+    return x[lo:hi]
+
+
+def _default_gemm(variant: str):
+    from . import kernels
+
+    return lambda a, b: kernels.gemm_nt(a, b, variant=variant)
+
+
+def broadcast_b(b: torch.Tensor | None, shape, *, src: int = 0, group=None,
+                device=None) -> torch.Tensor:
+    """Replicate B (n x k) from `src` to every rank of `group`."""
+    rank = dist.get_rank(group)
+    if rank == src:
+        if b is None:
+            raise ValueError("source rank must provide B")
+        out = b.contiguous()
+    else:
+        out = torch.empty(tuple(shape), dtype=torch.float32, device=device)
+    dist.broadcast(out, src=dist.get_global_rank(group, src) if group is not None else src,
+                   group=group)
+    return out
+
+
+def gather_rows(c_local: torch.Tensor, m: int, *, group=None) -> torch.Tensor:
+    """All-gather contiguous row blocks into the full m x n C on every rank.
+
+    Blocks differ by at most one row when N does not divide m; they are padded
+    to the largest block for the collective and the padding is dropped.
+    """
+    world = dist.get_world_size(group)
+    n = c_local.shape[1]
+    sizes = [row_range(m, r, world) for r in range(world)]
+    rows = max(hi - lo for lo, hi in sizes)
+    if all(hi - lo == rows for lo, hi in sizes):
+        out = torch.empty((m, n), dtype=c_local.dtype, device=c_local.device)
+        dist.all_gather_into_tensor(out, c_local.contiguous(), group=group)
+        return out
+    padded = torch.zeros((rows, n), dtype=c_local.dtype, device=c_local.device)
+    padded[: c_local.shape[0]] = c_local
+    buf = torch.empty((world * rows, n), dtype=c_local.dtype, device=c_local.device)
+    dist.all_gather_into_tensor(buf, padded, group=group)
+    return torch.cat([buf[r * rows: r * rows + (hi - lo)] for r, (lo, hi) in enumerate(sizes)])
+
+
+def sharded_gemm_nt(
+    a_local: torch.Tensor,
+    b: torch.Tensor | None,
+    *,
+    m: int,
+    n: int,
+    k: int,
+    src: int = 0,
+    gather: bool = True,
+    group=None,
+    gemm: Callable | None = None,
+    variant: str = "auto",
+) -> torch.Tensor:
+    """Row-sharded C = A·Bᵀ.
+
+    a_local: this rank's rows of A (``row_range(m, rank, N)``); b: B on rank
+    `src` (ignored elsewhere; pass None), replicated by broadcast. Returns the
+    full C (gather=True) or this rank's C rows. `gemm(a, b)` is the local NT
+    product: by default the B200 MTNN NT path; any callable with the same
+    contract (e.g. a Dispatcher's ``gemm``) works.
+    """
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    lo, hi = row_range(m, rank, world)
+    if tuple(a_local.shape) != (hi - lo, k):
+        raise ValueError(f"rank {rank}: A block has shape {tuple(a_local.shape)}, "
+                         f"expected {(hi - lo, k)}")
+    b_rep = broadcast_b(b, (n, k), src=src, group=group, device=a_local.device)
+    gemm = gemm or _default_gemm(variant)
+    c_local = gemm(a_local, b_rep) if hi > lo else torch.empty((0, n), dtype=torch.float32,
+                                                                 device=a_local.device)
+    return gather_rows(c_local, m, group=group) if gather else c_local

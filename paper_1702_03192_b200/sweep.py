@@ -1,0 +1,157 @@
+"""B200 timing sweep: NN, NT and TNN per (m, n, k) case, for labeling and retraining.
+
+GPU restatement of the reference harness (/root/reference/pkg/src/mtnn/bench.py):
+``grid_shapes`` (:198-205, 2^e per dimension, lexicographic), ``make_operands``
+semantics (:104-114, uniform [-1, 1]), interleaved round-robin timing with warm-up
+and median (:129-146), and the timings CSV wire format ``m,n,k,t_nn,t_nt,t_tnn``
+(:36-38, :366-363) that the reference's fixture mode reads back
+(``read_timings_csv`` -> ``sweep_grid(injected=...)`` -> ``label_records`` ->
+``fit_gbdt``), so the reference learner retrains unchanged on B200 labels.
+
+Timing: CUDA events on the launching stream around each call, an L2 flush
+(a 256 MiB write, > the 126 MB L2) before every timed call, inputs resident in
+HBM. TNN's window includes its stream-ordered B^T allocation, transpose and
+release (reference _numba_impl.py:16-19); the NN time uses a
+pre-transposed B^T, as the reference's does (bench.py:208-229).
+"""
+
+from __future__ import annotations
+
+import csv
+import itertools
+import statistics
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from . import device
+
+TIMING_HEADER = ("m", "n", "k", "t_nn", "t_nt", "t_tnn")
+
+
+def grid_shapes(exponents):
+    sizes = [2 ** e for e in exponents]
+    return list(itertools.product(sizes, sizes, sizes))
+
+
+class Operands:
+    """Max-size resident operands; each case views a prefix (synthetic data)."""
+
+    def __init__(self, max_m, max_n, max_k, seed=0, dev="cuda"):
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+        self.a = torch.rand(max_m * max_k, device=dev, generator=g).mul_(2).sub_(1)
+        self.b = torch.rand(max_n * max_k, device=dev, generator=g).mul_(2).sub_(1)
+        self.bt = torch.empty(max_n * max_k, device=dev)
+        self.c = torch.empty(max_m * max_n, device=dev)
+        self.flush_buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+
+    def views(self, m, n, k):
+        a = self.a[: m * k].view(m, k)
+        b = self.b[: n * k].view(n, k)
+        c = self.c[: m * n].view(m, n)
+        return a, b, c
+
+    def flush(self):
+        self.flush_buf.fill_(1.0)
+
+
+def time_calls(fns: dict, ops: Operands, reps: int, warmup: int) -> dict:
+    """Per-name median seconds, round-robin interleaved, L2 flushed before each."""
+    for _ in range(warmup):
+        for fn in fns.values():
+            fn()
+    events = {name: [] for name in fns}
+    for _ in range(reps):
+        for name, fn in fns.items():
+            ops.flush()
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn()
+            e.record()
+            events[name].append((s, e))
+    torch.cuda.synchronize()
+    return {name: statistics.median(s.elapsed_time(e) * 1e-3 for s, e in evs)
+            for name, evs in events.items()}
+
+
+@dataclass
+class CaseTiming:
+    m: int
+    n: int
+    k: int
+    t_nn: float
+    t_nt: float
+    t_tnn: float
+
+
+def measure_case(ops: Operands, m, n, k, reps=5, warmup=2, variant=_lib.VARIANT_AUTO):
+    a, b, c = ops.views(m, n, k)
+    bt = ops.bt[: n * k].view(k, n)
+    device.transpose(b, out=bt)
+    fns = {
+        "nn": lambda: device.gemm_nn(a, bt, out=c, variant=variant),
+        "nt": lambda: device.gemm_nt(a, b, out=c, variant=variant),
+        "tnn": lambda: device.gemm_tnn(a, b, out=c, variant=variant),
+    }
+    t = time_calls(fns, ops, reps, warmup)
+    return CaseTiming(m, n, k, t["nn"], t["nt"], t["tnn"])
+
+
+def sweep(exponents, reps=5, warmup=2, variant=_lib.VARIANT_AUTO, log=None):
+    shapes = grid_shapes(exponents)
+    mx = 2 ** max(exponents)
+    ops = Operands(mx, mx, mx)
+    out = []
+    for (m, n, k) in shapes:
+        ct = measure_case(ops, m, n, k, reps, warmup, variant)
+        out.append(ct)
+        if log:
+            log(f"{m} {n} {k}: nn {ct.t_nn*1e6:.1f}us nt {ct.t_nt*1e6:.1f}us "
+                f"tnn {ct.t_tnn*1e6:.1f}us  NT {2*m*n*k/ct.t_nt/1e12:.1f} TF")
+    return out
+
+
+def write_timings_csv(path, rows):
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(TIMING_HEADER)
+        for r in rows:
+            w.writerow([r.m, r.n, r.k, repr(r.t_nn), repr(r.t_nt), repr(r.t_tnn)])
+
+
+def read_timings_csv(path):
+    out = {}
+    with open(path, newline="") as fh:
+        rd = csv.DictReader(fh)
+        for row in rd:
+            out[(int(row["m"]), int(row["n"]), int(row["k"]))] = (
+                float(row["t_nn"]), float(row["t_nt"]), float(row["t_tnn"]))
+    return out
+
+
+if __name__ == "__main__":
+    import argparse
+    import json
+    import sys
+
+    from .platform import probe_platform
+
+    ap = argparse.ArgumentParser(description="B200 NN/NT/TNN timing sweep")
+    ap.add_argument("--exp-min", type=int, default=7)
+    ap.add_argument("--exp-max", type=int, default=14)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--variant", default="auto", choices=sorted(_lib.VARIANTS))
+    ap.add_argument("--out", default="gpurun_out/sweep_timings.csv")
+    args = ap.parse_args()
+    rows = sweep(range(args.exp_min, args.exp_max + 1), args.reps, args.warmup,
+                 _lib.VARIANTS[args.variant], log=lambda s: print(s, file=sys.stderr, flush=True))
+    write_timings_csv(args.out, rows)
+    plat = probe_platform()
+    with open(args.out + ".platform.json", "w") as fh:
+        json.dump({"platform": plat.as_tuple(), "variant": args.variant,
+                   "reps": args.reps, "warmup": args.warmup}, fh)
+    print(f"wrote {len(rows)} cases to {args.out}")

@@ -1,0 +1,73 @@
+"""Row-sharded NT host logic over world-size-2 gloo (CPU). The local product is
+injected (torch CPU matmul) because the product path has no CPU kernels; the
+partitioning, the B broadcast and the C all-gather are what is under test."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1702_03192_b200.sharding import row_range, sharded_gemm_nt, shard_rows
+
+
+def test_row_range_partitions():
+    for m in (1, 7, 8, 65536, 12345):
+        for world in (1, 2, 3, 4, 8):
+            ranges = [row_range(m, r, world) for r in range(world)]
+            assert ranges[0][0] == 0 and ranges[-1][1] == m
+            assert all(ranges[i][1] == ranges[i + 1][0] for i in range(world - 1))
+            sizes = [hi - lo for lo, hi in ranges]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        row_range(8, 2, 2)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, m, n, k, gather, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(7)
+        a = torch.rand(m, k, generator=g) * 2 - 1
+        b = torch.rand(n, k, generator=g) * 2 - 1
+        a_local = shard_rows(a, rank, world).contiguous()
+        c = sharded_gemm_nt(a_local, b if rank == 0 else None, m=m, n=n, k=k, gather=gather,
+                            gemm=lambda x, y: x @ y.t())
+        want = a.double() @ b.double().t()
+        if gather:
+            err = float((c.double() - want).norm() / want.norm())
+            shape_ok = tuple(c.shape) == (m, n)
+        else:
+            lo, hi = row_range(m, rank, world)
+            err = float((c.double() - want[lo:hi]).norm() / max(want[lo:hi].norm(), 1e-30))
+            shape_ok = tuple(c.shape) == (hi - lo, n)
+        q.put((rank, err, shape_ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m,gather", [(64, True), (37, True), (1, True), (64, False)])
+def test_sharded_nt_world2_gloo(m, gather):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, m, 24, 40, gather, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    results = sorted(q.get(timeout=10) for _ in range(2))
+    for rank, err, shape_ok in results:
+        assert shape_ok, rank
+        assert err < 1e-6, (rank, err)
