@@ -43,9 +43,10 @@ extern "C" {
 #define MTNN_ENOTSUP 95 /* no sm_100 device / unsupported variant   */
 
 /* GEMM variant selector (within one path; the NT-vs-TNN choice is the model's). */
-#define MTNN_VARIANT_AUTO 0     /* heuristic: tensor-core 3xTF32 when eligible, else FFMA */
-#define MTNN_VARIANT_TC3XTF32 1 /* tcgen05 kind::tf32, 3-term split, TMEM accumulator      */
+#define MTNN_VARIANT_AUTO 0     /* heuristic: tc3xf16s, else tc3xtf32, else FFMA           */
+#define MTNN_VARIANT_TC3XTF32 1 /* tcgen05 kind::tf32, hi/lo split, 3 MMAs per product     */
 #define MTNN_VARIANT_FFMA 2     /* SIMT FP32 FFMA (exact-order fp32, any shape)            */
+#define MTNN_VARIANT_TC3XF16S 3 /* tcgen05 kind::f16, per-row pow2-scaled fp16 hi/lo split */
 
 /* dispatcher choices (reference selector.py:43-51) */
 #define MTNN_CHOICE_NT 0
@@ -71,15 +72,17 @@ int mtnn_device_features(double out5[5]);
  * When enabled, every launch of the library's main kernels is bracketed with
  * CUDA events on its launch stream and tagged with its algorithmic work:
  * class 0 = tc3xtf32 GEMM (2mnk flops), 1 = FFMA GEMM (2mnk flops),
- * 2 = transpose (8*rows*cols bytes), 3 = 3xTF32 operand split (12 bytes per
- * element), 4 = split-K reduction (4*(splits+1) bytes per output).
+ * 2 = transpose (8*rows*cols bytes), 3 = operand split (bytes moved: 8 per
+ * element; 12 for the column-scaled fp16 split), 4 = split-K reduction
+ * (4*(splits+1) bytes per output), 5 = tc3xf16s GEMM (2mnk flops).
  * mtnn_profile_read synchronizes the recorded events and returns the totals. */
 #define MTNN_KCLASS_GEMM_TC 0
 #define MTNN_KCLASS_GEMM_FFMA 1
 #define MTNN_KCLASS_TRANSPOSE 2
 #define MTNN_KCLASS_SPLIT 3
 #define MTNN_KCLASS_REDUCE 4
-#define MTNN_KCLASS_COUNT 5
+#define MTNN_KCLASS_GEMM_TC_F16S 5
+#define MTNN_KCLASS_COUNT 6
 int mtnn_profile_enable(int on);
 int mtnn_profile_reset(void);
 int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* work);

@@ -23,14 +23,18 @@ ENOTSUP = 95
 VARIANT_AUTO = 0
 VARIANT_TC3XTF32 = 1
 VARIANT_FFMA = 2
-VARIANTS = {"auto": VARIANT_AUTO, "tc3xtf32": VARIANT_TC3XTF32, "ffma": VARIANT_FFMA}
+VARIANT_TC3XF16S = 3
+VARIANTS = {"auto": VARIANT_AUTO, "tc3xtf32": VARIANT_TC3XTF32, "ffma": VARIANT_FFMA,
+            "tc3xf16s": VARIANT_TC3XF16S}
 
 KCLASS_GEMM_TC = 0
 KCLASS_GEMM_FFMA = 1
 KCLASS_TRANSPOSE = 2
 KCLASS_SPLIT = 3
 KCLASS_REDUCE = 4
-KCLASS_NAMES = {0: "gemm_tc3xtf32", 1: "gemm_ffma", 2: "transpose", 3: "split_tf32", 4: "splitk_reduce"}
+KCLASS_GEMM_TC_F16S = 5
+KCLASS_NAMES = {0: "gemm_tc3xtf32", 1: "gemm_ffma", 2: "transpose", 3: "operand_split",
+                4: "splitk_reduce", 5: "gemm_tc3xf16s"}
 
 CHOICE_NT = 0
 CHOICE_TNN = 1

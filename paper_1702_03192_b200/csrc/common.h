@@ -64,11 +64,19 @@ int launch_transpose(const float* in, float* out, int64_t rows, int64_t cols,
                      cudaStream_t s);
 int launch_gemm_ffma(const float* A, const float* B, float* C, int64_t m, int64_t n,
                      int64_t k, bool b_is_nk, cudaStream_t s);
-// Tensor-core 3xTF32 GEMM. b_is_nk: B stored n x k (NT); else B^T stored k x n (NN).
+// Tensor-core FP32-accurate GEMMs (three MMAs per product on hi/lo operand halves).
+// TF32: hi = raw fp32 (truncated to tf32 by the tensor core), lo = x - trunc(x).
+// F16S: per-row power-of-two scaled fp16 hi/lo (split_f16.cu), 2x the MMA rate.
+// b_is_nk: B stored n x k (NT); else B^T stored k x n (NN).
 // Returns MTNN_ENOTSUP when the shape/alignment is ineligible.
+enum class TcKind { TF32, F16S };
 int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t n,
-                   int64_t k, bool b_is_nk, cudaStream_t s);
+                   int64_t k, bool b_is_nk, TcKind kind, cudaStream_t s);
 bool tc_eligible(const float* A, const float* B, const float* C, int64_t m, int64_t n,
-                 int64_t k, bool b_is_nk);
+                 int64_t k, bool b_is_nk, TcKind kind);
+int launch_split_rows_f16(const float* x, void* hi, void* lo, float* inv_scale, int64_t rows,
+                          int64_t k, cudaStream_t s);
+int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,
+                          unsigned* colmax_scratch, int64_t k, int64_t n, cudaStream_t s);
 
 }  // namespace mtnn

@@ -44,19 +44,46 @@ int launch_splitk_reduce(const float* part, float* C, int64_t count, int splits,
 namespace tc {
 
 constexpr int BM = 128;          // UMMA M (one CTA, 128 TMEM lanes)
-constexpr int BK = 16;           // fp32 elements per k-block (64 bytes, SWIZZLE_64B)
-constexpr int UMMA_K = 8;        // tf32 K per tcgen05.mma
 constexpr int kStages = 4;
 constexpr int kEpiWarp0 = 4;      // warps 0..3: TMA, MMA, TMEM alloc, spare
 constexpr int kEpiWarps = 16;     // 4 TMEM lane quarters x 4 column quarters
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
-constexpr uint32_t kLayoutSW128B32 = 1;  // UMMA SWIZZLE_128B_BASE32B
 constexpr uint32_t kLayoutSW64 = 4;      // UMMA SWIZZLE_64B
+
+// Operand kinds. Both keep 64-byte K-major rows per k-block (SWIZZLE_64B, one
+// UMMA K-step = 32 bytes), so the smem ring and the K-major descriptors are
+// shared; they differ in element type, MMA kind and the MN-major B layout.
+struct KindTF32 {  // hi = raw fp32 (read as trunc-tf32), lo = x - trunc(x)
+  static constexpr int kElemBytes = 4;
+  static constexpr int BK = 16;                 // elements per k-block
+  static constexpr int UMMA_K = 8;              // kind::tf32
+  static constexpr uint32_t kFmt = 2;           // instruction-descriptor TF32
+  static constexpr bool kScaled = false;
+  static constexpr CUtensorMapDataType kTmaType = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  // MN-major B^T: SWIZZLE_128B_BASE32B (the only MN-major tf32 layout), boxes of
+  // 32 columns x 16 k-rows (2 KiB), 4-row groups 512 B apart, K-step 8 rows.
+  static constexpr int kMnBox = 32;
+  static constexpr uint32_t kMnLayout = 1, kMnLBO = 2048, kMnSBO = 512, kMnKStep = 1024;
+  static constexpr CUtensorMapSwizzle kMnSwizzle = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+};
+struct KindF16S {  // per-row power-of-2 scaled fp16 hi/lo (split_f16.cu)
+  static constexpr int kElemBytes = 2;
+  static constexpr int BK = 32;
+  static constexpr int UMMA_K = 16;             // kind::f16
+  static constexpr uint32_t kFmt = 0;           // instruction-descriptor F16
+  static constexpr bool kScaled = true;
+  static constexpr CUtensorMapDataType kTmaType = CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  // MN-major B^T: SWIZZLE_128B, boxes of 64 columns x 32 k-rows (4 KiB), 8-row
+  // groups 1 KiB apart, K-step 16 rows.
+  static constexpr int kMnBox = 64;
+  static constexpr uint32_t kMnLayout = 2, kMnLBO = 4096, kMnSBO = 1024, kMnKStep = 2048;
+  static constexpr CUtensorMapSwizzle kMnSwizzle = CU_TENSOR_MAP_SWIZZLE_128B;
+};
 
 template <int BN>
 struct Smem {
-  static constexpr int kABytes = BM * BK * 4;            // 8 KiB
-  static constexpr int kBBytes = BN * BK * 4;            // 16 KiB at BN=256
+  static constexpr int kABytes = BM * 64;                // 8 KiB (64-byte k-block rows)
+  static constexpr int kBBytes = BN * 64;                // 16 KiB at BN=256
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
   static constexpr int kStagingBytes = 32 * 16 * 4;      // one 32x16 fp32 tile
   static constexpr int kRingBytes = kStages * kStageBytes;
@@ -201,9 +228,9 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
   return d;
 }
 
-// Instruction descriptor: D=f32, A=B=tf32, A K-major, B K- or MN-major, M=128, N.
-__host__ __device__ constexpr uint32_t make_idesc(int n, bool b_mn_major) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((b_mn_major ? 1u : 0u) << 16) |
+// Instruction descriptor: D=f32, A=B=fmt, A K-major, B K- or MN-major, M=128, N.
+__host__ __device__ constexpr uint32_t make_idesc(int n, bool b_mn_major, uint32_t fmt) {
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((b_mn_major ? 1u : 0u) << 16) |
          ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
@@ -212,6 +239,8 @@ struct Params {
   int chunk_kb;  // k-blocks per TMEM accumulation chunk (FP32 promotion period)
   int tiles_m, tiles_n, splits, kblocks_per_split, total_kblocks;
   int units;
+  const float* inv_scale_a;  // KindF16S: 1/s per row of A (m) and of B (n)
+  const float* inv_scale_b;
 };
 
 // Work-unit order: units are (k-split, tile); within a split, tiles walk
@@ -235,9 +264,9 @@ __device__ __forceinline__ void unit_coords(int u, const Params& p, int& split, 
 }
 
 // ------------------------------------------------------------------- kernel
-template <int BN, bool B_MN>
+template <int BN, bool B_MN, class Kind>
 __global__ void __launch_bounds__(kThreads, 1)
-gemm_tc3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi,
+gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
                      const __grid_constant__ CUtensorMap map_alo,
                      const __grid_constant__ CUtensorMap map_bhi,
                      const __grid_constant__ CUtensorMap map_blo,
@@ -305,21 +334,21 @@ gemm_tc3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi,
           const uint32_t fb = smem_u32(&full_bar[stage]);
           mbar_expect_tx(fb, S::kStageBytes);
           uint8_t* st = ring + stage * S::kStageBytes;
-          const int kx = kb * BK;
+          const int kx = kb * Kind::BK;
           tma_load_2d(smem_u32(st), &map_ahi, fb, kx, tm * BM);
           tma_load_2d(smem_u32(st + S::kABytes), &map_alo, fb, kx, tm * BM);
           if (!B_MN) {
             tma_load_2d(smem_u32(st + 2 * S::kABytes), &map_bhi, fb, kx, tn * BN);
             tma_load_2d(smem_u32(st + 2 * S::kABytes + S::kBBytes), &map_blo, fb, kx, tn * BN);
           } else {
-            // BN/32 boxes of [16 k-rows][32 n] (128-byte rows, 128B swizzle with
-            // 32-byte atoms — the only MN-major layout UMMA accepts for tf32), 2 KiB apart
+            // BN/kMnBox boxes of [BK k-rows][kMnBox columns] (128-byte rows), each
+            // one MN group of the canonical MN-major layout, kMnLBO bytes apart
 #pragma unroll
-            for (int g = 0; g < BN / 32; ++g) {
-              tma_load_2d(smem_u32(st + 2 * S::kABytes + g * 2048), &map_bhi, fb,
-                          tn * BN + g * 32, kx);
-              tma_load_2d(smem_u32(st + 2 * S::kABytes + S::kBBytes + g * 2048), &map_blo, fb,
-                          tn * BN + g * 32, kx);
+            for (int g = 0; g < BN / Kind::kMnBox; ++g) {
+              tma_load_2d(smem_u32(st + 2 * S::kABytes + g * Kind::kMnLBO), &map_bhi, fb,
+                          tn * BN + g * Kind::kMnBox, kx);
+              tma_load_2d(smem_u32(st + 2 * S::kABytes + S::kBBytes + g * Kind::kMnLBO),
+                          &map_blo, fb, tn * BN + g * Kind::kMnBox, kx);
             }
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -328,7 +357,7 @@ gemm_tc3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi,
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    constexpr uint32_t idesc = make_idesc(BN, B_MN);
+    constexpr uint32_t idesc = make_idesc(BN, B_MN, Kind::kFmt);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -352,7 +381,7 @@ gemm_tc3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi,
             const uint32_t b_hi = a_hi + 2 * S::kABytes;
             const uint32_t b_lo = b_hi + S::kBBytes;
 #pragma unroll
-            for (int ks = 0; ks < BK / UMMA_K; ++ks) {
+            for (int ks = 0; ks < Kind::BK / Kind::UMMA_K; ++ks) {
               // A: K-major SW64 — 64-byte rows, 8-row groups 512 B apart; k-step +32 B.
               const uint64_t dah = make_sdesc(a_hi + ks * 32, 16, 512, kLayoutSW64);
               const uint64_t dal = make_sdesc(a_lo + ks * 32, 16, 512, kLayoutSW64);
@@ -361,10 +390,11 @@ gemm_tc3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi,
                 dbh = make_sdesc(b_hi + ks * 32, 16, 512, kLayoutSW64);
                 dbl = make_sdesc(b_lo + ks * 32, 16, 512, kLayoutSW64);
               } else {
-                // B: MN-major SW128_BASE32B — 32-column groups 2 KiB apart (LBO),
-                // 4-k-row groups 512 B apart (SBO); an 8-deep k-step is +1 KiB.
-                dbh = make_sdesc(b_hi + ks * 1024, 2048, 512, kLayoutSW128B32);
-                dbl = make_sdesc(b_lo + ks * 1024, 2048, 512, kLayoutSW128B32);
+                // B: MN-major — column groups kMnLBO apart, k-row groups kMnSBO apart
+                dbh = make_sdesc(b_hi + ks * Kind::kMnKStep, Kind::kMnLBO, Kind::kMnSBO,
+                                 Kind::kMnLayout);
+                dbl = make_sdesc(b_lo + ks * Kind::kMnKStep, Kind::kMnLBO, Kind::kMnSBO,
+                                 Kind::kMnLayout);
               }
               const uint32_t accum = (kb == kc && ks == 0) ? 0u : 1u;
               tc_mma_tf32(tmem_d, dal, dbh, idesc, accum);
@@ -416,6 +446,11 @@ gemm_tc3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi,
         if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[acc]));
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
+      // KindF16S: undo the exact power-of-two operand scales while storing,
+      // C = (acc * 1/s_a[row]) * 1/s_b[col]
+      const int64_t row = (int64_t)tm * BM + q * 32 + lane;
+      const int64_t col0 = (int64_t)tn * BN + h * kColsPerWarp;
+      const float sa = (Kind::kScaled && row < p.m) ? __ldg(p.inv_scale_a + row) : 1.f;
       // Store: 32 rows x kColsPerWarp through a 32x16 staging tile (64B swizzle).
 #pragma unroll
       for (int c = 0; c < kColsPerWarp / 16; ++c) {
@@ -424,9 +459,19 @@ gemm_tc3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi,
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int pj = j ^ ((lane >> 1) & 3);
-          *reinterpret_cast<float4*>(stg + lane * 64 + pj * 16) =
-              make_float4(sum[c * 16 + 4 * j], sum[c * 16 + 4 * j + 1],
-                          sum[c * 16 + 4 * j + 2], sum[c * 16 + 4 * j + 3]);
+          float4 v = make_float4(sum[c * 16 + 4 * j], sum[c * 16 + 4 * j + 1],
+                                 sum[c * 16 + 4 * j + 2], sum[c * 16 + 4 * j + 3]);
+          if (Kind::kScaled) {
+            // the scale vector has n entries (n % 4 == 0): whole float4s are in range
+            const int64_t cj = col0 + c * 16 + 4 * j;
+            const float4 sb = cj < p.n ? __ldg(reinterpret_cast<const float4*>(p.inv_scale_b + cj))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+            v.x = (v.x * sa) * sb.x;
+            v.y = (v.y * sa) * sb.y;
+            v.z = (v.z * sa) * sb.z;
+            v.w = (v.w * sa) * sb.w;
+          }
+          *reinterpret_cast<float4*>(stg + lane * 64 + pj * 16) = v;
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -507,6 +552,8 @@ static int get_encode(EncodeTiledFn* out) {
   return MTNN_OK;
 }
 
+static thread_local CUtensorMapDataType encode_dtype = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+
 static int encode(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
                   const uint64_t* strides_bytes /* rank-1 */, const uint32_t* box,
                   CUtensorMapSwizzle swz) {
@@ -516,47 +563,49 @@ static int encode(CUtensorMap* map, const void* base, int rank, const uint64_t* 
   cuuint32_t b[5], es[5];
   for (int i = 0; i < rank; ++i) { d[i] = dims[i]; b[i] = box[i]; es[i] = 1; }
   for (int i = 0; i < rank - 1; ++i) st[i] = strides_bytes[i];
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), d, st, b,
+  CUresult r = fn(map, encode_dtype, rank, const_cast<void*>(base), d, st, b,
                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(MTNN_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return MTNN_OK;
 }
 
-template <int BN, bool B_MN>
-static int launch_impl(const float* ahi, const float* alo, const float* bhi,
-                       const float* blo, float* out, const Params& p, int grid,
+template <int BN, bool B_MN, class Kind>
+static int launch_impl(const void* ahi, const void* alo, const void* bhi,
+                       const void* blo, float* out, const Params& p, int grid,
                        cudaStream_t s) {
   using S = Smem<BN>;
   CUtensorMap mah, mal, mbh, mbl, mc;
+  encode_dtype = Kind::kTmaType;
+  const uint64_t eb = Kind::kElemBytes;
   {
     const uint64_t dims[2] = {(uint64_t)p.k, (uint64_t)p.m};
-    const uint64_t str[1] = {(uint64_t)p.k * 4};
-    const uint32_t box[2] = {BK, BM};
+    const uint64_t str[1] = {(uint64_t)p.k * eb};
+    const uint32_t box[2] = {(uint32_t)Kind::BK, BM};
     MTNN_TRY(encode(&mah, ahi, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
     MTNN_TRY(encode(&mal, alo, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
   }
   if (!B_MN) {
     const uint64_t dims[2] = {(uint64_t)p.k, (uint64_t)p.n};
-    const uint64_t str[1] = {(uint64_t)p.k * 4};
-    const uint32_t box[2] = {BK, BN};
+    const uint64_t str[1] = {(uint64_t)p.k * eb};
+    const uint32_t box[2] = {(uint32_t)Kind::BK, BN};
     MTNN_TRY(encode(&mbh, bhi, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
     MTNN_TRY(encode(&mbl, blo, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
   } else {
     const uint64_t dims[2] = {(uint64_t)p.n, (uint64_t)p.k};
-    const uint64_t str[1] = {(uint64_t)p.n * 4};
-    const uint32_t box[2] = {32, BK};
-    const CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
-    MTNN_TRY(encode(&mbh, bhi, 2, dims, str, box, sw));
-    MTNN_TRY(encode(&mbl, blo, 2, dims, str, box, sw));
+    const uint64_t str[1] = {(uint64_t)p.n * eb};
+    const uint32_t box[2] = {(uint32_t)Kind::kMnBox, (uint32_t)Kind::BK};
+    MTNN_TRY(encode(&mbh, bhi, 2, dims, str, box, Kind::kMnSwizzle));
+    MTNN_TRY(encode(&mbl, blo, 2, dims, str, box, Kind::kMnSwizzle));
   }
+  encode_dtype = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   {
     const uint64_t dims[3] = {(uint64_t)p.n, (uint64_t)p.m, (uint64_t)p.splits};
     const uint64_t str[2] = {(uint64_t)p.n * 4, (uint64_t)p.n * p.m * 4};
     const uint32_t box[3] = {16, 32, 1};
     MTNN_TRY(encode(&mc, out, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
   }
-  auto kern = gemm_tc3xtf32_kernel<BN, B_MN>;
+  auto kern = gemm_tc3x_kernel<BN, B_MN, Kind>;
   static bool attr_set = false;
   if (!attr_set) {
     MTNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -564,7 +613,8 @@ static int launch_impl(const float* ahi, const float* alo, const float* bhi,
     attr_set = true;
   }
   {
-    KernelTimer timer(MTNN_KCLASS_GEMM_TC, 2.0 * (double)p.m * (double)p.n * (double)p.k, s);
+    KernelTimer timer(Kind::kScaled ? MTNN_KCLASS_GEMM_TC_F16S : MTNN_KCLASS_GEMM_TC,
+                      2.0 * (double)p.m * (double)p.n * (double)p.k, s);
     kern<<<grid, kThreads, S::kTotal, s>>>(mah, mal, mbh, mbl, mc, p);
   }
   MTNN_CUDA_TRY(cudaGetLastError());
@@ -583,50 +633,57 @@ static bool split_mode_hi_copy() {
   return hi;
 }
 
-// k-blocks per TMEM accumulation chunk; MTNN_CHUNK_KB overrides (testing).
-static int chunk_kblocks() {
+// k-blocks per TMEM accumulation chunk (the FP32 promotion period); both kinds
+// default to 48 MMA accumulations per chunk (tf32: 8 x 16 = 128 k; f16: 8 x 32 =
+// 256 k). MTNN_CHUNK_KB overrides (testing).
+static int chunk_kblocks(TcKind) {
   static const int v = [] {
     const char* e = getenv("MTNN_CHUNK_KB");
     const int x = e ? atoi(e) : 0;
-    return x > 0 ? x : 8;  // 128 k per chunk: 1.2e-6 (mixed) / 2.6e-6 (all-positive)
+    return x > 0 ? x : 8;
   }();
   return v;
 }
 
 bool tc_eligible(const float* A, const float* B, const float* C, int64_t m, int64_t n,
-                 int64_t k, bool b_is_nk) {
+                 int64_t k, bool b_is_nk, TcKind kind) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (m <= 0 || n <= 0 || k <= 0) return false;
-  if (k % 4 != 0 || n % 4 != 0) return false;        // 16-byte TMA row strides
-  if (!b_is_nk && n % 16 != 0) return false;         // MN-major 16-column groups
+  if (k % 4 != 0 || n % 4 != 0) return false;        // 16-byte TMA row strides (fp32)
+  if (kind == TcKind::F16S && k % 8 != 0) return false;  // 16-byte rows of fp16 halves
+  if (!b_is_nk && n % 16 != 0) return false;         // MN-major column groups
   if (m > (1LL << 31) - 1 || n > (1LL << 31) - 1 || k > (1LL << 31) - 1) return false;
   return al16(A) && al16(B) && al16(C);
 }
 
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
 int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t n,
-                   int64_t k, bool b_is_nk, cudaStream_t s) {
-  if (!tc_eligible(A, B, C, m, n, k, b_is_nk))
-    return fail(MTNN_ENOTSUP, "tc3xtf32: shape/alignment not eligible (m=%lld n=%lld k=%lld)",
+                   int64_t k, bool b_is_nk, TcKind kind, cudaStream_t s) {
+  const char* name = kind == TcKind::F16S ? "tc3xf16s" : "tc3xtf32";
+  if (!tc_eligible(A, B, C, m, n, k, b_is_nk, kind))
+    return fail(MTNN_ENOTSUP, "%s: shape/alignment not eligible (m=%lld n=%lld k=%lld)", name,
                 (long long)m, (long long)n, (long long)k);
   const DeviceInfo* di = nullptr;
   MTNN_TRY(device_info(&di));
   constexpr int BN = 256;
   using S = tc::Smem<BN>;
   if (di->max_smem_optin < S::kTotal)
-    return fail(MTNN_ENOTSUP, "tc3xtf32: needs %d B smem, device allows %d", S::kTotal,
+    return fail(MTNN_ENOTSUP, "%s: needs %d B smem, device allows %d", name, S::kTotal,
                 di->max_smem_optin);
 
-  // operand split into one workspace: [A_lo | B_lo] (+ [A_hi | B_hi] when the
-  // hi parts are materialised); k % 4 == 0 so the counts are multiples of 4.
   const int64_t na = m * k, nb = n * k;
-  const bool hi_copy = split_mode_hi_copy();
+  const void *ahi, *alo, *bhi, *blo;
+  const float *inv_a = nullptr, *inv_b = nullptr;
   ScratchBuffer ws;
-  MTNN_TRY(ws.alloc((size_t)((hi_copy ? 2 : 1) * (na + nb)) * sizeof(float), s));
-  float* alo = static_cast<float*>(ws.ptr);
-  float* blo = alo + na;
-  const float* ahi = hi_copy ? blo + nb : A;
-  const float* bhi = hi_copy ? blo + nb + na : B;
-  {
+  if (kind == TcKind::TF32) {
+    // workspace [A_lo | B_lo] (+ [A_hi | B_hi] when materialised); k % 4 == 0
+    const bool hi_copy = split_mode_hi_copy();
+    MTNN_TRY(ws.alloc((size_t)((hi_copy ? 2 : 1) * (na + nb)) * sizeof(float), s));
+    float* a_lo = static_cast<float*>(ws.ptr);
+    float* b_lo = a_lo + na;
+    float* a_hi = hi_copy ? b_lo + nb : nullptr;
+    float* b_hi = hi_copy ? b_lo + nb + na : nullptr;
     const int64_t total4 = (na + nb) / 4;
     const int64_t blocks =
         std::max<int64_t>(1, std::min<int64_t>((total4 + 255) / 256, (int64_t)di->sm_count * 8));
@@ -635,22 +692,50 @@ int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t 
     auto b4 = reinterpret_cast<const float4*>(B);
     if (hi_copy)
       tc::split_tf32_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(
-          a4, reinterpret_cast<float4*>(const_cast<float*>(ahi)), reinterpret_cast<float4*>(alo),
-          na / 4, b4, reinterpret_cast<float4*>(const_cast<float*>(bhi)),
-          reinterpret_cast<float4*>(blo), nb / 4);
+          a4, reinterpret_cast<float4*>(a_hi), reinterpret_cast<float4*>(a_lo), na / 4, b4,
+          reinterpret_cast<float4*>(b_hi), reinterpret_cast<float4*>(b_lo), nb / 4);
     else
       tc::split_tf32_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(
-          a4, nullptr, reinterpret_cast<float4*>(alo), na / 4, b4, nullptr,
-          reinterpret_cast<float4*>(blo), nb / 4);
+          a4, nullptr, reinterpret_cast<float4*>(a_lo), na / 4, b4, nullptr,
+          reinterpret_cast<float4*>(b_lo), nb / 4);
     MTNN_CUDA_TRY(cudaGetLastError());
+    ahi = hi_copy ? a_hi : A;
+    bhi = hi_copy ? b_hi : B;
+    alo = a_lo;
+    blo = b_lo;
+  } else {
+    // workspace [A_h | A_l | B_h | B_l | 1/s_a | 1/s_b | colmax]
+    const size_t oa = align256((size_t)na * 2), ob = align256((size_t)nb * 2);
+    const size_t osa = align256((size_t)m * 4), osb = align256((size_t)n * 4);
+    const size_t ocm = b_is_nk ? 0 : align256((size_t)n * 4);
+    MTNN_TRY(ws.alloc(2 * oa + 2 * ob + osa + osb + ocm, s));
+    uint8_t* base = static_cast<uint8_t*>(ws.ptr);
+    void* a_h = base;
+    void* a_l = base + oa;
+    void* b_h = base + 2 * oa;
+    void* b_l = base + 2 * oa + ob;
+    float* sa = reinterpret_cast<float*>(base + 2 * oa + 2 * ob);
+    float* sb = reinterpret_cast<float*>(base + 2 * oa + 2 * ob + osa);
+    MTNN_TRY(launch_split_rows_f16(A, a_h, a_l, sa, m, k, s));
+    if (b_is_nk) {
+      MTNN_TRY(launch_split_rows_f16(B, b_h, b_l, sb, n, k, s));
+    } else {
+      unsigned* cm = reinterpret_cast<unsigned*>(base + 2 * oa + 2 * ob + osa + osb);
+      MTNN_TRY(launch_split_cols_f16(B, b_h, b_l, sb, cm, k, n, s));
+    }
+    ahi = a_h; alo = a_l; bhi = b_h; blo = b_l;
+    inv_a = sa; inv_b = sb;
   }
 
+  const int bk = kind == TcKind::F16S ? tc::KindF16S::BK : tc::KindTF32::BK;
   tc::Params p{};
   p.m = m; p.n = n; p.k = k;
-  p.chunk_kb = chunk_kblocks();
+  p.chunk_kb = chunk_kblocks(kind);
+  p.inv_scale_a = inv_a;
+  p.inv_scale_b = inv_b;
   p.tiles_m = (int)((m + tc::BM - 1) / tc::BM);
   p.tiles_n = (int)((n + BN - 1) / BN);
-  p.total_kblocks = (int)((k + tc::BK - 1) / tc::BK);
+  p.total_kblocks = (int)((k + bk - 1) / bk);
   const int tiles = p.tiles_m * p.tiles_n;
   int splits = 1;
   if (tiles < di->sm_count && p.total_kblocks >= 16) {
@@ -669,8 +754,13 @@ int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t 
     MTNN_TRY(part.alloc((size_t)splits * m * n * sizeof(float), s));
     out = static_cast<float*>(part.ptr);
   }
-  int rc = b_is_nk ? tc::launch_impl<BN, false>(ahi, alo, bhi, blo, out, p, grid, s)
-                   : tc::launch_impl<BN, true>(ahi, alo, bhi, blo, out, p, grid, s);
+  int rc;
+  if (kind == TcKind::F16S)
+    rc = b_is_nk ? tc::launch_impl<BN, false, tc::KindF16S>(ahi, alo, bhi, blo, out, p, grid, s)
+                 : tc::launch_impl<BN, true, tc::KindF16S>(ahi, alo, bhi, blo, out, p, grid, s);
+  else
+    rc = b_is_nk ? tc::launch_impl<BN, false, tc::KindTF32>(ahi, alo, bhi, blo, out, p, grid, s)
+                 : tc::launch_impl<BN, true, tc::KindTF32>(ahi, alo, bhi, blo, out, p, grid, s);
   MTNN_TRY(rc);
   if (splits > 1) MTNN_TRY(launch_splitk_reduce(out, C, m * n, splits, s));
   return MTNN_OK;

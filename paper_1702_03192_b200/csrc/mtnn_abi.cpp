@@ -103,20 +103,21 @@ static int check_dims(int64_t m, int64_t n, int64_t k) {
   return MTNN_OK;
 }
 
-static bool use_tc(int variant, const float* A, const float* B, const float* C, int64_t m,
-                   int64_t n, int64_t k, bool b_is_nk) {
-  if (variant == MTNN_VARIANT_FFMA) return false;
-  const bool ok = tc_eligible(A, B, C, m, n, k, b_is_nk);
-  if (variant == MTNN_VARIANT_TC3XTF32) return true;  // launch reports ineligibility
-  // AUTO: tensor cores once the problem is big enough to amortise the operand
-  // split; tiny problems keep the exact-order FFMA chain (bit-exact identity KATs).
-  return ok && (double)m * (double)n * (double)k >= 4194304.0;
+// AUTO: the FP16x3-scaled tensor-core path once the problem is big enough to
+// amortise the operand split (else the TF32 path if only that is eligible);
+// tiny problems keep the exact-order FFMA chain (bit-exact identity KATs).
+static int auto_variant(const float* A, const float* B, const float* C, int64_t m, int64_t n,
+                        int64_t k, bool b_is_nk) {
+  if ((double)m * (double)n * (double)k < 4194304.0) return MTNN_VARIANT_FFMA;
+  if (tc_eligible(A, B, C, m, n, k, b_is_nk, TcKind::F16S)) return MTNN_VARIANT_TC3XF16S;
+  if (tc_eligible(A, B, C, m, n, k, b_is_nk, TcKind::TF32)) return MTNN_VARIANT_TC3XTF32;
+  return MTNN_VARIANT_FFMA;
 }
 
 static int gemm_dispatch(const float* A, const float* B, float* C, int64_t m, int64_t n,
                          int64_t k, int variant, bool b_is_nk, cudaStream_t s) {
   MTNN_TRY(check_dims(m, n, k));
-  if (variant < 0 || variant > 2) return fail(MTNN_EINVAL, "unknown variant %d", variant);
+  if (variant < 0 || variant > 3) return fail(MTNN_EINVAL, "unknown variant %d", variant);
   const DeviceInfo* di = nullptr;
   MTNN_TRY(device_info(&di));
   if (m == 0 || n == 0) return MTNN_OK;
@@ -124,8 +125,11 @@ static int gemm_dispatch(const float* A, const float* B, float* C, int64_t m, in
     MTNN_CUDA_TRY(cudaMemsetAsync(C, 0, (size_t)m * n * sizeof(float), s));
     return MTNN_OK;
   }
-  if (use_tc(variant, A, B, C, m, n, k, b_is_nk))
-    return launch_gemm_tc(A, B, C, m, n, k, b_is_nk, s);
+  if (variant == MTNN_VARIANT_AUTO) variant = auto_variant(A, B, C, m, n, k, b_is_nk);
+  if (variant == MTNN_VARIANT_TC3XF16S)
+    return launch_gemm_tc(A, B, C, m, n, k, b_is_nk, TcKind::F16S, s);
+  if (variant == MTNN_VARIANT_TC3XTF32)
+    return launch_gemm_tc(A, B, C, m, n, k, b_is_nk, TcKind::TF32, s);
   return launch_gemm_ffma(A, B, C, m, n, k, b_is_nk, s);
 }
 

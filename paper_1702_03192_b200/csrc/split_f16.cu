@@ -1,0 +1,289 @@
+// Operand split for the FP16x3-scaled tensor-core GEMM (variant tc3xf16s).
+//
+// Each FP32 operand row (a row of A, a row of B for NT, a column of B^T for NN)
+// gets an exact power-of-two scale s = 2^(14 - ceil(log2(max|x|))) that puts its
+// largest magnitude in [2^13, 2^14] — inside FP16 range with headroom — and every
+// element is written as two FP16 halves:
+//     h = fp16_rn(x * s),   l = fp16_rn(x * s - h)        (x*s - h is exact in fp32)
+// so x*s = h + l + r with |r| <= 2^-24 |x*s|. The GEMM accumulates h*h + h*l + l*h
+// (the dropped l*l is ~2^-24 relative) in FP32 and multiplies each output by
+// 1/(s_row * s_col), which is exact. FP16 carries the same 11-bit significand as
+// TF32 but runs at twice the tensor-core rate, and the per-row scale removes its
+// range limit (subnormal tails sit ~2^-38 below the row maximum).
+//
+// Traffic: row-split (K-major operands) reads each row twice from L2 but DRAM
+// once — 4 B read + 4 B written per element; column-split (MN-major B^T) makes a
+// max pass then a split pass — 8 B read + 4 B written per element.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "common.h"
+
+namespace mtnn {
+namespace {
+
+// 2^(14 - ceil(log2(mx))) for finite mx > 0; 1 for 0; 1 for non-finite (the
+// Inf/NaN then propagates through the FP16 halves as it would in FP32).
+__device__ __forceinline__ float pow2_scale(float mx) {
+  if (!(mx > 0.f) || !isfinite(mx)) return 1.f;
+  int e;
+  const float f = frexpf(mx, &e);  // mx = f * 2^e, f in [0.5, 1)
+  const int c = (f == 0.5f) ? e - 1 : e;  // ceil(log2(mx))
+  return ldexpf(1.f, 14 - c);
+}
+
+__device__ __forceinline__ void split2(float v, float s, __half& h, __half& l) {
+  const float xs = v * s;
+  h = __float2half_rn(xs);
+  l = __float2half_rn(xs - __half2float(h));
+}
+
+// One warp per row (K-major operand, rows x k, k % 4 == 0): max, then split.
+// Both passes keep kUnroll independent 16-byte loads per lane in flight; the
+// second pass re-reads the row from L1/L2 (a row is at most 64 KiB).
+constexpr int kUnroll = 4;
+
+__device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
+
+__device__ __forceinline__ float absmax4(const float4& v) {
+  if (isnan(v.x) || isnan(v.y) || isnan(v.z) || isnan(v.w)) return INFINITY;
+  return fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+}
+
+__device__ __forceinline__ void split4(const float4& v, float s, uint2& hw, uint2& lw) {
+  __half h0, h1, h2, h3, l0, l1, l2, l3;
+  split2(v.x, s, h0, l0);
+  split2(v.y, s, h1, l1);
+  split2(v.z, s, h2, l2);
+  split2(v.w, s, h3, l3);
+  __half2 hp0 = __halves2half2(h0, h1), hp1 = __halves2half2(h2, h3);
+  __half2 lp0 = __halves2half2(l0, l1), lp1 = __halves2half2(l2, l3);
+  hw = make_uint2(*reinterpret_cast<uint32_t*>(&hp0), *reinterpret_cast<uint32_t*>(&hp1));
+  lw = make_uint2(*reinterpret_cast<uint32_t*>(&lp0), *reinterpret_cast<uint32_t*>(&lp1));
+}
+
+__global__ void __launch_bounds__(256)
+split_rows_f16_kernel(const float* __restrict__ x, __half* __restrict__ hi,
+                      __half* __restrict__ lo, float* __restrict__ inv_scale, int64_t rows,
+                      int64_t k) {
+  const int lane = threadIdx.x % 32;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / 32;
+  const int64_t k4 = k / 4;
+  constexpr int kStep = 32 * kUnroll;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const float4* row = reinterpret_cast<const float4*>(x + r * k);
+    float mx = 0.f;
+    int64_t i = lane;
+    for (; i + 32 * (kUnroll - 1) < k4; i += kStep) {
+      float4 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) v[u] = ldg4(row + i + 32 * u);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) mx = fmaxf(mx, absmax4(v[u]));
+    }
+    for (; i < k4; i += 32) mx = fmaxf(mx, absmax4(ldg4(row + i)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float s = pow2_scale(mx);
+    if (lane == 0) inv_scale[r] = 1.f / s;
+    uint2* hrow = reinterpret_cast<uint2*>(hi + r * k);
+    uint2* lrow = reinterpret_cast<uint2*>(lo + r * k);
+    i = lane;
+    for (; i + 32 * (kUnroll - 1) < k4; i += kStep) {
+      float4 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) v[u] = ldg4(row + i + 32 * u);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        uint2 hw, lw;
+        split4(v[u], s, hw, lw);
+        hrow[i + 32 * u] = hw;
+        lrow[i + 32 * u] = lw;
+      }
+    }
+    for (; i < k4; i += 32) {
+      uint2 hw, lw;
+      split4(ldg4(row + i), s, hw, lw);
+      hrow[i] = hw;
+      lrow[i] = lw;
+    }
+  }
+}
+
+// One CTA per row for long rows (k > kWarpRowMax): the row is staged in shared
+// memory by the max pass, so DRAM sees exactly one read and one write per element
+// (8 B) — with warp-per-row the ~600 MB of long rows in flight overflow L2 and the
+// split pass re-reads them from DRAM (12 B per element).
+constexpr int kWarpRowMax = 2048;
+constexpr int kRowThreads = 512;
+
+__global__ void __launch_bounds__(kRowThreads)
+split_rows_f16_smem_kernel(const float* __restrict__ x, __half* __restrict__ hi,
+                           __half* __restrict__ lo, float* __restrict__ inv_scale,
+                           int64_t rows, int64_t k) {
+  extern __shared__ float4 row_s[];
+  __shared__ float red[kRowThreads / 32];
+  const int64_t k4 = k / 4;
+  const int t = threadIdx.x;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const float4* row = reinterpret_cast<const float4*>(x + r * k);
+    float mx = 0.f;
+    int64_t i = t;
+    for (; i + kRowThreads * (kUnroll - 1) < k4; i += kRowThreads * kUnroll) {
+      float4 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) v[u] = ldg4(row + i + kRowThreads * u);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        row_s[i + kRowThreads * u] = v[u];
+        mx = fmaxf(mx, absmax4(v[u]));
+      }
+    }
+    for (; i < k4; i += kRowThreads) {
+      const float4 v = ldg4(row + i);
+      row_s[i] = v;
+      mx = fmaxf(mx, absmax4(v));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (t % 32 == 0) red[t / 32] = mx;
+    __syncthreads();
+    if (t < 32) {
+      float m2 = t < kRowThreads / 32 ? red[t] : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m2 = fmaxf(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+      if (t == 0) red[0] = m2;
+    }
+    __syncthreads();
+    const float s = pow2_scale(red[0]);
+    if (t == 0) inv_scale[r] = 1.f / s;
+    uint2* hrow = reinterpret_cast<uint2*>(hi + r * k);
+    uint2* lrow = reinterpret_cast<uint2*>(lo + r * k);
+    for (int64_t j = t; j < k4; j += kRowThreads) {
+      uint2 hw, lw;
+      split4(row_s[j], s, hw, lw);
+      hrow[j] = hw;
+      lrow[j] = lw;
+    }
+    __syncthreads();  // row_s and red are reused by the next row
+  }
+}
+
+// Column max of a k x n matrix (MN-major B^T): |x| as uint bits (monotonic for
+// non-negative floats; NaN maps above +Inf) folded with atomicMax.
+__global__ void __launch_bounds__(256)
+colmax_kernel(const float* __restrict__ x, unsigned* __restrict__ colmax_bits, int64_t k,
+              int64_t n, int64_t rows_per_block) {
+  const int64_t c4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // float4 column
+  if (c4 * 4 >= n) return;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block;
+  const int64_t r1 = min(k, r0 + rows_per_block);
+  float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
+  for (int64_t r = r0; r < r1; ++r) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(x + r * n) + c4);
+    m0 = isnan(v.x) ? INFINITY : fmaxf(m0, fabsf(v.x));
+    m1 = isnan(v.y) ? INFINITY : fmaxf(m1, fabsf(v.y));
+    m2 = isnan(v.z) ? INFINITY : fmaxf(m2, fabsf(v.z));
+    m3 = isnan(v.w) ? INFINITY : fmaxf(m3, fabsf(v.w));
+  }
+  atomicMax(colmax_bits + 4 * c4 + 0, __float_as_uint(m0));
+  atomicMax(colmax_bits + 4 * c4 + 1, __float_as_uint(m1));
+  atomicMax(colmax_bits + 4 * c4 + 2, __float_as_uint(m2));
+  atomicMax(colmax_bits + 4 * c4 + 3, __float_as_uint(m3));
+}
+
+// Elementwise split of a k x n matrix with per-column scales.
+__global__ void __launch_bounds__(256)
+split_cols_f16_kernel(const float* __restrict__ x, const unsigned* __restrict__ colmax_bits,
+                      __half* __restrict__ hi, __half* __restrict__ lo,
+                      float* __restrict__ inv_scale, int64_t k, int64_t n) {
+  const int64_t n4 = n / 4;
+  const int64_t total = k * n4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int64_t r = i / n4, c4 = i - r * n4;
+    const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
+    const float s0 = pow2_scale(__uint_as_float(colmax_bits[4 * c4 + 0]));
+    const float s1 = pow2_scale(__uint_as_float(colmax_bits[4 * c4 + 1]));
+    const float s2 = pow2_scale(__uint_as_float(colmax_bits[4 * c4 + 2]));
+    const float s3 = pow2_scale(__uint_as_float(colmax_bits[4 * c4 + 3]));
+    if (r == 0) {
+      inv_scale[4 * c4 + 0] = 1.f / s0;
+      inv_scale[4 * c4 + 1] = 1.f / s1;
+      inv_scale[4 * c4 + 2] = 1.f / s2;
+      inv_scale[4 * c4 + 3] = 1.f / s3;
+    }
+    __half h0, h1, h2, h3, l0, l1, l2, l3;
+    split2(v.x, s0, h0, l0);
+    split2(v.y, s1, h1, l1);
+    split2(v.z, s2, h2, l2);
+    split2(v.w, s3, h3, l3);
+    __half2 hp0 = __halves2half2(h0, h1), hp1 = __halves2half2(h2, h3);
+    __half2 lp0 = __halves2half2(l0, l1), lp1 = __halves2half2(l2, l3);
+    reinterpret_cast<uint2*>(hi)[i] =
+        make_uint2(*reinterpret_cast<uint32_t*>(&hp0), *reinterpret_cast<uint32_t*>(&hp1));
+    reinterpret_cast<uint2*>(lo)[i] =
+        make_uint2(*reinterpret_cast<uint32_t*>(&lp0), *reinterpret_cast<uint32_t*>(&lp1));
+  }
+}
+
+}  // namespace
+
+int launch_split_rows_f16(const float* x, void* hi, void* lo, float* inv_scale, int64_t rows,
+                          int64_t k, cudaStream_t s) {
+  if (rows <= 0) return MTNN_OK;
+  const DeviceInfo* di = nullptr;
+  MTNN_TRY(device_info(&di));
+  KernelTimer timer(MTNN_KCLASS_SPLIT, 8.0 * (double)rows * (double)k, s);
+  const size_t row_bytes = (size_t)k * sizeof(float);
+  if (k > kWarpRowMax && row_bytes <= 160 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      MTNN_CUDA_TRY(cudaFuncSetAttribute(split_rows_f16_smem_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+      attr = true;
+    }
+    const int per_sm = std::max<int>(1, std::min<int>(4, (int)((200 * 1024) / row_bytes)));
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)di->sm_count * per_sm));
+    split_rows_f16_smem_kernel<<<(unsigned)blocks, kRowThreads, row_bytes, s>>>(
+        x, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale, rows, k);
+  } else {
+    int64_t blocks = (rows + 7) / 8;
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)di->sm_count * 16));
+    split_rows_f16_kernel<<<(unsigned)blocks, 256, 0, s>>>(
+        x, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale, rows, k);
+  }
+  MTNN_CUDA_TRY(cudaGetLastError());
+  return MTNN_OK;
+}
+
+int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,
+                          unsigned* colmax_scratch, int64_t k, int64_t n, cudaStream_t s) {
+  if (k <= 0 || n <= 0) return MTNN_OK;
+  const DeviceInfo* di = nullptr;
+  MTNN_TRY(device_info(&di));
+  KernelTimer timer(MTNN_KCLASS_SPLIT, 12.0 * (double)k * (double)n, s);
+  MTNN_CUDA_TRY(cudaMemsetAsync(colmax_scratch, 0, (size_t)n * sizeof(unsigned), s));
+  const int64_t n4 = n / 4;
+  const int64_t gx = (n4 + 255) / 256;
+  // enough row blocks to fill the chip; each thread scans rows_per_block rows
+  int64_t gy = std::max<int64_t>(1, ((int64_t)di->sm_count * 8) / std::max<int64_t>(gx, 1));
+  gy = std::min<int64_t>(gy, std::max<int64_t>(1, k / 16));
+  const int64_t rpb = (k + gy - 1) / gy;
+  gy = (k + rpb - 1) / rpb;
+  colmax_kernel<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, s>>>(x, colmax_scratch, k, n, rpb);
+  MTNN_CUDA_TRY(cudaGetLastError());
+  const int64_t total = k * n4;
+  const int64_t blocks = std::max<int64_t>(
+      1, std::min<int64_t>((total + 255) / 256, (int64_t)di->sm_count * 8));
+  split_cols_f16_kernel<<<(unsigned)blocks, 256, 0, s>>>(
+      x, colmax_scratch, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale, k, n);
+  MTNN_CUDA_TRY(cudaGetLastError());
+  return MTNN_OK;
+}
+
+}  // namespace mtnn

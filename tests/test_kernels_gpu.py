@@ -17,15 +17,15 @@ pytestmark = pytest.mark.gpu
 
 TOL = 1e-4          # reference tolerance (test_kernels.py:17)
 FP32_GATE = 1e-5    # north_star: rel Frobenius vs float64-accumulated result
-VARIANTS = ("auto", "tc3xtf32", "ffma")
+VARIANTS = ("auto", "tc3xf16s", "tc3xtf32", "ffma")
 
 
 def eye(n):
     return np.eye(n, dtype=np.float32)
 
 
-def tc_ok(m, n, k):
-    return k % 4 == 0 and n % 4 == 0
+def tc_ok(m, n, k, v="tc3xtf32"):
+    return k % 4 == 0 and n % 4 == 0 and (v != "tc3xf16s" or k % 8 == 0)
 
 
 class TestKats:
@@ -68,6 +68,41 @@ class TestIdentities:
     def test_tc_identity_close(self, rng):
         a = random_matrix(rng, 256, 256)
         assert rel_frobenius(gemm_nt(a, eye(256), variant="tc3xtf32"), a) < 1e-6
+        assert rel_frobenius(gemm_nt(a, eye(256), variant="tc3xf16s"), a) < 1e-6
+
+
+class TestScaledF16Robustness:
+    """tc3xf16s: per-row power-of-two scaling keeps FP32 accuracy across magnitudes
+    FP16 cannot represent, and non-finite inputs propagate like FP32."""
+
+    def test_wide_dynamic_range(self, rng):
+        m, n, k = 384, 272, 520
+        # rows spanning e^-40..e^40 (A) and e^-20..e^20 (B): far outside FP16's range,
+        # products still inside FP32's
+        a = (rng.standard_normal((m, k)) * np.exp(rng.uniform(-40, 40, (m, 1)))).astype(np.float32)
+        b = (rng.standard_normal((n, k)) * np.exp(rng.uniform(-20, 20, (n, 1)))).astype(np.float32)
+        want = oracle.oracle_nt_blas(a, b)
+        for fn, bb in ((gemm_nt, b), (gemm_nn, np.ascontiguousarray(b.T))):
+            got = fn(a, bb, variant="tc3xf16s")
+            # relative error of every (row-block, column-block) — magnitudes differ by e^120
+            rel = np.abs(got - want) / (np.linalg.norm(a.astype(np.float64), axis=1)[:, None]
+                                        * np.linalg.norm(b.astype(np.float64), axis=1)[None, :])
+            assert rel.max() < 1e-6
+            err = np.linalg.norm(got - want, axis=1) / np.linalg.norm(want, axis=1)
+            assert err.max() < FP32_GATE
+
+    def test_zero_rows_and_nonfinite(self, rng):
+        a = random_matrix(rng, 256, 256)
+        b = random_matrix(rng, 256, 256)
+        a[3] = 0.0
+        a[5, 7] = np.inf
+        a[9, 1] = np.nan
+        got = gemm_nt(a, b, variant="tc3xf16s")
+        want = oracle.oracle_nt_blas(a, b)
+        assert np.all(got[3] == 0.0)
+        assert np.all(~np.isfinite(got[5])) and np.all(np.isnan(got[9]))
+        ok = np.ones(256, bool); ok[[5, 9]] = False
+        assert rel_frobenius(got[ok], want[ok]) < FP32_GATE
 
 
 class TestAgainstGolden:
@@ -78,12 +113,12 @@ class TestAgainstGolden:
             bt = np.ascontiguousarray(b.T)
             assert np.array_equal(transpose_oop(b), g[f"t{i}"])
             for v in VARIANTS:
-                if v == "tc3xtf32" and not tc_ok(m, n, k):
+                if v.startswith("tc") and not tc_ok(m, n, k, v):
                     continue
                 for got in (gemm_nt(a, b, variant=v), gemm_tnn(a, b, variant=v)):
                     assert rel_frobenius(got, f64) < FP32_GATE
                     assert rel_frobenius(got, g[f"nt{i}"]) < FP32_GATE
-                if v != "tc3xtf32" or n % 16 == 0:
+                if not v.startswith("tc") or n % 16 == 0:
                     assert rel_frobenius(gemm_nn(a, bt, variant=v), g[f"nn{i}"]) < FP32_GATE
 
     def test_bit_patterns(self, golden_kernels):
@@ -132,10 +167,10 @@ class TestRandomAgainstOracle:
         want = oracle.oracle_nt_blas(a, b)
         bt = np.ascontiguousarray(b.T)
         for v in VARIANTS:
-            if v == "tc3xtf32" and not tc_ok(m, n, k):
+            if v.startswith("tc") and not tc_ok(m, n, k, v):
                 continue
             assert rel_frobenius(gemm_nt(a, b, variant=v), want) < FP32_GATE, v
-            if v != "tc3xtf32" or n % 16 == 0:
+            if not v.startswith("tc") or n % 16 == 0:
                 assert rel_frobenius(gemm_nn(a, bt, variant=v), want) < FP32_GATE, v
                 assert rel_frobenius(gemm_tnn(a, b, variant=v), want) < FP32_GATE, v
 
