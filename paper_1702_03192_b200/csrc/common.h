@@ -74,6 +74,17 @@ int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t 
                    int64_t k, bool b_is_nk, TcKind kind, cudaStream_t s);
 bool tc_eligible(const float* A, const float* B, const float* C, int64_t m, int64_t n,
                  int64_t k, bool b_is_nk, TcKind kind);
+// Prepared (split) tensor-core operand: hi/lo halves, plus 1/scale per row for F16S.
+struct TcOperand {
+  const void* hi = nullptr;
+  const void* lo = nullptr;
+  const float* inv_scale = nullptr;
+};
+struct ScratchBuffer;
+int tc_prepare(const float* X, int64_t rows, int64_t k, bool mn_major, TcKind kind,
+               ScratchBuffer& ws, TcOperand* out, cudaStream_t s);
+int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n, int64_t k,
+           bool b_is_nk, TcKind kind, cudaStream_t s);
 int launch_split_rows_f16(const float* x, void* hi, void* lo, float* inv_scale, int64_t rows,
                           int64_t k, cudaStream_t s);
 int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,

@@ -658,81 +658,69 @@ bool tc_eligible(const float* A, const float* B, const float* C, int64_t m, int6
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t n,
-                   int64_t k, bool b_is_nk, TcKind kind, cudaStream_t s) {
-  const char* name = kind == TcKind::F16S ? "tc3xf16s" : "tc3xtf32";
-  if (!tc_eligible(A, B, C, m, n, k, b_is_nk, kind))
-    return fail(MTNN_ENOTSUP, "%s: shape/alignment not eligible (m=%lld n=%lld k=%lld)", name,
-                (long long)m, (long long)n, (long long)k);
+// Split one operand into its hi/lo halves (+ per-row scales for F16S).
+// K-major (rows x k: A, or B of NT) or MN-major (k x cols: B^T of NN).
+int tc_prepare(const float* X, int64_t rows, int64_t k, bool mn_major, TcKind kind,
+               ScratchBuffer& ws, TcOperand* out, cudaStream_t s) {
+  const DeviceInfo* di = nullptr;
+  MTNN_TRY(device_info(&di));
+  const int64_t count = rows * k;  // MN-major: k x rows (rows = n)
+  if (kind == TcKind::TF32) {
+    const bool hi_copy = split_mode_hi_copy();
+    MTNN_TRY(ws.alloc((size_t)((hi_copy ? 2 : 1) * count) * sizeof(float), s));
+    float* lo = static_cast<float*>(ws.ptr);
+    float* hi = hi_copy ? lo + count : nullptr;
+    const int64_t total4 = count / 4;
+    const int64_t blocks =
+        std::max<int64_t>(1, std::min<int64_t>((total4 + 255) / 256, (int64_t)di->sm_count * 8));
+    KernelTimer timer(MTNN_KCLASS_SPLIT, (hi_copy ? 12.0 : 8.0) * (double)count, s);
+    auto x4 = reinterpret_cast<const float4*>(X);
+    if (hi_copy)
+      tc::split_tf32_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(
+          x4, reinterpret_cast<float4*>(hi), reinterpret_cast<float4*>(lo), total4, nullptr,
+          nullptr, nullptr, 0);
+    else
+      tc::split_tf32_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(
+          x4, nullptr, reinterpret_cast<float4*>(lo), total4, nullptr, nullptr, nullptr, 0);
+    MTNN_CUDA_TRY(cudaGetLastError());
+    out->hi = hi_copy ? static_cast<const void*>(hi) : X;
+    out->lo = lo;
+    out->inv_scale = nullptr;
+    return MTNN_OK;
+  }
+  // F16S: [h | l | 1/s (+ column-max scratch)]
+  const size_t oh = align256((size_t)count * 2);
+  const size_t osc = align256((size_t)rows * 4);
+  MTNN_TRY(ws.alloc(2 * oh + osc + (mn_major ? osc : 0), s));
+  uint8_t* base = static_cast<uint8_t*>(ws.ptr);
+  float* inv = reinterpret_cast<float*>(base + 2 * oh);
+  if (!mn_major) {
+    MTNN_TRY(launch_split_rows_f16(X, base, base + oh, inv, rows, k, s));
+  } else {
+    unsigned* cm = reinterpret_cast<unsigned*>(base + 2 * oh + osc);
+    MTNN_TRY(launch_split_cols_f16(X, base, base + oh, inv, cm, k, rows, s));
+  }
+  out->hi = base;
+  out->lo = base + oh;
+  out->inv_scale = inv;
+  return MTNN_OK;
+}
+
+int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n, int64_t k,
+           bool b_is_nk, TcKind kind, cudaStream_t s) {
   const DeviceInfo* di = nullptr;
   MTNN_TRY(device_info(&di));
   constexpr int BN = 256;
   using S = tc::Smem<BN>;
   if (di->max_smem_optin < S::kTotal)
-    return fail(MTNN_ENOTSUP, "%s: needs %d B smem, device allows %d", name, S::kTotal,
+    return fail(MTNN_ENOTSUP, "tensor-core GEMM needs %d B smem, device allows %d", S::kTotal,
                 di->max_smem_optin);
-
-  const int64_t na = m * k, nb = n * k;
-  const void *ahi, *alo, *bhi, *blo;
-  const float *inv_a = nullptr, *inv_b = nullptr;
-  ScratchBuffer ws;
-  if (kind == TcKind::TF32) {
-    // workspace [A_lo | B_lo] (+ [A_hi | B_hi] when materialised); k % 4 == 0
-    const bool hi_copy = split_mode_hi_copy();
-    MTNN_TRY(ws.alloc((size_t)((hi_copy ? 2 : 1) * (na + nb)) * sizeof(float), s));
-    float* a_lo = static_cast<float*>(ws.ptr);
-    float* b_lo = a_lo + na;
-    float* a_hi = hi_copy ? b_lo + nb : nullptr;
-    float* b_hi = hi_copy ? b_lo + nb + na : nullptr;
-    const int64_t total4 = (na + nb) / 4;
-    const int64_t blocks =
-        std::max<int64_t>(1, std::min<int64_t>((total4 + 255) / 256, (int64_t)di->sm_count * 8));
-    KernelTimer timer(MTNN_KCLASS_SPLIT, (hi_copy ? 12.0 : 8.0) * (double)(na + nb), s);
-    auto a4 = reinterpret_cast<const float4*>(A);
-    auto b4 = reinterpret_cast<const float4*>(B);
-    if (hi_copy)
-      tc::split_tf32_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(
-          a4, reinterpret_cast<float4*>(a_hi), reinterpret_cast<float4*>(a_lo), na / 4, b4,
-          reinterpret_cast<float4*>(b_hi), reinterpret_cast<float4*>(b_lo), nb / 4);
-    else
-      tc::split_tf32_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(
-          a4, nullptr, reinterpret_cast<float4*>(a_lo), na / 4, b4, nullptr,
-          reinterpret_cast<float4*>(b_lo), nb / 4);
-    MTNN_CUDA_TRY(cudaGetLastError());
-    ahi = hi_copy ? a_hi : A;
-    bhi = hi_copy ? b_hi : B;
-    alo = a_lo;
-    blo = b_lo;
-  } else {
-    // workspace [A_h | A_l | B_h | B_l | 1/s_a | 1/s_b | colmax]
-    const size_t oa = align256((size_t)na * 2), ob = align256((size_t)nb * 2);
-    const size_t osa = align256((size_t)m * 4), osb = align256((size_t)n * 4);
-    const size_t ocm = b_is_nk ? 0 : align256((size_t)n * 4);
-    MTNN_TRY(ws.alloc(2 * oa + 2 * ob + osa + osb + ocm, s));
-    uint8_t* base = static_cast<uint8_t*>(ws.ptr);
-    void* a_h = base;
-    void* a_l = base + oa;
-    void* b_h = base + 2 * oa;
-    void* b_l = base + 2 * oa + ob;
-    float* sa = reinterpret_cast<float*>(base + 2 * oa + 2 * ob);
-    float* sb = reinterpret_cast<float*>(base + 2 * oa + 2 * ob + osa);
-    MTNN_TRY(launch_split_rows_f16(A, a_h, a_l, sa, m, k, s));
-    if (b_is_nk) {
-      MTNN_TRY(launch_split_rows_f16(B, b_h, b_l, sb, n, k, s));
-    } else {
-      unsigned* cm = reinterpret_cast<unsigned*>(base + 2 * oa + 2 * ob + osa + osb);
-      MTNN_TRY(launch_split_cols_f16(B, b_h, b_l, sb, cm, k, n, s));
-    }
-    ahi = a_h; alo = a_l; bhi = b_h; blo = b_l;
-    inv_a = sa; inv_b = sb;
-  }
-
   const int bk = kind == TcKind::F16S ? tc::KindF16S::BK : tc::KindTF32::BK;
   tc::Params p{};
   p.m = m; p.n = n; p.k = k;
   p.chunk_kb = chunk_kblocks(kind);
-  p.inv_scale_a = inv_a;
-  p.inv_scale_b = inv_b;
+  p.inv_scale_a = a.inv_scale;
+  p.inv_scale_b = b.inv_scale;
   p.tiles_m = (int)((m + tc::BM - 1) / tc::BM);
   p.tiles_n = (int)((n + BN - 1) / BN);
   p.total_kblocks = (int)((k + bk - 1) / bk);
@@ -756,14 +744,27 @@ int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t 
   }
   int rc;
   if (kind == TcKind::F16S)
-    rc = b_is_nk ? tc::launch_impl<BN, false, tc::KindF16S>(ahi, alo, bhi, blo, out, p, grid, s)
-                 : tc::launch_impl<BN, true, tc::KindF16S>(ahi, alo, bhi, blo, out, p, grid, s);
+    rc = b_is_nk ? tc::launch_impl<BN, false, tc::KindF16S>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s)
+                 : tc::launch_impl<BN, true, tc::KindF16S>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s);
   else
-    rc = b_is_nk ? tc::launch_impl<BN, false, tc::KindTF32>(ahi, alo, bhi, blo, out, p, grid, s)
-                 : tc::launch_impl<BN, true, tc::KindTF32>(ahi, alo, bhi, blo, out, p, grid, s);
+    rc = b_is_nk ? tc::launch_impl<BN, false, tc::KindTF32>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s)
+                 : tc::launch_impl<BN, true, tc::KindTF32>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s);
   MTNN_TRY(rc);
   if (splits > 1) MTNN_TRY(launch_splitk_reduce(out, C, m * n, splits, s));
   return MTNN_OK;
+}
+
+int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t n,
+                   int64_t k, bool b_is_nk, TcKind kind, cudaStream_t s) {
+  const char* name = kind == TcKind::F16S ? "tc3xf16s" : "tc3xtf32";
+  if (!tc_eligible(A, B, C, m, n, k, b_is_nk, kind))
+    return fail(MTNN_ENOTSUP, "%s: shape/alignment not eligible (m=%lld n=%lld k=%lld)", name,
+                (long long)m, (long long)n, (long long)k);
+  ScratchBuffer wa, wb;
+  TcOperand a{}, b{};
+  MTNN_TRY(tc_prepare(A, m, k, false, kind, wa, &a, s));
+  MTNN_TRY(tc_prepare(B, n, k, !b_is_nk, kind, wb, &b, s));
+  return tc_run(a, b, C, m, n, k, b_is_nk, kind, s);
 }
 
 }  // namespace mtnn

@@ -7,12 +7,15 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
 #include <chrono>
 #include <mutex>
 #include <string>
+#include <vector>
+#include <algorithm>
 
 #include "common.h"
 #include "model.h"
@@ -198,6 +201,164 @@ static int host_call(const float* A, size_t a_elems, const float* B, size_t b_el
   return MTNN_OK;
 }
 
+// ------------------------------------------- pipelined host-buffer GEMM
+// The drop-in (numpy) calls are PCIe-bound: a serial H2D(A) H2D(B) compute D2H(C)
+// leaves the copy engines idle half the time. Inside one call, B is copied (and,
+// on the tensor-core paths, split) once, then A/C are processed in row chunks on
+// three streams so H2D of chunk c+1, compute of chunk c and D2H of chunk c-1
+// overlap (H2D and D2H use separate copy engines). Rows of C depend only on the
+// same rows of A, so chunking does not change any result bit.
+enum class HostPath { NT, NN, TNN };
+
+struct PipeStreams {
+  cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
+  int device = -1;
+};
+static thread_local PipeStreams t_pipe;
+
+static int pipe_streams(PipeStreams** out) {
+  int dev = 0;
+  MTNN_CUDA_TRY(cudaGetDevice(&dev));
+  if (t_pipe.device != dev) {
+    MTNN_CUDA_TRY(cudaStreamCreateWithFlags(&t_pipe.in, cudaStreamNonBlocking));
+    MTNN_CUDA_TRY(cudaStreamCreateWithFlags(&t_pipe.comp, cudaStreamNonBlocking));
+    MTNN_CUDA_TRY(cudaStreamCreateWithFlags(&t_pipe.out, cudaStreamNonBlocking));
+    t_pipe.device = dev;
+  }
+  *out = &t_pipe;
+  return MTNN_OK;
+}
+
+struct EventSet {
+  std::vector<cudaEvent_t> ev;
+  ~EventSet() {
+    for (auto e : ev) (void)cudaEventDestroy(e);
+  }
+  int make(cudaEvent_t* out) {
+    cudaEvent_t e;
+    MTNN_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ev.push_back(e);
+    *out = e;
+    return MTNN_OK;
+  }
+};
+
+// Pipeline knobs: minimum problem bytes (A+B+C) to pipeline, and the target
+// bytes of A+C per chunk (MTNN_PIPE_MIN_MB / MTNN_PIPE_CHUNK_MB override).
+static double env_mb(const char* name, double dflt) {
+  const char* e = getenv(name);
+  const double v = e ? atof(e) : 0.0;
+  return (v > 0 ? v : dflt) * 1024.0 * 1024.0;
+}
+static double pipe_min_bytes() {
+  static const double v = env_mb("MTNN_PIPE_MIN_MB", 8.0);
+  return v;
+}
+static double pipe_chunk_bytes() {
+  static const double v = env_mb("MTNN_PIPE_CHUNK_MB", 16.0);
+  return v;
+}
+
+static int host_gemm(const float* A, const float* B, float* C, int64_t m, int64_t n,
+                     int64_t k, HostPath path, int variant) {
+  MTNN_TRY(check_dims(m, n, k));
+  if (variant < 0 || variant > 3) return fail(MTNN_EINVAL, "unknown variant %d", variant);
+  const double bytes = 4.0 * ((double)m * k + (double)n * k + (double)m * n);
+  if (bytes < pipe_min_bytes() || m < 256 || k == 0 || n == 0) {
+    // small problem: one serial round trip
+    return host_call(A, m * k, B, n * k, C, m * n,
+                     [&](const float* a, const float* b, float* c, cudaStream_t s) {
+                       if (path == HostPath::TNN) return tnn_device(a, b, c, m, n, k, variant, -1, s);
+                       return gemm_dispatch(a, b, c, m, n, k, variant, path == HostPath::NT, s);
+                     });
+  }
+  const DeviceInfo* di = nullptr;
+  MTNN_TRY(device_info(&di));
+  PipeStreams* ps = nullptr;
+  MTNN_TRY(pipe_streams(&ps));
+  EventSet evs;
+  ScratchBuffer da, db, dc, dbt, wb;
+  // destroyed first (declared last): on any exit, drain all three streams before
+  // the stream-ordered frees above can recycle memory another stream still uses
+  struct Drain {
+    PipeStreams* p;
+    ~Drain() {
+      (void)cudaStreamSynchronize(p->in);
+      (void)cudaStreamSynchronize(p->comp);
+      (void)cudaStreamSynchronize(p->out);
+    }
+  } drain{ps};
+  MTNN_TRY(da.alloc((size_t)(m * k) * 4, ps->in));
+  MTNN_TRY(db.alloc((size_t)(n * k) * 4, ps->in));
+  MTNN_TRY(dc.alloc((size_t)(m * n) * 4, ps->in));
+  cudaEvent_t ev_b;
+  MTNN_TRY(evs.make(&ev_b));
+  MTNN_CUDA_TRY(cudaMemcpyAsync(db.ptr, B, (size_t)(n * k) * 4, cudaMemcpyHostToDevice, ps->in));
+  MTNN_CUDA_TRY(cudaEventRecord(ev_b, ps->in));
+  MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->comp, ev_b, 0));
+  MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->out, ev_b, 0));  // dc allocation is ordered on `in`
+
+  // B operand on the compute stream: transposed for TNN, split once for TC paths
+  const float* bop = static_cast<const float*>(db.ptr);
+  bool b_is_nk = path == HostPath::NT;
+  if (path == HostPath::TNN) {
+    MTNN_TRY(dbt.alloc((size_t)(n * k) * 4, ps->comp));
+    MTNN_TRY(launch_transpose(bop, static_cast<float*>(dbt.ptr), n, k, ps->comp));
+    bop = static_cast<const float*>(dbt.ptr);
+    b_is_nk = false;
+  }
+  float* dcp = static_cast<float*>(dc.ptr);
+  const float* dap = static_cast<const float*>(da.ptr);
+  int v = variant == MTNN_VARIANT_AUTO ? auto_variant(dap, bop, dcp, m, n, k, b_is_nk) : variant;
+  const bool tc = v == MTNN_VARIANT_TC3XF16S || v == MTNN_VARIANT_TC3XTF32;
+  const TcKind kind = v == MTNN_VARIANT_TC3XF16S ? TcKind::F16S : TcKind::TF32;
+  if (tc && !tc_eligible(dap, bop, dcp, m, n, k, b_is_nk, kind))
+    return fail(MTNN_ENOTSUP, "tensor-core variant not eligible for (%lld, %lld, %lld)",
+                (long long)m, (long long)n, (long long)k);
+  TcOperand bp{};
+  if (tc) MTNN_TRY(tc_prepare(bop, n, k, !b_is_nk, kind, wb, &bp, ps->comp));
+
+  // row chunks: 2..8 chunks of >= 16 MiB of A+C, multiples of 128 rows
+  const double row_bytes = 4.0 * ((double)k + (double)n);
+  int chunks = (int)std::min<double>(16.0, std::max(2.0, (double)m * row_bytes / pipe_chunk_bytes()));
+  int64_t rows = ((m + chunks - 1) / chunks + 127) / 128 * 128;
+  chunks = (int)((m + rows - 1) / rows);
+  for (int c = 0; c < chunks; ++c) {
+    const int64_t r0 = (int64_t)c * rows;
+    const int64_t mr = std::min<int64_t>(rows, m - r0);
+    const float* a_c = dap + r0 * k;
+    float* c_c = dcp + r0 * n;
+    cudaEvent_t ev_in, ev_done;
+    MTNN_TRY(evs.make(&ev_in));
+    MTNN_TRY(evs.make(&ev_done));
+    MTNN_CUDA_TRY(cudaMemcpyAsync(const_cast<float*>(a_c), A + r0 * k, (size_t)(mr * k) * 4,
+                                  cudaMemcpyHostToDevice, ps->in));
+    MTNN_CUDA_TRY(cudaEventRecord(ev_in, ps->in));
+    MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->comp, ev_in, 0));
+    if (tc) {
+      ScratchBuffer wa;
+      TcOperand ap{};
+      MTNN_TRY(tc_prepare(a_c, mr, k, false, kind, wa, &ap, ps->comp));
+      MTNN_TRY(tc_run(ap, bp, c_c, mr, n, k, b_is_nk, kind, ps->comp));
+    } else {
+      MTNN_TRY(gemm_dispatch(a_c, bop, c_c, mr, n, k, v, b_is_nk, ps->comp));
+    }
+    MTNN_CUDA_TRY(cudaEventRecord(ev_done, ps->comp));
+    MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->out, ev_done, 0));
+    MTNN_CUDA_TRY(cudaMemcpyAsync(C + r0 * n, c_c, (size_t)(mr * n) * 4, cudaMemcpyDeviceToHost,
+                                  ps->out));
+  }
+  cudaError_t e1 = cudaStreamSynchronize(ps->out);
+  cudaError_t e2 = cudaStreamSynchronize(ps->comp);
+  cudaError_t e3 = cudaStreamSynchronize(ps->in);
+  for (cudaError_t e : {e1, e2, e3})
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      return fail(MTNN_ECUDA, "pipelined host GEMM: %s", cudaGetErrorString(e));
+    }
+  return MTNN_OK;
+}
+
 // ---------------------------------------------------------------- free memory
 static std::mutex g_free_mu;
 static double g_free_stamp[kMaxDevices];
@@ -280,20 +441,12 @@ int mtnn_gemm_tnn(const float* A, const float* B, float* C, int64_t m, int64_t n
 
 int mtnn_gemm_nt_host(const float* A, const float* B, float* C, int64_t m, int64_t n,
                       int64_t k, int variant) {
-  MTNN_TRY(check_dims(m, n, k));
-  return host_call(A, m * k, B, n * k, C, m * n,
-                   [&](const float* a, const float* b, float* c, cudaStream_t s) {
-                     return gemm_dispatch(a, b, c, m, n, k, variant, true, s);
-                   });
+  return host_gemm(A, B, C, m, n, k, HostPath::NT, variant);
 }
 
 int mtnn_gemm_nn_host(const float* A, const float* BT, float* C, int64_t m, int64_t n,
                       int64_t k, int variant) {
-  MTNN_TRY(check_dims(m, n, k));
-  return host_call(A, m * k, BT, k * n, C, m * n,
-                   [&](const float* a, const float* b, float* c, cudaStream_t s) {
-                     return gemm_dispatch(a, b, c, m, n, k, variant, false, s);
-                   });
+  return host_gemm(A, BT, C, m, n, k, HostPath::NN, variant);
 }
 
 int mtnn_transpose_host(const float* B, float* BT, int64_t rows, int64_t cols) {
@@ -311,10 +464,7 @@ int mtnn_gemm_tnn_host(const float* A, const float* B, float* C, int64_t m, int6
   if (mem_budget >= 0 && needed > mem_budget)  // before any allocation or copy
     return fail(MTNN_ENOMEM, "transpose buffer needs %lld bytes, budget is %lld",
                 (long long)needed, (long long)mem_budget);
-  return host_call(A, m * k, B, n * k, C, m * n,
-                   [&](const float* a, const float* b, float* c, cudaStream_t s) {
-                     return tnn_device(a, b, c, m, n, k, variant, -1, s);
-                   });
+  return host_gemm(A, B, C, m, n, k, HostPath::TNN, variant);
 }
 
 int mtnn_dispatch_gemm(const mtnn_model* model, const double prefix5[5], const float* A,
@@ -344,11 +494,21 @@ int mtnn_dispatch_gemm_host(const mtnn_model* model, const double prefix5[5], co
                             const float* B, float* C, int64_t m, int64_t n, int64_t k,
                             int64_t free_bytes, int variant, int* choice_out) {
   MTNN_TRY(check_dims(m, n, k));
-  return host_call(A, m * k, B, n * k, C, m * n,
-                   [&](const float* a, const float* b, float* c, cudaStream_t s) {
-                     return mtnn_dispatch_gemm(model, prefix5, a, b, c, m, n, k, free_bytes,
-                                               variant, s, choice_out);
-                   });
+  double raw = 0.0;
+  int choice = MTNN_CHOICE_NT, reason = 0;
+  MTNN_TRY(mtnn_select(model, prefix5, m, n, k, free_bytes, &raw, &choice, &reason));
+  if (choice == MTNN_CHOICE_TNN) {
+    const int rc = host_gemm(A, B, C, m, n, k, HostPath::TNN, variant);
+    if (rc == MTNN_OK) {
+      if (choice_out) *choice_out = MTNN_CHOICE_TNN;
+      return MTNN_OK;
+    }
+    if (rc != MTNN_ENOMEM) return rc;
+    fprintf(stderr, "mtnn: TNN allocation failed for (%lld, %lld, %lld); retrying as NT\n",
+            (long long)m, (long long)n, (long long)k);
+  }
+  if (choice_out) *choice_out = MTNN_CHOICE_NT;
+  return host_gemm(A, B, C, m, n, k, HostPath::NT, variant);
 }
 
 }  // extern "C"

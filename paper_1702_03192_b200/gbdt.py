@@ -226,9 +226,13 @@ class NativeModel:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is None or not h.value:
+            return
+        try:
             _lib.lib.mtnn_model_free(h)
-            self._h = ctypes.c_void_p()
+        except AttributeError:  # interpreter shutdown: module globals already cleared
+            pass
+        self._h = ctypes.c_void_p()
 
 
 # --------------------------------------------------------------- serialization
