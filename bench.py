@@ -180,6 +180,54 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------- workloads
+def lpt_assign(costs, world):
+    """Longest-processing-time-first assignment of independent cases to ranks."""
+    loads = [0.0] * world
+    owner = [0] * len(costs)
+    for i in sorted(range(len(costs)), key=lambda j: -costs[j]):
+        r = min(range(world), key=lambda q: loads[q])
+        owner[i] = r
+        loads[r] += costs[i]
+    return owner
+
+
+def build_workload(args, rank, world):
+    """Per-step call list for this rank: (op, m, n, k, flush_before).
+    op: "nt" = MTNN-dispatched NT, "nn" = NN product."""
+    if args.workload == "sweep":
+        shapes = grid(args.exp_min, args.exp_max)
+        owner = lpt_assign([2.0 * m * n * k for m, n, k in shapes], world)
+        calls = [("nt", m, n, k, True) for (m, n, k), o in zip(shapes, owner) if o == rank]
+        desc = (f"nt_sweep m,n,k in {{2^{args.exp_min}..2^{args.exp_max}}} ({len(shapes)} cases), "
+                f"MTNN-selected (configs[1])")
+        total = sum(2.0 * m * n * k for m, n, k in shapes)
+        par = "single GPU" if world == 1 else f"cases LPT-sharded over {world} GPUs (no collective)"
+        return calls, total, desc, "strong", par, shapes
+    if args.workload == "fcn":
+        hidden, batch, din0, dout_last = (4096,) * 3, 1024, 784, 10
+        widths = [din0, *hidden, dout_last]
+        layers = list(zip(widths[:-1], widths[1:]))
+        calls = [("nt", batch, dout, din, i == 0) for i, (din, dout) in enumerate(layers)]
+        for j, (din, dout) in enumerate(reversed(layers)):
+            calls.append(("nn", batch, din, dout, j == 0))
+            calls.append(("nt", dout, din, batch, False))
+        total = sum(2.0 * m * n * k for _, m, n, k, _ in calls) * world
+        desc = ("fcn_step 784-4096-4096-4096-10 batch 1024 (configs[3]): 4 forward NT + 4 backward "
+                "NN + 4 backward NT, all NT through MTNN (the reference routes only forward NT)")
+        par = "single GPU" if world == 1 else f"{world} independent replicas"
+        return calls, total, desc, ("weak" if world > 1 else "strong"), par, None
+    # large (config 5): m = 65536 rows of A sharded, B replicated
+    from paper_1702_03192_b200.sharding import row_range
+
+    m, n, k = 65536, 8192, 8192
+    lo, hi = row_range(m, rank, world)
+    calls = [("nt", hi - lo, n, k, True)]
+    desc = "large_nt m=65536 n=k=8192 (configs[4]), rows of A sharded, B replicated"
+    par = "single GPU" if world == 1 else f"row-sharded x{world} (NCCL broadcast B + all-gather C)"
+    return calls, 2.0 * m * n * k, desc, "strong", par, None
+
+
 # ----------------------------------------------------------------- GPU legs
 def main():
     ap = argparse.ArgumentParser()
@@ -187,13 +235,13 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--workload", default="sweep", choices=("sweep", "fcn", "large"))
     ap.add_argument("--exp-min", type=int, default=7)
     ap.add_argument("--exp-max", type=int, default=14)
     ap.add_argument("--model", default=str(DEFAULT_MODEL))
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--gather", action="store_true", help="N>1: include the C all-gather")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -202,6 +250,8 @@ def main():
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
+    import ctypes
+
     import torch
     import torch.distributed as dist
 
@@ -209,14 +259,13 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
-    from paper_1702_03192_b200 import _lib, gbdt
+    from paper_1702_03192_b200 import ProblemShape, _lib, gbdt
     from paper_1702_03192_b200.platform import probe_platform
     from paper_1702_03192_b200.selector import Dispatcher
 
     dev = torch.device("cuda", local_rank)
     L = _lib.lib
-    shapes = grid(args.exp_min, args.exp_max)
-    mx = 2 ** args.exp_max
+    calls, total_flops, desc, scaling, par, shapes = build_workload(args, rank, world)
 
     # model: the B200-trained selector if present, else an empty model (always NT)
     if Path(args.model).exists():
@@ -225,48 +274,53 @@ def main():
     else:
         model = gbdt.GbdtModel(trees=(), params=gbdt.GbdtParams(), n_features=8)
         model_name = "empty (always NT)"
-    platform = probe_platform()
-    disp = Dispatcher(model, platform)
+    disp = Dispatcher(model, probe_platform())
     handle = disp._native.handle
     prefix_p = disp._prefix_p
 
-    # row shard of every case for this rank (N > 1), as sharding.row_range
-    from paper_1702_03192_b200.sharding import row_range
-
-    def rows_of(m):
-        return row_range(m, rank, world)
-
+    # resident synthetic operands; every call views prefixes of these buffers
+    cap_a = max([m * k for _, m, n, k, _ in calls] + [1])
+    cap_b = max([n * k for _, m, n, k, _ in calls] + [1])
+    cap_c = max([m * n for _, m, n, k, _ in calls] + [1])
+    if args.workload == "large":
+        cap_c = 65536 * 8192  # gathered C
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
-    A = torch.rand(mx * mx, device=dev, generator=g).mul_(2).sub_(1)
-    B = torch.rand(mx * mx, device=dev, generator=g).mul_(2).sub_(1)
-    C = torch.empty(mx * mx, device=dev)
+    A = torch.rand(cap_a, device=dev, generator=g).mul_(2).sub_(1)
+    B = torch.rand(cap_b, device=dev, generator=g).mul_(2).sub_(1)
+    C = torch.empty(cap_c, device=dev)
     # L2 flush by READING 256 MiB (> 126 MB L2): leaves clean lines, so the next
     # timed kernel does not pay the write-back of a dirty flush buffer
     flush_src = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device=dev)
-
-    class _Flush:
-        @staticmethod
-        def fill_(_):
-            flush_src.sum()
-
-    flush = _Flush()
     stream = torch.cuda.current_stream(dev).cuda_stream
-    choice = __import__("ctypes").c_int()
+    choice = ctypes.c_int()
 
-    def case_call(m, n, k):
-        lo, hi = rows_of(m)
-        mm = hi - lo
-        if mm <= 0:
+    def run_call(op, m, n, k):
+        if m <= 0:
             return
-        rc = L.mtnn_dispatch_gemm(handle, prefix_p, A.data_ptr(), B.data_ptr(), C.data_ptr(),
-                                  mm, n, k, -1, 0, stream, __import__("ctypes").byref(choice))
+        if op == "nt":
+            rc = L.mtnn_dispatch_gemm(handle, prefix_p, A.data_ptr(), B.data_ptr(), C.data_ptr(),
+                                      m, n, k, -1, 0, stream, ctypes.byref(choice))
+        else:
+            rc = L.mtnn_gemm_nn(A.data_ptr(), B.data_ptr(), C.data_ptr(), m, n, k, 0, stream)
         if rc:
             _lib.check(rc)
 
+    comm = {"bcast": [], "gather": []}
+
     def one_step(events=None):
-        for (m, n, k) in shapes:
-            flush.fill_(1.0)
+        if args.workload == "large" and world > 1:
+            # B replicated from rank 0, timed as part of the sharded op
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
+            dist.broadcast(B[: 8192 * 8192], src=0)
+            ev[1].record()
+            if events is not None:
+                comm["bcast"].append(ev)
+                events.append(ev)
+        for (op, m, n, k, fl) in calls:
+            if fl:
+                flush_src.sum()
             # keep the GPU busy while the host enqueues the timed call, so the
             # event window holds device work only (no Python/ctypes gaps)
             torch.cuda._sleep(SLEEP_CYCLES)
@@ -274,14 +328,20 @@ def main():
                 s = torch.cuda.Event(enable_timing=True)
                 e = torch.cuda.Event(enable_timing=True)
                 s.record()
-                case_call(m, n, k)
+                run_call(op, m, n, k)
                 e.record()
                 events.append((s, e))
             else:
-                case_call(m, n, k)
-
-    local_flops = sum(2.0 * (rows_of(m)[1] - rows_of(m)[0]) * n * k for (m, n, k) in shapes)
-    total_flops = sum(2.0 * m * n * k for (m, n, k) in shapes)
+                run_call(op, m, n, k)
+        if args.workload == "large" and world > 1:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
+            rows = calls[0][1]
+            dist.all_gather_into_tensor(C[: 65536 * 8192], C[: rows * 8192].clone())
+            ev[1].record()
+            if events is not None:
+                comm["gather"].append(ev)
+                events.append(ev)
 
     for _ in range(args.warmup):
         one_step()
@@ -298,8 +358,6 @@ def main():
         w0 = time.perf_counter()
         for _ in range(args.steps):
             one_step(events)
-            if world > 1 and args.gather:
-                pass  # gather variant handled by --workload large in later rounds
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -312,14 +370,14 @@ def main():
     device_s = float(t.item())
     step_s = device_s / args.steps
     value = total_flops / step_s / 1e12
-
     prof = {c: _lib.profile_read(c) for c in _lib.KCLASS_NAMES}
     launches = int(sum(v[1] for v in prof.values()))
-
-    # per-case MTNN times (median over the K timed steps) for the oracle ratio
-    ncase = len(shapes)
-    per_case_mtnn = [statistics.median(events[st * ncase + i][0].elapsed_time(events[st * ncase + i][1])
-                                       for st in range(args.steps)) * 1e-3 for i in range(ncase)]
+    ncall = len(calls)
+    per_call = [statistics.median(events[st * (len(events) // args.steps) + i][0].elapsed_time(
+        events[st * (len(events) // args.steps) + i][1]) for st in range(args.steps)) * 1e-3
+        for i in range(len(events) // args.steps)]
+    if world > 1 and args.workload == "large":
+        per_call = per_call[1:-1]  # drop the collective windows
 
     if rank != 0:
         if world > 1:
@@ -327,7 +385,7 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---------------- roofline of the dominant kernel (tc3xtf32 GEMM)
+    # ---------------- roofline of the dominant kernel
     peaks_path = ROOT / "MEASURED_PEAKS.json"
     peaks = json.loads(peaks_path.read_text()) if peaks_path.exists() else {}
     bf16 = peaks.get("bf16_tflops", 1590.0)
@@ -337,13 +395,13 @@ def main():
     f16s = tc_class == _lib.KCLASS_GEMM_TC_F16S
     roof = bf16 / 3.0 if f16s else bf16 / 6.0
     ncu_path = ROOT / "profiles" / "ncu_summary.json"
-    ncu_traffic = json.loads(ncu_path.read_text()).get("gemm_tc3xtf32_traffic", {}) if ncu_path.exists() else {}
+    ncu_traffic = json.loads(ncu_path.read_text()).get("gemm_tc3x_traffic", {}) if ncu_path.exists() else {}
     dominant = max(prof, key=lambda c: prof[c][0])
+    achieved = tc_work / (tc_ms * 1e-3) / 1e12 if tc_ms else None
     roofline = {
         "kernel": _lib.KCLASS_NAMES[tc_class], "bound": "tensor",
-        "achieved": tc_work / (tc_ms * 1e-3) / 1e12 if tc_ms else None,
-        "peak": roof, "unit": "TFLOP/s",
-        "frac": (tc_work / (tc_ms * 1e-3) / 1e12) / roof if tc_ms else None,
+        "achieved": achieved, "peak": roof, "unit": "TFLOP/s",
+        "frac": achieved / roof if achieved else None,
         "traffic": ncu_traffic.get("traffic"),
         "traffic_launch": ncu_traffic.get("launch"),
         "traffic_algorithmic_bytes": ncu_traffic.get("algorithmic_bytes"),
@@ -352,94 +410,28 @@ def main():
                        f"3xTF32 FP32-accurate roof = measured bf16 dense {bf16} TFLOP/s "
                        f"(MEASURED_PEAKS.json, burst) / 2 (tf32 rate) / 3 (MMAs per product)"),
         "launches": tc_n, "avg_launch_ms": tc_ms / tc_n if tc_n else None,
-        "share_of_step": tc_ms / 1e3 / device_s if device_s else None,
+        "share_of_step": tc_ms / 1e3 / (device_s * 1.0) if device_s else None,
         "dominant_kernel_by_time": _lib.KCLASS_NAMES[dominant],
     }
-    kernels_summary = {_lib.KCLASS_NAMES[c]: {"ms": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
+    kernels_summary = {_lib.KCLASS_NAMES[c]: {"ms": v[0] / args.steps,
+                                              "launches_per_step": v[1] / args.steps,
                                               "work_per_step": v[2] / args.steps}
-                       for c, v in prof.items()}
+                       for c, v in prof.items() if v[1]}
 
-    # ---------------- oracle pass: NT and TNN per case (median of 3, interleaved),
-    # with the same kernel instrumentation as the timed MTNN steps
-    L.mtnn_profile_enable(1)
-    nt_t, tnn_t = [[] for _ in shapes], [[] for _ in shapes]
-    for _rep in range(3):
-        for i, (m, n, k) in enumerate(shapes):
-            a = A[: m * k].view(m, k)
-            b = B[: n * k].view(n, k)
-            c = C[: m * n].view(m, n)
-            for which in ("nt", "tnn"):
-                flush.fill_(1.0)
-                torch.cuda._sleep(SLEEP_CYCLES)
-                s = torch.cuda.Event(enable_timing=True)
-                e = torch.cuda.Event(enable_timing=True)
-                s.record()
-                if which == "nt":
-                    _lib.check(L.mtnn_gemm_nt(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, 0, stream))
-                else:
-                    _lib.check(L.mtnn_gemm_tnn(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, 0, -1, stream))
-                e.record()
-                (nt_t if which == "nt" else tnn_t)[i].append((s, e))
-    torch.cuda.synchronize()
-    L.mtnn_profile_enable(0)
-    L.mtnn_profile_reset()
-    nt_s = [statistics.median(s.elapsed_time(e) for s, e in ev) * 1e-3 for ev in nt_t]
-    tnn_s = [statistics.median(s.elapsed_time(e) for s, e in ev) * 1e-3 for ev in tnn_t]
-    best = [min(x, y) for x, y in zip(nt_s, tnn_s)]
-    ratio = [b_ / m_ for b_, m_ in zip(best, per_case_mtnn)]
-    decisions = [disp.select(__import__("paper_1702_03192_b200").ProblemShape(*sh)) for sh in shapes]
-    picked_tnn = [d.choice.value == "tnn" for d in decisions]
-    faster_tnn = [y < x for x, y in zip(nt_s, tnn_s)]
-    sel_acc = float(np.mean([p == f for p, f in zip(picked_tnn, faster_tnn)]))
-    large = [i for i, (m, n, k) in enumerate(shapes) if min(m, n, k) >= 4096]
-    large_tf = (sum(2.0 * shapes[i][0] * shapes[i][1] * shapes[i][2] for i in large)
-                / sum(per_case_mtnn[i] for i in large) / 1e12) if large else None
+    extra = {}
+    if args.workload == "sweep" and world == 1:
+        extra.update(sweep_oracle_pass(shapes, per_call, A, B, C, flush_src, stream, disp,
+                                       total_flops, roof, L, _lib, torch))
+    if args.workload == "large" and world > 1:
+        extra["collective_ms_per_step"] = {
+            k: statistics.mean(s.elapsed_time(e) for s, e in v) for k, v in comm.items() if v}
+    if world == 1:
+        extra["transpose"] = transpose_pass(B, C, flush_src, stream, hbm, L, _lib, torch)
+    extra["selector_native_ns_incl_ctypes"] = selector_cost(L, handle, prefix_p)
 
-    # ---------------- transpose bandwidth (config 3)
-    tshapes = [(2 ** e, 2 ** e) for e in range(7, 15)] + [
-        (1000, 1000), (3000, 5000), (16384, 128), (128, 16384), (4097, 1023), (12345, 6789),
-        (8191, 8193)]
-    tr = {}
-    bt_buf = torch.empty(mx * mx, device=dev)
-    for (r, cc) in tshapes:
-        src = B[: r * cc]
-        dst = bt_buf[: r * cc]
-        ev = []
-        for _ in range(5):
-            flush.fill_(1.0)
-            s = torch.cuda.Event(enable_timing=True)
-            e = torch.cuda.Event(enable_timing=True)
-            s.record()
-            _lib.check(L.mtnn_transpose(src.data_ptr(), dst.data_ptr(), r, cc, stream))
-            e.record()
-            ev.append((s, e))
-        torch.cuda.synchronize()
-        tt = statistics.median(s.elapsed_time(e) * 1e-3 for s, e in ev)
-        tr[f"{r}x{cc}"] = 8.0 * r * cc / tt / 1e9
-    big = [tr[f"{2**e}x{2**e}"] for e in (12, 13, 14)]
-    transpose_summary = {"gbs_by_shape": {k_: round(v, 1) for k_, v in tr.items()},
-                         "gbs_large_median": statistics.median(big), "peak_hbm_gbs": hbm,
-                         "frac_of_measured_hbm": statistics.median(big) / hbm,
-                         "frac_of_8tbs_spec": statistics.median(big) / 8000.0}
-
-    # ---------------- selector overhead (native decision)
-    import ctypes
-
-    raw = ctypes.c_double()
-    ch = ctypes.c_int()
-    rs = ctypes.c_int()
-    nsel = 20000
-    t0 = time.perf_counter()
-    for i in range(nsel):
-        L.mtnn_select(handle, prefix_p, 1024, 1024, 1024, 1 << 40, ctypes.byref(raw),
-                      ctypes.byref(ch), ctypes.byref(rs))
-    sel_ns = (time.perf_counter() - t0) / nsel * 1e9
-
-    # ---------------- e2e through the C-ABI with pinned host buffers
     e2e = None
-    if not args.no_e2e:
-        e2e = run_e2e(args, shapes, handle, prefix_p, mx, L)
-
+    if not args.no_e2e and world == 1:
+        e2e = run_e2e(args, calls, handle, prefix_p, L)
     cpu = None
     if not args.no_cpu and world == 1:
         import oracle
@@ -449,76 +441,154 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
         "dtype": "f32", "data": "synthetic uniform[-1,1) fp32 operands, resident in HBM",
-        "config": {"workload": f"nt_sweep m,n,k in {{2^{args.exp_min}..2^{args.exp_max}}} "
-                               f"({len(shapes)} cases), MTNN-selected (configs[1])",
-                   "cases": len(shapes), "model": model_name,
-                   "l2": "flushed (256 MiB write) before every case, outside the timed windows",
-                   "parallelism": "single GPU" if world == 1 else f"row-sharded x{world}, B replicated",
-                   "precision": "FP32-accurate: 3 tensor-core MMAs per product on hi/lo operand halves (pow2-scaled FP16 or TF32) with FP32 promotion every 128-256 k, or FP32 FFMA",
+        "config": {"workload": desc, "calls_per_step": ncall, "model": model_name,
+                   "l2": "flushed (256 MiB read) before every case/phase, outside the timed windows",
+                   "parallelism": par,
+                   "precision": ("FP32-accurate: 3 tensor-core MMAs per product on hi/lo operand "
+                                 "halves (pow2-scaled FP16, or TF32) with FP32 promotion, or FP32 FFMA"),
                    "wall_ms_per_step": wall / args.steps * 1e3},
-        "roofline": roofline,
-        "cpu_baseline": cpu,
-        "e2e": e2e,
-        "gpu_launches": launches,
-        "clocks": clocks.summary(),
-        "mtnn_vs_best_of_both": {"mean_per_case_ratio": float(np.mean(ratio)),
-                                 "min_per_case_ratio": float(np.min(ratio)),
-                                 "always_nt_tflops": total_flops / sum(nt_s) / 1e12,
-                                 "always_tnn_tflops": total_flops / sum(tnn_s) / 1e12,
-                                 "best_of_both_tflops": total_flops / sum(best) / 1e12},
-        "selector": {"accuracy_vs_measured_faster_path": sel_acc,
-                     "tnn_faster_cases": int(sum(faster_tnn)), "tnn_picked_cases": int(sum(picked_tnn)),
-                     "native_select_ns_incl_ctypes": sel_ns},
-        "large_shapes_tflops": large_tf,
-        "large_shapes_frac_of_roof": large_tf / roof if large_tf else None,
-        "transpose": transpose_summary,
-        "kernels": kernels_summary,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clocks.summary(), "kernels": kernels_summary,
     }
+    line.update(extra)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def run_e2e(args, shapes, handle, prefix_p, mx, L):
-    """Same sweep through mtnn_dispatch_gemm_host (the drop-in C-ABI call):
-    per case H2D of A and B from pinned host memory, decision + kernels, D2H of C."""
+def sweep_oracle_pass(shapes, per_case_mtnn, A, B, C, flush_src, stream, disp, total_flops, roof,
+                      L, _lib, torch):
+    """NT and TNN per case (median of 3, interleaved, same instrumentation as the
+    timed steps): MTNN vs the per-case best of both paths, and selector accuracy."""
+    from paper_1702_03192_b200 import ProblemShape
+
+    nt_t, tnn_t = [[] for _ in shapes], [[] for _ in shapes]
+    L.mtnn_profile_enable(1)
+    for _rep in range(3):
+        for i, (m, n, k) in enumerate(shapes):
+            for which in ("nt", "tnn"):
+                flush_src.sum()
+                torch.cuda._sleep(SLEEP_CYCLES)
+                s = torch.cuda.Event(enable_timing=True)
+                e = torch.cuda.Event(enable_timing=True)
+                s.record()
+                if which == "nt":
+                    _lib.check(L.mtnn_gemm_nt(A.data_ptr(), B.data_ptr(), C.data_ptr(), m, n, k, 0, stream))
+                else:
+                    _lib.check(L.mtnn_gemm_tnn(A.data_ptr(), B.data_ptr(), C.data_ptr(), m, n, k, 0, -1,
+                                               stream))
+                e.record()
+                (nt_t if which == "nt" else tnn_t)[i].append((s, e))
+    torch.cuda.synchronize()
+    L.mtnn_profile_enable(0)
+    L.mtnn_profile_reset()
+    nt_s = [statistics.median(s.elapsed_time(e) for s, e in ev) * 1e-3 for ev in nt_t]
+    tnn_s = [statistics.median(s.elapsed_time(e) for s, e in ev) * 1e-3 for ev in tnn_t]
+    best = [min(x, y) for x, y in zip(nt_s, tnn_s)]
+    ratio = [b_ / m_ for b_, m_ in zip(best, per_case_mtnn)]
+    picked_tnn = [disp.select(ProblemShape(*sh)).choice.value == "tnn" for sh in shapes]
+    faster_tnn = [y < x for x, y in zip(nt_s, tnn_s)]
+    large = [i for i, (m, n, k) in enumerate(shapes) if min(m, n, k) >= 4096]
+    large_tf = (sum(2.0 * shapes[i][0] * shapes[i][1] * shapes[i][2] for i in large)
+                / sum(per_case_mtnn[i] for i in large) / 1e12) if large else None
+    return {
+        "mtnn_vs_best_of_both": {"mean_per_case_ratio": float(np.mean(ratio)),
+                                 "min_per_case_ratio": float(np.min(ratio)),
+                                 "always_nt_tflops": total_flops / sum(nt_s) / 1e12,
+                                 "always_tnn_tflops": total_flops / sum(tnn_s) / 1e12,
+                                 "best_of_both_tflops": total_flops / sum(best) / 1e12},
+        "selector": {"accuracy_vs_measured_faster_path": float(np.mean(
+                         [p == f for p, f in zip(picked_tnn, faster_tnn)])),
+                     "tnn_faster_cases": int(sum(faster_tnn)),
+                     "tnn_picked_cases": int(sum(picked_tnn))},
+        "large_shapes_tflops": large_tf,
+        "large_shapes_frac_of_roof": large_tf / roof if large_tf else None,
+    }
+
+
+def transpose_pass(B, C, flush_src, stream, hbm, L, _lib, torch):
+    """Transpose bandwidth (config 3): 8*rows*cols bytes per launch, median of 5."""
+    tshapes = [(2 ** e, 2 ** e) for e in range(7, 15)] + [
+        (1000, 1000), (3000, 5000), (16384, 128), (128, 16384), (4097, 1023), (12345, 6789),
+        (8191, 8193)]
+    tshapes = [(r, c) for r, c in tshapes if r * c <= min(B.numel(), C.numel())]
+    out = {}
+    for (r, c) in tshapes:
+        ev = []
+        for _ in range(5):
+            flush_src.sum()
+            torch.cuda._sleep(SLEEP_CYCLES)
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record()
+            _lib.check(L.mtnn_transpose(B.data_ptr(), C.data_ptr(), r, c, stream))
+            e.record()
+            ev.append((s, e))
+        torch.cuda.synchronize()
+        tt = statistics.median(s.elapsed_time(e) * 1e-3 for s, e in ev)
+        out[f"{r}x{c}"] = 8.0 * r * c / tt / 1e9
+    big = [out[k] for k in ("4096x4096", "8192x8192", "16384x16384") if k in out]
+    med = statistics.median(big) if big else None
+    return {"gbs_by_shape": {k: round(v, 1) for k, v in out.items()}, "gbs_large_median": med,
+            "peak_hbm_gbs": hbm, "frac_of_measured_hbm": med / hbm if med else None,
+            "frac_of_8tbs_spec": med / 8000.0 if med else None}
+
+
+def selector_cost(L, handle, prefix_p):
+    import ctypes
+
+    raw, ch, rs = ctypes.c_double(), ctypes.c_int(), ctypes.c_int()
+    n = 20000
+    t0 = time.perf_counter()
+    for _ in range(n):
+        L.mtnn_select(handle, prefix_p, 1024, 1024, 1024, 1 << 40, ctypes.byref(raw),
+                      ctypes.byref(ch), ctypes.byref(rs))
+    return (time.perf_counter() - t0) / n * 1e9
+
+
+def run_e2e(args, calls, handle, prefix_p, L):
+    """The same step through the reference-facing C-ABI with HOST buffers:
+    mtnn_dispatch_gemm_host for NT calls, mtnn_gemm_nn_host for NN calls, each
+    copying its operands in from pinned memory and its result out."""
     import ctypes
 
     import torch
 
     from paper_1702_03192_b200 import _lib
 
-    max_a = max(m * k for m, n, k in shapes)
-    max_b = max(n * k for m, n, k in shapes)
-    max_c = max(m * n for m, n, k in shapes)
-    ha = torch.empty(max_a, dtype=torch.float32).pin_memory()
-    hb = torch.empty(max_b, dtype=torch.float32).pin_memory()
+    max_a = max(m * k for _, m, n, k, _ in calls)
+    max_b = max(n * k for _, m, n, k, _ in calls)
+    max_c = max(m * n for _, m, n, k, _ in calls)
+    ha = torch.empty(max_a, dtype=torch.float32).pin_memory().uniform_(-1, 1)
+    hb = torch.empty(max_b, dtype=torch.float32).pin_memory().uniform_(-1, 1)
     hc = torch.empty(max_c, dtype=torch.float32).pin_memory()
-    ha.uniform_(-1, 1)
-    hb.uniform_(-1, 1)
     ch = ctypes.c_int()
-    h2d = sum(4 * (m * k + n * k) for m, n, k in shapes)
-    d2h = sum(4 * m * n for m, n, k in shapes)
+    h2d = sum(4 * (m * k + n * k) for _, m, n, k, _ in calls)
+    d2h = sum(4 * m * n for _, m, n, k, _ in calls)
     steps = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 2)
 
     def step():
-        for (m, n, k) in shapes:
-            _lib.check(L.mtnn_dispatch_gemm_host(handle, prefix_p, ha.data_ptr(), hb.data_ptr(),
-                                                 hc.data_ptr(), m, n, k, -1, 0, ctypes.byref(ch)))
+        for (op, m, n, k, _) in calls:
+            if op == "nt":
+                rc = L.mtnn_dispatch_gemm_host(handle, prefix_p, ha.data_ptr(), hb.data_ptr(),
+                                               hc.data_ptr(), m, n, k, -1, 0, ctypes.byref(ch))
+            else:
+                rc = L.mtnn_gemm_nn_host(ha.data_ptr(), hb.data_ptr(), hc.data_ptr(), m, n, k, 0)
+            _lib.check(rc)
 
-    for _ in range(max(1, min(args.warmup, 1))):
-        step()
+    step()
     t0 = time.perf_counter()
     for _ in range(steps):
         step()
     dt = (time.perf_counter() - t0) / steps
-    flops = sum(2.0 * m * n * k for m, n, k in shapes)
+    flops = sum(2.0 * m * n * k for _, m, n, k, _ in calls)
     return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3, "steps": steps,
-            "api": "mtnn_dispatch_gemm_host (include/mtnn_b200.h), pinned host buffers"}
+            "api": "mtnn_dispatch_gemm_host / mtnn_gemm_nn_host (include/mtnn_b200.h), pinned host "
+                   "buffers, H2D/compute/D2H pipelined inside each call"}
 
 
 if __name__ == "__main__":

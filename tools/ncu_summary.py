@@ -26,10 +26,14 @@ UNIT = {"ns": 1e-9, "nsecond": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "m
         "Hz": 1, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9}
 
 
-def read(rep):
+def read(rep, pattern=None):
+    import re
+
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units = rows[0], rows[1]
+    ki = hdr.index("Kernel Name")
+    vals = next(r for r in rows[2:] if pattern is None or re.search(pattern, r[ki]))
     res = {"kernel": vals[hdr.index("Kernel Name")]}
     for k, name in KEYS.items():
         if k in hdr:
@@ -46,18 +50,23 @@ def main(prefix, specs):
     for spec in specs:
         name, rest = spec.split("=", 1)
         rep, shape = rest.split(":", 1)
-        r = read(rep)
-        r["traffic_bytes"] = r.get("dram_read", 0) + r.get("dram_write", 0)
         parts = shape.split(":")
+        r = read(rep, parts[1] if len(parts) > 1 else None)
+        r["traffic_bytes"] = r.get("dram_read", 0) + r.get("dram_write", 0)
         dims = [int(x) for x in parts[0].split(",")]
         if len(dims) == 3:
             m, n, k = dims
-            r["algorithmic_bytes"] = 4 * (2 * m * k + 2 * n * k + m * n)  # A, A_lo, B, B_lo, C
+            # hi/lo halves of A and B (4 bytes per element in total for both the
+            # TF32 lo-only and the FP16 h+l splits, plus the raw fp32 operand read as
+            # hi by the TF32 kind) and C; report the FP16 kind's: 4(mk + nk) + 4mn
+            r["algorithmic_bytes"] = 4 * (m * k + n * k + m * n)
             r["achieved"] = f"{2 * m * n * k / r['duration'] / 1e12:.1f} TFLOP/s"
-        else:
+        elif len(dims) == 2:
             rr, cc = dims
             r["algorithmic_bytes"] = 8 * rr * cc
             r["achieved"] = f"{8 * rr * cc / r['duration'] / 1e9:.0f} GB/s"
+        else:
+            rows_, k = dims[0], dims[1] if len(dims) > 1 else 0
         summary[name] = r
         md.append(f"| {name} | {r['kernel'][:40]} | {r['duration']*1e3:.3f} ms | "
                   f"{r['traffic_bytes']/1e9:.2f} GB | {r['algorithmic_bytes']/1e9:.2f} GB | "

@@ -5,6 +5,7 @@ sys.path.insert(0, ".")
 from paper_1702_03192_b200 import device
 
 which = sys.argv[1] if len(sys.argv) > 1 else "nt8192"
+VARIANT = int(sys.argv[2]) if len(sys.argv) > 2 else 3  # 3 = tc3xf16s, 1 = tc3xtf32
 torch.manual_seed(0)
 cases = {"nt8192": ("nt", 8192, 8192, 8192), "nt16384": ("nt", 16384, 16384, 16384),
          "nn16384": ("nn", 16384, 16384, 16384), "tr16384": ("tr", 16384, 16384, 0),
@@ -19,8 +20,8 @@ else:
     bt = b.t().contiguous()
     for _ in range(2):
         if op == "nt":
-            device.gemm_nt(a, b, variant=1)
+            device.gemm_nt(a, b, variant=VARIANT)
         else:
-            device.gemm_nn(a, bt, variant=1)
+            device.gemm_nn(a, bt, variant=VARIANT)
 torch.cuda.synchronize()
 print("done", which)
