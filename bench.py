@@ -131,9 +131,16 @@ def cpu_sample_shapes(max_seconds_hint: float):
     return grid(7, 11)
 
 
-def cpu_baseline(threads: int):
-    import oracle
+def host_threads() -> int:
+    """All host cores this process may run on (torchrun sets OMP_NUM_THREADS=1,
+    so the OpenMP default is not the machine's core count)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
+
+def cpu_baseline(threads: int):
     shapes = cpu_sample_shapes(20.0)
     cpu_sample_run(shapes[:8], threads)  # warm caches / thread pool
     flops, best, s_nt, s_tnn = cpu_sample_run(shapes, threads)
@@ -144,7 +151,6 @@ def cpu_baseline(threads: int):
                    f"MTNN), {threads} threads; always-NT {flops / s_nt / 1e12:.4f}, "
                    f"always-TNN {flops / s_tnn / 1e12:.4f} TFLOP/s"),
         "seconds": best,
-        "max_threads": oracle.max_threads(),
     }
 
 
@@ -153,9 +159,7 @@ def run_reference(args, rank, world):
     port), timed on the host cores; rank 0 only."""
     if rank != 0:
         return
-    import oracle
-
-    threads = oracle.max_threads()
+    threads = host_threads()
     shapes = cpu_sample_shapes(20.0)
     for _ in range(args.warmup):
         cpu_sample_run(shapes[:16], threads)
@@ -255,9 +259,16 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # one rank per GPU; MTNN_BENCH_SHARE_GPU=1 maps ranks onto the visible GPUs
+    # modulo their count and uses gloo (test mode for the N>1 path on one GPU)
+    share = os.environ.get("MTNN_BENCH_SHARE_GPU") == "1"
+    local_rank = local_rank % torch.cuda.device_count() if share else local_rank
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     from paper_1702_03192_b200 import ProblemShape, _lib, gbdt
     from paper_1702_03192_b200.platform import probe_platform
@@ -337,7 +348,10 @@ def main():
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record()
             rows = calls[0][1]
-            dist.all_gather_into_tensor(C[: 65536 * 8192], C[: rows * 8192].clone())
+            if dist.get_backend() == "nccl":
+                dist.all_gather_into_tensor(C[: 65536 * 8192], C[: rows * 8192].clone())
+            else:  # gloo test mode (equal row blocks)
+                dist.all_gather(list(C[: 65536 * 8192].chunk(world)), C[: rows * 8192].clone())
             ev[1].record()
             if events is not None:
                 comm["gather"].append(ev)
@@ -364,7 +378,8 @@ def main():
         wall = time.perf_counter() - w0
     L.mtnn_profile_enable(0)
     device_s = sum(s.elapsed_time(e) for s, e in events) * 1e-3
-    t = torch.tensor([device_s], dtype=torch.float64, device=dev)
+    t = torch.tensor([device_s], dtype=torch.float64,
+                     device=dev if not share else "cpu")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     device_s = float(t.item())
@@ -434,9 +449,7 @@ def main():
         e2e = run_e2e(args, calls, handle, prefix_p, L)
     cpu = None
     if not args.no_cpu and world == 1:
-        import oracle
-
-        cpu = cpu_baseline(oracle.max_threads())
+        cpu = cpu_baseline(host_threads())
 
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
