@@ -83,6 +83,7 @@ struct TcOperand {
 struct ScratchBuffer;
 int tc_prepare(const float* X, int64_t rows, int64_t k, bool mn_major, TcKind kind,
                ScratchBuffer& ws, TcOperand* out, cudaStream_t s);
+int tf32_inkernel_operand(int64_t m, int64_t n);
 int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n, int64_t k,
            bool b_is_nk, TcKind kind, cudaStream_t s);
 int launch_split_rows_f16(const float* x, void* hi, void* lo, float* inv_scale, int64_t rows,

@@ -30,6 +30,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cmath>
 #include <mutex>
 #include <stdlib.h>
 
@@ -179,14 +180,24 @@ __device__ __forceinline__ void tc_commit(uint32_t bar) {
                    bar)
                : "memory");
 }
-__device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                            uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
+template <bool kF16>
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  if constexpr (kF16) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
 }
 // 32 lanes x 32 consecutive fp32 columns -> 32 registers per thread.
 __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
@@ -264,7 +275,13 @@ __device__ __forceinline__ void unit_coords(int u, const Params& p, int& split, 
 }
 
 // ------------------------------------------------------------------- kernel
-template <int BN, bool B_MN, class Kind>
+// kConv (KindTF32 only): 0 = both lo halves come from the pre-pass; 1 / 2 = the
+// lo half of A / B is computed in-kernel from the raw tile TMA just landed:
+// lo = x - trunc_tf32(x) is elementwise, so writing it at the same offsets of
+// the lo tile keeps the swizzled UMMA layout. Warps 2-3 (idle after TMEM
+// allocation) do it; the MMA warp then waits on conv_bar instead of full_bar.
+// That operand is read from DRAM once (4 B per element) and needs no pre-pass.
+template <int BN, bool B_MN, class Kind, int kConv>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
                      const __grid_constant__ CUtensorMap map_alo,
@@ -283,7 +300,10 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
   uint64_t* empty_bar = bars + kStages;      // [kStages]
   uint64_t* tfull_bar = bars + 2 * kStages;  // [2]
   uint64_t* tempty_bar = bars + 2 * kStages + 2;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  uint64_t* conv_bar = bars + 2 * kStages + 4;     // [kStages] (kConv != 0)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kStages + 4);
+  static_assert(kConv == 0 || !Kind::kScaled, "in-kernel lo split is TF32-only");
+  constexpr int kConvBytes = kConv == 1 ? S::kABytes : kConv == 2 ? S::kBBytes : 0;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -304,6 +324,7 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
       mbar_init(smem_u32(&tfull_bar[s]), 1);
       mbar_init(smem_u32(&tempty_bar[s]), kEpiWarps);  // one arrive per epilogue warp
     }
+    for (int s = 0; s < kStages; ++s) mbar_init(smem_u32(&conv_bar[s]), 2);  // warps 2, 3
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -332,14 +353,15 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
           const uint32_t fb = smem_u32(&full_bar[stage]);
-          mbar_expect_tx(fb, S::kStageBytes);
+          mbar_expect_tx(fb, S::kStageBytes - kConvBytes);
           uint8_t* st = ring + stage * S::kStageBytes;
           const int kx = kb * Kind::BK;
           tma_load_2d(smem_u32(st), &map_ahi, fb, kx, tm * BM);
-          tma_load_2d(smem_u32(st + S::kABytes), &map_alo, fb, kx, tm * BM);
+          if (kConv != 1) tma_load_2d(smem_u32(st + S::kABytes), &map_alo, fb, kx, tm * BM);
           if (!B_MN) {
             tma_load_2d(smem_u32(st + 2 * S::kABytes), &map_bhi, fb, kx, tn * BN);
-            tma_load_2d(smem_u32(st + 2 * S::kABytes + S::kBBytes), &map_blo, fb, kx, tn * BN);
+            if (kConv != 2)
+              tma_load_2d(smem_u32(st + 2 * S::kABytes + S::kBBytes), &map_blo, fb, kx, tn * BN);
           } else {
             // BN/kMnBox boxes of [BK k-rows][kMnBox columns] (128-byte rows), each
             // one MN group of the canonical MN-major layout, kMnLBO bytes apart
@@ -347,8 +369,9 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
             for (int g = 0; g < BN / Kind::kMnBox; ++g) {
               tma_load_2d(smem_u32(st + 2 * S::kABytes + g * Kind::kMnLBO), &map_bhi, fb,
                           tn * BN + g * Kind::kMnBox, kx);
-              tma_load_2d(smem_u32(st + 2 * S::kABytes + S::kBBytes + g * Kind::kMnLBO),
-                          &map_blo, fb, tn * BN + g * Kind::kMnBox, kx);
+              if (kConv != 2)
+                tma_load_2d(smem_u32(st + 2 * S::kABytes + S::kBBytes + g * Kind::kMnLBO),
+                            &map_blo, fb, tn * BN + g * Kind::kMnBox, kx);
             }
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -372,7 +395,7 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
         for (int kb = kc; kb < kce; ++kb) {
-          mbar_wait(smem_u32(&full_bar[stage]), phase);
+          mbar_wait(smem_u32(kConv ? &conv_bar[stage] : &full_bar[stage]), phase);
           tc_fence_after();
           if (elect_one()) {
             uint8_t* st = ring + stage * S::kStageBytes;
@@ -397,9 +420,9 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
                                  Kind::kMnLayout);
               }
               const uint32_t accum = (kb == kc && ks == 0) ? 0u : 1u;
-              tc_mma_tf32(tmem_d, dal, dbh, idesc, accum);
-              tc_mma_tf32(tmem_d, dah, dbl, idesc, 1u);
-              tc_mma_tf32(tmem_d, dah, dbh, idesc, 1u);
+              tc_mma<Kind::kScaled>(tmem_d, dal, dbh, idesc, accum);
+              tc_mma<Kind::kScaled>(tmem_d, dah, dbl, idesc, 1u);
+              tc_mma<Kind::kScaled>(tmem_d, dah, dbh, idesc, 1u);
             }
             tc_commit(smem_u32(&empty_bar[stage]));
             if (kb == kce - 1) tc_commit(smem_u32(&tfull_bar[acc]));
@@ -408,6 +431,34 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (kConv != 0 && (warp == 2 || warp == 3)) {
+    // ===================== in-kernel lo split (TF32, one operand) =====================
+    const int t = threadIdx.x - 64;  // 0..63
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const int split = u / (p.tiles_m * p.tiles_n);
+      const int kb0 = split * kb_per;
+      const int kb1 = min(p.total_kblocks, kb0 + kb_per);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(smem_u32(&full_bar[stage]), phase);
+        uint8_t* raw = ring + stage * S::kStageBytes + (kConv == 1 ? 0 : 2 * S::kABytes);
+        uint8_t* lo = raw + kConvBytes;
+#pragma unroll 4
+        for (int i = t; i < kConvBytes / 16; i += 64) {
+          float4 v = *reinterpret_cast<const float4*>(raw + 16 * i);
+          v.x -= __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+          v.y -= __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+          v.z -= __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+          v.w -= __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          *reinterpret_cast<float4*>(lo + 16 * i) = v;
+        }
+        fence_proxy_async_smem();  // generic-proxy smem writes -> visible to UMMA
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&conv_bar[stage]));
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp >= kEpiWarp0) {
@@ -570,7 +621,7 @@ static int encode(CUtensorMap* map, const void* base, int rank, const uint64_t* 
   return MTNN_OK;
 }
 
-template <int BN, bool B_MN, class Kind>
+template <int BN, bool B_MN, class Kind, int kConv = 0>
 static int launch_impl(const void* ahi, const void* alo, const void* bhi,
                        const void* blo, float* out, const Params& p, int grid,
                        cudaStream_t s) {
@@ -583,8 +634,9 @@ static int launch_impl(const void* ahi, const void* alo, const void* bhi,
     const uint64_t str[1] = {(uint64_t)p.k * eb};
     const uint32_t box[2] = {(uint32_t)Kind::BK, BM};
     MTNN_TRY(encode(&mah, ahi, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
-    MTNN_TRY(encode(&mal, alo, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
+    MTNN_TRY(encode(&mal, alo ? alo : ahi, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
   }
+  if (!blo) blo = bhi;  // computed in-kernel (kConv == 2): the map is never used
   if (!B_MN) {
     const uint64_t dims[2] = {(uint64_t)p.k, (uint64_t)p.n};
     const uint64_t str[1] = {(uint64_t)p.k * eb};
@@ -605,7 +657,7 @@ static int launch_impl(const void* ahi, const void* alo, const void* bhi,
     const uint32_t box[3] = {16, 32, 1};
     MTNN_TRY(encode(&mc, out, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
   }
-  auto kern = gemm_tc3x_kernel<BN, B_MN, Kind>;
+  auto kern = gemm_tc3x_kernel<BN, B_MN, Kind, kConv>;
   static bool attr_set = false;
   if (!attr_set) {
     MTNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -643,6 +695,20 @@ static int chunk_kblocks(TcKind) {
     return x > 0 ? x : 8;
   }();
   return v;
+}
+
+// TF32 kind, opt-in (MTNN_TF32_INKERNEL=1): the kernel computes the larger
+// operand's lo half itself so only the smaller one is pre-split (1 = A, 2 = B).
+// Measured on the B200 it gains <= 3% on skinny shapes (which are bound by tile
+// waste and split-K waves, not split traffic) and costs ~22% on compute-bound
+// shapes (smem/ALU contention with the MMA), so it is off by default.
+int tf32_inkernel_operand(int64_t m, int64_t n) {
+  static const bool on = [] {
+    const char* e = getenv("MTNN_TF32_INKERNEL");
+    return e && e[0] == '1';
+  }();
+  if (!on) return 0;
+  return m >= n ? 1 : 2;
 }
 
 bool tc_eligible(const float* A, const float* B, const float* C, int64_t m, int64_t n,
@@ -706,8 +772,40 @@ int tc_prepare(const float* X, int64_t rows, int64_t k, bool mn_major, TcKind ki
   return MTNN_OK;
 }
 
+// Split-K factor: minimise (waves of units) x (k-blocks per unit + per-unit
+// overhead) plus the partial-sum traffic a split adds (the GEMM writes `s`
+// partial C's, the reduction reads them and writes C). Wave quantisation
+// matters: 64 tiles x 3 splits = 192 units is two waves on 148 SMs and slower
+// than 2 splits in one wave.
+static int choose_splits(int tiles, int kblocks, int64_t m, int64_t n, int sms) {
+  constexpr double kKblockSeconds = 0.5e-6;  // ~6 MMAs x 128 clk at ~1.6 GHz
+  constexpr double kUnitOverheadKb = 2.0;    // prologue + epilogue drain, in k-blocks
+  constexpr double kHbm = 5.0e12;
+  if (tiles >= 4 * sms || kblocks < 8) return 1;
+  const double mn = (double)m * (double)n;
+  int best = 1;
+  double best_t = 1e300;
+  for (int s = 1; s <= 32 && s <= kblocks / 4; ++s) {
+    const int per = (kblocks + s - 1) / s;
+    const int real_s = (kblocks + per - 1) / per;
+    if (real_s != s) continue;
+    const double waves = std::ceil((double)tiles * s / sms);
+    double t = waves * (per + kUnitOverheadKb) * kKblockSeconds;
+    if (s > 1) t += 4.0 * (2.0 * s + 1.0) * mn / kHbm;
+    if (t < best_t * 0.98) {  // prefer fewer splits unless clearly better
+      best_t = t;
+      best = s;
+    }
+  }
+  return best;
+}
+
 int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n, int64_t k,
            bool b_is_nk, TcKind kind, cudaStream_t s) {
+  // an operand without a lo half has it computed in-kernel (TF32 only, one operand)
+  const int conv = a.lo == nullptr ? 1 : b.lo == nullptr ? 2 : 0;
+  if (conv && (kind != TcKind::TF32 || (a.lo == nullptr && b.lo == nullptr)))
+    return fail(MTNN_EINVAL, "in-kernel lo split needs the TF32 kind and one prepared operand");
   const DeviceInfo* di = nullptr;
   MTNN_TRY(device_info(&di));
   constexpr int BN = 256;
@@ -725,11 +823,7 @@ int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t 
   p.tiles_n = (int)((n + BN - 1) / BN);
   p.total_kblocks = (int)((k + bk - 1) / bk);
   const int tiles = p.tiles_m * p.tiles_n;
-  int splits = 1;
-  if (tiles < di->sm_count && p.total_kblocks >= 16) {
-    splits = std::min((di->sm_count + tiles - 1) / tiles, p.total_kblocks / 8);
-    splits = std::max(1, std::min(splits, 32));
-  }
+  int splits = choose_splits(tiles, p.total_kblocks, m, n, di->sm_count);
   p.kblocks_per_split = (p.total_kblocks + splits - 1) / splits;
   splits = (p.total_kblocks + p.kblocks_per_split - 1) / p.kblocks_per_split;
   p.splits = splits;
@@ -746,6 +840,12 @@ int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t 
   if (kind == TcKind::F16S)
     rc = b_is_nk ? tc::launch_impl<BN, false, tc::KindF16S>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s)
                  : tc::launch_impl<BN, true, tc::KindF16S>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s);
+  else if (conv == 1)
+    rc = b_is_nk ? tc::launch_impl<BN, false, tc::KindTF32, 1>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s)
+                 : tc::launch_impl<BN, true, tc::KindTF32, 1>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s);
+  else if (conv == 2)
+    rc = b_is_nk ? tc::launch_impl<BN, false, tc::KindTF32, 2>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s)
+                 : tc::launch_impl<BN, true, tc::KindTF32, 2>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s);
   else
     rc = b_is_nk ? tc::launch_impl<BN, false, tc::KindTF32>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s)
                  : tc::launch_impl<BN, true, tc::KindTF32>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s);
@@ -762,8 +862,9 @@ int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t 
                 (long long)m, (long long)n, (long long)k);
   ScratchBuffer wa, wb;
   TcOperand a{}, b{};
-  MTNN_TRY(tc_prepare(A, m, k, false, kind, wa, &a, s));
-  MTNN_TRY(tc_prepare(B, n, k, !b_is_nk, kind, wb, &b, s));
+  const int conv = kind == TcKind::TF32 ? tf32_inkernel_operand(m, n) : 0;
+  if (conv == 1) a.hi = A; else MTNN_TRY(tc_prepare(A, m, k, false, kind, wa, &a, s));
+  if (conv == 2) b.hi = B; else MTNN_TRY(tc_prepare(B, n, k, !b_is_nk, kind, wb, &b, s));
   return tc_run(a, b, C, m, n, k, b_is_nk, kind, s);
 }
 

@@ -261,3 +261,29 @@ class TestPipelinedHostPath:
         assert rel_frobenius(got[rows], want) < FP32_GATE
         dev = gemm_nt(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy()
         assert rel_frobenius(gemm_nt(a, b), dev) < 1e-6
+
+
+def test_tf32_inkernel_split_opt_in(tmp_path):
+    """MTNN_TF32_INKERNEL=1: the TF32 kernel computes the larger operand's lo half
+    in shared memory; results stay within the FP32 gate (fresh process: the
+    switch is read once)."""
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    code = (
+        "import numpy as np, oracle\n"
+        "from paper_1702_03192_b200 import gemm_nt, gemm_nn\n"
+        "rng = np.random.default_rng(3)\n"
+        "for m, n, k in ((1024, 256, 2048), (256, 1024, 2048), (2048, 2048, 512)):\n"
+        "    a = rng.uniform(-1, 1, (m, k)).astype(np.float32)\n"
+        "    b = rng.uniform(-1, 1, (n, k)).astype(np.float32)\n"
+        "    want = oracle.oracle_nt_blas(a, b)\n"
+        "    assert oracle.rel_frobenius(gemm_nt(a, b, variant='tc3xtf32'), want) < 1e-5\n"
+        "    assert oracle.rel_frobenius(gemm_nn(a, np.ascontiguousarray(b.T), variant='tc3xtf32'), want) < 1e-5\n"
+        "print('ok')\n")
+    env = dict(__import__("os").environ, MTNN_TF32_INKERNEL="1", PYTHONPATH=str(ROOT))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         cwd=str(ROOT), timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr
