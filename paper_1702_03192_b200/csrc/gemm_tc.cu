@@ -800,15 +800,11 @@ static int choose_splits(int tiles, int kblocks, int64_t m, int64_t n, int sms) 
   return best;
 }
 
-int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n, int64_t k,
-           bool b_is_nk, TcKind kind, cudaStream_t s) {
-  // an operand without a lo half has it computed in-kernel (TF32 only, one operand)
-  const int conv = a.lo == nullptr ? 1 : b.lo == nullptr ? 2 : 0;
-  if (conv && (kind != TcKind::TF32 || (a.lo == nullptr && b.lo == nullptr)))
-    return fail(MTNN_EINVAL, "in-kernel lo split needs the TF32 kind and one prepared operand");
+template <int BN>
+static int tc_run_bn(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n,
+                     int64_t k, bool b_is_nk, TcKind kind, int conv, cudaStream_t s) {
   const DeviceInfo* di = nullptr;
   MTNN_TRY(device_info(&di));
-  constexpr int BN = 256;
   using S = tc::Smem<BN>;
   if (di->max_smem_optin < S::kTotal)
     return fail(MTNN_ENOTSUP, "tensor-core GEMM needs %d B smem, device allows %d", S::kTotal,
@@ -852,6 +848,18 @@ int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t 
   MTNN_TRY(rc);
   if (splits > 1) MTNN_TRY(launch_splitk_reduce(out, C, m * n, splits, s));
   return MTNN_OK;
+}
+
+// N tile: 256 (UMMA N=256, best smem-read/MMA ratio) unless n <= 128, where a
+// 256-wide tile would waste half its MMAs on zero columns.
+int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n, int64_t k,
+           bool b_is_nk, TcKind kind, cudaStream_t s) {
+  // an operand without a lo half has it computed in-kernel (TF32 only, one operand)
+  const int conv = a.lo == nullptr ? 1 : b.lo == nullptr ? 2 : 0;
+  if (conv && (kind != TcKind::TF32 || (a.lo == nullptr && b.lo == nullptr)))
+    return fail(MTNN_EINVAL, "in-kernel lo split needs the TF32 kind and one prepared operand");
+  if (n <= 128) return tc_run_bn<128>(a, b, C, m, n, k, b_is_nk, kind, conv, s);
+  return tc_run_bn<256>(a, b, C, m, n, k, b_is_nk, kind, conv, s);
 }
 
 int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t n,

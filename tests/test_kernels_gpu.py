@@ -287,3 +287,16 @@ def test_tf32_inkernel_split_opt_in(tmp_path):
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                          cwd=str(ROOT), timeout=300)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr
+
+
+@pytest.mark.parametrize("shape", [(1000, 128, 512), (4096, 64, 1024), (300, 112, 2048), (2048, 16, 256)])
+def test_narrow_n_tile(rng, shape):
+    """n <= 128 runs the BN=128 tile (no half-empty N=256 tiles); every variant
+    and both B layouts stay within the FP32 gate."""
+    m, n, k = shape
+    a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+    want = oracle.oracle_nt_blas(a, b)
+    for v in ("tc3xf16s", "tc3xtf32"):
+        assert rel_frobenius(gemm_nt(a, b, variant=v), want) < FP32_GATE
+        if n % 16 == 0:
+            assert rel_frobenius(gemm_nn(a, np.ascontiguousarray(b.T), variant=v), want) < FP32_GATE
