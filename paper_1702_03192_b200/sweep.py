@@ -9,8 +9,9 @@ and median (:129-146), and the timings CSV wire format ``m,n,k,t_nn,t_nt,t_tnn``
 ``fit_gbdt``), so the reference learner retrains unchanged on B200 labels.
 
 Timing: CUDA events on the launching stream around each call, an L2 flush
-(a 256 MiB write, > the 126 MB L2) before every timed call, inputs resident in
-HBM. TNN's window includes its stream-ordered B^T allocation, transpose and
+(a 256 MiB read, > the 126 MB L2, leaving no dirty lines to write back) and a
+short GPU spin (so the host's enqueue gaps stay outside the window) before every
+timed call, inputs resident in HBM. TNN's window includes its stream-ordered B^T allocation, transpose and
 release (reference _numba_impl.py:16-19); the NN time uses a
 pre-transposed B^T, as the reference's does (bench.py:208-229).
 """
@@ -28,6 +29,9 @@ from . import _lib
 from . import device
 
 TIMING_HEADER = ("m", "n", "k", "t_nn", "t_nt", "t_tnn")
+# wire contracts shared with the reference learner (bench.py:34-38)
+SAMPLE_HEADER = ("gm", "sm", "cc", "mbw", "l2c", "m", "n", "k", "label")
+RECORD_HEADER = ("m", "n", "k", "p_nn", "p_nt", "p_tnn", "t_nt", "t_tnn")
 
 
 def grid_shapes(exponents):
@@ -45,7 +49,7 @@ class Operands:
         self.b = torch.rand(max_n * max_k, device=dev, generator=g).mul_(2).sub_(1)
         self.bt = torch.empty(max_n * max_k, device=dev)
         self.c = torch.empty(max_m * max_n, device=dev)
-        self.flush_buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+        self.flush_buf = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device=dev)
 
     def views(self, m, n, k):
         a = self.a[: m * k].view(m, k)
@@ -54,7 +58,8 @@ class Operands:
         return a, b, c
 
     def flush(self):
-        self.flush_buf.fill_(1.0)
+        self.flush_buf.sum()
+        torch.cuda._sleep(200_000)
 
 
 def time_calls(fns: dict, ops: Operands, reps: int, warmup: int) -> dict:
@@ -120,6 +125,47 @@ def write_timings_csv(path, rows):
         w.writerow(TIMING_HEADER)
         for r in rows:
             w.writerow([r.m, r.n, r.k, repr(r.t_nn), repr(r.t_nt), repr(r.t_tnn)])
+
+
+def gflops(m, n, k, seconds):
+    if not seconds > 0:
+        raise ValueError(f"duration must be positive, got {seconds}")
+    return 2.0 * m * n * k / (seconds * 1e9)
+
+
+def record_of(r: CaseTiming) -> tuple:
+    """(m, n, k, p_nn, p_nt, p_tnn, t_nt, t_tnn) — the reference BenchRecord row."""
+    return (r.m, r.n, r.k, gflops(r.m, r.n, r.k, r.t_nn), gflops(r.m, r.n, r.k, r.t_nt),
+            gflops(r.m, r.n, r.k, r.t_tnn), r.t_nt, r.t_tnn)
+
+
+def label_of(r: CaseTiming) -> int:
+    """+1 (NT) iff p_nt - p_tnn >= 0, else -1 (TNN) — reference bench.py:296-303."""
+    rec = record_of(r)
+    return 1 if rec[4] - rec[5] >= 0 else -1
+
+
+def write_records_csv(path, rows):
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(RECORD_HEADER)
+        for r in rows:
+            w.writerow(list(record_of(r)))
+
+
+def write_samples_csv(path, rows, platform):
+    """Training samples (5 platform features + m, n, k, label), floats as repr."""
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(SAMPLE_HEADER)
+        for r in rows:
+            feats = tuple(platform.as_tuple()) + (float(r.m), float(r.n), float(r.k))
+            w.writerow([repr(float(v)) for v in feats] + [label_of(r)])
+
+
+def rows_from_timings(timings: dict) -> list:
+    """CaseTiming rows from {(m, n, k): (t_nn, t_nt, t_tnn)} (injected timings)."""
+    return [CaseTiming(m, n, k, *t) for (m, n, k), t in timings.items()]
 
 
 def read_timings_csv(path):

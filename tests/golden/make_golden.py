@@ -168,6 +168,35 @@ def main():
         ops[f"shape{i}"] = np.array(shape + (seed,))
         ops[f"a{i}"], ops[f"b{i}"], ops[f"bkn{i}"] = a, b, b_kn
     np.savez_compressed(OUT / "operands.npz", **ops)
+    # ------------------------------------------------------------- evaluation layer
+    from mtnn import metrics
+
+    ev = {}
+    for i, n_cases in enumerate((40, 7)):
+        p = rng.uniform(1.0, 400.0, size=(n_cases, 3))
+        p[::5, 2] = p[::5, 0]          # some cases equal to a branch (copied mode)
+        p[1, 2] = 2.5 * p[1, 0]        # >= 2.0 histogram bucket
+        cases = [metrics.EvalCase(shape=mtnn.ProblemShape(1, 1, 1), p_nt=a_, p_tnn=b_, p_mtnn=c_)
+                 for a_, b_, c_ in p]
+        rep = metrics.aggregate(cases, p_mtnn_mode="copied" if i else "remeasured")
+        ev[f"p{i}"] = p
+        ev[f"vals{i}"] = np.array([rep.mtnn_vs_nt, rep.mtnn_vs_tnn, rep.gow_avg, rep.gow_max,
+                                   rep.lub_avg, rep.lub_min])
+        ev[f"hist{i}"] = np.array(rep.ratio_histogram)
+        (OUT / f"report{i}.txt").write_text(metrics.render_report(rep) + "\n")
+    np.savez_compressed(OUT / "evaluate.npz", **ev)
+    # records / samples CSV wire formats from injected (synthetic) timings
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as td:
+        injected = {tuple(s): bench.synthetic_timings(s) for s in bench.grid_shapes(range(5, 8))}
+        recs = bench.sweep_grid(range(5, 8), plat_a, injected=injected)
+        bench.write_records_csv(f"{td}/r.csv", recs)
+        bench.write_samples_csv(f"{td}/s.csv", bench.label_records(recs, plat_a))
+        bench.write_timings_csv(f"{td}/t.csv", range(5, 8))
+        for name in ("r", "s", "t"):
+            (OUT / f"wire_{name}.csv").write_text(open(f"{td}/{name}.csv").read())
+
     meta = {"reference": str(REF), "backend": mtnn.active_backend(),
             "numpy": np.__version__, "models": sorted(models)}
     (OUT / "MANIFEST.json").write_text(json.dumps(meta, indent=1))
