@@ -87,6 +87,18 @@ int mtnn_profile_enable(int on);
 int mtnn_profile_reset(void);
 int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* work);
 
+/* ---- tuning knobs (no reference counterpart; the reference's block/tile
+ * hints, kernels/__init__.py:41-42, are the closest analogue) -------------
+ * "f16s_inkernel_max_short": tc3xf16s splits the long operand inside the GEMM
+ *   (no split pass; a read-only row-max pass gives the row scales) when the
+ *   output's short side is at most this and its long side >= 1024; 0 disables.
+ *   Default 256, the best on the B200 sweep (env MTNN_F16S_INKERNEL_MAX,
+ *   MTNN_F16S_INKERNEL=0 disables). The halves equal the split pass's; only
+ *   the output tiling (and so the split-K order) may differ. Unknown keys ->
+ *   MTNN_EINVAL. */
+int mtnn_config_set(const char* key, int64_t value);
+int mtnn_config_get(const char* key, int64_t* value);
+
 /* ---- device-resident kernels ----------------------------------------- */
 /* C = A x B^T directly. Replaces _impl.gemm_nt / gemm_nt_parallel
  * (_numba_impl.py:139-166; caller kernels/__init__.py:105-116). */

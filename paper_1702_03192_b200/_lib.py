@@ -68,6 +68,8 @@ def _load():
         "mtnn_profile_enable": (c_int, [c_int]),
         "mtnn_profile_reset": (c_int, []),
         "mtnn_profile_read": (c_int, [c_int, _DP, _I64P, _DP]),
+        "mtnn_config_set": (c_int, [c_char_p, c_int64]),
+        "mtnn_config_get": (c_int, [c_char_p, _I64P]),
         "mtnn_gemm_nt": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p]),
         "mtnn_gemm_nn": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p]),
         "mtnn_transpose": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p]),
@@ -127,6 +129,16 @@ def profile_read(kclass: int):
     ms, n, w = ctypes.c_double(), c_int64(), ctypes.c_double()
     check(lib.mtnn_profile_read(kclass, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(w)))
     return ms.value, n.value, w.value
+
+
+def config_set(key: str, value: int) -> None:
+    check(lib.mtnn_config_set(key.encode(), int(value)))
+
+
+def config_get(key: str) -> int:
+    v = c_int64()
+    check(lib.mtnn_config_get(key.encode(), ctypes.byref(v)))
+    return v.value
 
 
 def exported_symbols() -> list[str]:

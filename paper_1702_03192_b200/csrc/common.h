@@ -81,13 +81,21 @@ struct TcOperand {
   const float* inv_scale = nullptr;
 };
 struct ScratchBuffer;
+// inkernel: the operand is split inside the GEMM from its raw rows (hi = X,
+// lo = nullptr); F16S then only computes the row scales (read-only pass).
 int tc_prepare(const float* X, int64_t rows, int64_t k, bool mn_major, TcKind kind,
-               ScratchBuffer& ws, TcOperand* out, cudaStream_t s);
-int tf32_inkernel_operand(int64_t m, int64_t n);
+               bool inkernel, ScratchBuffer& ws, TcOperand* out, cudaStream_t s);
+// Which operand (1 = A, 2 = B, 0 = none) the GEMM splits in-kernel for this shape.
+int tc_inkernel_operand(int64_t m, int64_t n, bool b_is_nk, TcKind kind);
+// Run-time knob (mtnn_config_set): largest output short side split in-kernel.
+int64_t f16s_inkernel_max_short();
+void set_f16s_inkernel_max_short(int64_t v);
 int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n, int64_t k,
            bool b_is_nk, TcKind kind, cudaStream_t s);
 int launch_split_rows_f16(const float* x, void* hi, void* lo, float* inv_scale, int64_t rows,
                           int64_t k, cudaStream_t s);
+// 1/s per row (s = split_rows_f16's power-of-two row scale), reading x only.
+int launch_rowmax_f16(const float* x, float* inv_scale, int64_t rows, int64_t k, cudaStream_t s);
 int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,
                           unsigned* colmax_scratch, int64_t k, int64_t n, cudaStream_t s);
 

@@ -26,10 +26,12 @@
 // host splits K so the grid reaches all SMs and a deterministic reduction kernel
 // sums the fp32 partials.
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <mutex>
 #include <stdlib.h>
@@ -49,6 +51,17 @@ constexpr int kStages = 4;
 constexpr int kEpiWarp0 = 4;      // warps 0..3: TMA, MMA, TMEM alloc, spare
 constexpr int kEpiWarps = 16;     // 4 TMEM lane quarters x 4 column quarters
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
+// Warp roles. F16S in-kernel conversion (kConv != 0, BN = 128): 8 epilogue
+// warps (4 lane quarters x 2 column halves) and 8 converter warps (two groups
+// of 4 taking alternate k-blocks, one thread per row of the converted tile).
+constexpr int kF16ConvRows = 128;
+template <bool kF16Conv>
+struct Roles {
+  static constexpr int kEpi = kF16Conv ? 8 : kEpiWarps;
+  static constexpr int kConvWarps = kF16Conv ? 8 : 0;
+  static constexpr int kConv0 = kEpiWarp0 + kEpi;  // first converter warp
+  static constexpr int kThreads = 32 * (kEpiWarp0 + kEpi + kConvWarps);
+};
 constexpr uint32_t kLayoutSW64 = 4;      // UMMA SWIZZLE_64B
 
 // Operand kinds. Both keep 64-byte K-major rows per k-block (SWIZZLE_64B, one
@@ -81,21 +94,42 @@ struct KindF16S {  // per-row power-of-2 scaled fp16 hi/lo (split_f16.cu)
   static constexpr CUtensorMapSwizzle kMnSwizzle = CU_TENSOR_MAP_SWIZZLE_128B;
 };
 
-template <int BN>
+// kRawBytes: slot size of the raw fp32 tile of an operand converted in-kernel
+// (F16S, kConv != 0): 128 rows x 32 k x 4 B, TMA SWIZZLE_128B. Those tiles get
+// their own deeper ring (kRawStages) so more DRAM bytes are in flight per SM
+// than the 3-stage h/l ring alone would allow — the converted operand streams
+// from DRAM, the other one from L2.
+template <int BN, int kRawBytes = 0, int kEpi = kEpiWarps>
 struct Smem {
   static constexpr int kABytes = BM * 64;                // 8 KiB (64-byte k-block rows)
   static constexpr int kBBytes = BN * 64;                // 16 KiB at BN=256
+  static constexpr int kStages = kRawBytes ? 3 : 4;      // h/l ring
+  static constexpr int kRawStages = kRawBytes ? 7 : 0;   // raw fp32 ring
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
   static constexpr int kStagingBytes = 32 * 16 * 4;      // one 32x16 fp32 tile
   static constexpr int kRingBytes = kStages * kStageBytes;
-  static constexpr int kEpiBytes = kEpiWarps * kStagingBytes;
+  static constexpr int kRawOff = kRingBytes;             // 1024-aligned
+  static constexpr int kRawRingBytes = kRawStages * kRawBytes;
+  static constexpr int kEpiBytes = kEpi * kStagingBytes;
   static constexpr int kBarBytes = 256;
-  static constexpr int kTotal = 1024 + kRingBytes + kEpiBytes + kBarBytes;
+  static constexpr int kTotal = 1024 + kRingBytes + kRawRingBytes + kEpiBytes + kBarBytes;
 };
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ float4 lds128f(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, const uint4& v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
 }
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
@@ -274,36 +308,79 @@ __device__ __forceinline__ void unit_coords(int u, const Params& p, int& split, 
   tn = r / gm;
 }
 
+// FP16 hi/lo of 8 consecutive k-values of one row with the row's exact
+// power-of-two scale s — the same operations as split_f16.cu's split2, so the
+// halves (and every C bit) equal the pre-split path's.
+__device__ __forceinline__ void split8_f16(const float4& x0, const float4& x1, float s,
+                                          uint4& hw, uint4& lw) {
+  const float v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+  uint32_t hp[4], lp[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    // packed round-to-nearest conversions: per element identical to
+    // __float2half_rn, two per instruction
+    const float a = v[2 * i] * s, b = v[2 * i + 1] * s;
+    const __half2 h2 = __floats2half2_rn(a, b);
+    const float2 hf = __half22float2(h2);
+    const __half2 l2 = __floats2half2_rn(a - hf.x, b - hf.y);
+    hp[i] = *reinterpret_cast<const uint32_t*>(&h2);
+    lp[i] = *reinterpret_cast<const uint32_t*>(&l2);
+  }
+  hw = make_uint4(hp[0], hp[1], hp[2], hp[3]);
+  lw = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+}
+
 // ------------------------------------------------------------------- kernel
-// kConv (KindTF32 only): 0 = both lo halves come from the pre-pass; 1 / 2 = the
-// lo half of A / B is computed in-kernel from the raw tile TMA just landed:
-// lo = x - trunc_tf32(x) is elementwise, so writing it at the same offsets of
-// the lo tile keeps the swizzled UMMA layout. Warps 2-3 (idle after TMEM
-// allocation) do it; the MMA warp then waits on conv_bar instead of full_bar.
-// That operand is read from DRAM once (4 B per element) and needs no pre-pass.
+// kConv: 0 = both operands come split from the pre-pass; 1 / 2 = operand A / B
+// is read raw (fp32, 4 B per element from DRAM, no split pass) and split
+// in-kernel from the tile TMA just landed; the MMA warp then waits on conv_bar
+// instead of full_bar.
+//   KindTF32: lo = x - trunc_tf32(x) is elementwise, written at the same offsets
+//     of the lo tile (the raw tile itself is hi); warps 2-3 (idle after TMEM
+//     allocation) do it.
+//   KindF16S: the raw tile lands in its own SWIZZLE_128B slot and 4 extra warps
+//     (one thread per tile row, kF16ConvRows = 128 = the converted tile's rows)
+//     write h/l into the operand's SWIZZLE_64B slots with the row scale from a
+//     read-only row-max pre-pass (4 B per element instead of the split's 8).
 template <int BN, bool B_MN, class Kind, int kConv>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Roles<kConv != 0 && Kind::kScaled>::kThreads, 1)
 gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
                      const __grid_constant__ CUtensorMap map_alo,
                      const __grid_constant__ CUtensorMap map_bhi,
                      const __grid_constant__ CUtensorMap map_blo,
                      const __grid_constant__ CUtensorMap map_c, const Params p) {
-  using S = Smem<BN>;
-  constexpr int kColsPerWarp = BN / 4;  // each epilogue warp owns a column quarter
+  constexpr bool kF16Conv = kConv != 0 && Kind::kScaled;
+  static_assert(!kF16Conv || (kConv == 1 ? BM : BN) == kF16ConvRows,
+                "F16S in-kernel conversion needs a 128-row converted tile");
+  static_assert(!(kF16Conv && kConv == 2 && B_MN), "in-kernel F16S split of B needs K-major B (NT)");
+  using R = Roles<kF16Conv>;
+  using S = Smem<BN, kF16Conv ? kF16ConvRows * 128 : 0, R::kEpi>;
+  constexpr int kColsPerWarp = BN / (R::kEpi / 4);  // each epilogue warp: a column slice
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int kStages = S::kStages;
+  constexpr int kRawStages = S::kRawStages;
+  static_assert(3 * kStages + 4 + 2 * kRawStages <= S::kBarBytes / 8 - 1, "barrier space");
   uint8_t* ring = smem;
-  uint8_t* epi = smem + S::kRingBytes;
+  uint8_t* raw_ring = smem + S::kRawOff;
+  uint8_t* epi = smem + S::kRingBytes + S::kRawRingBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(epi + S::kEpiBytes);
   uint64_t* full_bar = bars;                 // [kStages]
   uint64_t* empty_bar = bars + kStages;      // [kStages]
   uint64_t* tfull_bar = bars + 2 * kStages;  // [2]
   uint64_t* tempty_bar = bars + 2 * kStages + 2;  // [2]
   uint64_t* conv_bar = bars + 2 * kStages + 4;     // [kStages] (kConv != 0)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kStages + 4);
-  static_assert(kConv == 0 || !Kind::kScaled, "in-kernel lo split is TF32-only");
+  uint64_t* rfull_bar = bars + 3 * kStages + 4;    // [kRawStages] (F16S conversion)
+  uint64_t* rempty_bar = rfull_bar + kRawStages;   // [kRawStages]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty_bar + kRawStages);
+  // TMA bytes per h/l stage: F16S conversion loads only the other operand's
+  // halves (the raw tile arrives on its own ring); TF32 conversion skips the
+  // converted lo slot.
   constexpr int kConvBytes = kConv == 1 ? S::kABytes : kConv == 2 ? S::kBBytes : 0;
+  constexpr int kExpectBytes = kF16Conv ? S::kStageBytes - 2 * kConvBytes
+                                        : S::kStageBytes - kConvBytes;
+  constexpr int kRawTileBytes = kF16ConvRows * 128;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -322,9 +399,14 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(smem_u32(&tfull_bar[s]), 1);
-      mbar_init(smem_u32(&tempty_bar[s]), kEpiWarps);  // one arrive per epilogue warp
+      mbar_init(smem_u32(&tempty_bar[s]), R::kEpi);  // one arrive per epilogue warp
     }
-    for (int s = 0; s < kStages; ++s) mbar_init(smem_u32(&conv_bar[s]), 2);  // warps 2, 3
+    for (int s = 0; s < kStages; ++s)
+      mbar_init(smem_u32(&conv_bar[s]), kF16Conv ? R::kConvWarps / 2 : 2);  // one converter group
+    for (int s = 0; s < kRawStages; ++s) {
+      mbar_init(smem_u32(&rfull_bar[s]), 1);
+      mbar_init(smem_u32(&rempty_bar[s]), R::kConvWarps / 2);
+    }
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -353,12 +435,16 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
           const uint32_t fb = smem_u32(&full_bar[stage]);
-          mbar_expect_tx(fb, S::kStageBytes - kConvBytes);
+          mbar_expect_tx(fb, kExpectBytes);
           uint8_t* st = ring + stage * S::kStageBytes;
           const int kx = kb * Kind::BK;
-          tma_load_2d(smem_u32(st), &map_ahi, fb, kx, tm * BM);
-          if (kConv != 1) tma_load_2d(smem_u32(st + S::kABytes), &map_alo, fb, kx, tm * BM);
-          if (!B_MN) {
+          if (!(kF16Conv && kConv == 1)) {  // (raw A: warp 3)
+            tma_load_2d(smem_u32(st), &map_ahi, fb, kx, tm * BM);
+            if (kConv != 1) tma_load_2d(smem_u32(st + S::kABytes), &map_alo, fb, kx, tm * BM);
+          }
+          if (kF16Conv && kConv == 2) {
+            // raw B: warp 3
+          } else if (!B_MN) {
             tma_load_2d(smem_u32(st + 2 * S::kABytes), &map_bhi, fb, kx, tn * BN);
             if (kConv != 2)
               tma_load_2d(smem_u32(st + 2 * S::kABytes + S::kBBytes), &map_blo, fb, kx, tn * BN);
@@ -395,7 +481,10 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
         for (int kb = kc; kb < kce; ++kb) {
-          mbar_wait(smem_u32(kConv ? &conv_bar[stage] : &full_bar[stage]), phase);
+          // TF32 conversion waits full_bar itself, so conv_bar implies it; the F16S
+          // converters do not (the raw tile has its own ring)
+          if (kConv == 0 || kF16Conv) mbar_wait(smem_u32(&full_bar[stage]), phase);
+          if (kConv != 0) mbar_wait(smem_u32(&conv_bar[stage]), phase);
           tc_fence_after();
           if (elect_one()) {
             uint8_t* st = ring + stage * S::kStageBytes;
@@ -433,7 +522,84 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else if (kConv != 0 && (warp == 2 || warp == 3)) {
+  } else if (kF16Conv && warp == 3) {
+    // ===================== TMA producer of the raw (converted) operand =====================
+    if (elect_one()) {
+      int rs = 0;
+      uint32_t rphase = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        int split, tm, tn;
+        unit_coords(u, p, split, tm, tn);
+        const int kb0 = split * kb_per;
+        const int kb1 = min(p.total_kblocks, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(smem_u32(&rempty_bar[rs]), rphase ^ 1);
+          const uint32_t fb = smem_u32(&rfull_bar[rs]);
+          mbar_expect_tx(fb, kRawTileBytes);
+          const uint32_t dst = smem_u32(raw_ring + rs * kRawTileBytes);
+          if (kConv == 1) tma_load_2d(dst, &map_ahi, fb, kb * Kind::BK, tm * BM);
+          else tma_load_2d(dst, &map_bhi, fb, kb * Kind::BK, tn * BN);
+          if (++rs == kRawStages) { rs = 0; rphase ^= 1; }
+        }
+      }
+    }
+  } else if (kF16Conv && warp >= R::kConv0) {
+    // ===================== in-kernel FP16 split (F16S, one operand) =====================
+    // Two groups of 4 warps take alternate k-blocks, so each group's serial
+    // chain (raw wait, LDS, convert, h/l-slot wait, STS, proxy fence, arrive)
+    // has two MMA k-blocks of time. Thread r of a group owns row r of the
+    // converted tile: reads its 128-byte raw row (SWIZZLE_128B: 16-byte chunk c at
+    // c ^ (r & 7)) and writes 64-byte h and l rows (SWIZZLE_64B: chunk c at
+    // c ^ ((r >> 1) & 3)); both patterns keep each warp's 16-byte accesses
+    // conflict-free.
+    const int t = threadIdx.x - 32 * R::kConv0;
+    const int r = t % kF16ConvRows;             // tile row
+    const int grp = t / kF16ConvRows;           // k-block parity this thread converts
+    const int sw128 = r & 7, sw64 = (r >> 1) & 3;
+    const float* inv = kConv == 1 ? p.inv_scale_a : p.inv_scale_b;
+    const int64_t nrows = kConv == 1 ? p.m : p.n;
+    int stage = 0, rs = 0, parity = 0;
+    uint32_t phase = 0, rphase = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      int split, tm, tn;
+      unit_coords(u, p, split, tm, tn);
+      const int64_t row = (int64_t)(kConv == 1 ? tm * BM : tn * BN) + r;
+      const float sc = row < nrows ? 1.f / __ldg(inv + row) : 1.f;  // exact: powers of two
+      const int kb0 = split * kb_per;
+      const int kb1 = min(p.total_kblocks, kb0 + kb_per);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        if (parity == grp) {
+          // raw tile -> registers -> halves; the raw slot is released as soon as
+          // its values are consumed, before waiting for the h/l slot
+          mbar_wait(smem_u32(&rfull_bar[rs]), rphase);
+          const uint32_t raw = smem_u32(raw_ring + rs * kRawTileBytes) + r * 128;
+          float4 x[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) x[j] = lds128f(raw + ((j ^ sw128) << 4));
+          uint4 hw[4], lw[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) split8_f16(x[2 * j], x[2 * j + 1], sc, hw[j], lw[j]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&rempty_bar[rs]));
+          mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);  // MMA done with the h/l slot
+          const uint32_t hrow = smem_u32(ring + stage * S::kStageBytes) +
+                                (kConv == 1 ? 0 : 2 * S::kABytes) + r * 64;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t off = (j ^ sw64) << 4;
+            sts128(hrow + off, hw[j]);
+            sts128(hrow + kConvBytes + off, lw[j]);
+          }
+          fence_proxy_async_smem();  // generic-proxy smem writes -> visible to UMMA
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&conv_bar[stage]));
+        }
+        parity ^= 1;
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        if (++rs == kRawStages) { rs = 0; rphase ^= 1; }
+      }
+    }
+  } else if (kConv != 0 && !Kind::kScaled && (warp == 2 || warp == 3)) {
     // ===================== in-kernel lo split (TF32, one operand) =====================
     const int t = threadIdx.x - 64;  // 0..63
     int stage = 0;
@@ -468,7 +634,7 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
     // chunk is then added into round-to-nearest FP32 register sums here.
     const int e = warp - kEpiWarp0;
     const int q = warp % 4;             // TMEM lane quarter this warp may access
-    const int h = e / 4;                // column quarter
+    const int h = e / 4;                // column slice
     uint8_t* stg = epi + e * S::kStagingBytes;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -625,19 +791,37 @@ template <int BN, bool B_MN, class Kind, int kConv = 0>
 static int launch_impl(const void* ahi, const void* alo, const void* bhi,
                        const void* blo, float* out, const Params& p, int grid,
                        cudaStream_t s) {
-  using S = Smem<BN>;
+  constexpr bool kF16Conv = kConv != 0 && Kind::kScaled;
+  using S = Smem<BN, kF16Conv ? kF16ConvRows * 128 : 0, Roles<kF16Conv>::kEpi>;
+  constexpr int kNumThreads = Roles<kF16Conv>::kThreads;
   CUtensorMap mah, mal, mbh, mbl, mc;
-  encode_dtype = Kind::kTmaType;
   const uint64_t eb = Kind::kElemBytes;
-  {
+  // F16S operand converted in-kernel: its fp32 rows as [BK k][128 rows] boxes
+  // of 128-byte rows (SWIZZLE_128B), into the stage's raw slot
+  auto encode_raw = [&](CUtensorMap* map, const void* base, int64_t rows) {
+    encode_dtype = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const uint64_t dims[2] = {(uint64_t)p.k, (uint64_t)rows};
+    const uint64_t str[1] = {(uint64_t)p.k * 4};
+    const uint32_t box[2] = {(uint32_t)Kind::BK, (uint32_t)kF16ConvRows};
+    return encode(map, base, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+  };
+  encode_dtype = Kind::kTmaType;
+  if (kF16Conv && kConv == 1) {
+    MTNN_TRY(encode_raw(&mah, ahi, p.m));
+    mal = mah;  // never used
+  } else {
     const uint64_t dims[2] = {(uint64_t)p.k, (uint64_t)p.m};
     const uint64_t str[1] = {(uint64_t)p.k * eb};
     const uint32_t box[2] = {(uint32_t)Kind::BK, BM};
     MTNN_TRY(encode(&mah, ahi, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
     MTNN_TRY(encode(&mal, alo ? alo : ahi, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
   }
+  encode_dtype = Kind::kTmaType;
   if (!blo) blo = bhi;  // computed in-kernel (kConv == 2): the map is never used
-  if (!B_MN) {
+  if (kF16Conv && kConv == 2) {
+    MTNN_TRY(encode_raw(&mbh, bhi, p.n));
+    mbl = mbh;
+  } else if (!B_MN) {
     const uint64_t dims[2] = {(uint64_t)p.k, (uint64_t)p.n};
     const uint64_t str[1] = {(uint64_t)p.k * eb};
     const uint32_t box[2] = {(uint32_t)Kind::BK, BN};
@@ -667,7 +851,7 @@ static int launch_impl(const void* ahi, const void* alo, const void* bhi,
   {
     KernelTimer timer(Kind::kScaled ? MTNN_KCLASS_GEMM_TC_F16S : MTNN_KCLASS_GEMM_TC,
                       2.0 * (double)p.m * (double)p.n * (double)p.k, s);
-    kern<<<grid, kThreads, S::kTotal, s>>>(mah, mal, mbh, mbl, mc, p);
+    kern<<<grid, kNumThreads, S::kTotal, s>>>(mah, mal, mbh, mbl, mc, p);
   }
   MTNN_CUDA_TRY(cudaGetLastError());
   return MTNN_OK;
@@ -702,13 +886,48 @@ static int chunk_kblocks(TcKind) {
 // Measured on the B200 it gains <= 3% on skinny shapes (which are bound by tile
 // waste and split-K waves, not split traffic) and costs ~22% on compute-bound
 // shapes (smem/ALU contention with the MMA), so it is off by default.
-int tf32_inkernel_operand(int64_t m, int64_t n) {
+static int tf32_inkernel_operand(int64_t m, int64_t n) {
   static const bool on = [] {
     const char* e = getenv("MTNN_TF32_INKERNEL");
     return e && e[0] == '1';
   }();
   if (!on) return 0;
   return m >= n ? 1 : 2;
+}
+
+// F16S kind: skinny problems (the output's short side <= 256 by default, the
+// long side >= 1024) read the long operand raw and split it in-kernel, so DRAM
+// sees 4 B (row-max pass) + 4 B (GEMM) per element of it instead of the split's
+// 8 B plus the GEMM's 4 B; those shapes are HBM-bound on that operand. Wide
+// problems keep the pre-split operands: each operand tile there is consumed by
+// many output tiles, so converting per tile would multiply the conversion work.
+// MTNN_F16S_INKERNEL=0 disables; MTNN_F16S_INKERNEL_MAX overrides the threshold.
+// mtnn_config_set("f16s_inkernel_max_short", v) changes it at run time.
+static std::atomic<int64_t> g_f16s_inkernel_max{-1};
+
+int64_t f16s_inkernel_max_short() {
+  int64_t v = g_f16s_inkernel_max.load(std::memory_order_relaxed);
+  if (v >= 0) return v;
+  const char* e = getenv("MTNN_F16S_INKERNEL");
+  const char* t = getenv("MTNN_F16S_INKERNEL_MAX");
+  const long long x = t ? atoll(t) : 0;
+  v = (e && e[0] == '0') ? 0 : (x > 0 ? x : 256);
+  g_f16s_inkernel_max.store(v, std::memory_order_relaxed);
+  return v;
+}
+
+void set_f16s_inkernel_max_short(int64_t v) { g_f16s_inkernel_max.store(v, std::memory_order_relaxed); }
+
+static int f16s_inkernel_operand(int64_t m, int64_t n, bool b_is_nk) {
+  const int64_t max_short = f16s_inkernel_max_short();
+  const int64_t lo = std::min(m, n), hi = std::max(m, n);
+  if (lo > max_short || hi < 1024) return 0;
+  if (m >= n) return 1;
+  return b_is_nk ? 2 : 0;  // B^T (MN-major) is always pre-split
+}
+
+int tc_inkernel_operand(int64_t m, int64_t n, bool b_is_nk, TcKind kind) {
+  return kind == TcKind::TF32 ? tf32_inkernel_operand(m, n) : f16s_inkernel_operand(m, n, b_is_nk);
 }
 
 bool tc_eligible(const float* A, const float* B, const float* C, int64_t m, int64_t n,
@@ -727,10 +946,25 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // Split one operand into its hi/lo halves (+ per-row scales for F16S).
 // K-major (rows x k: A, or B of NT) or MN-major (k x cols: B^T of NN).
 int tc_prepare(const float* X, int64_t rows, int64_t k, bool mn_major, TcKind kind,
-               ScratchBuffer& ws, TcOperand* out, cudaStream_t s) {
+               bool inkernel, ScratchBuffer& ws, TcOperand* out, cudaStream_t s) {
   const DeviceInfo* di = nullptr;
   MTNN_TRY(device_info(&di));
   const int64_t count = rows * k;  // MN-major: k x rows (rows = n)
+  if (inkernel) {
+    // split in-kernel from the raw rows (K-major only); F16S needs the row scales
+    if (mn_major && kind == TcKind::F16S)
+      return fail(MTNN_EINVAL, "in-kernel F16S split needs a K-major operand");
+    out->hi = X;
+    out->lo = nullptr;
+    out->inv_scale = nullptr;
+    if (kind == TcKind::F16S) {
+      MTNN_TRY(ws.alloc((size_t)rows * sizeof(float), s));
+      float* inv = static_cast<float*>(ws.ptr);
+      MTNN_TRY(launch_rowmax_f16(X, inv, rows, k, s));
+      out->inv_scale = inv;
+    }
+    return MTNN_OK;
+  }
   if (kind == TcKind::TF32) {
     const bool hi_copy = split_mode_hi_copy();
     MTNN_TRY(ws.alloc((size_t)((hi_copy ? 2 : 1) * count) * sizeof(float), s));
@@ -833,10 +1067,22 @@ static int tc_run_bn(const TcOperand& a, const TcOperand& b, float* C, int64_t m
     out = static_cast<float*>(part.ptr);
   }
   int rc;
-  if (kind == TcKind::F16S)
+  if (kind == TcKind::F16S && conv == 0)
     rc = b_is_nk ? tc::launch_impl<BN, false, tc::KindF16S>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s)
                  : tc::launch_impl<BN, true, tc::KindF16S>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s);
-  else if (conv == 1)
+  else if (conv != 0 && kind == TcKind::F16S) {
+    if constexpr (BN == tc::kF16ConvRows) {
+      if (conv == 1)
+        rc = b_is_nk ? tc::launch_impl<BN, false, tc::KindF16S, 1>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s)
+                     : tc::launch_impl<BN, true, tc::KindF16S, 1>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s);
+      else if (b_is_nk)
+        rc = tc::launch_impl<BN, false, tc::KindF16S, 2>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s);
+      else
+        rc = fail(MTNN_EINVAL, "in-kernel split of B^T (MN-major) is not supported");
+    } else {
+      rc = fail(MTNN_EINVAL, "in-kernel F16S split needs the 128-wide N tile");
+    }
+  } else if (conv == 1)
     rc = b_is_nk ? tc::launch_impl<BN, false, tc::KindTF32, 1>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s)
                  : tc::launch_impl<BN, true, tc::KindTF32, 1>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s);
   else if (conv == 2)
@@ -856,9 +1102,13 @@ int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t 
            bool b_is_nk, TcKind kind, cudaStream_t s) {
   // an operand without a lo half has it computed in-kernel (TF32 only, one operand)
   const int conv = a.lo == nullptr ? 1 : b.lo == nullptr ? 2 : 0;
-  if (conv && (kind != TcKind::TF32 || (a.lo == nullptr && b.lo == nullptr)))
-    return fail(MTNN_EINVAL, "in-kernel lo split needs the TF32 kind and one prepared operand");
-  if (n <= 128) return tc_run_bn<128>(a, b, C, m, n, k, b_is_nk, kind, conv, s);
+  if (conv && a.lo == nullptr && b.lo == nullptr)
+    return fail(MTNN_EINVAL, "in-kernel operand split needs one prepared operand");
+  if (conv && kind == TcKind::F16S && (conv == 1 ? a.inv_scale : b.inv_scale) == nullptr)
+    return fail(MTNN_EINVAL, "in-kernel F16S split needs the operand's row scales");
+  // F16S in-kernel split: 128-wide N tile (raw slot + 4-stage ring fit the smem)
+  if (n <= 128 || (conv && kind == TcKind::F16S))
+    return tc_run_bn<128>(a, b, C, m, n, k, b_is_nk, kind, conv, s);
   return tc_run_bn<256>(a, b, C, m, n, k, b_is_nk, kind, conv, s);
 }
 
@@ -870,9 +1120,9 @@ int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t 
                 (long long)m, (long long)n, (long long)k);
   ScratchBuffer wa, wb;
   TcOperand a{}, b{};
-  const int conv = kind == TcKind::TF32 ? tf32_inkernel_operand(m, n) : 0;
-  if (conv == 1) a.hi = A; else MTNN_TRY(tc_prepare(A, m, k, false, kind, wa, &a, s));
-  if (conv == 2) b.hi = B; else MTNN_TRY(tc_prepare(B, n, k, !b_is_nk, kind, wb, &b, s));
+  const int conv = tc_inkernel_operand(m, n, b_is_nk, kind);
+  MTNN_TRY(tc_prepare(A, m, k, false, kind, conv == 1, wa, &a, s));
+  MTNN_TRY(tc_prepare(B, n, k, !b_is_nk, kind, conv == 2, wb, &b, s));
   return tc_run(a, b, C, m, n, k, b_is_nk, kind, s);
 }
 

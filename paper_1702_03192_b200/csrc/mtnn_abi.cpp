@@ -321,11 +321,9 @@ static int host_gemm(const float* A, const float* B, float* C, int64_t m, int64_
     return fail(MTNN_ENOTSUP, "tensor-core variant not eligible for (%lld, %lld, %lld)",
                 (long long)m, (long long)n, (long long)k);
   TcOperand bp{};
-  const int conv = (tc && kind == TcKind::TF32) ? tf32_inkernel_operand(m, n) : 0;
-  if (tc) {
-    if (conv == 2) bp.hi = bop;
-    else MTNN_TRY(tc_prepare(bop, n, k, !b_is_nk, kind, wb, &bp, ps->comp));
-  }
+  // in-kernel split choice for the whole problem (chunks keep its operand roles)
+  const int conv = tc ? tc_inkernel_operand(m, n, b_is_nk, kind) : 0;
+  if (tc) MTNN_TRY(tc_prepare(bop, n, k, !b_is_nk, kind, conv == 2, wb, &bp, ps->comp));
 
   // row chunks: 2..8 chunks of >= 16 MiB of A+C, multiples of 128 rows
   const double row_bytes = 4.0 * ((double)k + (double)n);
@@ -347,8 +345,7 @@ static int host_gemm(const float* A, const float* B, float* C, int64_t m, int64_
     if (tc) {
       ScratchBuffer wa;
       TcOperand ap{};
-      if (conv == 1) ap.hi = a_c;
-      else MTNN_TRY(tc_prepare(a_c, mr, k, false, kind, wa, &ap, ps->comp));
+      MTNN_TRY(tc_prepare(a_c, mr, k, false, kind, conv == 1, wa, &ap, ps->comp));
       MTNN_TRY(tc_run(ap, bp, c_c, mr, n, k, b_is_nk, kind, ps->comp));
     } else {
       MTNN_TRY(gemm_dispatch(a_c, bop, c_c, mr, n, k, v, b_is_nk, ps->comp));
@@ -425,6 +422,25 @@ int mtnn_device_features(double out5[5]) {
   out5[3] = (double)di->bus_width;                         // mbw: bits
   out5[4] = (double)di->l2_bytes / 1024.0;                 // l2c: KB
   return MTNN_OK;
+}
+
+int mtnn_config_set(const char* key, int64_t value) {
+  if (!key) return fail(MTNN_EINVAL, "null config key");
+  if (strcmp(key, "f16s_inkernel_max_short") == 0) {
+    if (value < 0) return fail(MTNN_EINVAL, "f16s_inkernel_max_short must be >= 0");
+    set_f16s_inkernel_max_short(value);
+    return MTNN_OK;
+  }
+  return fail(MTNN_EINVAL, "unknown config key '%s'", key);
+}
+
+int mtnn_config_get(const char* key, int64_t* value) {
+  if (!key || !value) return fail(MTNN_EINVAL, "null argument");
+  if (strcmp(key, "f16s_inkernel_max_short") == 0) {
+    *value = f16s_inkernel_max_short();
+    return MTNN_OK;
+  }
+  return fail(MTNN_EINVAL, "unknown config key '%s'", key);
 }
 
 int mtnn_gemm_nt(const float* A, const float* B, float* C, int64_t m, int64_t n, int64_t k,

@@ -26,13 +26,15 @@ namespace mtnn {
 namespace {
 
 // 2^(14 - ceil(log2(mx))) for finite mx > 0; 1 for 0; 1 for non-finite (the
-// Inf/NaN then propagates through the FP16 halves as it would in FP32).
+// Inf/NaN then propagates through the FP16 halves as it would in FP32). The
+// exponent is capped at 2^126 so rows whose max is below 2^-112 keep a finite
+// scale (and 1/s stays a normal float); their halves then lose low bits.
 __device__ __forceinline__ float pow2_scale(float mx) {
   if (!(mx > 0.f) || !isfinite(mx)) return 1.f;
   int e;
   const float f = frexpf(mx, &e);  // mx = f * 2^e, f in [0.5, 1)
   const int c = (f == 0.5f) ? e - 1 : e;  // ceil(log2(mx))
-  return ldexpf(1.f, 14 - c);
+  return ldexpf(1.f, min(14 - c, 126));
 }
 
 __device__ __forceinline__ void split2(float v, float s, __half& h, __half& l) {
@@ -173,6 +175,36 @@ split_rows_f16_smem_kernel(const float* __restrict__ x, __half* __restrict__ hi,
   }
 }
 
+// Row scales only (the GEMM splits this operand in-kernel): one warp per row,
+// kUnroll independent 16-byte loads per lane in flight, 4 B read per element.
+// Same max and scale as split_rows_f16_kernel, so the in-kernel halves match the
+// pre-split ones bit for bit.
+__global__ void __launch_bounds__(256)
+rowmax_f16_kernel(const float* __restrict__ x, float* __restrict__ inv_scale, int64_t rows,
+                  int64_t k) {
+  const int lane = threadIdx.x % 32;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / 32;
+  const int64_t k4 = k / 4;
+  constexpr int kStep = 32 * kUnroll;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const float4* row = reinterpret_cast<const float4*>(x + r * k);
+    float mx = 0.f;
+    int64_t i = lane;
+    for (; i + 32 * (kUnroll - 1) < k4; i += kStep) {
+      float4 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) v[u] = ldg4(row + i + 32 * u);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) mx = fmaxf(mx, absmax4(v[u]));
+    }
+    for (; i < k4; i += 32) mx = fmaxf(mx, absmax4(ldg4(row + i)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) inv_scale[r] = 1.f / pow2_scale(mx);
+  }
+}
+
 // Column max of a k x n matrix (MN-major B^T): |x| as uint bits (monotonic for
 // non-negative floats; NaN maps above +Inf) folded with atomicMax.
 __global__ void __launch_bounds__(256)
@@ -257,6 +289,19 @@ int launch_split_rows_f16(const float* x, void* hi, void* lo, float* inv_scale, 
     split_rows_f16_kernel<<<(unsigned)blocks, 256, 0, s>>>(
         x, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale, rows, k);
   }
+  MTNN_CUDA_TRY(cudaGetLastError());
+  return MTNN_OK;
+}
+
+int launch_rowmax_f16(const float* x, float* inv_scale, int64_t rows, int64_t k,
+                      cudaStream_t s) {
+  if (rows <= 0) return MTNN_OK;
+  const DeviceInfo* di = nullptr;
+  MTNN_TRY(device_info(&di));
+  KernelTimer timer(MTNN_KCLASS_SPLIT, 4.0 * (double)rows * (double)k, s);
+  int64_t blocks = (rows + 7) / 8;
+  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)di->sm_count * 8));
+  rowmax_f16_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, inv_scale, rows, k);
   MTNN_CUDA_TRY(cudaGetLastError());
   return MTNN_OK;
 }

@@ -108,3 +108,19 @@ def test_native_raw_validates_like_predict_raw():
         native.raw(np.zeros(7))
     with pytest.raises(ValueError, match="finite"):
         native.raw(np.array([1, 1, 1, 1, 1, np.nan, 1, 1.0]))
+
+
+def test_config_knobs_roundtrip_and_reject_unknown():
+    key = "f16s_inkernel_max_short"
+    old = _lib.config_get(key)
+    try:
+        _lib.config_set(key, 0)
+        assert _lib.config_get(key) == 0
+        _lib.config_set(key, 256)
+        assert _lib.config_get(key) == 256
+        with pytest.raises(ValueError, match=">= 0"):
+            _lib.config_set(key, -1)
+    finally:
+        _lib.config_set(key, old)
+    with pytest.raises(ValueError, match="unknown config key"):
+        _lib.config_set("no_such_knob", 1)

@@ -300,3 +300,78 @@ def test_narrow_n_tile(rng, shape):
         assert rel_frobenius(gemm_nt(a, b, variant=v), want) < FP32_GATE
         if n % 16 == 0:
             assert rel_frobenius(gemm_nn(a, np.ascontiguousarray(b.T), variant=v), want) < FP32_GATE
+
+
+class TestF16SInKernelSplit:
+    """Skinny shapes split the long operand inside the GEMM (raw fp32 tile ->
+    fp16 h/l in shared memory, row scales from a read-only pre-pass). The halves
+    are computed by the same operations as the split pass, so with the same
+    output tiling (n <= 128: both paths use the 128-wide tile and the same
+    split-K) C is bit-identical to the pre-split path (knob
+    f16s_inkernel_max_short = 0); otherwise only the split-K summation order
+    differs."""
+
+    KEY = "f16s_inkernel_max_short"
+
+    def _both(self, fn, *args):
+        from paper_1702_03192_b200 import _lib
+
+        old = _lib.config_get(self.KEY)
+        try:
+            _lib.config_set(self.KEY, 0)
+            pre = fn(*args, variant="tc3xf16s")
+            _lib.config_set(self.KEY, 1 << 20)
+            ink = fn(*args, variant="tc3xf16s")
+        finally:
+            _lib.config_set(self.KEY, old)
+        return pre, ink
+
+    @pytest.mark.parametrize("shape", [(128, 4096, 2048), (4096, 128, 2048), (100, 3000, 1000),
+                                       (3000, 96, 1000), (512, 2048, 4104), (300, 1100, 520),
+                                       (1, 1024, 64), (1024, 4, 8)])
+    def test_bit_identical_to_presplit_and_within_gate(self, rng, shape):
+        m, n, k = shape
+        a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+        want = oracle.oracle_nt_blas(a, b)
+        pre, ink = self._both(gemm_nt, a, b)
+        self._same(pre, ink, n)
+        assert rel_frobenius(ink, want) < FP32_GATE
+        if n % 16 == 0:  # NN: only A (K-major) is split in-kernel
+            bt = np.ascontiguousarray(b.T)
+            pre, ink = self._both(gemm_nn, a, bt)
+            self._same(pre, ink, n)
+            assert rel_frobenius(ink, want) < FP32_GATE
+
+    @staticmethod
+    def _same(pre, ink, n):
+        if n <= 128:
+            assert np.array_equal(pre.view(np.uint32), ink.view(np.uint32))
+        else:
+            assert rel_frobenius(ink, pre) < 1e-6
+
+    def test_dynamic_range_and_nonfinite(self, rng):
+        m, n, k = 2048, 192, 776
+        a = (rng.standard_normal((m, k)) * np.exp(rng.uniform(-40, 40, (m, 1)))).astype(np.float32)
+        b = (rng.standard_normal((n, k)) * np.exp(rng.uniform(-20, 20, (n, 1)))).astype(np.float32)
+        a[7] = 0.0
+        a[11, 5] = np.nan
+        a[13, 9] = np.inf
+        pre, ink = self._both(gemm_nt, a, b)
+        assert np.array_equal(np.isnan(pre), np.isnan(ink))
+        assert np.all(ink[7] == 0.0) and np.all(np.isnan(ink[11])) and np.all(~np.isfinite(ink[13]))
+        ok = np.ones(m, bool); ok[[11, 13]] = False
+        want = oracle.oracle_nt_blas(a[ok], b)
+        err = np.linalg.norm(ink[ok] - want, axis=1) / np.maximum(np.linalg.norm(want, axis=1), 1e-300)
+        assert err[np.linalg.norm(want, axis=1) > 0].max() < FP32_GATE
+
+    def test_device_and_pipelined_host_paths(self, rng):
+        import torch
+
+        m, n, k = 384, 8192, 2048   # m >= 256: the host path pipelines A/C chunks
+        a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+        ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+        dev = gemm_nt(ta, tb).cpu().numpy()
+        host = gemm_nt(a, b)   # row chunks: split-K may differ from the whole call
+        assert rel_frobenius(host, dev) < 1e-6
+        rows = np.sort(rng.choice(m, 48, replace=False))
+        assert rel_frobenius(host[rows], oracle.oracle_nt_rows(a, b, rows, np.arange(n))) < FP32_GATE

@@ -9,7 +9,9 @@ VARIANT = int(sys.argv[2]) if len(sys.argv) > 2 else 3  # 3 = tc3xf16s, 1 = tc3x
 torch.manual_seed(0)
 cases = {"nt8192": ("nt", 8192, 8192, 8192), "nt16384": ("nt", 16384, 16384, 16384),
          "nn16384": ("nn", 16384, 16384, 16384), "tr16384": ("tr", 16384, 16384, 0),
-         "nt4096": ("nt", 4096, 4096, 4096)}
+         "nt4096": ("nt", 4096, 4096, 4096), "skinny_m128": ("nt", 128, 16384, 16384),
+         "skinny_n128": ("nt", 16384, 128, 16384), "skinny_m256": ("nt", 256, 16384, 16384),
+         "smallk256": ("nt", 16384, 16384, 256)}
 op, m, n, k = cases[which]
 if op == "tr":
     b = torch.rand(m, n, device="cuda"); out = torch.empty(n, m, device="cuda")
