@@ -362,8 +362,14 @@ def main():
     torch.cuda.synchronize()
 
     # ---------------- timed region: K steps
+    # Only the GEMM launches carry timing events here (the roofline kernel): a
+    # timestamp event pair serialises the stream around its launch, which costs
+    # ~4% of a sweep step when every split/reduce launch is bracketed too. All
+    # launches are still counted. The per-class breakdown comes from one extra
+    # fully instrumented step after the timed region.
     L.mtnn_profile_reset()
-    L.mtnn_profile_enable(1)
+    L.mtnn_profile_enable_classes((1 << _lib.KCLASS_GEMM_TC) | (1 << _lib.KCLASS_GEMM_TC_F16S)
+                                  | (1 << _lib.KCLASS_GEMM_FFMA))
     events = []
     with ClockSampler(local_rank) as clocks:
         if world > 1:
@@ -387,6 +393,14 @@ def main():
     value = total_flops / step_s / 1e12
     prof = {c: _lib.profile_read(c) for c in _lib.KCLASS_NAMES}
     launches = int(sum(v[1] for v in prof.values()))
+    # per-class breakdown: one extra step with every launch timed
+    L.mtnn_profile_reset()
+    L.mtnn_profile_enable(1)
+    one_step()
+    torch.cuda.synchronize()
+    L.mtnn_profile_enable(0)
+    prof_all = {c: _lib.profile_read(c) for c in _lib.KCLASS_NAMES}
+    L.mtnn_profile_reset()
     ncall = len(calls)
     per_call = [statistics.median(events[st * (len(events) // args.steps) + i][0].elapsed_time(
         events[st * (len(events) // args.steps) + i][1]) for st in range(args.steps)) * 1e-3
@@ -404,14 +418,19 @@ def main():
     peaks_path = ROOT / "MEASURED_PEAKS.json"
     peaks = json.loads(peaks_path.read_text()) if peaks_path.exists() else {}
     bf16 = peaks.get("bf16_tflops", 1590.0)
+    # a sweep/fcn/large step keeps the tensor cores busy for 10s-100s of ms under
+    # the board power cap: the sustained bf16 figure is the roof for a kernel
+    # timed inside such a step (B200_PROFILING.md); the burst one is listed too
+    bf16_sus = peaks.get("bf16_tflops_sustained", bf16)
     hbm = peaks.get("hbm_gbs", 6650.0)
     tc_class = max((_lib.KCLASS_GEMM_TC_F16S, _lib.KCLASS_GEMM_TC), key=lambda c: prof[c][0])
     tc_ms, tc_n, tc_work = prof[tc_class]
     f16s = tc_class == _lib.KCLASS_GEMM_TC_F16S
-    roof = bf16 / 3.0 if f16s else bf16 / 6.0
+    roof = bf16_sus / 3.0 if f16s else bf16_sus / 6.0
+    roof_burst = bf16 / 3.0 if f16s else bf16 / 6.0
     ncu_path = ROOT / "profiles" / "ncu_summary.json"
     ncu_traffic = json.loads(ncu_path.read_text()).get("gemm_tc3x_traffic", {}) if ncu_path.exists() else {}
-    dominant = max(prof, key=lambda c: prof[c][0])
+    dominant = max(prof_all, key=lambda c: prof_all[c][0])
     achieved = tc_work / (tc_ms * 1e-3) / 1e12 if tc_ms else None
     roofline = {
         "kernel": _lib.KCLASS_NAMES[tc_class], "bound": "tensor",
@@ -420,18 +439,20 @@ def main():
         "traffic": ncu_traffic.get("traffic"),
         "traffic_launch": ncu_traffic.get("launch"),
         "traffic_algorithmic_bytes": ncu_traffic.get("algorithmic_bytes"),
-        "peak_basis": (f"FP32-accurate roof = measured bf16 dense {bf16} TFLOP/s (MEASURED_PEAKS.json, "
-                       f"burst) / 3 MMAs per product (fp16 = bf16 rate)" if f16s else
-                       f"3xTF32 FP32-accurate roof = measured bf16 dense {bf16} TFLOP/s "
-                       f"(MEASURED_PEAKS.json, burst) / 2 (tf32 rate) / 3 (MMAs per product)"),
+        "peak_basis": (f"FP32-accurate roof = measured bf16 dense {bf16_sus} TFLOP/s (MEASURED_PEAKS.json, "
+                       f"sustained: the kernel runs inside a long back-to-back step) / 3 MMAs per "
+                       f"product (fp16 = bf16 rate)" if f16s else
+                       f"3xTF32 FP32-accurate roof = measured bf16 dense {bf16_sus} TFLOP/s "
+                       f"(MEASURED_PEAKS.json, sustained) / 2 (tf32 rate) / 3 (MMAs per product)"),
+        "peak_burst": roof_burst, "frac_of_burst": achieved / roof_burst if achieved else None,
         "launches": tc_n, "avg_launch_ms": tc_ms / tc_n if tc_n else None,
         "share_of_step": tc_ms / 1e3 / (device_s * 1.0) if device_s else None,
         "dominant_kernel_by_time": _lib.KCLASS_NAMES[dominant],
     }
-    kernels_summary = {_lib.KCLASS_NAMES[c]: {"ms": v[0] / args.steps,
-                                              "launches_per_step": v[1] / args.steps,
-                                              "work_per_step": v[2] / args.steps}
-                       for c, v in prof.items() if v[1]}
+    kernels_summary = {_lib.KCLASS_NAMES[c]: {"ms": v[0], "launches_per_step": v[1],
+                                              "work_per_step": v[2]}
+                       for c, v in prof_all.items() if v[1]}
+    kernels_summary["source"] = "one extra step with every launch timed (after the K timed steps)"
 
     extra = {}
     if args.workload == "sweep" and world == 1:
@@ -479,7 +500,9 @@ def sweep_oracle_pass(shapes, per_case_mtnn, A, B, C, flush_src, stream, disp, t
     from paper_1702_03192_b200 import ProblemShape
 
     nt_t, tnn_t = [[] for _ in shapes], [[] for _ in shapes]
-    L.mtnn_profile_enable(1)
+    # the same instrumentation as the timed steps (GEMM launches timed only)
+    L.mtnn_profile_enable_classes((1 << _lib.KCLASS_GEMM_TC) | (1 << _lib.KCLASS_GEMM_TC_F16S)
+                                  | (1 << _lib.KCLASS_GEMM_FFMA))
     for _rep in range(3):
         for i, (m, n, k) in enumerate(shapes):
             for which in ("nt", "tnn"):

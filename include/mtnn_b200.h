@@ -84,6 +84,12 @@ int mtnn_device_features(double out5[5]);
 #define MTNN_KCLASS_GEMM_TC_F16S 5
 #define MTNN_KCLASS_COUNT 6
 int mtnn_profile_enable(int on);
+/* Time only the classes whose bit (1 << class) is set: every timed launch is
+ * bracketed by two timestamp events, which serialise the stream around it, so
+ * a benchmark can time its dominant kernel without paying that on the rest.
+ * While profiling is on (either call), launches and work of EVERY class are
+ * counted; mtnn_profile_read's total_ms covers the timed classes only. */
+int mtnn_profile_enable_classes(unsigned mask);
 int mtnn_profile_reset(void);
 int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* work);
 

@@ -66,6 +66,7 @@ def _load():
         "mtnn_device_free_bytes": (c_int, [_I64P]),
         "mtnn_device_features": (c_int, [_DP]),
         "mtnn_profile_enable": (c_int, [c_int]),
+        "mtnn_profile_enable_classes": (c_int, [ctypes.c_uint]),
         "mtnn_profile_reset": (c_int, []),
         "mtnn_profile_read": (c_int, [c_int, _DP, _I64P, _DP]),
         "mtnn_config_set": (c_int, [c_char_p, c_int64]),

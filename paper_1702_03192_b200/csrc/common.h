@@ -85,6 +85,10 @@ struct ScratchBuffer;
 // lo = nullptr); F16S then only computes the row scales (read-only pass).
 int tc_prepare(const float* X, int64_t rows, int64_t k, bool mn_major, TcKind kind,
                bool inkernel, ScratchBuffer& ws, TcOperand* out, cudaStream_t s);
+// Both operands of one GEMM; F16S with K-major B runs a single split launch.
+int tc_prepare_pair(const float* A, int64_t m, const float* B, int64_t n, int64_t k,
+                    bool b_mn_major, TcKind kind, int conv, ScratchBuffer& wa, ScratchBuffer& wb,
+                    TcOperand* a, TcOperand* b, cudaStream_t s);
 // Which operand (1 = A, 2 = B, 0 = none) the GEMM splits in-kernel for this shape.
 int tc_inkernel_operand(int64_t m, int64_t n, bool b_is_nk, TcKind kind);
 // Run-time knob (mtnn_config_set): largest output short side split in-kernel.
@@ -94,6 +98,11 @@ int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t 
            bool b_is_nk, TcKind kind, cudaStream_t s);
 int launch_split_rows_f16(const float* x, void* hi, void* lo, float* inv_scale, int64_t rows,
                           int64_t k, cudaStream_t s);
+// Both K-major operands of one GEMM in one launch: rows of x0 then x1 (same k);
+// hiN == nullptr -> row scales only for that operand.
+int launch_split_rows_f16_pair(const float* x0, void* hi0, void* lo0, float* inv0, int64_t rows0,
+                               const float* x1, void* hi1, void* lo1, float* inv1, int64_t rows1,
+                               int64_t k, cudaStream_t s);
 // 1/s per row (s = split_rows_f16's power-of-two row scale), reading x only.
 int launch_rowmax_f16(const float* x, float* inv_scale, int64_t rows, int64_t k, cudaStream_t s);
 int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,

@@ -1006,6 +1006,31 @@ int tc_prepare(const float* X, int64_t rows, int64_t k, bool mn_major, TcKind ki
   return MTNN_OK;
 }
 
+int tc_prepare_pair(const float* A, int64_t m, const float* B, int64_t n, int64_t k,
+                    bool b_mn_major, TcKind kind, int conv, ScratchBuffer& wa, ScratchBuffer& wb,
+                    TcOperand* a, TcOperand* b, cudaStream_t s) {
+  if (kind != TcKind::F16S || b_mn_major) {
+    MTNN_TRY(tc_prepare(A, m, k, false, kind, conv == 1, wa, a, s));
+    return tc_prepare(B, n, k, b_mn_major, kind, conv == 2, wb, b, s);
+  }
+  // F16S, both K-major: [h | l | 1/s] per split operand, [1/s] per in-kernel one
+  auto layout = [&](const float* X, int64_t rows, bool ink, ScratchBuffer& ws, TcOperand* o) {
+    const size_t oh = ink ? 0 : align256((size_t)rows * k * 2);
+    MTNN_TRY(ws.alloc(2 * oh + align256((size_t)rows * 4), s));
+    uint8_t* base = static_cast<uint8_t*>(ws.ptr);
+    o->hi = ink ? static_cast<const void*>(X) : base;
+    o->lo = ink ? nullptr : base + oh;
+    o->inv_scale = reinterpret_cast<float*>(base + 2 * oh);
+    return MTNN_OK;
+  };
+  MTNN_TRY(layout(A, m, conv == 1, wa, a));
+  MTNN_TRY(layout(B, n, conv == 2, wb, b));
+  return launch_split_rows_f16_pair(
+      A, conv == 1 ? nullptr : const_cast<void*>(a->hi), const_cast<void*>(a->lo),
+      const_cast<float*>(a->inv_scale), m, B, conv == 2 ? nullptr : const_cast<void*>(b->hi),
+      const_cast<void*>(b->lo), const_cast<float*>(b->inv_scale), n, k, s);
+}
+
 // Split-K factor: minimise (waves of units) x (k-blocks per unit + per-unit
 // overhead) plus the partial-sum traffic a split adds (the GEMM writes `s`
 // partial C's, the reduction reads them and writes C). Wave quantisation
@@ -1121,8 +1146,7 @@ int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t 
   ScratchBuffer wa, wb;
   TcOperand a{}, b{};
   const int conv = tc_inkernel_operand(m, n, b_is_nk, kind);
-  MTNN_TRY(tc_prepare(A, m, k, false, kind, conv == 1, wa, &a, s));
-  MTNN_TRY(tc_prepare(B, n, k, !b_is_nk, kind, conv == 2, wb, &b, s));
+  MTNN_TRY(tc_prepare_pair(A, m, B, n, k, !b_is_nk, kind, conv, wa, wb, &a, &b, s));
   return tc_run(a, b, C, m, n, k, b_is_nk, kind, s);
 }
 

@@ -19,7 +19,8 @@ struct Pending {
   cudaEvent_t start, stop;
 };
 
-std::atomic<bool> g_enabled{false};
+std::atomic<unsigned> g_mask{0};  // bit c: time kernel class c
+std::atomic<bool> g_counting{false};  // count launches and work of every class
 std::mutex g_mu;
 std::vector<Pending> g_pending;
 std::vector<cudaEvent_t> g_free_events;
@@ -47,7 +48,13 @@ cudaEvent_t take_event() {
 }  // namespace
 
 KernelTimer::KernelTimer(int kc, double w, cudaStream_t s) : kclass(kc), work(w), stream(s) {
-  if (!g_enabled.load(std::memory_order_relaxed)) return;
+  if (!g_counting.load(std::memory_order_relaxed)) return;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);  // every launch is counted while profiling
+    g_launches[kc] += 1;
+    g_work[kc] += w;
+  }
+  if (!((g_mask.load(std::memory_order_relaxed) >> kc) & 1u)) return;
   start = take_event();
   if (start && cudaEventRecord(start, stream) != cudaSuccess) {
     (void)cudaGetLastError();
@@ -73,7 +80,14 @@ using namespace mtnn;
 extern "C" {
 
 int mtnn_profile_enable(int on) {
-  g_enabled.store(on != 0);
+  g_mask.store(on ? (1u << MTNN_KCLASS_COUNT) - 1u : 0u);
+  g_counting.store(on != 0);
+  return MTNN_OK;
+}
+
+int mtnn_profile_enable_classes(unsigned mask) {
+  g_mask.store(mask & ((1u << MTNN_KCLASS_COUNT) - 1u));
+  g_counting.store(true);
   return MTNN_OK;
 }
 
@@ -103,8 +117,6 @@ int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* w
       return fail(MTNN_ECUDA, "profile event: %s", cudaGetErrorString(e));
     }
     g_ms[p.kclass] += ms;
-    g_work[p.kclass] += p.work;
-    g_launches[p.kclass] += 1;
     g_free_events.push_back(p.start);
     g_free_events.push_back(p.stop);
   }

@@ -43,10 +43,7 @@ __device__ __forceinline__ void split2(float v, float s, __half& h, __half& l) {
   l = __float2half_rn(xs - __half2float(h));
 }
 
-// One warp per row (K-major operand, rows x k, k % 4 == 0): max, then split.
-// Both passes keep kUnroll independent 16-byte loads per lane in flight; the
-// second pass re-reads the row from L1/L2 (a row is at most 64 KiB).
-constexpr int kUnroll = 4;
+constexpr int kUnroll = 4;  // independent 16-byte loads per lane in flight
 
 __device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
 
@@ -67,42 +64,64 @@ __device__ __forceinline__ void split4(const float4& v, float s, uint2& hw, uint
   lw = make_uint2(*reinterpret_cast<uint32_t*>(&lp0), *reinterpret_cast<uint32_t*>(&lp1));
 }
 
+// A launch serves up to two K-major operands (A and B of one GEMM, same k):
+// job 0 owns virtual rows [0, j0.rows), job 1 the next j1.rows. A job with
+// hi == nullptr only computes its row scales (the GEMM splits it in-kernel).
+struct RowJob {
+  const float* x;
+  __half* hi;
+  __half* lo;
+  float* inv_scale;
+  int64_t rows;
+};
+
+__device__ __forceinline__ const RowJob& pick(const RowJob& j0, const RowJob& j1, int64_t v,
+                                              int64_t& r) {
+  if (v < j0.rows) { r = v; return j0; }
+  r = v - j0.rows;
+  return j1;
+}
+
+// One warp per row: max, then (split jobs) split. Both passes keep kUnroll
+// independent 16-byte loads per lane in flight; the second pass re-reads the
+// row from L1/L2 (a row is at most 8 KiB here).
 __global__ void __launch_bounds__(256)
-split_rows_f16_kernel(const float* __restrict__ x, __half* __restrict__ hi,
-                      __half* __restrict__ lo, float* __restrict__ inv_scale, int64_t rows,
-                      int64_t k) {
+split_rows_f16_kernel(const RowJob j0, const RowJob j1, int64_t k) {
   const int lane = threadIdx.x % 32;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / 32;
   const int64_t k4 = k / 4;
   constexpr int kStep = 32 * kUnroll;
-  for (int64_t r = warp; r < rows; r += nwarps) {
-    const float4* row = reinterpret_cast<const float4*>(x + r * k);
+  for (int64_t v = warp; v < j0.rows + j1.rows; v += nwarps) {
+    int64_t r;
+    const RowJob& j = pick(j0, j1, v, r);
+    const float4* row = reinterpret_cast<const float4*>(j.x + r * k);
     float mx = 0.f;
     int64_t i = lane;
     for (; i + 32 * (kUnroll - 1) < k4; i += kStep) {
-      float4 v[kUnroll];
+      float4 x[kUnroll];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) v[u] = ldg4(row + i + 32 * u);
+      for (int u = 0; u < kUnroll; ++u) x[u] = ldg4(row + i + 32 * u);
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) mx = fmaxf(mx, absmax4(v[u]));
+      for (int u = 0; u < kUnroll; ++u) mx = fmaxf(mx, absmax4(x[u]));
     }
     for (; i < k4; i += 32) mx = fmaxf(mx, absmax4(ldg4(row + i)));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     const float s = pow2_scale(mx);
-    if (lane == 0) inv_scale[r] = 1.f / s;
-    uint2* hrow = reinterpret_cast<uint2*>(hi + r * k);
-    uint2* lrow = reinterpret_cast<uint2*>(lo + r * k);
+    if (lane == 0) j.inv_scale[r] = 1.f / s;
+    if (j.hi == nullptr) continue;  // row scales only
+    uint2* hrow = reinterpret_cast<uint2*>(j.hi + r * k);
+    uint2* lrow = reinterpret_cast<uint2*>(j.lo + r * k);
     i = lane;
     for (; i + 32 * (kUnroll - 1) < k4; i += kStep) {
-      float4 v[kUnroll];
+      float4 x[kUnroll];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) v[u] = ldg4(row + i + 32 * u);
+      for (int u = 0; u < kUnroll; ++u) x[u] = ldg4(row + i + 32 * u);
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         uint2 hw, lw;
-        split4(v[u], s, hw, lw);
+        split4(x[u], s, hw, lw);
         hrow[i + 32 * u] = hw;
         lrow[i + 32 * u] = lw;
       }
@@ -116,39 +135,41 @@ split_rows_f16_kernel(const float* __restrict__ x, __half* __restrict__ hi,
   }
 }
 
-// One CTA per row for long rows (k > kWarpRowMax): the row is staged in shared
-// memory by the max pass, so DRAM sees exactly one read and one write per element
-// (8 B) — with warp-per-row the ~600 MB of long rows in flight overflow L2 and the
-// split pass re-reads them from DRAM (12 B per element).
+// One CTA per row for long rows (k > kWarpRowMax): split jobs stage the row in
+// shared memory during the max pass, so DRAM sees exactly one read and one write
+// per element (8 B) — with warp-per-row the ~600 MB of long rows in flight
+// overflow L2 and the split pass re-reads them from DRAM (12 B per element).
+// Row-scale-only jobs just read (4 B per element).
 constexpr int kWarpRowMax = 2048;
 constexpr int kRowThreads = 512;
 
 __global__ void __launch_bounds__(kRowThreads)
-split_rows_f16_smem_kernel(const float* __restrict__ x, __half* __restrict__ hi,
-                           __half* __restrict__ lo, float* __restrict__ inv_scale,
-                           int64_t rows, int64_t k) {
+split_rows_f16_smem_kernel(const RowJob j0, const RowJob j1, int64_t k) {
   extern __shared__ float4 row_s[];
   __shared__ float red[kRowThreads / 32];
   const int64_t k4 = k / 4;
   const int t = threadIdx.x;
-  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
-    const float4* row = reinterpret_cast<const float4*>(x + r * k);
+  for (int64_t v = blockIdx.x; v < j0.rows + j1.rows; v += gridDim.x) {
+    int64_t r;
+    const RowJob& j = pick(j0, j1, v, r);
+    const bool stage = j.hi != nullptr;
+    const float4* row = reinterpret_cast<const float4*>(j.x + r * k);
     float mx = 0.f;
     int64_t i = t;
     for (; i + kRowThreads * (kUnroll - 1) < k4; i += kRowThreads * kUnroll) {
-      float4 v[kUnroll];
+      float4 x[kUnroll];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) v[u] = ldg4(row + i + kRowThreads * u);
+      for (int u = 0; u < kUnroll; ++u) x[u] = ldg4(row + i + kRowThreads * u);
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
-        row_s[i + kRowThreads * u] = v[u];
-        mx = fmaxf(mx, absmax4(v[u]));
+        if (stage) row_s[i + kRowThreads * u] = x[u];
+        mx = fmaxf(mx, absmax4(x[u]));
       }
     }
     for (; i < k4; i += kRowThreads) {
-      const float4 v = ldg4(row + i);
-      row_s[i] = v;
-      mx = fmaxf(mx, absmax4(v));
+      const float4 x = ldg4(row + i);
+      if (stage) row_s[i] = x;
+      mx = fmaxf(mx, absmax4(x));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -162,46 +183,18 @@ split_rows_f16_smem_kernel(const float* __restrict__ x, __half* __restrict__ hi,
     }
     __syncthreads();
     const float s = pow2_scale(red[0]);
-    if (t == 0) inv_scale[r] = 1.f / s;
-    uint2* hrow = reinterpret_cast<uint2*>(hi + r * k);
-    uint2* lrow = reinterpret_cast<uint2*>(lo + r * k);
-    for (int64_t j = t; j < k4; j += kRowThreads) {
-      uint2 hw, lw;
-      split4(row_s[j], s, hw, lw);
-      hrow[j] = hw;
-      lrow[j] = lw;
+    if (t == 0) j.inv_scale[r] = 1.f / s;
+    if (stage) {
+      uint2* hrow = reinterpret_cast<uint2*>(j.hi + r * k);
+      uint2* lrow = reinterpret_cast<uint2*>(j.lo + r * k);
+      for (int64_t q = t; q < k4; q += kRowThreads) {
+        uint2 hw, lw;
+        split4(row_s[q], s, hw, lw);
+        hrow[q] = hw;
+        lrow[q] = lw;
+      }
     }
     __syncthreads();  // row_s and red are reused by the next row
-  }
-}
-
-// Row scales only (the GEMM splits this operand in-kernel): one warp per row,
-// kUnroll independent 16-byte loads per lane in flight, 4 B read per element.
-// Same max and scale as split_rows_f16_kernel, so the in-kernel halves match the
-// pre-split ones bit for bit.
-__global__ void __launch_bounds__(256)
-rowmax_f16_kernel(const float* __restrict__ x, float* __restrict__ inv_scale, int64_t rows,
-                  int64_t k) {
-  const int lane = threadIdx.x % 32;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / 32;
-  const int64_t k4 = k / 4;
-  constexpr int kStep = 32 * kUnroll;
-  for (int64_t r = warp; r < rows; r += nwarps) {
-    const float4* row = reinterpret_cast<const float4*>(x + r * k);
-    float mx = 0.f;
-    int64_t i = lane;
-    for (; i + 32 * (kUnroll - 1) < k4; i += kStep) {
-      float4 v[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) v[u] = ldg4(row + i + 32 * u);
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) mx = fmaxf(mx, absmax4(v[u]));
-    }
-    for (; i < k4; i += 32) mx = fmaxf(mx, absmax4(ldg4(row + i)));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) inv_scale[r] = 1.f / pow2_scale(mx);
   }
 }
 
@@ -265,14 +258,25 @@ split_cols_f16_kernel(const float* __restrict__ x, const unsigned* __restrict__ 
 
 }  // namespace
 
-int launch_split_rows_f16(const float* x, void* hi, void* lo, float* inv_scale, int64_t rows,
-                          int64_t k, cudaStream_t s) {
-  if (rows <= 0) return MTNN_OK;
+// Splits (hi != nullptr) or row-scales (hi == nullptr) the rows of up to two
+// K-major operands sharing k, in one launch.
+int launch_split_rows_f16_pair(const float* x0, void* hi0, void* lo0, float* inv0, int64_t rows0,
+                               const float* x1, void* hi1, void* lo1, float* inv1, int64_t rows1,
+                               int64_t k, cudaStream_t s) {
+  if (rows0 < 0) rows0 = 0;
+  if (rows1 < 0) rows1 = 0;
+  if (rows0 + rows1 == 0) return MTNN_OK;
   const DeviceInfo* di = nullptr;
   MTNN_TRY(device_info(&di));
-  KernelTimer timer(MTNN_KCLASS_SPLIT, 8.0 * (double)rows * (double)k, s);
+  const RowJob j0{x0, static_cast<__half*>(hi0), static_cast<__half*>(lo0), inv0, rows0};
+  const RowJob j1{x1, static_cast<__half*>(hi1), static_cast<__half*>(lo1), inv1, rows1};
+  const int64_t rows = rows0 + rows1;
+  KernelTimer timer(MTNN_KCLASS_SPLIT,
+                    ((hi0 ? 8.0 : 4.0) * (double)rows0 + (hi1 ? 8.0 : 4.0) * (double)rows1) * (double)k,
+                    s);
   const size_t row_bytes = (size_t)k * sizeof(float);
-  if (k > kWarpRowMax && row_bytes <= 160 * 1024) {
+  const bool any_split = (hi0 && rows0) || (hi1 && rows1);
+  if (k > kWarpRowMax && row_bytes <= 160 * 1024 && any_split) {
     static bool attr = false;
     if (!attr) {
       MTNN_CUDA_TRY(cudaFuncSetAttribute(split_rows_f16_smem_kernel,
@@ -281,29 +285,26 @@ int launch_split_rows_f16(const float* x, void* hi, void* lo, float* inv_scale, 
     }
     const int per_sm = std::max<int>(1, std::min<int>(4, (int)((200 * 1024) / row_bytes)));
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)di->sm_count * per_sm));
-    split_rows_f16_smem_kernel<<<(unsigned)blocks, kRowThreads, row_bytes, s>>>(
-        x, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale, rows, k);
+    split_rows_f16_smem_kernel<<<(unsigned)blocks, kRowThreads, row_bytes, s>>>(j0, j1, k);
   } else {
     int64_t blocks = (rows + 7) / 8;
     blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)di->sm_count * 16));
-    split_rows_f16_kernel<<<(unsigned)blocks, 256, 0, s>>>(
-        x, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale, rows, k);
+    split_rows_f16_kernel<<<(unsigned)blocks, 256, 0, s>>>(j0, j1, k);
   }
   MTNN_CUDA_TRY(cudaGetLastError());
   return MTNN_OK;
 }
 
+int launch_split_rows_f16(const float* x, void* hi, void* lo, float* inv_scale, int64_t rows,
+                          int64_t k, cudaStream_t s) {
+  return launch_split_rows_f16_pair(x, hi, lo, inv_scale, rows, nullptr, nullptr, nullptr, nullptr,
+                                    0, k, s);
+}
+
 int launch_rowmax_f16(const float* x, float* inv_scale, int64_t rows, int64_t k,
                       cudaStream_t s) {
-  if (rows <= 0) return MTNN_OK;
-  const DeviceInfo* di = nullptr;
-  MTNN_TRY(device_info(&di));
-  KernelTimer timer(MTNN_KCLASS_SPLIT, 4.0 * (double)rows * (double)k, s);
-  int64_t blocks = (rows + 7) / 8;
-  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)di->sm_count * 8));
-  rowmax_f16_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, inv_scale, rows, k);
-  MTNN_CUDA_TRY(cudaGetLastError());
-  return MTNN_OK;
+  return launch_split_rows_f16_pair(x, nullptr, nullptr, inv_scale, rows, nullptr, nullptr,
+                                    nullptr, nullptr, 0, k, s);
 }
 
 int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,
