@@ -100,8 +100,12 @@ int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* w
  *   output's short side is at most this and its long side >= 1024; 0 disables.
  *   Default 256, the best on the B200 sweep (env MTNN_F16S_INKERNEL_MAX,
  *   MTNN_F16S_INKERNEL=0 disables). The halves equal the split pass's; only
- *   the output tiling (and so the split-K order) may differ. Unknown keys ->
- *   MTNN_EINVAL. */
+ *   the output tiling (and so the split-K order) may differ.
+ * "host_pipeline_blocked": 1 (default; env MTNN_PIPE_BLOCKED=0 turns it off):
+ *   host-buffer NT calls on the tc3xf16s path with n >= 1024, k <= 4096 stream B in row
+ *   blocks against A's first row block so C leaves while B arrives; 0 = copy B
+ *   first, then pipeline A/C row chunks.
+ * Unknown keys -> MTNN_EINVAL. */
 int mtnn_config_set(const char* key, int64_t value);
 int mtnn_config_get(const char* key, int64_t* value);
 

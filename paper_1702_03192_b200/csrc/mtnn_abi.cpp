@@ -3,6 +3,7 @@
 // Host orchestration for the MTNN hot path: argument validation, variant choice,
 // TNN's stream-ordered B^T buffer, the host-buffer (numpy-semantics) variants and
 // the dispatcher (Algorithm 2; reference selector.py:192-221).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdarg.h>
@@ -264,11 +265,168 @@ static double pipe_chunk_bytes() {
   return v;
 }
 
+// MTNN_PIPE_BLOCKED=0 / mtnn_config_set("host_pipeline_blocked", 0) keeps the
+// B-first pipeline for every host-buffer GEMM.
+static std::atomic<int> g_pipe_blocked{-1};
+static bool blocked_pipeline_enabled() {
+  int v = g_pipe_blocked.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = getenv("MTNN_PIPE_BLOCKED");
+    v = (e && e[0] == '0') ? 0 : 1;
+    g_pipe_blocked.store(v, std::memory_order_relaxed);
+  }
+  return v != 0;
+}
+
+// NT on the FP16x3 tensor-core path with a wide B. A B-first pipeline leaves
+// the D2H engine idle until all of B is in. Here A's first row block goes in,
+// then B in row blocks: each B block is split into its rows of the full split
+// operand and multiplied with A's first block at once, and that C block leaves
+// by a 2-D copy into C's rows while the next B block arrives. The remaining
+// row blocks of A then run against the complete B, full-width, and leave as
+// contiguous rows. (An L-shaped A_0 B_0 A_1 B_1 ... order, which makes C blocks
+// earlier in theory, measured slower on the B200: more, smaller GEMMs.) Each
+// operand block is split once; kernels and operand halves are the device path's
+// (only split-K order may differ).
+static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_t m, int64_t n,
+                                int64_t k, int conv) {
+  PipeStreams* ps = nullptr;
+  MTNN_TRY(pipe_streams(&ps));
+  EventSet evs;
+  ScratchBuffer da, db, dc, wa, wb;
+  struct Drain {
+    PipeStreams* p;
+    ~Drain() {
+      (void)cudaStreamSynchronize(p->in);
+      (void)cudaStreamSynchronize(p->comp);
+      (void)cudaStreamSynchronize(p->out);
+    }
+  } drain{ps};
+  // block rows: ~1/16 of the input bytes per input block (<= 128 MiB), at least
+  // 1024 rows (C blocks >= 4 MiB), 128-row multiples
+  const double per_block = std::min(128.0 * (1 << 20), 4.0 * ((double)m + (double)n) * (double)k / 16.0);
+  int64_t R = (int64_t)(per_block / (4.0 * (double)k));
+  R = std::max<int64_t>(1024, R / 128 * 128);
+  const int64_t mb = std::min(R, m), nb = std::min(R, n);
+  const int64_t QA = (m + mb - 1) / mb, QB = (n + nb - 1) / nb;
+  MTNN_TRY(da.alloc((size_t)(m * k) * 4, ps->in));
+  MTNN_TRY(db.alloc((size_t)(n * k) * 4, ps->in));
+  MTNN_TRY(dc.alloc((size_t)(m * n) * 4, ps->in));  // C blocks, each contiguous
+  float* dap = static_cast<float*>(da.ptr);
+  float* dbp = static_cast<float*>(db.ptr);
+  float* dcp = static_cast<float*>(dc.ptr);
+  // split operands: [h | l | 1/s] (A always; B unless conv == 2: 1/s only)
+  auto carve = [&](ScratchBuffer& w, int64_t rows, bool halves, __half_raw** h, __half_raw** l,
+                   float** inv) {
+    const size_t oh = halves ? (((size_t)(rows * k) * 2 + 255) & ~size_t(255)) : 0;
+    MTNN_TRY(w.alloc(2 * oh + (size_t)rows * 4 + 256, ps->in));
+    uint8_t* base = static_cast<uint8_t*>(w.ptr);
+    *h = halves ? reinterpret_cast<__half_raw*>(base) : nullptr;
+    *l = halves ? reinterpret_cast<__half_raw*>(base + oh) : nullptr;
+    *inv = reinterpret_cast<float*>(base + 2 * oh);
+    return MTNN_OK;
+  };
+  __half_raw *ah, *al, *bh, *bl;
+  float *ainv, *binv;
+  MTNN_TRY(carve(wa, m, true, &ah, &al, &ainv));
+  MTNN_TRY(carve(wb, n, conv != 2, &bh, &bl, &binv));
+  auto a_rows = [&](int64_t i0) {
+    TcOperand o{};
+    o.hi = ah + i0 * k;
+    o.lo = al + i0 * k;
+    o.inv_scale = ainv + i0;
+    return o;
+  };
+  auto b_rows = [&](int64_t j0) {
+    TcOperand o{};
+    o.hi = conv == 2 ? static_cast<const void*>(dbp + j0 * k) : static_cast<const void*>(bh + j0 * k);
+    o.lo = conv == 2 ? nullptr : static_cast<const void*>(bl + j0 * k);
+    o.inv_scale = binv + j0;
+    return o;
+  };
+  cudaEvent_t ev;
+  MTNN_TRY(evs.make(&ev));
+  MTNN_CUDA_TRY(cudaEventRecord(ev, ps->in));  // allocations above are ordered on `in`
+  MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->comp, ev, 0));
+  MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->out, ev, 0));
+  // copy one operand block in, split it on the compute stream
+  auto bring = [&](bool is_a, int64_t q) {
+    const int64_t r0 = q * (is_a ? mb : nb);
+    const int64_t rows = std::min(is_a ? mb : nb, (is_a ? m : n) - r0);
+    float* dst = (is_a ? dap : dbp) + r0 * k;
+    MTNN_CUDA_TRY(cudaMemcpyAsync(dst, (is_a ? A : B) + r0 * k, (size_t)(rows * k) * 4,
+                                  cudaMemcpyHostToDevice, ps->in));
+    cudaEvent_t e;
+    MTNN_TRY(evs.make(&e));
+    MTNN_CUDA_TRY(cudaEventRecord(e, ps->in));
+    MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->comp, e, 0));
+    const TcOperand o = is_a ? a_rows(r0) : b_rows(r0);
+    const bool halves = is_a || conv != 2;
+    return launch_split_rows_f16_pair(dst, halves ? const_cast<void*>(o.hi) : nullptr,
+                                      const_cast<void*>(o.lo), const_cast<float*>(o.inv_scale),
+                                      rows, nullptr, nullptr, nullptr, nullptr, 0, k, ps->comp);
+  };
+  // multiply C block (i, j) and send it out
+  auto block = [&](int64_t i, int64_t j) {
+    const int64_t i0 = i * mb, j0 = j * nb;
+    const int64_t mi = std::min(mb, m - i0), nj = std::min(nb, n - j0);
+    float* cij = dcp + i0 * n + mi * j0;  // rows i0.. of C, block j: mi x nj contiguous
+    MTNN_TRY(tc_run(a_rows(i0), b_rows(j0), cij, mi, nj, k, true, TcKind::F16S, ps->comp));
+    cudaEvent_t e;
+    MTNN_TRY(evs.make(&e));
+    MTNN_CUDA_TRY(cudaEventRecord(e, ps->comp));
+    MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->out, e, 0));
+    MTNN_CUDA_TRY(cudaMemcpy2DAsync(C + i0 * n + j0, (size_t)n * 4, cij, (size_t)nj * 4,
+                                    (size_t)nj * 4, (size_t)mi, cudaMemcpyDeviceToHost, ps->out));
+    return MTNN_OK;
+  };
+  MTNN_TRY(bring(true, 0));
+  for (int64_t j = 0; j < QB; ++j) {
+    MTNN_TRY(bring(false, j));
+    MTNN_TRY(block(0, j));
+  }
+  for (int64_t i = 1; i < QA; ++i) {  // rows i*mb.. against all of B, full width
+    MTNN_TRY(bring(true, i));
+    const int64_t i0 = i * mb, mi = std::min(mb, m - i0);
+    float* ci = dcp + i0 * n;
+    MTNN_TRY(tc_run(a_rows(i0), b_rows(0), ci, mi, n, k, true, TcKind::F16S, ps->comp));
+    MTNN_TRY(evs.make(&ev));
+    MTNN_CUDA_TRY(cudaEventRecord(ev, ps->comp));
+    MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->out, ev, 0));
+    MTNN_CUDA_TRY(cudaMemcpyAsync(C + i0 * n, ci, (size_t)(mi * n) * 4, cudaMemcpyDeviceToHost,
+                                  ps->out));
+  }
+  cudaError_t e1 = cudaStreamSynchronize(ps->out);
+  cudaError_t e2 = cudaStreamSynchronize(ps->comp);
+  cudaError_t e3 = cudaStreamSynchronize(ps->in);
+  for (cudaError_t e : {e1, e2, e3})
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      return fail(MTNN_ECUDA, "blocked host GEMM: %s", cudaGetErrorString(e));
+    }
+  return MTNN_OK;
+}
+
 static int host_gemm(const float* A, const float* B, float* C, int64_t m, int64_t n,
                      int64_t k, HostPath path, int variant) {
   MTNN_TRY(check_dims(m, n, k));
   if (variant < 0 || variant > 3) return fail(MTNN_EINVAL, "unknown variant %d", variant);
   const double bytes = 4.0 * ((double)m * k + (double)n * k + (double)m * n);
+  // blocked pipeline for k <= 4096: measured on the B200 (tools/probe_e2e_ab.py,
+  // interleaved per case) it gains 3-14% there and loses 2-7% at k = 16384,
+  // where the row chunks' H2D already dominates
+  if (path == HostPath::NT && bytes >= pipe_min_bytes() && n >= 1024 && m > 0 && k > 0 &&
+      k <= 4096 && blocked_pipeline_enabled()) {
+    // eligibility of the tensor-core F16S path is a property of shapes/alignment
+    // only; 16-byte aligned stand-ins decide it before any device allocation
+    const float* al = reinterpret_cast<const float*>(uintptr_t(256));
+    const int v = variant == MTNN_VARIANT_AUTO ? auto_variant(al, al, const_cast<float*>(al), m, n, k, true)
+                                               : variant;
+    if (v == MTNN_VARIANT_TC3XF16S && tc_eligible(al, al, const_cast<float*>(al), m, n, k, true, TcKind::F16S)) {
+      const int conv = tc_inkernel_operand(m, n, true, TcKind::F16S);
+      if (conv != 1) return host_gemm_nt_blocked(A, B, C, m, n, k, conv);
+    }
+  }
   if (bytes < pipe_min_bytes() || m < 256 || k == 0 || n == 0) {
     // small problem: one serial round trip
     return host_call(A, m * k, B, n * k, C, m * n,
@@ -431,6 +589,11 @@ int mtnn_config_set(const char* key, int64_t value) {
     set_f16s_inkernel_max_short(value);
     return MTNN_OK;
   }
+  if (strcmp(key, "host_pipeline_blocked") == 0) {
+    if (value != 0 && value != 1) return fail(MTNN_EINVAL, "host_pipeline_blocked must be 0 or 1");
+    g_pipe_blocked.store((int)value, std::memory_order_relaxed);
+    return MTNN_OK;
+  }
   return fail(MTNN_EINVAL, "unknown config key '%s'", key);
 }
 
@@ -438,6 +601,10 @@ int mtnn_config_get(const char* key, int64_t* value) {
   if (!key || !value) return fail(MTNN_EINVAL, "null argument");
   if (strcmp(key, "f16s_inkernel_max_short") == 0) {
     *value = f16s_inkernel_max_short();
+    return MTNN_OK;
+  }
+  if (strcmp(key, "host_pipeline_blocked") == 0) {
+    *value = blocked_pipeline_enabled() ? 1 : 0;
     return MTNN_OK;
   }
   return fail(MTNN_EINVAL, "unknown config key '%s'", key);
