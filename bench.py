@@ -418,16 +418,17 @@ def main():
     peaks_path = ROOT / "MEASURED_PEAKS.json"
     peaks = json.loads(peaks_path.read_text()) if peaks_path.exists() else {}
     bf16 = peaks.get("bf16_tflops", 1590.0)
-    # a sweep/fcn/large step keeps the tensor cores busy for 10s-100s of ms under
-    # the board power cap: the sustained bf16 figure is the roof for a kernel
-    # timed inside such a step (B200_PROFILING.md); the burst one is listed too
+    # roof = the burst bf16 figure: the sweep step is 10s-100s of ms of GEMMs
+    # separated by flushes and spin kernels, and boxes that stay cool run it above
+    # the 4 s back-to-back "sustained" cuBLAS figure (frac > 1 seen), so only the
+    # burst figure bounds it; the sustained fraction is listed beside it
     bf16_sus = peaks.get("bf16_tflops_sustained", bf16)
     hbm = peaks.get("hbm_gbs", 6650.0)
     tc_class = max((_lib.KCLASS_GEMM_TC_F16S, _lib.KCLASS_GEMM_TC), key=lambda c: prof[c][0])
     tc_ms, tc_n, tc_work = prof[tc_class]
     f16s = tc_class == _lib.KCLASS_GEMM_TC_F16S
-    roof = bf16_sus / 3.0 if f16s else bf16_sus / 6.0
-    roof_burst = bf16 / 3.0 if f16s else bf16 / 6.0
+    roof = bf16 / 3.0 if f16s else bf16 / 6.0
+    roof_sus = bf16_sus / 3.0 if f16s else bf16_sus / 6.0
     ncu_path = ROOT / "profiles" / "ncu_summary.json"
     ncu_traffic = json.loads(ncu_path.read_text()).get("gemm_tc3x_traffic", {}) if ncu_path.exists() else {}
     dominant = max(prof_all, key=lambda c: prof_all[c][0])
@@ -439,12 +440,11 @@ def main():
         "traffic": ncu_traffic.get("traffic"),
         "traffic_launch": ncu_traffic.get("launch"),
         "traffic_algorithmic_bytes": ncu_traffic.get("algorithmic_bytes"),
-        "peak_basis": (f"FP32-accurate roof = measured bf16 dense {bf16_sus} TFLOP/s (MEASURED_PEAKS.json, "
-                       f"sustained: the kernel runs inside a long back-to-back step) / 3 MMAs per "
-                       f"product (fp16 = bf16 rate)" if f16s else
-                       f"3xTF32 FP32-accurate roof = measured bf16 dense {bf16_sus} TFLOP/s "
-                       f"(MEASURED_PEAKS.json, sustained) / 2 (tf32 rate) / 3 (MMAs per product)"),
-        "peak_burst": roof_burst, "frac_of_burst": achieved / roof_burst if achieved else None,
+        "peak_basis": (f"FP32-accurate roof = measured bf16 dense {bf16} TFLOP/s (MEASURED_PEAKS.json, "
+                       f"burst) / 3 MMAs per product (fp16 = bf16 rate)" if f16s else
+                       f"3xTF32 FP32-accurate roof = measured bf16 dense {bf16} TFLOP/s "
+                       f"(MEASURED_PEAKS.json, burst) / 2 (tf32 rate) / 3 (MMAs per product)"),
+        "peak_sustained": roof_sus, "frac_of_sustained": achieved / roof_sus if achieved else None,
         "launches": tc_n, "avg_launch_ms": tc_ms / tc_n if tc_n else None,
         "share_of_step": tc_ms / 1e3 / (device_s * 1.0) if device_s else None,
         "dominant_kernel_by_time": _lib.KCLASS_NAMES[dominant],
