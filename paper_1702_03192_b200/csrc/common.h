@@ -72,6 +72,8 @@ int launch_gemm_ffma(const float* A, const float* B, float* C, int64_t m, int64_
 enum class TcKind { TF32, F16S };
 int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t n,
                    int64_t k, bool b_is_nk, TcKind kind, cudaStream_t s);
+bool tc_eligible_operands(const float* A, const float* B, int64_t m, int64_t n, int64_t k,
+                          bool b_is_nk, TcKind kind);
 bool tc_eligible(const float* A, const float* B, const float* C, int64_t m, int64_t n,
                  int64_t k, bool b_is_nk, TcKind kind);
 // Prepared (split) tensor-core operand: hi/lo halves, plus 1/scale per row for F16S.
@@ -94,8 +96,9 @@ int tc_inkernel_operand(int64_t m, int64_t n, bool b_is_nk, TcKind kind);
 // Run-time knob (mtnn_config_set): largest output short side split in-kernel.
 int64_t f16s_inkernel_max_short();
 void set_f16s_inkernel_max_short(int64_t v);
+// ldc: C row stride in elements (-1 = n); a larger one pads each C row.
 int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n, int64_t k,
-           bool b_is_nk, TcKind kind, cudaStream_t s);
+           bool b_is_nk, TcKind kind, cudaStream_t s, int64_t ldc = -1);
 int launch_split_rows_f16(const float* x, void* hi, void* lo, float* inv_scale, int64_t rows,
                           int64_t k, cudaStream_t s);
 // Both K-major operands of one GEMM in one launch: rows of x0 then x1 (same k);

@@ -281,6 +281,7 @@ __host__ __device__ constexpr uint32_t make_idesc(int n, bool b_mn_major, uint32
 
 struct Params {
   int64_t m, n, k;
+  int64_t ldc;   // C row stride in elements (>= n; > n for a row-padded output)
   int chunk_kb;  // k-blocks per TMEM accumulation chunk (FP32 promotion period)
   int tiles_m, tiles_n, splits, kblocks_per_split, total_kblocks;
   int units;
@@ -836,8 +837,8 @@ static int launch_impl(const void* ahi, const void* alo, const void* bhi,
   }
   encode_dtype = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   {
-    const uint64_t dims[3] = {(uint64_t)p.n, (uint64_t)p.m, (uint64_t)p.splits};
-    const uint64_t str[2] = {(uint64_t)p.n * 4, (uint64_t)p.n * p.m * 4};
+    const uint64_t dims[3] = {(uint64_t)p.ldc, (uint64_t)p.m, (uint64_t)p.splits};
+    const uint64_t str[2] = {(uint64_t)p.ldc * 4, (uint64_t)p.ldc * p.m * 4};
     const uint32_t box[3] = {16, 32, 1};
     MTNN_TRY(encode(&mc, out, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
   }
@@ -930,15 +931,24 @@ int tc_inkernel_operand(int64_t m, int64_t n, bool b_is_nk, TcKind kind) {
   return kind == TcKind::TF32 ? tf32_inkernel_operand(m, n) : f16s_inkernel_operand(m, n, b_is_nk);
 }
 
-bool tc_eligible(const float* A, const float* B, const float* C, int64_t m, int64_t n,
-                 int64_t k, bool b_is_nk, TcKind kind) {
+// Operands only: A and B (or B^T) can feed TMA (16-byte aligned bases and row
+// strides; F16S halves need k % 8; MN-major B^T needs n % 16 column groups).
+bool tc_eligible_operands(const float* A, const float* B, int64_t m, int64_t n, int64_t k,
+                          bool b_is_nk, TcKind kind) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (m <= 0 || n <= 0 || k <= 0) return false;
-  if (k % 4 != 0 || n % 4 != 0) return false;        // 16-byte TMA row strides (fp32)
+  if (k % 4 != 0) return false;                          // 16-byte TMA row strides (fp32)
   if (kind == TcKind::F16S && k % 8 != 0) return false;  // 16-byte rows of fp16 halves
-  if (!b_is_nk && n % 16 != 0) return false;         // MN-major column groups
+  if (!b_is_nk && n % 16 != 0) return false;             // MN-major column groups
   if (m > (1LL << 31) - 1 || n > (1LL << 31) - 1 || k > (1LL << 31) - 1) return false;
-  return al16(A) && al16(B) && al16(C);
+  return al16(A) && al16(B);
+}
+
+// Operands and C: C is stored by TMA too (n % 4, 16-byte aligned base).
+bool tc_eligible(const float* A, const float* B, const float* C, int64_t m, int64_t n,
+                 int64_t k, bool b_is_nk, TcKind kind) {
+  if (!tc_eligible_operands(A, B, m, n, k, b_is_nk, kind)) return false;
+  return n % 4 == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -1061,7 +1071,7 @@ static int choose_splits(int tiles, int kblocks, int64_t m, int64_t n, int sms) 
 
 template <int BN>
 static int tc_run_bn(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n,
-                     int64_t k, bool b_is_nk, TcKind kind, int conv, cudaStream_t s) {
+                     int64_t k, int64_t ldc, bool b_is_nk, TcKind kind, int conv, cudaStream_t s) {
   const DeviceInfo* di = nullptr;
   MTNN_TRY(device_info(&di));
   using S = tc::Smem<BN>;
@@ -1070,7 +1080,7 @@ static int tc_run_bn(const TcOperand& a, const TcOperand& b, float* C, int64_t m
                 di->max_smem_optin);
   const int bk = kind == TcKind::F16S ? tc::KindF16S::BK : tc::KindTF32::BK;
   tc::Params p{};
-  p.m = m; p.n = n; p.k = k;
+  p.m = m; p.n = n; p.k = k; p.ldc = ldc;
   p.chunk_kb = chunk_kblocks(kind);
   p.inv_scale_a = a.inv_scale;
   p.inv_scale_b = b.inv_scale;
@@ -1088,7 +1098,7 @@ static int tc_run_bn(const TcOperand& a, const TcOperand& b, float* C, int64_t m
   float* out = C;
   ScratchBuffer part;
   if (splits > 1) {
-    MTNN_TRY(part.alloc((size_t)splits * m * n * sizeof(float), s));
+    MTNN_TRY(part.alloc((size_t)splits * m * ldc * sizeof(float), s));
     out = static_cast<float*>(part.ptr);
   }
   int rc;
@@ -1117,14 +1127,14 @@ static int tc_run_bn(const TcOperand& a, const TcOperand& b, float* C, int64_t m
     rc = b_is_nk ? tc::launch_impl<BN, false, tc::KindTF32>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s)
                  : tc::launch_impl<BN, true, tc::KindTF32>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s);
   MTNN_TRY(rc);
-  if (splits > 1) MTNN_TRY(launch_splitk_reduce(out, C, m * n, splits, s));
+  if (splits > 1) MTNN_TRY(launch_splitk_reduce(out, C, m * ldc, splits, s));
   return MTNN_OK;
 }
 
 // N tile: 256 (UMMA N=256, best smem-read/MMA ratio) unless n <= 128, where a
 // 256-wide tile would waste half its MMAs on zero columns.
 int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n, int64_t k,
-           bool b_is_nk, TcKind kind, cudaStream_t s) {
+           bool b_is_nk, TcKind kind, cudaStream_t s, int64_t ldc) {
   // an operand without a lo half has it computed in-kernel (TF32 only, one operand)
   const int conv = a.lo == nullptr ? 1 : b.lo == nullptr ? 2 : 0;
   if (conv && a.lo == nullptr && b.lo == nullptr)
@@ -1133,21 +1143,31 @@ int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t 
     return fail(MTNN_EINVAL, "in-kernel F16S split needs the operand's row scales");
   // F16S in-kernel split: 128-wide N tile (raw slot + 4-stage ring fit the smem)
   if (n <= 128 || (conv && kind == TcKind::F16S))
-    return tc_run_bn<128>(a, b, C, m, n, k, b_is_nk, kind, conv, s);
-  return tc_run_bn<256>(a, b, C, m, n, k, b_is_nk, kind, conv, s);
+    return tc_run_bn<128>(a, b, C, m, n, k, ldc < n ? n : ldc, b_is_nk, kind, conv, s);
+  return tc_run_bn<256>(a, b, C, m, n, k, ldc < n ? n : ldc, b_is_nk, kind, conv, s);
 }
 
 int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t n,
                    int64_t k, bool b_is_nk, TcKind kind, cudaStream_t s) {
   const char* name = kind == TcKind::F16S ? "tc3xf16s" : "tc3xtf32";
-  if (!tc_eligible(A, B, C, m, n, k, b_is_nk, kind))
+  if (!tc_eligible_operands(A, B, m, n, k, b_is_nk, kind))
     return fail(MTNN_ENOTSUP, "%s: shape/alignment not eligible (m=%lld n=%lld k=%lld)", name,
                 (long long)m, (long long)n, (long long)k);
-  ScratchBuffer wa, wb;
+  ScratchBuffer wa, wb, wc;
   TcOperand a{}, b{};
   const int conv = tc_inkernel_operand(m, n, b_is_nk, kind);
   MTNN_TRY(tc_prepare_pair(A, m, B, n, k, !b_is_nk, kind, conv, wa, wb, &a, &b, s));
-  return tc_run(a, b, C, m, n, k, b_is_nk, kind, s);
+  if (tc_eligible(A, B, C, m, n, k, b_is_nk, kind)) return tc_run(a, b, C, m, n, k, b_is_nk, kind, s);
+  // C cannot be a TMA store target (n % 4 != 0, e.g. a 10-class output layer, or
+  // an unaligned base): compute into a row-padded buffer and copy the n columns
+  // out (B's missing rows are TMA zero fill, so the padding columns are zeros)
+  const int64_t np = (n + 3) / 4 * 4;
+  MTNN_TRY(wc.alloc((size_t)(m * np) * sizeof(float), s));
+  float* cp = static_cast<float*>(wc.ptr);
+  MTNN_TRY(tc_run(a, b, cp, m, n, k, b_is_nk, kind, s, np));
+  MTNN_CUDA_TRY(cudaMemcpy2DAsync(C, (size_t)n * 4, cp, (size_t)np * 4, (size_t)n * 4, (size_t)m,
+                                  cudaMemcpyDeviceToDevice, s));
+  return MTNN_OK;
 }
 
 }  // namespace mtnn

@@ -118,8 +118,9 @@ static int check_dims(int64_t m, int64_t n, int64_t k) {
 static int auto_variant(const float* A, const float* B, const float* C, int64_t m, int64_t n,
                         int64_t k, bool b_is_nk) {
   if ((double)m * (double)n * (double)k < 4194304.0) return MTNN_VARIANT_FFMA;
-  if (tc_eligible(A, B, C, m, n, k, b_is_nk, TcKind::F16S)) return MTNN_VARIANT_TC3XF16S;
-  if (tc_eligible(A, B, C, m, n, k, b_is_nk, TcKind::TF32)) return MTNN_VARIANT_TC3XTF32;
+  // (an ineligible C — n % 4 != 0 or unaligned — is handled by a padded output)
+  if (tc_eligible_operands(A, B, m, n, k, b_is_nk, TcKind::F16S)) return MTNN_VARIANT_TC3XF16S;
+  if (tc_eligible_operands(A, B, m, n, k, b_is_nk, TcKind::TF32)) return MTNN_VARIANT_TC3XTF32;
   return MTNN_VARIANT_FFMA;
 }
 
@@ -427,8 +428,9 @@ static int host_gemm(const float* A, const float* B, float* C, int64_t m, int64_
       if (conv != 1) return host_gemm_nt_blocked(A, B, C, m, n, k, conv);
     }
   }
-  if (bytes < pipe_min_bytes() || m < 256 || k == 0 || n == 0) {
-    // small problem: one serial round trip
+  if (bytes < pipe_min_bytes() || m < 256 || k == 0 || n == 0 || n % 4 != 0) {
+    // small problem (or rows of C that TMA cannot store in place, n % 4 != 0:
+    // the device path pads them): one serial round trip
     return host_call(A, m * k, B, n * k, C, m * n,
                      [&](const float* a, const float* b, float* c, cudaStream_t s) {
                        if (path == HostPath::TNN) return tnn_device(a, b, c, m, n, k, variant, -1, s);
