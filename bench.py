@@ -198,7 +198,8 @@ def lpt_assign(costs, world):
 
 def build_workload(args, rank, world):
     """Per-step call list for this rank: (op, m, n, k, flush_before).
-    op: "nt" = MTNN-dispatched NT, "nn" = NN product."""
+    op: "nt" = MTNN-dispatched NT, "nn" = NN product, "grad" = an FCN weight-gradient
+    NT (MTNN-dispatched into its own buffer; all-reduced across ranks when N > 1)."""
     if args.workload == "sweep":
         shapes = grid(args.exp_min, args.exp_max)
         owner = lpt_assign([2.0 * m * n * k for m, n, k in shapes], world)
@@ -215,11 +216,13 @@ def build_workload(args, rank, world):
         calls = [("nt", batch, dout, din, i == 0) for i, (din, dout) in enumerate(layers)]
         for j, (din, dout) in enumerate(reversed(layers)):
             calls.append(("nn", batch, din, dout, j == 0))
-            calls.append(("nt", dout, din, batch, False))
+            calls.append(("grad", dout, din, batch, False))  # weight gradient (an NT)
         total = sum(2.0 * m * n * k for _, m, n, k, _ in calls) * world
         desc = ("fcn_step 784-4096-4096-4096-10 batch 1024 (configs[3]): 4 forward NT + 4 backward "
                 "NN + 4 backward NT, all NT through MTNN (the reference routes only forward NT)")
-        par = "single GPU" if world == 1 else f"{world} independent replicas"
+        par = ("single GPU" if world == 1 else
+               f"data parallel x{world}: batch 1024 per GPU, weight gradients all-reduced (NCCL, "
+               f"overlapped with the remaining backward GEMMs)")
         return calls, total, desc, ("weak" if world > 1 else "strong"), par, None
     # large (config 5): m = 65536 rows of A sharded, B replicated
     from paper_1702_03192_b200.sharding import row_range
@@ -306,10 +309,21 @@ def main():
     stream = torch.cuda.current_stream(dev).cuda_stream
     choice = ctypes.c_int()
 
-    def run_call(op, m, n, k):
+    # FCN weight gradients get their own buffers (all-reduced across ranks while
+    # later backward GEMMs run)
+    grad_bufs = {}
+    if args.workload == "fcn":
+        for i, (op, m, n, k, _) in enumerate(calls):
+            if op == "grad":
+                grad_bufs[i] = torch.empty(m * n, device=dev)
+
+    def run_call(op, m, n, k, out=None):
         if m <= 0:
             return
-        if op == "nt":
+        if op == "grad":
+            rc = L.mtnn_dispatch_gemm(handle, prefix_p, A.data_ptr(), B.data_ptr(), out.data_ptr(),
+                                      m, n, k, -1, 0, stream, ctypes.byref(choice))
+        elif op == "nt":
             rc = L.mtnn_dispatch_gemm(handle, prefix_p, A.data_ptr(), B.data_ptr(), C.data_ptr(),
                                       m, n, k, -1, 0, stream, ctypes.byref(choice))
         else:
@@ -317,7 +331,9 @@ def main():
         if rc:
             _lib.check(rc)
 
-    comm = {"bcast": [], "gather": []}
+    comm = {"bcast": [], "gather": [], "allreduce": []}
+
+    from paper_1702_03192_b200.sharding import allreduce_weight_grad as allreduce_grad
 
     def one_step(events=None):
         if args.workload == "large" and world > 1:
@@ -329,7 +345,8 @@ def main():
             if events is not None:
                 comm["bcast"].append(ev)
                 events.append(ev)
-        for (op, m, n, k, fl) in calls:
+        works = []
+        for i, (op, m, n, k, fl) in enumerate(calls):
             if fl:
                 flush_src.sum()
             # keep the GPU busy while the host enqueues the timed call, so the
@@ -339,11 +356,25 @@ def main():
                 s = torch.cuda.Event(enable_timing=True)
                 e = torch.cuda.Event(enable_timing=True)
                 s.record()
-                run_call(op, m, n, k)
+                run_call(op, m, n, k, grad_bufs.get(i))
                 e.record()
                 events.append((s, e))
             else:
-                run_call(op, m, n, k)
+                run_call(op, m, n, k, grad_bufs.get(i))
+            if op == "grad" and world > 1:
+                works.append(allreduce_grad(grad_bufs[i]))
+        if args.workload == "fcn" and world > 1:
+            # the all-reduces still in flight after the last GEMM: their tail is
+            # part of the step
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
+            for w in works:
+                if w is not None:
+                    w.wait()
+            ev[1].record()
+            if events is not None:
+                comm["allreduce"].append(ev)
+                events.append(ev)
         if args.workload == "large" and world > 1:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record()
@@ -407,6 +438,8 @@ def main():
         for i in range(len(events) // args.steps)]
     if world > 1 and args.workload == "large":
         per_call = per_call[1:-1]  # drop the collective windows
+    if world > 1 and args.workload == "fcn":
+        per_call = per_call[:-1]
 
     if rank != 0:
         if world > 1:
@@ -458,7 +491,7 @@ def main():
     if args.workload == "sweep" and world == 1:
         extra.update(sweep_oracle_pass(shapes, per_call, A, B, C, flush_src, stream, disp,
                                        total_flops, roof, L, _lib, torch))
-    if args.workload == "large" and world > 1:
+    if args.workload in ("large", "fcn") and world > 1:
         extra["collective_ms_per_step"] = {
             k: statistics.mean(s.elapsed_time(e) for s, e in v) for k, v in comm.items() if v}
     if world == 1:
@@ -608,7 +641,7 @@ def run_e2e(args, calls, handle, prefix_p, L):
 
     def step():
         for (op, m, n, k, _) in calls:
-            if op == "nt":
+            if op in ("nt", "grad"):
                 rc = L.mtnn_dispatch_gemm_host(handle, prefix_p, ha.data_ptr(), hb.data_ptr(),
                                                hc.data_ptr(), m, n, k, -1, 0, ctypes.byref(ch))
             else:

@@ -107,3 +107,46 @@ def sharded_gemm_nt(
     c_local = gemm(a_local, b_rep) if hi > lo else torch.empty((0, n), dtype=torch.float32,
                                                                  device=a_local.device)
     return gather_rows(c_local, m, group=group) if gather else c_local
+
+
+# ------------------------------------------------------------------ FC layers
+# Data-parallel FC training step (SURVEY §8e "FC batches"): each rank runs the
+# layer GEMMs on its own batch rows — the forward NT (b_r, dout, din) is a
+# row-sharded product with the weights replicated — and the weight-gradient NT
+# (dout, din, b_r) contracts over the batch, so the per-rank partial gradients
+# are summed by one all-reduce (the path's only exchange step besides B's
+# replication).
+
+
+def allreduce_weight_grad(grad: torch.Tensor, *, group=None, async_op: bool = True):
+    """Sum a weight gradient over the ranks of `group`, in place.
+
+    NCCL: asynchronous (returns the work handle; NCCL's stream waits for the
+    GEMM that wrote `grad`, so later GEMMs overlap it — call ``wait()`` before
+    using `grad`). Other backends (gloo test mode): synchronous through host
+    memory, returns None.
+    """
+    if dist.get_backend(group) == "nccl":
+        return dist.all_reduce(grad, group=group, async_op=async_op)
+    t = grad.detach().cpu() if grad.is_cuda else grad
+    dist.all_reduce(t, group=group)
+    if t is not grad:
+        grad.copy_(t)
+    return None
+
+
+def dp_weight_grad(dz_local: torch.Tensor, x_local: torch.Tensor, *, group=None,
+                   gemm: Callable | None = None, variant: str = "auto") -> torch.Tensor:
+    """dW = Σ_ranks dZ_rᵀ·X_r for one FC layer (dout x din).
+
+    dz_local: this rank's (dout x b_r) output-gradient block (batch on columns,
+    the reference's "nt-fixed" operand layout, fcn.py:191), x_local: its
+    (din x b_r) input block. Local NT product (dout, din, b_r), then the
+    all-reduce; returns the summed gradient on every rank.
+    """
+    gemm = gemm or _default_gemm(variant)
+    g = gemm(dz_local.contiguous(), x_local.contiguous())
+    work = allreduce_weight_grad(g, group=group)
+    if work is not None:
+        work.wait()
+    return g

@@ -71,3 +71,39 @@ def test_sharded_nt_world2_gloo(m, gather):
     for rank, err, shape_ok in results:
         assert shape_ok, rank
         assert err < 1e-6, (rank, err)
+
+
+def _dp_worker(rank, world, port, dout, din, batch, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1702_03192_b200.sharding import dp_weight_grad
+
+        g = torch.Generator().manual_seed(11)
+        dz = torch.rand(dout, batch, generator=g) * 2 - 1   # full batch, same on every rank
+        x = torch.rand(din, batch, generator=g) * 2 - 1
+        lo, hi = row_range(batch, rank, world)               # this rank's batch columns
+        dw = dp_weight_grad(dz[:, lo:hi], x[:, lo:hi], gemm=lambda a, b: a @ b.t())
+        want = dz.double() @ x.double().t()
+        q.put((rank, float((dw.double() - want).norm() / want.norm())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("batch", [64, 37])
+def test_dp_weight_grad_world2_gloo(batch):
+    """Data-parallel FC step: per-rank weight gradients over batch shards,
+    summed by the all-reduce, equal the full-batch gradient."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dp_worker, args=(r, world, port, 24, 40, batch, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, err in res:
+        assert err < 1e-6, (rank, err)

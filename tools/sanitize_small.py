@@ -1,0 +1,21 @@
+"""Small calls through every kernel family, for compute-sanitizer runs."""
+import sys, numpy as np
+sys.path.insert(0, ".")
+import oracle
+from paper_1702_03192_b200 import _lib, gemm_nt, gemm_nn, gemm_tnn, transpose_oop
+rng = np.random.default_rng(5)
+for (m, n, k) in [(128, 2048, 256), (2048, 128, 256), (300, 1100, 520), (256, 384, 264), (1024, 10, 512), (130, 260, 64)]:
+    a = rng.uniform(-1, 1, (m, k)).astype(np.float32); b = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    want = oracle.oracle_nt_blas(a, b)
+    for v in ("auto", "tc3xf16s", "tc3xtf32", "ffma"):
+        for fn in (gemm_nt, gemm_tnn):
+            try:
+                got = fn(a, b, variant=v)
+            except Exception as e:
+                print("skip", (m, n, k), v, fn.__name__, type(e).__name__); continue
+            assert oracle.rel_frobenius(got, want) < 1e-5, ((m, n, k), v, fn.__name__)
+    if n % 16 == 0:
+        got = gemm_nn(a, np.ascontiguousarray(b.T))
+        assert oracle.rel_frobenius(got, want) < 1e-5
+    assert np.array_equal(transpose_oop(b), b.T)
+print("sanitize run ok")
