@@ -101,6 +101,11 @@ int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* w
  *   Default 256, the best on the B200 sweep (env MTNN_F16S_INKERNEL_MAX,
  *   MTNN_F16S_INKERNEL=0 disables). The halves equal the split pass's; only
  *   the output tiling (and so the split-K order) may differ.
+ * "tc_pair": 1 (default; env MTNN_TC_PAIR=0 turns it off): NT problems with
+ *   >= 74 256x256 output tiles run on CTA pairs (tcgen05 cta_group::2, M = 256,
+ *   each CTA loading half of B); 2 forces it whenever structurally possible
+ *   (tests), 0 keeps the single-CTA 128x256 tiles. Bit-identical results at the
+ *   same split-K.
  * "host_pipeline_blocked": 1 (default; env MTNN_PIPE_BLOCKED=0 turns it off):
  *   host-buffer NT calls on the tc3xf16s path with n >= 1024, k <= 4096 stream B in row
  *   blocks against A's first row block so C leaves while B arrives; 0 = copy B

@@ -284,6 +284,8 @@ struct Params {
   int64_t ldc;   // C row stride in elements (>= n; > n for a row-padded output)
   int chunk_kb;  // k-blocks per TMEM accumulation chunk (FP32 promotion period)
   int tiles_m, tiles_n, splits, kblocks_per_split, total_kblocks;
+  int tiles_mp;  // CTA-pair kernel: pairs of m-tiles
+  int group_m;   // CTA-pair kernel: m-tile pairs per raster group
   int units;
   const float* inv_scale_a;  // KindF16S: 1/s per row of A (m) and of B (n)
   const float* inv_scale_b;
@@ -858,6 +860,365 @@ static int launch_impl(const void* ahi, const void* alo, const void* bhi,
   return MTNN_OK;
 }
 
+
+// ======================================================================
+// CTA-pair variant (tcgen05 cta_group::2): a cluster of two CTAs on one TPC
+// computes a 256 x 256 output tile with M = 256 MMAs issued by the leader CTA.
+// Each CTA loads its own 128 rows of A and HALF (128 rows) of the tile's B, so
+// per SM the smem/L2 operand traffic per flop drops by a third against the
+// 128 x 256 single-CTA tile (A 128 + B 256 rows per 128 x 256 outputs -> A 128 +
+// B 128), and each wave of 74 pair tiles touches half as many B panels, which
+// halves the DRAM re-reads. Per CTA: 6-stage ring of 32 KiB stages (A h/l +
+// half-B h/l), 2 x 256 TMEM columns (its 128 rows of the double-buffered
+// accumulator), the same FP32-promotion epilogue on its own rows.
+// Barriers: full[s] lives in the leader (2 arrivals: the leader's expect_tx and
+// the peer's remote arrive; both CTAs' TMA bytes complete on it); the leader's
+// commits multicast to empty[s] / tfull[] in both CTAs; tempty[] in the leader
+// counts the epilogue warps of both CTAs.
+constexpr int kPairStages = 6;
+constexpr int kPairBN = 256;            // output tile N (both CTAs)
+constexpr int kPairHalfN = kPairBN / 2;  // B rows loaded per CTA
+struct PairSmem {
+  static constexpr int kABytes = BM * 64;
+  static constexpr int kBBytes = kPairHalfN * 64;
+  static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;  // 32 KiB
+  static constexpr int kRingBytes = kPairStages * kStageBytes;
+  static constexpr int kStagingBytes = 32 * 16 * 4;
+  static constexpr int kEpiBytes = kEpiWarps * kStagingBytes;
+  static constexpr int kBarBytes = 256;
+  static constexpr int kTotal = 1024 + kRingBytes + kEpiBytes + kBarBytes;
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+// arrive on the barrier at the same offset in cluster CTA `cta`
+__device__ __forceinline__ void mbar_arrive_cta(uint32_t bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(bar),
+      "r"(cta)
+      : "memory");
+}
+// 2-SM TMA load: lands in this CTA's smem, completes on the LEADER's barrier
+// (peer bit of the cluster address cleared)
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map,
+                                                 uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+      : "memory");
+}
+template <bool kF16>
+__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  const uint32_t z = 0;
+  if constexpr (kF16) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n\t}" ::"r"(
+            tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(z)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n\t}" ::"r"(
+            tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(z)
+        : "memory");
+  }
+}
+// commit this CTA's outstanding MMAs; arrive on the barrier in both CTAs
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .b16 msk;\n\t"
+      "mov.b16 msk, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], msk;\n\t}" ::"r"(bar)
+      : "memory");
+}
+
+// units are (k-split, pair tile); pair tile = (pair of m-tiles, n-tile), grouped
+// raster over kGroupM / 2 pairs (the same 16 m-tiles as the single-CTA order)
+__device__ __forceinline__ void pair_unit_coords(int u, const Params& p, int& split, int& tmp,
+                                                 int& tn) {
+  const int tiles = p.tiles_mp * p.tiles_n;
+  split = u / tiles;
+  const int t = u - split * tiles;
+  const int kGroupP = p.group_m;
+  const int per_group = kGroupP * p.tiles_n;
+  const int group = t / per_group;
+  const int first = group * kGroupP;
+  const int gm = min(kGroupP, p.tiles_mp - first);
+  const int r = t - group * per_group;
+  tmp = first + r % gm;
+  tn = r / gm;
+}
+
+template <class Kind>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
+                      const __grid_constant__ CUtensorMap map_alo,
+                      const __grid_constant__ CUtensorMap map_bhi,
+                      const __grid_constant__ CUtensorMap map_blo,
+                      const __grid_constant__ CUtensorMap map_c, const Params p) {
+  using S = PairSmem;
+  constexpr int BN = kPairBN;
+  constexpr int kColsPerWarp = BN / 4;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* ring = smem;
+  uint8_t* epi = smem + S::kRingBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi + S::kEpiBytes);
+  uint64_t* full_bar = bars;                          // [kPairStages] (leader's used)
+  uint64_t* empty_bar = bars + kPairStages;           // [kPairStages]
+  uint64_t* tfull_bar = bars + 2 * kPairStages;       // [2]
+  uint64_t* tempty_bar = bars + 2 * kPairStages + 2;  // [2] (leader's used)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kPairStages + 4);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x / 2;
+  const int nclusters = gridDim.x / 2;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ahi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_alo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_c)) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kPairStages; ++s) {
+      mbar_init(smem_u32(&full_bar[s]), 2);
+      mbar_init(smem_u32(&empty_bar[s]), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(smem_u32(&tfull_bar[s]), 1);
+      mbar_init(smem_u32(&tempty_bar[s]), 2 * kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int kb_per = p.kblocks_per_split;
+
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs) =====================
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = cluster; u < p.units; u += nclusters) {
+        int split, tmp, tn;
+        pair_unit_coords(u, p, split, tmp, tn);
+        const int tm = 2 * tmp + (int)rank;
+        const int kb0 = split * kb_per;
+        const int kb1 = min(p.total_kblocks, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+          const uint32_t fb = smem_u32(&full_bar[stage]);
+          const uint32_t st = smem_u32(ring + stage * S::kStageBytes);
+          const int kx = kb * Kind::BK;
+          const int brow = tn * BN + (int)rank * kPairHalfN;
+          tma_load_2d_pair(st, &map_ahi, fb, kx, tm * BM);
+          tma_load_2d_pair(st + S::kABytes, &map_alo, fb, kx, tm * BM);
+          tma_load_2d_pair(st + 2 * S::kABytes, &map_bhi, fb, kx, brow);
+          tma_load_2d_pair(st + 2 * S::kABytes + S::kBBytes, &map_blo, fb, kx, brow);
+          if (leader) mbar_expect_tx(fb, 2 * S::kStageBytes);  // both CTAs' bytes
+          else mbar_arrive_cta(fb, 0);
+          if (++stage == kPairStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA) =====================
+    if (leader) {
+      constexpr uint32_t idesc = (1u << 4) | (Kind::kFmt << 7) | (Kind::kFmt << 10) |
+                                 ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = cluster; u < p.units; u += nclusters) {
+        const int split = u / (p.tiles_mp * p.tiles_n);
+        const int kb0 = split * kb_per;
+        const int kb1 = min(p.total_kblocks, kb0 + kb_per);
+        for (int kc = kb0; kc < kb1; kc += p.chunk_kb) {
+          const int kce = min(kb1, kc + p.chunk_kb);
+          mbar_wait(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
+          tc_fence_after();
+          const uint32_t tmem_d = tmem_base + acc * BN;
+          for (int kb = kc; kb < kce; ++kb) {
+            mbar_wait(smem_u32(&full_bar[stage]), phase);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint32_t a_hi = smem_u32(ring + stage * S::kStageBytes);
+              const uint32_t a_lo = a_hi + S::kABytes;
+              const uint32_t b_hi = a_hi + 2 * S::kABytes;
+              const uint32_t b_lo = b_hi + S::kBBytes;
+#pragma unroll
+              for (int ks = 0; ks < Kind::BK / Kind::UMMA_K; ++ks) {
+                const uint64_t dah = make_sdesc(a_hi + ks * 32, 16, 512, kLayoutSW64);
+                const uint64_t dal = make_sdesc(a_lo + ks * 32, 16, 512, kLayoutSW64);
+                const uint64_t dbh = make_sdesc(b_hi + ks * 32, 16, 512, kLayoutSW64);
+                const uint64_t dbl = make_sdesc(b_lo + ks * 32, 16, 512, kLayoutSW64);
+                const uint32_t accum = (kb == kc && ks == 0) ? 0u : 1u;
+                tc_mma_pair<Kind::kScaled>(tmem_d, dal, dbh, idesc, accum);
+                tc_mma_pair<Kind::kScaled>(tmem_d, dah, dbl, idesc, 1u);
+                tc_mma_pair<Kind::kScaled>(tmem_d, dah, dbh, idesc, 1u);
+              }
+              tc_commit_pair(smem_u32(&empty_bar[stage]));
+              if (kb == kce - 1) tc_commit_pair(smem_u32(&tfull_bar[acc]));
+            }
+            __syncwarp();
+            if (++stage == kPairStages) { stage = 0; phase ^= 1; }
+          }
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ===================== epilogue (both CTAs, own 128 rows) =====================
+    const int e = warp - kEpiWarp0;
+    const int q = warp % 4;
+    const int h = e / 4;
+    uint8_t* stg = epi + e * S::kStagingBytes;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = cluster; u < p.units; u += nclusters) {
+      int split, tmp, tn;
+      pair_unit_coords(u, p, split, tmp, tn);
+      const int tm = 2 * tmp + (int)rank;
+      const int kb0 = split * kb_per;
+      const int kb1 = min(p.total_kblocks, kb0 + kb_per);
+      float sum[kColsPerWarp];
+#pragma unroll
+      for (int j = 0; j < kColsPerWarp; ++j) sum[j] = 0.f;
+      for (int kc = kb0; kc < kb1; kc += p.chunk_kb) {
+        mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + h * kColsPerWarp;
+#pragma unroll
+        for (int c = 0; c < kColsPerWarp / 16; ++c) {
+          uint32_t r[16];
+          tmem_ld_32x32b_x16(taddr + c * 16, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) sum[c * 16 + j] += __uint_as_float(r[j]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cta(smem_u32(&tempty_bar[acc]), 0);  // the leader's
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+      const int64_t row = (int64_t)tm * BM + q * 32 + lane;
+      const int64_t col0 = (int64_t)tn * BN + h * kColsPerWarp;
+      const float sa = (Kind::kScaled && row < p.m) ? __ldg(p.inv_scale_a + row) : 1.f;
+#pragma unroll
+      for (int c = 0; c < kColsPerWarp / 16; ++c) {
+        if (lane == 0) tma_store_wait_read<0>();
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int pj = j ^ ((lane >> 1) & 3);
+          float4 v = make_float4(sum[c * 16 + 4 * j], sum[c * 16 + 4 * j + 1],
+                                 sum[c * 16 + 4 * j + 2], sum[c * 16 + 4 * j + 3]);
+          if (Kind::kScaled) {
+            const int64_t cj = col0 + c * 16 + 4 * j;
+            const float4 sb = cj < p.n ? __ldg(reinterpret_cast<const float4*>(p.inv_scale_b + cj))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+            v.x = (v.x * sa) * sb.x;
+            v.y = (v.y * sa) * sb.y;
+            v.z = (v.z * sa) * sb.z;
+            v.w = (v.w * sa) * sb.w;
+          }
+          *reinterpret_cast<float4*>(stg + lane * 64 + pj * 16) = v;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&map_c, smem_u32(stg), tn * BN + h * kColsPerWarp + c * 16,
+                       tm * BM + q * 32, split);
+          tma_store_commit();
+        }
+      }
+    }
+    if (lane == 0) tma_store_wait_all();
+  }
+
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs done with the accumulator before it is freed
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(2 * BN));
+  }
+}
+
+template <class Kind>
+static int launch_pair_impl(const void* ahi, const void* alo, const void* bhi, const void* blo,
+                            float* out, const Params& p, int clusters, cudaStream_t s) {
+  using S = PairSmem;
+  CUtensorMap mah, mal, mbh, mbl, mc;
+  const uint64_t eb = Kind::kElemBytes;
+  encode_dtype = Kind::kTmaType;
+  {
+    const uint64_t dims[2] = {(uint64_t)p.k, (uint64_t)p.m};
+    const uint64_t str[1] = {(uint64_t)p.k * eb};
+    const uint32_t box[2] = {(uint32_t)Kind::BK, BM};
+    MTNN_TRY(encode(&mah, ahi, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
+    MTNN_TRY(encode(&mal, alo, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)p.k, (uint64_t)p.n};
+    const uint64_t str[1] = {(uint64_t)p.k * eb};
+    const uint32_t box[2] = {(uint32_t)Kind::BK, (uint32_t)kPairHalfN};
+    MTNN_TRY(encode(&mbh, bhi, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
+    MTNN_TRY(encode(&mbl, blo, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
+  }
+  encode_dtype = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  {
+    const uint64_t dims[3] = {(uint64_t)p.ldc, (uint64_t)p.m, (uint64_t)p.splits};
+    const uint64_t str[2] = {(uint64_t)p.ldc * 4, (uint64_t)p.ldc * p.m * 4};
+    const uint32_t box[3] = {16, 32, 1};
+    MTNN_TRY(encode(&mc, out, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
+  }
+  auto kern = gemm_tc3x_pair_kernel<Kind>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    MTNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       S::kTotal));
+    attr_set = true;
+  }
+  {
+    KernelTimer timer(Kind::kScaled ? MTNN_KCLASS_GEMM_TC_F16S : MTNN_KCLASS_GEMM_TC,
+                      2.0 * (double)p.m * (double)p.n * (double)p.k, s);
+    kern<<<2 * clusters, kThreads, S::kTotal, s>>>(mah, mal, mbh, mbl, mc, p);
+  }
+  MTNN_CUDA_TRY(cudaGetLastError());
+  return MTNN_OK;
+}
 }  // namespace tc
 
 // Split mode: "trunc" (default, lo only; the tensor core truncates the raw
@@ -1069,6 +1430,65 @@ static int choose_splits(int tiles, int kblocks, int64_t m, int64_t n, int sms) 
   return best;
 }
 
+// CTA-pair kernel switch: mtnn_config_set("tc_pair", 0/1), env MTNN_TC_PAIR=0.
+static std::atomic<int> g_tc_pair{-1};
+// 0 = off, 1 = on for large problems (default), 2 = whenever structurally possible (tests)
+int tc_pair_mode() {
+  int v = g_tc_pair.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = getenv("MTNN_TC_PAIR");
+    v = (e && e[0] == '0') ? 0 : 1;
+    g_tc_pair.store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+void set_tc_pair_mode(int v) { g_tc_pair.store(v, std::memory_order_relaxed); }
+
+// 256 x 256 output tiles on CTA pairs (NT, pre-split operands).
+static int tc_run_pair(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n,
+                       int64_t k, int64_t ldc, TcKind kind, cudaStream_t s) {
+  const DeviceInfo* di = nullptr;
+  MTNN_TRY(device_info(&di));
+  if (di->max_smem_optin < tc::PairSmem::kTotal)
+    return fail(MTNN_ENOTSUP, "CTA-pair GEMM needs %d B smem, device allows %d",
+                tc::PairSmem::kTotal, di->max_smem_optin);
+  const int bk = kind == TcKind::F16S ? tc::KindF16S::BK : tc::KindTF32::BK;
+  tc::Params p{};
+  p.m = m; p.n = n; p.k = k; p.ldc = ldc;
+  p.chunk_kb = chunk_kblocks(kind);
+  p.inv_scale_a = a.inv_scale;
+  p.inv_scale_b = b.inv_scale;
+  p.tiles_m = (int)((m + tc::BM - 1) / tc::BM);
+  p.tiles_mp = (p.tiles_m + 1) / 2;
+  {
+    const char* e = getenv("MTNN_PAIR_GROUP");
+    const int g = e ? atoi(e) : 0;
+    p.group_m = g > 0 ? g : tc::kGroupM;  // 16 pairs = 32 m-tiles: least DRAM traffic measured
+  }
+  p.tiles_n = (int)((n + tc::kPairBN - 1) / tc::kPairBN);
+  p.total_kblocks = (int)((k + bk - 1) / bk);
+  const int pairs = di->sm_count / 2;
+  const int tiles = p.tiles_mp * p.tiles_n;
+  int splits = choose_splits(tiles, p.total_kblocks, m, n, pairs);
+  p.kblocks_per_split = (p.total_kblocks + splits - 1) / splits;
+  splits = (p.total_kblocks + p.kblocks_per_split - 1) / p.kblocks_per_split;
+  p.splits = splits;
+  p.units = tiles * splits;
+  const int clusters = std::min(p.units, pairs);
+  float* out = C;
+  ScratchBuffer part;
+  if (splits > 1) {
+    MTNN_TRY(part.alloc((size_t)splits * m * ldc * sizeof(float), s));
+    out = static_cast<float*>(part.ptr);
+  }
+  const int rc = kind == TcKind::F16S
+                     ? tc::launch_pair_impl<tc::KindF16S>(a.hi, a.lo, b.hi, b.lo, out, p, clusters, s)
+                     : tc::launch_pair_impl<tc::KindTF32>(a.hi, a.lo, b.hi, b.lo, out, p, clusters, s);
+  MTNN_TRY(rc);
+  if (splits > 1) MTNN_TRY(launch_splitk_reduce(out, C, m * ldc, splits, s));
+  return MTNN_OK;
+}
+
 template <int BN>
 static int tc_run_bn(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n,
                      int64_t k, int64_t ldc, bool b_is_nk, TcKind kind, int conv, cudaStream_t s) {
@@ -1141,6 +1561,12 @@ int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t 
     return fail(MTNN_EINVAL, "in-kernel operand split needs one prepared operand");
   if (conv && kind == TcKind::F16S && (conv == 1 ? a.inv_scale : b.inv_scale) == nullptr)
     return fail(MTNN_EINVAL, "in-kernel F16S split needs the operand's row scales");
+  // CTA pairs for NT problems with enough 256 x 256 tiles to fill the chip's 74 TPCs
+  // at least once (split-K would otherwise be needed for occupancy)
+  const int pair = tc_pair_mode();
+  if (conv == 0 && b_is_nk && n > 128 && m > 128 &&
+      (pair == 2 || (pair == 1 && ((m + 255) / 256) * ((n + 255) / 256) >= 74)))
+    return tc_run_pair(a, b, C, m, n, k, ldc < n ? n : ldc, kind, s);
   // F16S in-kernel split: 128-wide N tile (raw slot + 4-stage ring fit the smem)
   if (n <= 128 || (conv && kind == TcKind::F16S))
     return tc_run_bn<128>(a, b, C, m, n, k, ldc < n ? n : ldc, b_is_nk, kind, conv, s);

@@ -415,3 +415,34 @@ def test_output_rows_not_tma_storable(rng, shape):
     dev = gemm_nt(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy()
     assert rel_frobenius(dev, want) < FP32_GATE
     assert rel_frobenius(gemm_tnn(a, b), want) < FP32_GATE
+
+
+class TestCtaPairTiles:
+    """NT problems with >= 74 256x256 tiles run on CTA pairs (tcgen05
+    cta_group::2: M = 256 MMAs, each CTA loading half of B). Each output element
+    sees the same MMAs in the same order as on the single-CTA 128x256 tile, so
+    with the same split-K the results are bit-identical; knob tc_pair = 2 forces
+    the pair kernel on small shapes (ragged m and n, odd m-tile counts, split-K)."""
+
+    @pytest.mark.parametrize("shape", [(256, 256, 64), (300, 520, 136), (1000, 900, 2048),
+                                       (640, 4096, 8192), (2560, 2048, 1024)])
+    def test_pair_matches_single(self, rng, shape):
+        import torch
+
+        from paper_1702_03192_b200 import _lib
+
+        m, n, k = shape
+        a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+        ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+        want = oracle.oracle_nt_blas(a, b)
+        old = _lib.config_get("tc_pair")
+        try:
+            for v in ("tc3xf16s", "tc3xtf32"):
+                _lib.config_set("tc_pair", 0)
+                single = gemm_nt(ta, tb, variant=v).cpu().numpy()
+                _lib.config_set("tc_pair", 2)
+                pair = gemm_nt(ta, tb, variant=v).cpu().numpy()
+                assert rel_frobenius(pair, want) < FP32_GATE
+                assert rel_frobenius(pair, single) < 1e-6
+        finally:
+            _lib.config_set("tc_pair", old)
