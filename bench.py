@@ -231,7 +231,10 @@ def build_workload(args, rank, world):
     lo, hi = row_range(m, rank, world)
     calls = [("nt", hi - lo, n, k, True)]
     desc = "large_nt m=65536 n=k=8192 (configs[4]), rows of A sharded, B replicated"
-    par = "single GPU" if world == 1 else f"row-sharded x{world} (NCCL broadcast B + all-gather C)"
+    par = ("single GPU" if world == 1 else
+           f"row-sharded x{world}: NCCL broadcast of B, then the all-gather of C "
+           + ("fused into the GEMM epilogue (peer stores over NVLink)" if args.gather == "fused"
+              else "by ncclAllGather"))
     return calls, 2.0 * m * n * k, desc, "strong", par, None
 
 
@@ -249,6 +252,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--gather", default="fused", choices=("fused", "nccl"),
+                    help="large workload, N > 1: all-gather of C fused into the GEMM epilogue "
+                         "(peer stores over CUDA IPC / NVLink) or an ncclAllGather after it")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -317,8 +323,26 @@ def main():
             if op == "grad":
                 grad_bufs[i] = torch.empty(m * n, device=dev)
 
+    # large workload, N > 1, fused gather: every rank's full C is mapped by the
+    # others (CUDA IPC) and the GEMM epilogue stores each tile into all of them
+    peer_gather, gather_mode = None, None
+    if args.workload == "large" and world > 1:
+        gather_mode = args.gather
+        if args.gather == "fused":
+            from paper_1702_03192_b200.sharding import PeerGather, row_range
+
+            try:
+                peer_gather = PeerGather(C[: 65536 * 8192].view(65536, 8192))
+                large_row0 = row_range(65536, rank, world)[0]
+            except Exception as exc:  # no IPC between these processes: NCCL fallback
+                gather_mode = f"nccl (fused unavailable: {type(exc).__name__}: {exc})"[:200]
+                peer_gather = None
+
     def run_call(op, m, n, k, out=None):
         if m <= 0:
+            return
+        if peer_gather is not None:
+            peer_gather.gemm(A[: m * k].view(m, k), B[: n * k].view(n, k), large_row0, sync=False)
             return
         if op == "grad":
             rc = L.mtnn_dispatch_gemm(handle, prefix_p, A.data_ptr(), B.data_ptr(), out.data_ptr(),
@@ -375,7 +399,7 @@ def main():
             if events is not None:
                 comm["allreduce"].append(ev)
                 events.append(ev)
-        if args.workload == "large" and world > 1:
+        if args.workload == "large" and world > 1 and peer_gather is None:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record()
             rows = calls[0][1]
@@ -437,7 +461,8 @@ def main():
         events[st * (len(events) // args.steps) + i][1]) for st in range(args.steps)) * 1e-3
         for i in range(len(events) // args.steps)]
     if world > 1 and args.workload == "large":
-        per_call = per_call[1:-1]  # drop the collective windows
+        # drop the collective windows (broadcast, and the all-gather unless fused)
+        per_call = per_call[1:] if peer_gather is not None else per_call[1:-1]
     if world > 1 and args.workload == "fcn":
         per_call = per_call[:-1]
 
@@ -494,6 +519,8 @@ def main():
     if args.workload in ("large", "fcn") and world > 1:
         extra["collective_ms_per_step"] = {
             k: statistics.mean(s.elapsed_time(e) for s, e in v) for k, v in comm.items() if v}
+    if gather_mode is not None:
+        extra["gather"] = gather_mode
     if world == 1:
         extra["transpose"] = transpose_pass(B, C, flush_src, stream, hbm, L, _lib, torch)
     extra["selector_native_ns_incl_ctypes"] = selector_cost(L, handle, prefix_p)

@@ -133,6 +133,25 @@ int mtnn_transpose(const float* B, float* BT, int64_t rows, int64_t cols, void* 
 int mtnn_gemm_tnn(const float* A, const float* B, float* C, int64_t m, int64_t n,
                   int64_t k, int variant, int64_t mem_budget, void* stream);
 
+/* ---- multi-GPU: row-sharded NT with the all-gather fused ----
+ * Rank r owns rows [row0, row0 + m_local) of A and C (B replicated). The GEMM
+ * epilogue stores each C tile into this rank's C (full m x n, row-major) AND
+ * into every peer's C (peer_C[i]: the other ranks' full C buffers mapped into
+ * this process with mtnn_ipc_open), so the gather runs tile by tile under the
+ * MMAs over NVLink instead of an ncclAllGather after them. C is complete on a
+ * rank once every rank's call has finished (the caller's barrier). Up to 7
+ * peers; tc3xf16s on CTA pairs (shapes it cannot take: local GEMM + device-to-
+ * device copies). No reference counterpart (the reference has no multi-GPU). */
+int mtnn_gemm_nt_allgather(const float* A_local, const float* B, float* C, float* const* peer_C,
+                           int npeers, int64_t row0, int64_t m_local, int64_t n, int64_t k,
+                           void* stream);
+/* CUDA IPC for the peer C buffers: export a device pointer (64-byte handle +
+ * its offset inside its allocation) / map a peer's (ref-counted per handle) /
+ * unmap. Errors: MTNN_EINVAL (not device memory, unknown pointer), MTNN_ECUDA. */
+int mtnn_ipc_handle(const void* ptr, unsigned char handle[64], int64_t* offset);
+int mtnn_ipc_open(const unsigned char handle[64], int64_t offset, void** ptr);
+int mtnn_ipc_close(void* ptr);
+
 /* ---- host-buffer (drop-in) variants: synchronous, numpy semantics ------ */
 int mtnn_gemm_nt_host(const float* A, const float* B, float* C, int64_t m, int64_t n,
                       int64_t k, int variant);

@@ -71,6 +71,11 @@ def _load():
         "mtnn_profile_read": (c_int, [c_int, _DP, _I64P, _DP]),
         "mtnn_config_set": (c_int, [c_char_p, c_int64]),
         "mtnn_config_get": (c_int, [c_char_p, _I64P]),
+        "mtnn_gemm_nt_allgather": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(c_void_p), c_int,
+                                           c_int64, c_int64, c_int64, c_int64, c_void_p]),
+        "mtnn_ipc_handle": (c_int, [c_void_p, c_void_p, _I64P]),
+        "mtnn_ipc_open": (c_int, [c_void_p, c_int64, POINTER(c_void_p)]),
+        "mtnn_ipc_close": (c_int, [c_void_p]),
         "mtnn_gemm_nt": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p]),
         "mtnn_gemm_nn": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p]),
         "mtnn_transpose": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p]),

@@ -102,6 +102,13 @@ void set_tc_pair_mode(int v);
 // ldc: C row stride in elements (-1 = n); a larger one pads each C row.
 int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n, int64_t k,
            bool b_is_nk, TcKind kind, cudaStream_t s, int64_t ldc = -1);
+// Row block of a row-sharded NT with the all-gather fused into the epilogue
+// (peers: the same rows of other ranks' C buffers, mapped into this process).
+int gemm_nt_allgather(const float* A, const float* B, float* C_local, float* const* peers,
+                      int npeers, int64_t m, int64_t n, int64_t k, cudaStream_t s);
+// The library's AUTO NT dispatch (mtnn_abi.cpp), for internal fallbacks.
+int gemm_dispatch_nt(const float* A, const float* B, float* C, int64_t m, int64_t n, int64_t k,
+                     cudaStream_t s);
 int launch_split_rows_f16(const float* x, void* hi, void* lo, float* inv_scale, int64_t rows,
                           int64_t k, cudaStream_t s);
 // Both K-major operands of one GEMM in one launch: rows of x0 then x1 (same k);

@@ -35,6 +35,7 @@
 #include <cmath>
 #include <mutex>
 #include <stdlib.h>
+#include <string.h>
 
 #include "common.h"
 #include "workspace.h"
@@ -286,6 +287,7 @@ struct Params {
   int tiles_m, tiles_n, splits, kblocks_per_split, total_kblocks;
   int tiles_mp;  // CTA-pair kernel: pairs of m-tiles
   int group_m;   // CTA-pair kernel: m-tile pairs per raster group
+  int npeers;    // CTA-pair kernel: peer C buffers the epilogue also stores to
   int units;
   const float* inv_scale_a;  // KindF16S: 1/s per row of A (m) and of B (n)
   const float* inv_scale_b;
@@ -875,6 +877,13 @@ static int launch_impl(const void* ahi, const void* alo, const void* bhi,
 // the peer's remote arrive; both CTAs' TMA bytes complete on it); the leader's
 // commits multicast to empty[s] / tfull[] in both CTAs; tempty[] in the leader
 // counts the epilogue warps of both CTAs.
+// Fused all-gather: the epilogue also stores every C tile into up to
+// kMaxPeers other C buffers (peer GPUs' memory mapped into this process over
+// NVLink, CUDA IPC), so the gather overlaps the MMAs tile by tile.
+constexpr int kMaxPeers = 7;
+struct PeerMaps {
+  CUtensorMap map[kMaxPeers];
+};
 constexpr int kPairStages = 6;
 constexpr int kPairBN = 256;            // output tile N (both CTAs)
 constexpr int kPairHalfN = kPairBN / 2;  // B rows loaded per CTA
@@ -971,7 +980,8 @@ gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
                       const __grid_constant__ CUtensorMap map_alo,
                       const __grid_constant__ CUtensorMap map_bhi,
                       const __grid_constant__ CUtensorMap map_blo,
-                      const __grid_constant__ CUtensorMap map_c, const Params p) {
+                      const __grid_constant__ CUtensorMap map_c, const Params p,
+                      const __grid_constant__ PeerMaps peers) {
   using S = PairSmem;
   constexpr int BN = kPairBN;
   constexpr int kColsPerWarp = BN / 4;
@@ -1160,6 +1170,9 @@ gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
         if (lane == 0) {
           tma_store_3d(&map_c, smem_u32(stg), tn * BN + h * kColsPerWarp + c * 16,
                        tm * BM + q * 32, split);
+          for (int d = 0; d < p.npeers; ++d)  // the same tile into each peer's C
+            tma_store_3d(&peers.map[d], smem_u32(stg), tn * BN + h * kColsPerWarp + c * 16,
+                         tm * BM + q * 32, split);
           tma_store_commit();
         }
       }
@@ -1178,9 +1191,12 @@ gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
 
 template <class Kind>
 static int launch_pair_impl(const void* ahi, const void* alo, const void* bhi, const void* blo,
-                            float* out, const Params& p, int clusters, cudaStream_t s) {
+                            float* out, const Params& p, int clusters, cudaStream_t s,
+                            float* const* peer_out = nullptr) {
   using S = PairSmem;
   CUtensorMap mah, mal, mbh, mbl, mc;
+  PeerMaps peers;
+  memset(&peers, 0, sizeof(peers));
   const uint64_t eb = Kind::kElemBytes;
   encode_dtype = Kind::kTmaType;
   {
@@ -1203,6 +1219,8 @@ static int launch_pair_impl(const void* ahi, const void* alo, const void* bhi, c
     const uint64_t str[2] = {(uint64_t)p.ldc * 4, (uint64_t)p.ldc * p.m * 4};
     const uint32_t box[3] = {16, 32, 1};
     MTNN_TRY(encode(&mc, out, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
+    for (int d = 0; d < p.npeers; ++d)
+      MTNN_TRY(encode(&peers.map[d], peer_out[d], 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
   }
   auto kern = gemm_tc3x_pair_kernel<Kind>;
   static bool attr_set = false;
@@ -1214,7 +1232,7 @@ static int launch_pair_impl(const void* ahi, const void* alo, const void* bhi, c
   {
     KernelTimer timer(Kind::kScaled ? MTNN_KCLASS_GEMM_TC_F16S : MTNN_KCLASS_GEMM_TC,
                       2.0 * (double)p.m * (double)p.n * (double)p.k, s);
-    kern<<<2 * clusters, kThreads, S::kTotal, s>>>(mah, mal, mbh, mbl, mc, p);
+    kern<<<2 * clusters, kThreads, S::kTotal, s>>>(mah, mal, mbh, mbl, mc, p, peers);
   }
   MTNN_CUDA_TRY(cudaGetLastError());
   return MTNN_OK;
@@ -1446,7 +1464,8 @@ void set_tc_pair_mode(int v) { g_tc_pair.store(v, std::memory_order_relaxed); }
 
 // 256 x 256 output tiles on CTA pairs (NT, pre-split operands).
 static int tc_run_pair(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n,
-                       int64_t k, int64_t ldc, TcKind kind, cudaStream_t s) {
+                       int64_t k, int64_t ldc, TcKind kind, cudaStream_t s,
+                       float* const* peers = nullptr, int npeers = 0) {
   const DeviceInfo* di = nullptr;
   MTNN_TRY(device_info(&di));
   if (di->max_smem_optin < tc::PairSmem::kTotal)
@@ -1469,7 +1488,9 @@ static int tc_run_pair(const TcOperand& a, const TcOperand& b, float* C, int64_t
   p.total_kblocks = (int)((k + bk - 1) / bk);
   const int pairs = di->sm_count / 2;
   const int tiles = p.tiles_mp * p.tiles_n;
-  int splits = choose_splits(tiles, p.total_kblocks, m, n, pairs);
+  // peer stores go straight from the epilogue: no split-K partials
+  int splits = npeers > 0 ? 1 : choose_splits(tiles, p.total_kblocks, m, n, pairs);
+  p.npeers = npeers;
   p.kblocks_per_split = (p.total_kblocks + splits - 1) / splits;
   splits = (p.total_kblocks + p.kblocks_per_split - 1) / p.kblocks_per_split;
   p.splits = splits;
@@ -1482,8 +1503,8 @@ static int tc_run_pair(const TcOperand& a, const TcOperand& b, float* C, int64_t
     out = static_cast<float*>(part.ptr);
   }
   const int rc = kind == TcKind::F16S
-                     ? tc::launch_pair_impl<tc::KindF16S>(a.hi, a.lo, b.hi, b.lo, out, p, clusters, s)
-                     : tc::launch_pair_impl<tc::KindTF32>(a.hi, a.lo, b.hi, b.lo, out, p, clusters, s);
+                     ? tc::launch_pair_impl<tc::KindF16S>(a.hi, a.lo, b.hi, b.lo, out, p, clusters, s, peers)
+                     : tc::launch_pair_impl<tc::KindTF32>(a.hi, a.lo, b.hi, b.lo, out, p, clusters, s, peers);
   MTNN_TRY(rc);
   if (splits > 1) MTNN_TRY(launch_splitk_reduce(out, C, m * ldc, splits, s));
   return MTNN_OK;
@@ -1571,6 +1592,32 @@ int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t 
   if (n <= 128 || (conv && kind == TcKind::F16S))
     return tc_run_bn<128>(a, b, C, m, n, k, ldc < n ? n : ldc, b_is_nk, kind, conv, s);
   return tc_run_bn<256>(a, b, C, m, n, k, ldc < n ? n : ldc, b_is_nk, kind, conv, s);
+}
+
+// Row block of a row-sharded NT with the all-gather fused into the epilogue:
+// C_local = A_local x B^T (m_local x n, row stride n) is stored into C_local and
+// into each peer pointer (the same rows of the peers' C). CTA-pair tc3xf16s
+// kernel with the peer stores; shapes it cannot take are computed locally and
+// pushed to the peers by device-to-device copies on the same stream.
+int gemm_nt_allgather(const float* A, const float* B, float* C_local, float* const* peers,
+                      int npeers, int64_t m, int64_t n, int64_t k, cudaStream_t s) {
+  if (npeers < 0 || npeers > tc::kMaxPeers)
+    return fail(MTNN_EINVAL, "npeers must be in [0, %d], got %d", tc::kMaxPeers, npeers);
+  if (m == 0 || n == 0) return MTNN_OK;
+  const bool pair_ok = m > 128 && n > 128 && k > 0 && tc_eligible(A, B, C_local, m, n, k, true, TcKind::F16S);
+  bool peers_ok = true;
+  for (int d = 0; d < npeers; ++d) peers_ok = peers_ok && (reinterpret_cast<uintptr_t>(peers[d]) & 15) == 0;
+  if (pair_ok && peers_ok) {
+    ScratchBuffer wa, wb;
+    TcOperand a{}, b{};
+    MTNN_TRY(tc_prepare_pair(A, m, B, n, k, false, TcKind::F16S, 0, wa, wb, &a, &b, s));
+    return tc_run_pair(a, b, C_local, m, n, k, n, TcKind::F16S, s, peers, npeers);
+  }
+  MTNN_TRY(gemm_dispatch_nt(A, B, C_local, m, n, k, s));
+  for (int d = 0; d < npeers; ++d)
+    MTNN_CUDA_TRY(cudaMemcpyAsync(peers[d], C_local, (size_t)(m * n) * sizeof(float),
+                                  cudaMemcpyDefault, s));
+  return MTNN_OK;
 }
 
 int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t n,

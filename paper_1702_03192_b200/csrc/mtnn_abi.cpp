@@ -143,6 +143,11 @@ static int gemm_dispatch(const float* A, const float* B, float* C, int64_t m, in
   return launch_gemm_ffma(A, B, C, m, n, k, b_is_nk, s);
 }
 
+int gemm_dispatch_nt(const float* A, const float* B, float* C, int64_t m, int64_t n, int64_t k,
+                     cudaStream_t s) {
+  return gemm_dispatch(A, B, C, m, n, k, MTNN_VARIANT_AUTO, true, s);
+}
+
 static int tnn_device(const float* A, const float* B, float* C, int64_t m, int64_t n,
                       int64_t k, int variant, int64_t mem_budget, cudaStream_t s) {
   MTNN_TRY(check_dims(m, n, k));
@@ -619,6 +624,20 @@ int mtnn_config_get(const char* key, int64_t* value) {
     return MTNN_OK;
   }
   return fail(MTNN_EINVAL, "unknown config key '%s'", key);
+}
+
+int mtnn_gemm_nt_allgather(const float* A_local, const float* B, float* C, float* const* peer_C,
+                           int npeers, int64_t row0, int64_t m_local, int64_t n, int64_t k,
+                           void* stream) {
+  MTNN_TRY(check_dims(m_local, n, k));
+  if (row0 < 0) return fail(MTNN_EINVAL, "row0 must be >= 0");
+  if (npeers > 0 && !peer_C) return fail(MTNN_EINVAL, "null peer list");
+  const DeviceInfo* di = nullptr;
+  MTNN_TRY(device_info(&di));
+  float* peers[8] = {};
+  for (int d = 0; d < npeers && d < 8; ++d) peers[d] = peer_C[d] + row0 * n;
+  return gemm_nt_allgather(A_local, B, C + row0 * n, peers, npeers, m_local, n, k,
+                           static_cast<cudaStream_t>(stream));
 }
 
 int mtnn_gemm_nt(const float* A, const float* B, float* C, int64_t m, int64_t n, int64_t k,

@@ -150,3 +150,66 @@ def dp_weight_grad(dz_local: torch.Tensor, x_local: torch.Tensor, *, group=None,
     if work is not None:
         work.wait()
     return g
+
+
+# ------------------------------------------------------- fused all-gather
+class PeerGather:
+    """Row-sharded NT with the all-gather fused into the GEMM.
+
+    Every rank holds the full (m, n) C buffer `c`; at construction the ranks
+    exchange CUDA IPC handles of their buffers (``all_gather_object`` over the
+    process group — plumbing only) and map each other's. ``gemm(a_local, b,
+    row0)`` then runs ``mtnn_gemm_nt_allgather``: the CTA-pair GEMM epilogue
+    stores every C tile of this rank's row block into its own C and straight
+    into each peer's C over NVLink, so the gather overlaps the MMAs instead of
+    following them as an ``ncclAllGather``. C is complete on every rank after
+    all ranks' calls finish; ``gemm`` synchronises the stream and the group.
+    """
+
+    def __init__(self, c: torch.Tensor, *, group=None):
+        import ctypes
+
+        from . import _lib
+
+        if not (c.is_cuda and c.dtype == torch.float32 and c.is_contiguous() and c.dim() == 2):
+            raise ValueError("c must be a contiguous 2-D float32 CUDA tensor")
+        self.c, self.group = c, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        handle = (ctypes.c_char * 64)()
+        off = ctypes.c_int64()
+        _lib.check(_lib.lib.mtnn_ipc_handle(c.data_ptr(), ctypes.addressof(handle), ctypes.byref(off)))
+        infos = [None] * self.world
+        dist.all_gather_object(infos, (bytes(handle), off.value), group=group)
+        self.peers = []
+        for r, (h, o) in enumerate(infos):
+            if r == self.rank:
+                continue
+            buf = ctypes.create_string_buffer(h, 64)
+            p = ctypes.c_void_p()
+            _lib.check(_lib.lib.mtnn_ipc_open(ctypes.addressof(buf), o, ctypes.byref(p)))
+            self.peers.append(p.value)
+        self._peer_arr = (ctypes.c_void_p * max(1, len(self.peers)))(*self.peers)
+
+    def gemm(self, a_local: torch.Tensor, b: torch.Tensor, row0: int, *, sync: bool = True):
+        from . import _lib
+
+        m, n = self.c.shape
+        mloc, k = a_local.shape
+        if tuple(b.shape) != (n, k) or row0 < 0 or row0 + mloc > m:
+            raise ValueError(f"shapes: a_local {tuple(a_local.shape)}, b {tuple(b.shape)}, "
+                             f"row0 {row0}, C {tuple(self.c.shape)}")
+        stream = torch.cuda.current_stream(self.c.device).cuda_stream
+        _lib.check(_lib.lib.mtnn_gemm_nt_allgather(
+            a_local.contiguous().data_ptr(), b.contiguous().data_ptr(), self.c.data_ptr(),
+            self._peer_arr, len(self.peers), row0, mloc, n, k, stream))
+        if sync:
+            torch.cuda.synchronize(self.c.device)
+            dist.barrier(group=self.group)
+        return self.c
+
+    def close(self):
+        from . import _lib
+
+        for p in self.peers:
+            _lib.check(_lib.lib.mtnn_ipc_close(p))
+        self.peers = []

@@ -107,3 +107,74 @@ def test_dp_weight_grad_world2_gloo(batch):
         assert p.exitcode == 0
     for rank, err in res:
         assert err < 1e-6, (rank, err)
+
+
+# ---------------------------------------------------------------- GPU
+def _fused_worker(rank, world, port, m, n, k, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_1702_03192_b200.sharding import PeerGather
+
+        torch.cuda.set_device(0)  # the ranks share one GPU: IPC maps between processes
+        g = torch.Generator().manual_seed(5)
+        a = torch.rand(m, k, generator=g) * 2 - 1
+        b = torch.rand(n, k, generator=g) * 2 - 1
+        lo, hi = row_range(m, rank, world)
+        c = torch.full((m, n), float("nan"), device="cuda")
+        pg = PeerGather(c)
+        pg.gemm(a[lo:hi].cuda(), b.cuda(), lo)
+        got = c.cpu().numpy()
+        rows = np.unique(np.r_[0, m - 1, np.arange(0, m, 37)])
+        want = oracle.oracle_nt_rows(a.numpy(), b.numpy(), rows, np.arange(n))
+        q.put((rank, oracle.rel_frobenius(got[rows], want), bool(np.isfinite(got).all())))
+        pg.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,k", [(1024, 768, 512), (600, 300, 264)])
+def test_fused_allgather_two_processes_one_gpu(m, n, k):
+    """Two ranks (processes) share the GPU; each computes its row block with
+    the all-gather fused into the GEMM epilogue (stores into the other rank's
+    IPC-mapped C). Both ranks then hold the full C (no NaN left, oracle match)."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, m, n, k, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, err, finite in res:
+        assert finite, rank
+        assert err < 1e-5, (rank, err)
+
+
+@pytest.mark.gpu
+def test_fused_allgather_local_destinations():
+    """The multi-destination epilogue on one process: peers are other local C
+    buffers; the row block lands identically in all of them, other rows untouched."""
+    from paper_1702_03192_b200 import _lib
+    import ctypes
+
+    m, n, k, row0, mloc = 2048, 1024, 512, 512, 1024
+    g = torch.Generator().manual_seed(2)
+    a = (torch.rand(mloc, k, generator=g) * 2 - 1).cuda()
+    b = (torch.rand(n, k, generator=g) * 2 - 1).cuda()
+    cs = [torch.zeros(m, n, device="cuda") for _ in range(4)]
+    peers = (ctypes.c_void_p * 3)(*[c.data_ptr() for c in cs[1:]])
+    _lib.check(_lib.lib.mtnn_gemm_nt_allgather(a.data_ptr(), b.data_ptr(), cs[0].data_ptr(), peers, 3,
+                                               row0, mloc, n, k, torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    want = (a.double() @ b.double().t())
+    for c in cs:
+        blk = c[row0:row0 + mloc].double()
+        assert float((blk - want).norm() / want.norm()) < 1e-5
+        assert torch.equal(c[row0:row0 + mloc], cs[0][row0:row0 + mloc])
+        assert float(c[:row0].abs().sum()) == 0.0 and float(c[row0 + mloc:].abs().sum()) == 0.0
