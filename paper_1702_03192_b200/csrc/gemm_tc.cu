@@ -1582,11 +1582,15 @@ int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t 
     return fail(MTNN_EINVAL, "in-kernel operand split needs one prepared operand");
   if (conv && kind == TcKind::F16S && (conv == 1 ? a.inv_scale : b.inv_scale) == nullptr)
     return fail(MTNN_EINVAL, "in-kernel F16S split needs the operand's row scales");
-  // CTA pairs for NT problems with enough 256 x 256 tiles to fill the chip's 74 TPCs
-  // at least once (split-K would otherwise be needed for occupancy)
+  // CTA pairs for NT problems with enough 256 x 256 tiles to fill the chip's 74
+  // TPCs at least once (split-K would otherwise be needed for occupancy) and
+  // k <= 4096. Back-to-back at the power cap (tools/probe_pair_sustained.py)
+  // pairs win 20% at k = 1024, 11% at 2048, tie at 4096 and lose 5% at 8192:
+  // their DRAM traffic is ~1.6x the single-CTA kernel's (ncu), which at long k
+  // costs more energy than the third of L2->SM traffic they save.
   const int pair = tc_pair_mode();
   if (conv == 0 && b_is_nk && n > 128 && m > 128 &&
-      (pair == 2 || (pair == 1 && ((m + 255) / 256) * ((n + 255) / 256) >= 74)))
+      (pair == 2 || (pair == 1 && k <= 4096 && ((m + 255) / 256) * ((n + 255) / 256) >= 74)))
     return tc_run_pair(a, b, C, m, n, k, ldc < n ? n : ldc, kind, s);
   // F16S in-kernel split: 128-wide N tile (raw slot + 4-stage ring fit the smem)
   if (n <= 128 || (conv && kind == TcKind::F16S))
