@@ -7,7 +7,11 @@ dev = torch.device("cuda:0"); s = torch.cuda.current_stream().cuda_stream
 flush = torch.ones(64 * 2**20, device=dev)
 A = torch.rand(16384 * 16384, device=dev); B = torch.rand(16384 * 16384, device=dev); C = torch.empty(16384 * 16384, device=dev)
 tot = 0.0
-for (m, n, k) in [(2048, 2048, 2048), (4096, 4096, 1024), (8192, 8192, 512), (16384, 16384, 2048), (1024, 1024, 1024), (512, 8192, 256)]:
+import os
+shapes = [(2048, 2048, 2048), (4096, 4096, 1024), (8192, 8192, 512), (16384, 16384, 2048), (1024, 1024, 1024), (512, 8192, 256)]
+if os.environ.get('LONGK'):
+    shapes = [(8192, 8192, 8192), (16384, 16384, 16384), (4096, 4096, 4096), (16384, 8192, 8192), (128, 16384, 16384), (2048, 2048, 8192)]
+for (m, n, k) in shapes:
     L.mtnn_profile_reset(); L.mtnn_profile_enable(1)
     for rep in range(5):
         flush.sum(); torch.cuda._sleep(100000)
