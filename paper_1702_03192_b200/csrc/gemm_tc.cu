@@ -974,7 +974,7 @@ __device__ __forceinline__ void pair_unit_coords(int u, const Params& p, int& sp
   tn = r / gm;
 }
 
-template <class Kind>
+template <bool B_MN, class Kind>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
                       const __grid_constant__ CUtensorMap map_alo,
@@ -1053,8 +1053,20 @@ gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
           const int brow = tn * BN + (int)rank * kPairHalfN;
           tma_load_2d_pair(st, &map_ahi, fb, kx, tm * BM);
           tma_load_2d_pair(st + S::kABytes, &map_alo, fb, kx, tm * BM);
-          tma_load_2d_pair(st + 2 * S::kABytes, &map_bhi, fb, kx, brow);
-          tma_load_2d_pair(st + 2 * S::kABytes + S::kBBytes, &map_blo, fb, kx, brow);
+          if (!B_MN) {
+            tma_load_2d_pair(st + 2 * S::kABytes, &map_bhi, fb, kx, brow);
+            tma_load_2d_pair(st + 2 * S::kABytes + S::kBBytes, &map_blo, fb, kx, brow);
+          } else {
+            // this CTA's 128 columns of B^T: boxes of [BK k-rows][kMnBox columns],
+            // one MN group of the canonical MN-major layout each, kMnLBO apart
+#pragma unroll
+            for (int g = 0; g < kPairHalfN / Kind::kMnBox; ++g) {
+              tma_load_2d_pair(st + 2 * S::kABytes + g * Kind::kMnLBO, &map_bhi, fb,
+                               brow + g * Kind::kMnBox, kx);
+              tma_load_2d_pair(st + 2 * S::kABytes + S::kBBytes + g * Kind::kMnLBO, &map_blo, fb,
+                               brow + g * Kind::kMnBox, kx);
+            }
+          }
           if (leader) mbar_expect_tx(fb, 2 * S::kStageBytes);  // both CTAs' bytes
           else mbar_arrive_cta(fb, 0);
           if (++stage == kPairStages) { stage = 0; phase ^= 1; }
@@ -1065,7 +1077,8 @@ gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
     // ===================== MMA issuer (leader CTA) =====================
     if (leader) {
       constexpr uint32_t idesc = (1u << 4) | (Kind::kFmt << 7) | (Kind::kFmt << 10) |
-                                 ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+                                 ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
+                                 ((uint32_t)(256 >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -1091,8 +1104,16 @@ gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
               for (int ks = 0; ks < Kind::BK / Kind::UMMA_K; ++ks) {
                 const uint64_t dah = make_sdesc(a_hi + ks * 32, 16, 512, kLayoutSW64);
                 const uint64_t dal = make_sdesc(a_lo + ks * 32, 16, 512, kLayoutSW64);
-                const uint64_t dbh = make_sdesc(b_hi + ks * 32, 16, 512, kLayoutSW64);
-                const uint64_t dbl = make_sdesc(b_lo + ks * 32, 16, 512, kLayoutSW64);
+                uint64_t dbh, dbl;
+                if (!B_MN) {
+                  dbh = make_sdesc(b_hi + ks * 32, 16, 512, kLayoutSW64);
+                  dbl = make_sdesc(b_lo + ks * 32, 16, 512, kLayoutSW64);
+                } else {
+                  dbh = make_sdesc(b_hi + ks * Kind::kMnKStep, Kind::kMnLBO, Kind::kMnSBO,
+                                   Kind::kMnLayout);
+                  dbl = make_sdesc(b_lo + ks * Kind::kMnKStep, Kind::kMnLBO, Kind::kMnSBO,
+                                   Kind::kMnLayout);
+                }
                 const uint32_t accum = (kb == kc && ks == 0) ? 0u : 1u;
                 tc_mma_pair<Kind::kScaled>(tmem_d, dal, dbh, idesc, accum);
                 tc_mma_pair<Kind::kScaled>(tmem_d, dah, dbl, idesc, 1u);
@@ -1189,7 +1210,7 @@ gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
   }
 }
 
-template <class Kind>
+template <bool B_MN, class Kind>
 static int launch_pair_impl(const void* ahi, const void* alo, const void* bhi, const void* blo,
                             float* out, const Params& p, int clusters, cudaStream_t s,
                             float* const* peer_out = nullptr) {
@@ -1206,12 +1227,18 @@ static int launch_pair_impl(const void* ahi, const void* alo, const void* bhi, c
     MTNN_TRY(encode(&mah, ahi, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
     MTNN_TRY(encode(&mal, alo, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
   }
-  {
+  if (!B_MN) {
     const uint64_t dims[2] = {(uint64_t)p.k, (uint64_t)p.n};
     const uint64_t str[1] = {(uint64_t)p.k * eb};
     const uint32_t box[2] = {(uint32_t)Kind::BK, (uint32_t)kPairHalfN};
     MTNN_TRY(encode(&mbh, bhi, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
     MTNN_TRY(encode(&mbl, blo, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
+  } else {
+    const uint64_t dims[2] = {(uint64_t)p.n, (uint64_t)p.k};
+    const uint64_t str[1] = {(uint64_t)p.n * eb};
+    const uint32_t box[2] = {(uint32_t)Kind::kMnBox, (uint32_t)Kind::BK};
+    MTNN_TRY(encode(&mbh, bhi, 2, dims, str, box, Kind::kMnSwizzle));
+    MTNN_TRY(encode(&mbl, blo, 2, dims, str, box, Kind::kMnSwizzle));
   }
   encode_dtype = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   {
@@ -1222,7 +1249,7 @@ static int launch_pair_impl(const void* ahi, const void* alo, const void* bhi, c
     for (int d = 0; d < p.npeers; ++d)
       MTNN_TRY(encode(&peers.map[d], peer_out[d], 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
   }
-  auto kern = gemm_tc3x_pair_kernel<Kind>;
+  auto kern = gemm_tc3x_pair_kernel<B_MN, Kind>;
   static bool attr_set = false;
   if (!attr_set) {
     MTNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1448,6 +1475,10 @@ static int choose_splits(int tiles, int kblocks, int64_t m, int64_t n, int sms) 
   return best;
 }
 
+// MN-major B^T on CTA pairs: each CTA's 128 columns are whole 64-column TMA
+// boxes; n a multiple of 16 (the NN eligibility rule) keeps every box start on a
+// 16-byte boundary, and boxes past n are zero-filled.
+constexpr int kPairMnCols = 16;
 // CTA-pair kernel switch: mtnn_config_set("tc_pair", 0/1), env MTNN_TC_PAIR=0.
 static std::atomic<int> g_tc_pair{-1};
 // 0 = off, 1 = on for large problems (default), 2 = whenever structurally possible (tests)
@@ -1464,7 +1495,7 @@ void set_tc_pair_mode(int v) { g_tc_pair.store(v, std::memory_order_relaxed); }
 
 // 256 x 256 output tiles on CTA pairs (NT, pre-split operands).
 static int tc_run_pair(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n,
-                       int64_t k, int64_t ldc, TcKind kind, cudaStream_t s,
+                       int64_t k, int64_t ldc, bool b_is_nk, TcKind kind, cudaStream_t s,
                        float* const* peers = nullptr, int npeers = 0) {
   const DeviceInfo* di = nullptr;
   MTNN_TRY(device_info(&di));
@@ -1502,9 +1533,13 @@ static int tc_run_pair(const TcOperand& a, const TcOperand& b, float* C, int64_t
     MTNN_TRY(part.alloc((size_t)splits * m * ldc * sizeof(float), s));
     out = static_cast<float*>(part.ptr);
   }
-  const int rc = kind == TcKind::F16S
-                     ? tc::launch_pair_impl<tc::KindF16S>(a.hi, a.lo, b.hi, b.lo, out, p, clusters, s, peers)
-                     : tc::launch_pair_impl<tc::KindTF32>(a.hi, a.lo, b.hi, b.lo, out, p, clusters, s, peers);
+  int rc;
+  if (kind == TcKind::F16S)
+    rc = b_is_nk ? tc::launch_pair_impl<false, tc::KindF16S>(a.hi, a.lo, b.hi, b.lo, out, p, clusters, s, peers)
+                 : tc::launch_pair_impl<true, tc::KindF16S>(a.hi, a.lo, b.hi, b.lo, out, p, clusters, s, peers);
+  else
+    rc = b_is_nk ? tc::launch_pair_impl<false, tc::KindTF32>(a.hi, a.lo, b.hi, b.lo, out, p, clusters, s, peers)
+                 : tc::launch_pair_impl<true, tc::KindTF32>(a.hi, a.lo, b.hi, b.lo, out, p, clusters, s, peers);
   MTNN_TRY(rc);
   if (splits > 1) MTNN_TRY(launch_splitk_reduce(out, C, m * ldc, splits, s));
   return MTNN_OK;
@@ -1589,9 +1624,9 @@ int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t 
   // their DRAM traffic is ~1.6x the single-CTA kernel's (ncu), which at long k
   // costs more energy than the third of L2->SM traffic they save.
   const int pair = tc_pair_mode();
-  if (conv == 0 && b_is_nk && n > 128 && m > 128 &&
+  if (conv == 0 && n > 128 && m > 128 && (b_is_nk || n % kPairMnCols == 0) &&
       (pair == 2 || (pair == 1 && k <= 4096 && ((m + 255) / 256) * ((n + 255) / 256) >= 74)))
-    return tc_run_pair(a, b, C, m, n, k, ldc < n ? n : ldc, kind, s);
+    return tc_run_pair(a, b, C, m, n, k, ldc < n ? n : ldc, b_is_nk, kind, s);
   // F16S in-kernel split: 128-wide N tile (raw slot + 4-stage ring fit the smem)
   if (n <= 128 || (conv && kind == TcKind::F16S))
     return tc_run_bn<128>(a, b, C, m, n, k, ldc < n ? n : ldc, b_is_nk, kind, conv, s);
@@ -1615,7 +1650,7 @@ int gemm_nt_allgather(const float* A, const float* B, float* C_local, float* con
     ScratchBuffer wa, wb;
     TcOperand a{}, b{};
     MTNN_TRY(tc_prepare_pair(A, m, B, n, k, false, TcKind::F16S, 0, wa, wb, &a, &b, s));
-    return tc_run_pair(a, b, C_local, m, n, k, n, TcKind::F16S, s, peers, npeers);
+    return tc_run_pair(a, b, C_local, m, n, k, n, true, TcKind::F16S, s, peers, npeers);
   }
   MTNN_TRY(gemm_dispatch_nt(A, B, C_local, m, n, k, s));
   for (int d = 0; d < npeers; ++d)

@@ -425,7 +425,7 @@ class TestCtaPairTiles:
     the pair kernel on small shapes (ragged m and n, odd m-tile counts, split-K)."""
 
     @pytest.mark.parametrize("shape", [(256, 256, 64), (300, 520, 136), (1000, 900, 2048),
-                                       (640, 4096, 8192), (2560, 2048, 1024)])
+                                       (640, 4096, 8192), (2560, 2048, 1024), (384, 400, 96)])
     def test_pair_matches_single(self, rng, shape):
         import torch
 
@@ -444,5 +444,13 @@ class TestCtaPairTiles:
                 pair = gemm_nt(ta, tb, variant=v).cpu().numpy()
                 assert rel_frobenius(pair, want) < FP32_GATE
                 assert rel_frobenius(pair, single) < 1e-6
+                if n % 16 == 0:  # NN: B^T MN-major, each CTA loading half its columns
+                    tbt = tb.t().contiguous()
+                    _lib.config_set("tc_pair", 0)
+                    single = gemm_nn(ta, tbt, variant=v).cpu().numpy()
+                    _lib.config_set("tc_pair", 2)
+                    pair = gemm_nn(ta, tbt, variant=v).cpu().numpy()
+                    assert rel_frobenius(pair, want) < FP32_GATE
+                    assert rel_frobenius(pair, single) < 1e-6
         finally:
             _lib.config_set("tc_pair", old)
