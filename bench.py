@@ -466,6 +466,26 @@ def main():
     if world > 1 and args.workload == "fcn":
         per_call = per_call[:-1]
 
+    # e2e through the host-buffer API: every rank runs its own cases (the sweep
+    # at N > 1: its LPT share), the job time is the slowest rank's
+    e2e = None
+    if not args.no_e2e and (world == 1 or args.workload == "sweep"):
+        if world > 1:
+            dist.barrier()
+        e2e = run_e2e(args, calls, handle, prefix_p, L)
+        if world > 1:
+            red = torch.tensor([e2e["ms_per_step"], float(e2e["h2d_bytes_per_step"]),
+                                float(e2e["d2h_bytes_per_step"])], dtype=torch.float64,
+                               device=dev if not share else "cpu")
+            mx = red.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(red, op=dist.ReduceOp.SUM)
+            ms = float(mx[0].item())
+            e2e.update({"value": total_flops / (ms * 1e-3) / 1e12, "ms_per_step": ms,
+                        "h2d_bytes_per_step": int(red[1].item()),
+                        "d2h_bytes_per_step": int(red[2].item()),
+                        "ranks": f"{world} ranks, each its own cases; max over ranks"})
+
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -525,9 +545,6 @@ def main():
         extra["transpose"] = transpose_pass(B, C, flush_src, stream, hbm, L, _lib, torch)
     extra["selector_native_ns_incl_ctypes"] = selector_cost(L, handle, prefix_p)
 
-    e2e = None
-    if not args.no_e2e and world == 1:
-        e2e = run_e2e(args, calls, handle, prefix_p, L)
     cpu = None
     if not args.no_cpu and world == 1:
         cpu = cpu_baseline(host_threads())
@@ -655,9 +672,9 @@ def run_e2e(args, calls, handle, prefix_p, L):
 
     from paper_1702_03192_b200 import _lib
 
-    max_a = max(m * k for _, m, n, k, _ in calls)
-    max_b = max(n * k for _, m, n, k, _ in calls)
-    max_c = max(m * n for _, m, n, k, _ in calls)
+    max_a = max([m * k for _, m, n, k, _ in calls] + [1])
+    max_b = max([n * k for _, m, n, k, _ in calls] + [1])
+    max_c = max([m * n for _, m, n, k, _ in calls] + [1])
     ha = torch.empty(max_a, dtype=torch.float32).pin_memory().uniform_(-1, 1)
     hb = torch.empty(max_b, dtype=torch.float32).pin_memory().uniform_(-1, 1)
     hc = torch.empty(max_c, dtype=torch.float32).pin_memory()
@@ -679,7 +696,7 @@ def run_e2e(args, calls, handle, prefix_p, L):
     t0 = time.perf_counter()
     for _ in range(steps):
         step()
-    dt = (time.perf_counter() - t0) / steps
+    dt = max((time.perf_counter() - t0) / steps, 1e-9)
     flops = sum(2.0 * m * n * k for _, m, n, k, _ in calls)
     return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3, "steps": steps,
