@@ -1510,11 +1510,7 @@ static int tc_run_pair(const TcOperand& a, const TcOperand& b, float* C, int64_t
   p.inv_scale_b = b.inv_scale;
   p.tiles_m = (int)((m + tc::BM - 1) / tc::BM);
   p.tiles_mp = (p.tiles_m + 1) / 2;
-  {
-    const char* e = getenv("MTNN_PAIR_GROUP");
-    const int g = e ? atoi(e) : 0;
-    p.group_m = g > 0 ? g : tc::kGroupM;  // 16 pairs = 32 m-tiles: least DRAM traffic measured
-  }
+  p.group_m = tc::kGroupM;  // 16 pairs = 32 m-tiles per raster group: least DRAM traffic of 2..37
   p.tiles_n = (int)((n + tc::kPairBN - 1) / tc::kPairBN);
   p.total_kblocks = (int)((k + bk - 1) / bk);
   const int pairs = di->sm_count / 2;
