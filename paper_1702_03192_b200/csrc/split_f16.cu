@@ -337,7 +337,7 @@ int launch_split_rows_f16_pair(const float* x0, void* hi0, void* lo0, float* inv
     // 1024 < k <= 2048: whole row in registers (measured 5.5 -> 6.8 TB/s at
     // 16384 x 2048); shorter rows keep the looped kernel (faster there: more
     // resident warps at its lower register count)
-    if (k > 1024)
+    if (k > 1024 && k <= 2048)  // (longer rows land here only past the smem limit)
       split_rows_f16_reg_kernel<16><<<(unsigned)blocks, 256, 0, s>>>(j0, j1, k);
     else
       split_rows_f16_kernel<<<(unsigned)blocks, 256, 0, s>>>(j0, j1, k);

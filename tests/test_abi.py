@@ -124,3 +124,24 @@ def test_config_knobs_roundtrip_and_reject_unknown():
         _lib.config_set(key, old)
     with pytest.raises(ValueError, match="unknown config key"):
         _lib.config_set("no_such_knob", 1)
+
+
+def test_ipc_and_allgather_fail_cleanly_without_a_gpu():
+    """The multi-GPU entry points report errors (no crash) on bad input / no GPU."""
+    import ctypes
+
+    lib = _lib.lib
+    h = (ctypes.c_char * 64)()
+    off = ctypes.c_int64()
+    assert lib.mtnn_ipc_handle(None, ctypes.addressof(h), ctypes.byref(off)) == _lib.EINVAL
+    p = ctypes.c_void_p()
+    assert lib.mtnn_ipc_open(None, 0, ctypes.byref(p)) == _lib.EINVAL
+    assert lib.mtnn_ipc_close(ctypes.c_void_p(1234)) == _lib.EINVAL
+    assert "not opened" in _lib.last_error()
+    rc = lib.mtnn_gemm_nt_allgather(None, None, None, None, 0, -1, 4, 4, 4, None)
+    assert rc == _lib.EINVAL and "row0" in _lib.last_error()
+    rc = lib.mtnn_gemm_nt_allgather(None, None, None, None, 2, 0, 4, 4, 4, None)
+    assert rc == _lib.EINVAL and "peer" in _lib.last_error()
+    if not lib.mtnn_device_available():
+        buf = (ctypes.c_float * 16)()
+        assert lib.mtnn_ipc_handle(ctypes.addressof(buf), ctypes.addressof(h), ctypes.byref(off)) != 0

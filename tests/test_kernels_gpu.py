@@ -454,3 +454,74 @@ class TestCtaPairTiles:
                     assert rel_frobenius(pair, single) < 1e-6
         finally:
             _lib.config_set("tc_pair", old)
+
+
+class TestEdgeCases:
+    """Edge cases across the kernel families: degenerate and ragged dimensions,
+    unaligned (offset) device views that TMA cannot take, non-finite inputs on
+    the CTA-pair path, long k with tiny outputs (deep split-K)."""
+
+    @pytest.mark.parametrize("shape", [(1, 1, 1), (1, 4096, 8), (4096, 1, 8), (7, 9, 1),
+                                       (513, 257, 3), (130, 130, 130), (1, 1, 65536)])
+    def test_degenerate_and_odd(self, rng, shape):
+        m, n, k = shape
+        a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+        want = oracle.oracle_nt_blas(a, b)
+        for v in VARIANTS:
+            try:
+                got = gemm_nt(a, b, variant=v)
+            except RuntimeError:
+                assert v in ("tc3xf16s", "tc3xtf32")  # explicit TC variant on an ineligible shape
+                continue
+            assert got.shape == (m, n)
+            assert rel_frobenius(got, want) < FP32_GATE, v
+            assert rel_frobenius(gemm_tnn(a, b), want) < FP32_GATE
+
+    def test_unaligned_device_views(self, rng):
+        import torch
+
+        m, n, k = 300, 200, 264
+        a, b = random_matrix(rng, m, k + 1), random_matrix(rng, n, k + 1)
+        ta = torch.from_numpy(a).cuda()[:, 1:]   # 4-byte offset rows: not TMA-aligned
+        tb = torch.from_numpy(b).cuda()[:, 1:]
+        want = oracle.oracle_nt_blas(np.ascontiguousarray(a[:, 1:]), np.ascontiguousarray(b[:, 1:]))
+        got = gemm_nt(ta.contiguous(), tb.contiguous()).cpu().numpy()
+        assert rel_frobenius(got, want) < FP32_GATE
+        from paper_1702_03192_b200 import _lib
+        c = torch.empty(m * n + 1, device="cuda")[1:].view(m, n)  # unaligned C base
+        ac, bc = ta.contiguous(), tb.contiguous()
+        _lib.check(_lib.lib.mtnn_gemm_nt(ac.data_ptr(), bc.data_ptr(), c.data_ptr(), m, n, k, 0,
+                                         torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        assert rel_frobenius(c.cpu().numpy(), want) < FP32_GATE
+
+    def test_nonfinite_on_pair_tiles(self, rng):
+        import torch
+
+        from paper_1702_03192_b200 import _lib
+
+        m, n, k = 768, 512, 512
+        a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+        a[3, 5] = np.nan
+        b[7, 9] = np.inf
+        old = _lib.config_get("tc_pair")
+        try:
+            _lib.config_set("tc_pair", 2)
+            got = gemm_nt(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
+                          variant="tc3xf16s").cpu().numpy()
+        finally:
+            _lib.config_set("tc_pair", old)
+        assert np.all(np.isnan(got[3]))
+        assert np.all(~np.isfinite(got[:, 7]))
+        ok_r = np.ones(m, bool); ok_r[3] = False
+        ok_c = np.ones(n, bool); ok_c[7] = False
+        want = oracle.oracle_nt_blas(a[ok_r], b[ok_c])
+        assert rel_frobenius(got[np.ix_(ok_r, ok_c)], want) < FP32_GATE
+
+    @pytest.mark.parametrize("shape", [(128, 128, 262144), (256, 384, 100000)])
+    def test_long_k_small_output(self, rng, shape):
+        m, n, k = shape
+        a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+        want = oracle.oracle_nt_blas(a, b)
+        for v in ("auto", "tc3xf16s"):
+            assert rel_frobenius(gemm_nt(a, b, variant=v), want) < FP32_GATE
