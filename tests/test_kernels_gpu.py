@@ -525,3 +525,31 @@ class TestEdgeCases:
         want = oracle.oracle_nt_blas(a, b)
         for v in ("auto", "tc3xf16s"):
             assert rel_frobenius(gemm_nt(a, b, variant=v), want) < FP32_GATE
+
+
+@pytest.mark.parametrize("shape", [(4096, 4098, 1024), (2050, 8190, 512)])
+def test_pair_tiles_with_padded_output(rng, shape):
+    """n % 4 != 0 on a problem large enough for CTA pairs: the pair kernel writes
+    the row-padded C (ldc = n rounded up), the n columns are copied out."""
+    m, n, k = shape
+    a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+    got = gemm_nt(a, b)
+    rows = np.unique(np.r_[0, m - 1, rng.choice(m, 60, replace=False)])
+    cols = np.unique(np.r_[0, n - 1, rng.choice(n, 200, replace=False)])
+    assert rel_frobenius(got[np.ix_(rows, cols)], oracle.oracle_nt_rows(a, b, rows, cols)) < FP32_GATE
+
+
+@pytest.mark.parametrize("path", ["nt", "nn", "tnn"])
+def test_host_pipeline_with_inkernel_split_of_a(rng, path):
+    """Host-buffer call on the B-first pipeline (k > 4096) whose shape splits A
+    in-kernel (n <= 256, m >= 1024): every A row chunk gets its own row scales."""
+    m, n, k = 4096, 208, 8192
+    a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+    if path == "nt":
+        got = gemm_nt(a, b)
+    elif path == "nn":
+        got = gemm_nn(a, np.ascontiguousarray(b.T))
+    else:
+        got = gemm_tnn(a, b)
+    rows = np.sort(rng.choice(m, 64, replace=False))
+    assert rel_frobenius(got[rows], oracle.oracle_nt_rows(a, b, rows, np.arange(n))) < FP32_GATE

@@ -157,13 +157,14 @@ def test_fused_allgather_two_processes_one_gpu(m, n, k):
 
 
 @pytest.mark.gpu
-def test_fused_allgather_local_destinations():
+@pytest.mark.parametrize("m,n,k,row0,mloc", [(2048, 1024, 512, 512, 1024), (256, 300, 64, 100, 64)])
+def test_fused_allgather_local_destinations(m, n, k, row0, mloc):
     """The multi-destination epilogue on one process: peers are other local C
-    buffers; the row block lands identically in all of them, other rows untouched."""
+    buffers; the row block lands identically in all of them, other rows untouched
+    (second case: too small for CTA pairs, so the local-GEMM + peer-copy fallback)."""
     from paper_1702_03192_b200 import _lib
     import ctypes
 
-    m, n, k, row0, mloc = 2048, 1024, 512, 512, 1024
     g = torch.Generator().manual_seed(2)
     a = (torch.rand(mloc, k, generator=g) * 2 - 1).cuda()
     b = (torch.rand(n, k, generator=g) * 2 - 1).cuda()
