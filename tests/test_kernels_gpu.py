@@ -553,3 +553,31 @@ def test_host_pipeline_with_inkernel_split_of_a(rng, path):
         got = gemm_tnn(a, b)
     rows = np.sort(rng.choice(m, 64, replace=False))
     assert rel_frobenius(got[rows], oracle.oracle_nt_rows(a, b, rows, np.arange(n))) < FP32_GATE
+
+
+def test_random_shape_fuzz(rng):
+    """60 random shapes (1..2600 per dimension, biased toward odd sizes and the
+    path boundaries: 128/256/1024 short sides, k near multiples of 8/32) through
+    every entry point (host NT / NN / TNN, device NT) and variant, against the
+    float64 oracle on sampled rows."""
+    import torch
+
+    picks = [1, 2, 3, 5, 8, 16, 31, 64, 127, 128, 129, 200, 255, 256, 257, 500, 512, 513,
+             1000, 1023, 1024, 1025, 2047, 2600]
+    for _ in range(60):
+        m, n, k = (int(rng.choice(picks)) if rng.random() < 0.6 else int(rng.integers(1, 2600))
+                   for _ in range(3))
+        a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+        rows = np.unique(rng.choice(m, min(m, 24), replace=False))
+        want = oracle.oracle_nt_rows(a, b, rows, np.arange(n))
+        for v in VARIANTS:
+            try:
+                got = gemm_nt(a, b, variant=v)
+            except RuntimeError:
+                assert v in ("tc3xf16s", "tc3xtf32"), (m, n, k, v)
+                continue
+            assert rel_frobenius(got[rows], want) < FP32_GATE, (m, n, k, v)
+        assert rel_frobenius(gemm_tnn(a, b)[rows], want) < FP32_GATE, (m, n, k, "tnn")
+        assert rel_frobenius(gemm_nn(a, np.ascontiguousarray(b.T))[rows], want) < FP32_GATE, (m, n, k, "nn")
+        dev = gemm_nt(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy()
+        assert rel_frobenius(dev[rows], want) < FP32_GATE, (m, n, k, "device")
