@@ -1,30 +1,36 @@
-// Tensor-core FP32-accurate GEMM for sm_100a: tcgen05 kind::tf32, 3xTF32 split,
-// TMA-fed shared memory, TMEM accumulators. Serves both MTNN paths:
+// Tensor-core FP32-accurate GEMMs for sm_100a: tcgen05 MMAs on hi/lo operand
+// halves, TMA-fed shared memory, TMEM accumulators. Serves both MTNN paths:
 //   NT  C = A * B^T  with B stored n x k (K-major UMMA B operand)
 //       — reference kernels/_numba_impl.py:139-166 (gemm_nt), PAPER.md:249-257;
 //   NN  C = A * BT   with BT stored k x n (MN-major UMMA B operand)
 //       — reference kernels/_numba_impl.py:31-136 (gemm_nn), the second half of
 //         TNN.
 //
-// FP32 accuracy from TF32 tensor cores: every operand x is split once, before the
-// GEMM, into hi = rna_tf32(x) and lo = x - hi (exact in fp32, |lo| <= 2^-11 |x|),
-// and the kernel accumulates hi*hi + hi*lo + lo*hi in the fp32 TMEM accumulator
-// (the lo*lo term is below fp32 resolution). Measured emulation error at k=16384
-// is ~1.4e-6 relative Frobenius, inside the 1e-5 gate.
+// FP32 accuracy from 11-bit-significand tensor-core inputs: every operand x is
+// split into hi + lo and the kernel accumulates hi*hi + hi*lo + lo*hi (the
+// dropped lo*lo is ~2^-22 relative):
+//   KindF16S (default): per-row power-of-two scale s, h = fp16(x*s),
+//     l = fp16(x*s - h) (split_f16.cu); kind::f16 MMAs at twice the TF32 rate;
+//     the epilogue multiplies by 1/(s_row * s_col), exact.
+//   KindTF32: hi = the raw fp32 operand (the tensor core truncates it to tf32),
+//     lo = x - trunc_tf32(x); kind::tf32 MMAs.
+// The TMEM accumulator truncates (measured -0.5 ulp bias per accumulation), so
+// each accumulation covers chunk_kb k-blocks (48 MMAs) and the epilogue adds
+// the chunks into round-to-nearest FP32 registers (FP32 promotion).
 //
-// Kernel structure (persistent, one CTA per SM, warp-specialised):
-//   warp 0      TMA producer: per k-block loads A_hi, A_lo, B_hi, B_lo tiles
-//               (16-wide k slices, 64-byte swizzle) into a 4-stage smem ring;
-//   warp 1      MMA issuer: one elected lane issues 3 tcgen05.mma per 8-wide
-//               k-step into a TMEM accumulator (M=128, N=BN), commits smem slots
-//               back to the producer and finished tiles to the epilogue;
-//   warp 2      TMEM allocator (2 x BN columns: double-buffered accumulator so the
-//               epilogue of tile i overlaps the MMAs of tile i+1);
-//   warps 4..7  epilogue: tcgen05.ld 32 lanes x 32 columns, swizzled STS into a
-//               per-warp staging tile, TMA store (clips partial tiles).
-// Work units are (k-split, m-tile, n-tile); with few output tiles and long k the
-// host splits K so the grid reaches all SMs and a deterministic reduction kernel
-// sums the fp32 partials.
+// Kernels:
+//   gemm_tc3x_kernel<BN, B_MN, Kind, kConv>: persistent, one CTA per SM,
+//     warp-specialised — warp 0 TMA producer (4-stage ring), warp 1 one-lane
+//     MMA issuer (M = 128, N = BN), warp 2 TMEM allocator (2 x BN columns:
+//     double-buffered accumulator so the epilogue of tile i overlaps the MMAs of
+//     tile i+1), epilogue warps (tcgen05.ld, FP32 promotion, swizzled staging,
+//     TMA store). kConv != 0: one operand split in shared memory from raw fp32
+//     tiles (skinny problems; see the kernel).
+//   gemm_tc3x_pair_kernel<B_MN, Kind>: the CTA-pair (cta_group::2) variant,
+//     256 x 256 tiles, optional peer stores (fused all-gather).
+// Work units are (k-split, tile); with few output tiles and long k the host
+// splits K so the grid reaches all SMs and a deterministic reduction kernel sums
+// the fp32 partials.
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
