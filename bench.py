@@ -544,6 +544,9 @@ def main():
     if world == 1:
         extra["transpose"] = transpose_pass(B, C, flush_src, stream, hbm, L, _lib, torch)
     extra["selector_native_ns_incl_ctypes"] = selector_cost(L, handle, prefix_p)
+    ns = ctypes.c_double()
+    if L.mtnn_select_cost_ns(handle, prefix_p, 1000000, ctypes.byref(ns)) == 0:
+        extra["selector_native_ns"] = ns.value  # the C++ decision alone
 
     cpu = None
     if not args.no_cpu and world == 1:

@@ -195,6 +195,11 @@ int mtnn_model_raw(const mtnn_model* model, const double* x, int64_t nx, double*
 int mtnn_select(const mtnn_model* model, const double prefix5[5], int64_t m, int64_t n,
                 int64_t k, int64_t free_bytes, double* raw_out, int* choice_out,
                 int* reason_out);
+/* Host cost of one mtnn_select decision in C++ (no FFI), averaged over `iters`
+ * decisions on sweep shapes with ample free memory: the paper's "0.005 ms"
+ * predict budget measured on this build. */
+int mtnn_select_cost_ns(const mtnn_model* model, const double prefix5[5], int64_t iters,
+                        double* ns_per_call);
 /* Dispatcher.gemm (selector.py:192-221): select, run TNN or NT; a TNN
  * allocation failure is retried as NT (choice_out reports what ran). */
 int mtnn_dispatch_gemm(const mtnn_model* model, const double prefix5[5], const float* A,

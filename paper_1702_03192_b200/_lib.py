@@ -96,6 +96,7 @@ def _load():
         "mtnn_model_raw": (c_int, [c_void_p, _DP, c_int64, _DP]),
         "mtnn_select": (c_int, [c_void_p, _DP, c_int64, c_int64, c_int64, c_int64, _DP,
                                 POINTER(c_int), POINTER(c_int)]),
+        "mtnn_select_cost_ns": (c_int, [c_void_p, _DP, c_int64, _DP]),
         "mtnn_dispatch_gemm": (c_int, [c_void_p, _DP, c_void_p, c_void_p, c_void_p, c_int64, c_int64,
                                        c_int64, c_int64, c_int, c_void_p, POINTER(c_int)]),
         "mtnn_dispatch_gemm_host": (c_int, [c_void_p, _DP, c_void_p, c_void_p, c_void_p, c_int64,

@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <memory>
+#include <chrono>
 #include <string>
 #include <vector>
 
@@ -462,6 +463,27 @@ int mtnn_select(const mtnn_model* model, const double prefix5[5], int64_t m, int
   if (raw_out) *raw_out = raw;
   if (choice_out) *choice_out = choice;
   if (reason_out) *reason_out = reason;
+  return MTNN_OK;
+}
+
+int mtnn_select_cost_ns(const mtnn_model* model, const double prefix5[5], int64_t iters,
+                        double* ns_per_call) {
+  if (!model || !prefix5 || !ns_per_call || iters <= 0) return fail(MTNN_EINVAL, "bad argument");
+  // shapes from the sweep grid, cycled, so the walk takes different branches
+  static const int64_t dims[8] = {128, 256, 512, 1024, 2048, 4096, 8192, 16384};
+  volatile int sink = 0;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int64_t i = 0; i < iters; ++i) {
+    double raw;
+    int choice, reason;
+    const int rc = mtnn_select(model, prefix5, dims[i & 7], dims[(i >> 3) & 7], dims[(i >> 6) & 7],
+                               int64_t(1) << 40, &raw, &choice, &reason);
+    if (rc != MTNN_OK) return rc;
+    sink = sink + choice;
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  (void)sink;
+  *ns_per_call = std::chrono::duration<double, std::nano>(t1 - t0).count() / (double)iters;
   return MTNN_OK;
 }
 

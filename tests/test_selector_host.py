@@ -131,3 +131,17 @@ def test_native_decision_is_sub_microsecond(platform_a):
     per_call = min(batches)
     # the ctypes round trip dominates; the measured total bounds the native cost
     assert per_call < 5e-6
+
+
+def test_native_decision_cost_without_ffi(platform_a):
+    """mtnn_select in C++ alone (no ctypes round trip) is sub-microsecond."""
+    import ctypes
+
+    from paper_1702_03192_b200 import _lib
+
+    native = gbdt.NativeModel.from_json(golden_model_text("fixture"))
+    prefix = np.array(platform_a.as_tuple())
+    ns = ctypes.c_double()
+    _lib.check(_lib.lib.mtnn_select_cost_ns(native.handle, prefix.ctypes.data_as(_lib._DP),
+                                            200000, ctypes.byref(ns)))
+    assert 0 < ns.value < 1000.0, ns.value
