@@ -1492,7 +1492,7 @@ int tc_pair_mode() {
   int v = g_tc_pair.load(std::memory_order_relaxed);
   if (v < 0) {
     const char* e = getenv("MTNN_TC_PAIR");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = e ? std::min(2, std::max(0, atoi(e))) : 1;
     g_tc_pair.store(v, std::memory_order_relaxed);
   }
   return v;
