@@ -17,7 +17,8 @@
 //     CTA, 8 CTAs per SM) to cover HBM latency;
 //   * a 1-D grid over tiles, so any shape up to 2^31 tiles launches.
 // Shapes whose rows are not 16-byte multiples (cols % 4 or rows % 4 != 0, or
-// unaligned base pointers) take a scalar 32x32 padded-tile kernel instead.
+// unaligned base pointers) take a 4-byte-word 64x64 padded-tile kernel instead
+// (32x32 below 64 rows or columns).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -120,6 +121,41 @@ transpose_scalar_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ 
   }
 }
 
+// Fallback for rows/cols that are not 16-byte multiples: 64x64 tiles of 4-byte
+// words, 16 loads per thread issued before any use (16 KiB in flight per CTA),
+// padded shared memory; each warp still reads and writes 128 contiguous bytes
+// per row. Used for odd shapes of the transpose sweep (e.g. 4097 x 1023).
+__global__ void __launch_bounds__(256)
+transpose_scalar64_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                          int64_t rows, int64_t cols, int64_t tiles_c) {
+  __shared__ uint32_t smem[64][65];
+  const int64_t tile = blockIdx.x;
+  const int64_t tr = tile / tiles_c;
+  const int64_t tc = tile - tr * tiles_c;
+  const int64_t r0 = tr * 64, c0 = tc * 64;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8
+  uint32_t v[16];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t r = r0 + ty + 8 * i, c = c0 + tx + 32 * h;
+      v[2 * i + h] = (r < rows && c < cols) ? __ldg(in + r * cols + c) : 0u;
+    }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) smem[ty + 8 * i][tx + 32 * h] = v[2 * i + h];
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t orow = c0 + ty + 8 * i, ocol = r0 + tx + 32 * h;
+      if (orow < cols && ocol < rows) out[orow * rows + ocol] = smem[tx + 32 * h][ty + 8 * i];
+    }
+}
+
 }  // namespace
 
 int launch_transpose(const float* in, float* out, int64_t rows, int64_t cols,
@@ -135,6 +171,14 @@ int launch_transpose(const float* in, float* out, int64_t rows, int64_t cols,
     const int64_t tiles = tiles_r * tiles_c;
     if (tiles > 0x7fffffffLL) return fail(MTNN_EINVAL, "transpose: matrix too large");
     transpose_vec4_kernel<<<(unsigned)tiles, kThreads, 0, s>>>(
+        reinterpret_cast<const uint32_t*>(in), reinterpret_cast<uint32_t*>(out), rows,
+        cols, tiles_c);
+  } else if (rows >= 64 && cols >= 64) {
+    const int64_t tiles_r = (rows + 63) / 64;
+    const int64_t tiles_c = (cols + 63) / 64;
+    const int64_t tiles = tiles_r * tiles_c;
+    if (tiles > 0x7fffffffLL) return fail(MTNN_EINVAL, "transpose: matrix too large");
+    transpose_scalar64_kernel<<<(unsigned)tiles, 256, 0, s>>>(
         reinterpret_cast<const uint32_t*>(in), reinterpret_cast<uint32_t*>(out), rows,
         cols, tiles_c);
   } else {
