@@ -542,6 +542,9 @@ def main():
     if gather_mode is not None:
         extra["gather"] = gather_mode
     if world == 1:
+        # a short idle first: the pass measures single transposes, not the power
+        # state the preceding back-to-back sweep passes leave behind
+        time.sleep(1.5)
         extra["transpose"] = transpose_pass(B, C, flush_src, stream, hbm, L, _lib, torch)
     extra["selector_native_ns_incl_ctypes"] = selector_cost(L, handle, prefix_p)
     ns = ctypes.c_double()
