@@ -301,6 +301,72 @@ split_cols_f16_kernel(const float* __restrict__ x, const unsigned* __restrict__ 
   }
 }
 
+// Column split in one launch (MN-major B^T, k x n, n % 16 == 0): one CTA per
+// strip of 32 columns (128 bytes per row), 512 threads = 8 16-byte columns x 64
+// row lanes. Pass 1 reads the strip for the column maxima (reduced through
+// shared memory), pass 2 re-reads it — from L2 while the strips in flight fit
+// there — and writes the halves: 8 B of DRAM traffic per element instead of the
+// two-kernel path's 12, and no scratch or memset.
+constexpr int kStripCols = 32;
+constexpr int kStripLanes = 64;
+
+__global__ void __launch_bounds__(8 * kStripLanes)
+split_cols_strip_kernel(const float* __restrict__ x, __half* __restrict__ hi,
+                        __half* __restrict__ lo, float* __restrict__ inv_scale, int64_t k,
+                        int64_t n) {
+  __shared__ float4 red[kStripLanes][8];
+  __shared__ float4 scale[8];
+  const int c4 = threadIdx.x % 8;
+  const int rl = threadIdx.x / 8;
+  const int64_t col = (int64_t)blockIdx.x * kStripCols + 4 * c4;
+  const bool active = col < n;  // n % 4 == 0: the whole float4 is in range
+  float4 mx = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (active) {
+#pragma unroll 4
+    for (int64_t r = rl; r < k; r += kStripLanes) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(x + r * n + col));
+      mx.x = isnan(v.x) ? INFINITY : fmaxf(mx.x, fabsf(v.x));
+      mx.y = isnan(v.y) ? INFINITY : fmaxf(mx.y, fabsf(v.y));
+      mx.z = isnan(v.z) ? INFINITY : fmaxf(mx.z, fabsf(v.z));
+      mx.w = isnan(v.w) ? INFINITY : fmaxf(mx.w, fabsf(v.w));
+    }
+  }
+  red[rl][c4] = mx;
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    float4 m = red[0][threadIdx.x];
+    for (int i = 1; i < kStripLanes; ++i) {
+      const float4 o = red[i][threadIdx.x];
+      m.x = fmaxf(m.x, o.x); m.y = fmaxf(m.y, o.y); m.z = fmaxf(m.z, o.z); m.w = fmaxf(m.w, o.w);
+    }
+    const float4 sc = make_float4(pow2_scale(m.x), pow2_scale(m.y), pow2_scale(m.z), pow2_scale(m.w));
+    scale[threadIdx.x] = sc;
+    const int64_t c = (int64_t)blockIdx.x * kStripCols + 4 * threadIdx.x;
+    if (c < n)
+      *reinterpret_cast<float4*>(inv_scale + c) =
+          make_float4(1.f / sc.x, 1.f / sc.y, 1.f / sc.z, 1.f / sc.w);
+  }
+  __syncthreads();
+  if (!active) return;
+  const float4 sc = scale[c4];
+#pragma unroll 4
+  for (int64_t r = rl; r < k; r += kStripLanes) {
+    const int64_t i = r * n + col;
+    const float4 v = __ldg(reinterpret_cast<const float4*>(x + i));
+    __half h0, h1, h2, h3, l0, l1, l2, l3;
+    split2(v.x, sc.x, h0, l0);
+    split2(v.y, sc.y, h1, l1);
+    split2(v.z, sc.z, h2, l2);
+    split2(v.w, sc.w, h3, l3);
+    __half2 hp0 = __halves2half2(h0, h1), hp1 = __halves2half2(h2, h3);
+    __half2 lp0 = __halves2half2(l0, l1), lp1 = __halves2half2(l2, l3);
+    reinterpret_cast<uint2*>(hi)[i / 4] =
+        make_uint2(*reinterpret_cast<uint32_t*>(&hp0), *reinterpret_cast<uint32_t*>(&hp1));
+    reinterpret_cast<uint2*>(lo)[i / 4] =
+        make_uint2(*reinterpret_cast<uint32_t*>(&lp0), *reinterpret_cast<uint32_t*>(&lp1));
+  }
+}
+
 }  // namespace
 
 // Splits (hi != nullptr) or row-scales (hi == nullptr) the rows of up to two
@@ -363,6 +429,21 @@ int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,
   if (k <= 0 || n <= 0) return MTNN_OK;
   const DeviceInfo* di = nullptr;
   MTNN_TRY(device_info(&di));
+  const int64_t strips = (n + kStripCols - 1) / kStripCols;
+  // one launch while the strips in flight (~2 per SM) keep their re-read in L2
+  // and there are enough of them to cover the SMs
+  static const bool strip_on = [] {
+    const char* e = getenv("MTNN_SPLIT_STRIP");
+    return !(e && e[0] == '0');
+  }();
+  if (strip_on && strips >= di->sm_count / 2 &&
+      (double)std::min<int64_t>(strips, 2 * di->sm_count) * (double)k * 128.0 <= 64.0 * (1 << 20)) {
+    KernelTimer timer(MTNN_KCLASS_SPLIT, 8.0 * (double)k * (double)n, s);
+    split_cols_strip_kernel<<<(unsigned)strips, 8 * kStripLanes, 0, s>>>(
+        x, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale, k, n);
+    MTNN_CUDA_TRY(cudaGetLastError());
+    return MTNN_OK;
+  }
   KernelTimer timer(MTNN_KCLASS_SPLIT, 12.0 * (double)k * (double)n, s);
   MTNN_CUDA_TRY(cudaMemsetAsync(colmax_scratch, 0, (size_t)n * sizeof(unsigned), s));
   const int64_t n4 = n / 4;
