@@ -180,7 +180,8 @@ split_rows_f16_reg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
   }
 }
 
-// One CTA per row for long rows (k > kWarpRowMax): split jobs stage the row in
+// One CTA per row for rows too long for registers (16384 < k, row <= 160 KiB;
+// all k > kWarpRowMax with MTNN_SPLIT_CTAREG=0): split jobs stage the row in
 // shared memory during the max pass, so DRAM sees exactly one read and one write
 // per element (8 B) — with warp-per-row the ~600 MB of long rows in flight
 // overflow L2 and the split pass re-reads them from DRAM (12 B per element).
@@ -241,6 +242,81 @@ split_rows_f16_smem_kernel(const RowJob j0, const RowJob j1, int64_t k) {
     }
     __syncthreads();  // row_s and red are reused by the next row
   }
+}
+
+// One CTA per row with the row in registers (2048 < k <= 256 * 4 * kV): every
+// thread issues its kV 16-byte loads before the first use, the row max goes
+// through one shared-memory round (double-buffered by row parity, so one
+// barrier per row), and the halves are written from the same registers. Several
+// CTAs per SM keep 80-128 KiB of loads in flight per SM; the smem-staged kernel
+// above serialises load, reduce and store phases inside one CTA.
+constexpr int kCtaRowThreads = 256;
+
+template <int kV>
+__global__ void __launch_bounds__(kCtaRowThreads)
+split_rows_f16_ctareg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
+  __shared__ float red[2][kCtaRowThreads / 32];
+  const int64_t k4 = k / 4;
+  const int t = threadIdx.x;
+  int parity = 0;
+  for (int64_t v = blockIdx.x; v < j0.rows + j1.rows; v += gridDim.x, parity ^= 1) {
+    int64_t r;
+    const RowJob& j = pick(j0, j1, v, r);
+    const float4* row = reinterpret_cast<const float4*>(j.x + r * k);
+    float4 x[kV];
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const int64_t i = t + kCtaRowThreads * u;
+      x[u] = i < k4 ? ldg4(row + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float mx = 0.f;
+#pragma unroll
+    for (int u = 0; u < kV; ++u) mx = fmaxf(mx, absmax4(x[u]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (t % 32 == 0) red[parity][t / 32] = mx;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kCtaRowThreads / 32; ++w) mx = fmaxf(mx, red[parity][w]);
+    const float s = pow2_scale(mx);
+    if (t == 0) j.inv_scale[r] = 1.f / s;
+    if (j.hi == nullptr) continue;  // row scales only
+    uint2* hrow = reinterpret_cast<uint2*>(j.hi + r * k);
+    uint2* lrow = reinterpret_cast<uint2*>(j.lo + r * k);
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const int64_t i = t + kCtaRowThreads * u;
+      if (i < k4) {
+        uint2 hw, lw;
+        split4(x[u], s, hw, lw);
+        hrow[i] = hw;
+        lrow[i] = lw;
+      }
+    }
+  }
+}
+
+template <int kV>
+int launch_ctareg(const RowJob& j0, const RowJob& j1, int64_t rows, int64_t k, int sm_count,
+                  cudaStream_t s) {
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    MTNN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, split_rows_f16_ctareg_kernel<kV>, kCtaRowThreads, 0));
+    per_sm = std::max(per_sm, 1);
+  }
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)sm_count * per_sm));
+  split_rows_f16_ctareg_kernel<kV><<<(unsigned)blocks, kCtaRowThreads, 0, s>>>(j0, j1, k);
+  return MTNN_OK;
+}
+
+bool ctareg_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MTNN_SPLIT_CTAREG");  // 0: smem-staged kernel (A/B runs)
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
 }
 
 // Column max of a k x n matrix (MN-major B^T): |x| as uint bits (monotonic for
@@ -387,7 +463,15 @@ int launch_split_rows_f16_pair(const float* x0, void* hi0, void* lo0, float* inv
                     s);
   const size_t row_bytes = (size_t)k * sizeof(float);
   const bool any_split = (hi0 && rows0) || (hi1 && rows1);
-  if (k > kWarpRowMax && row_bytes <= 160 * 1024 && any_split) {
+  if (k > kWarpRowMax && k <= 16384 && ctareg_enabled()) {
+    // measured (16384 x 8192 rows of 8192): 384 -> 280 us; 4096^2 x 4096: 101 -> 51 us
+    if (k <= 4096)
+      MTNN_TRY(launch_ctareg<4>(j0, j1, rows, k, di->sm_count, s));
+    else if (k <= 8192)
+      MTNN_TRY(launch_ctareg<8>(j0, j1, rows, k, di->sm_count, s));
+    else
+      MTNN_TRY(launch_ctareg<16>(j0, j1, rows, k, di->sm_count, s));
+  } else if (k > kWarpRowMax && row_bytes <= 160 * 1024 && any_split) {
     static bool attr = false;
     if (!attr) {
       MTNN_CUDA_TRY(cudaFuncSetAttribute(split_rows_f16_smem_kernel,
@@ -399,11 +483,17 @@ int launch_split_rows_f16_pair(const float* x0, void* hi0, void* lo0, float* inv
     split_rows_f16_smem_kernel<<<(unsigned)blocks, kRowThreads, row_bytes, s>>>(j0, j1, k);
   } else {
     int64_t blocks = (rows + 7) / 8;
-    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)di->sm_count * 16));
-    // 1024 < k <= 2048: whole row in registers (measured 5.5 -> 6.8 TB/s at
-    // 16384 x 2048); shorter rows keep the looped kernel (faster there: more
-    // resident warps at its lower register count)
-    if (k > 1024 && k <= 2048)  // (longer rows land here only past the smem limit)
+    // rows of <= 512 and 1024 < k <= 2048: whole row in registers, every load
+    // issued before the first use (16384 x 2048: 5.5 -> 6.8 TB/s; 32768 rows of
+    // 256: 18.3 -> 16.4 us); k = 1024 keeps the looped kernel (more resident
+    // warps at its lower register count: 40.8 vs 42.5 us at 32768 rows)
+    const bool reg = k <= 512 || (k > 1024 && k <= 2048);  // (longer rows: past the smem limit)
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)di->sm_count * (reg && k <= 512 ? 8 : 16)));
+    if (k <= 256)
+      split_rows_f16_reg_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(j0, j1, k);
+    else if (k <= 512)
+      split_rows_f16_reg_kernel<4><<<(unsigned)blocks, 256, 0, s>>>(j0, j1, k);
+    else if (reg)
       split_rows_f16_reg_kernel<16><<<(unsigned)blocks, 256, 0, s>>>(j0, j1, k);
     else
       split_rows_f16_kernel<<<(unsigned)blocks, 256, 0, s>>>(j0, j1, k);

@@ -581,3 +581,26 @@ def test_random_shape_fuzz(rng):
         assert rel_frobenius(gemm_nn(a, np.ascontiguousarray(b.T))[rows], want) < FP32_GATE, (m, n, k, "nn")
         dev = gemm_nt(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy()
         assert rel_frobenius(dev[rows], want) < FP32_GATE, (m, n, k, "device")
+
+
+@pytest.mark.parametrize("k", [8, 96, 256, 264, 512, 520, 1024, 1032, 2048, 2056, 4096, 4104,
+                               8192, 8200, 16384, 16392, 40960, 41000])
+@pytest.mark.parametrize("n", [384, 200])
+def test_row_split_every_branch(rng, k, n):
+    """Every row-split kernel (looped / register warp-per-row / register
+    CTA-per-row / smem-staged / past the smem limit) picked by k, for pre-split
+    operands (n = 384) and row-scale-only jobs of the in-kernel split (n = 200),
+    on rows whose magnitudes span 2^-40..2^40: each output row within the gate
+    relative to its own norm; a NaN at a row's last element poisons exactly
+    that row."""
+    m = 384
+    a = random_matrix(rng, m, k) * np.exp2(rng.integers(-40, 41, m)).astype(np.float32)[:, None]
+    b = random_matrix(rng, n, k) * np.exp2(rng.integers(-40, 41, n)).astype(np.float32)[:, None]
+    a[5, k - 1] = np.nan
+    got = gemm_nt(a, b, variant="tc3xf16s")
+    assert np.all(np.isnan(got[5]))
+    ok = np.arange(m) != 5
+    want = oracle.oracle_nt_blas(a[ok], b)
+    g = got[ok]
+    err = np.linalg.norm(g - want, axis=1) / np.linalg.norm(want, axis=1)
+    assert err.max() < FP32_GATE, (k, n, float(err.max()))
