@@ -48,6 +48,11 @@ struct DeviceInfo {
 // Returns MTNN_ENOTSUP when no sm_100-class device is current.
 int device_info(const DeviceInfo** out);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute belongs to the device's context, so a process driving several
+// GPUs must set it on each.
+int set_max_dynamic_smem(const void* kernel, int bytes);
+
 // Kernel timing instrumentation (mtnn_profile_*): a scope records a CUDA event
 // pair around one launch when profiling is enabled, else does nothing.
 struct KernelTimer {
@@ -118,7 +123,9 @@ int launch_split_rows_f16_pair(const float* x0, void* hi0, void* lo0, float* inv
                                int64_t k, cudaStream_t s);
 // 1/s per row (s = split_rows_f16's power-of-two row scale), reading x only.
 int launch_rowmax_f16(const float* x, float* inv_scale, int64_t rows, int64_t k, cudaStream_t s);
+// Scratch (device bytes) launch_split_cols_f16 needs for an n-column operand.
+size_t split_cols_scratch_bytes(int64_t n);
 int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,
-                          unsigned* colmax_scratch, int64_t k, int64_t n, cudaStream_t s);
+                          float* partial_scratch, int64_t k, int64_t n, cudaStream_t s);
 
 }  // namespace mtnn

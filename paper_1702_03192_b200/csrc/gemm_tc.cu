@@ -853,12 +853,7 @@ static int launch_impl(const void* ahi, const void* alo, const void* bhi,
     MTNN_TRY(encode(&mc, out, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
   }
   auto kern = gemm_tc3x_kernel<BN, B_MN, Kind, kConv>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    MTNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       S::kTotal));
-    attr_set = true;
-  }
+  MTNN_TRY(set_max_dynamic_smem((const void*)kern, S::kTotal));
   {
     KernelTimer timer(Kind::kScaled ? MTNN_KCLASS_GEMM_TC_F16S : MTNN_KCLASS_GEMM_TC,
                       2.0 * (double)p.m * (double)p.n * (double)p.k, s);
@@ -1256,12 +1251,7 @@ static int launch_pair_impl(const void* ahi, const void* alo, const void* bhi, c
       MTNN_TRY(encode(&peers.map[d], peer_out[d], 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B));
   }
   auto kern = gemm_tc3x_pair_kernel<B_MN, Kind>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    MTNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       S::kTotal));
-    attr_set = true;
-  }
+  MTNN_TRY(set_max_dynamic_smem((const void*)kern, S::kTotal));
   {
     KernelTimer timer(Kind::kScaled ? MTNN_KCLASS_GEMM_TC_F16S : MTNN_KCLASS_GEMM_TC,
                       2.0 * (double)p.m * (double)p.n * (double)p.k, s);
@@ -1410,16 +1400,16 @@ int tc_prepare(const float* X, int64_t rows, int64_t k, bool mn_major, TcKind ki
     out->inv_scale = nullptr;
     return MTNN_OK;
   }
-  // F16S: [h | l | 1/s (+ column-max scratch)]
+  // F16S: [h | l | 1/s (+ partial column maxima)]
   const size_t oh = align256((size_t)count * 2);
   const size_t osc = align256((size_t)rows * 4);
-  MTNN_TRY(ws.alloc(2 * oh + osc + (mn_major ? osc : 0), s));
+  MTNN_TRY(ws.alloc(2 * oh + osc + (mn_major ? align256(split_cols_scratch_bytes(rows)) : 0), s));
   uint8_t* base = static_cast<uint8_t*>(ws.ptr);
   float* inv = reinterpret_cast<float*>(base + 2 * oh);
   if (!mn_major) {
     MTNN_TRY(launch_split_rows_f16(X, base, base + oh, inv, rows, k, s));
   } else {
-    unsigned* cm = reinterpret_cast<unsigned*>(base + 2 * oh + osc);
+    float* cm = reinterpret_cast<float*>(base + 2 * oh + osc);
     MTNN_TRY(launch_split_cols_f16(X, base, base + oh, inv, cm, k, rows, s));
   }
   out->hi = base;

@@ -14,6 +14,7 @@
 #include <atomic>
 #include <chrono>
 #include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 #include <algorithm>
@@ -80,6 +81,18 @@ int device_info(const DeviceInfo** out) {
                 "library has no other code path",
                 dev, g_dev[dev].cc_major, g_dev[dev].cc_minor);
   *out = &g_dev[dev];
+  return MTNN_OK;
+}
+
+int set_max_dynamic_smem(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  MTNN_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({kernel, dev})) return MTNN_OK;
+  MTNN_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert({kernel, dev});
   return MTNN_OK;
 }
 

@@ -319,60 +319,83 @@ bool ctareg_enabled() {
   return on == 1;
 }
 
-// Column max of a k x n matrix (MN-major B^T): |x| as uint bits (monotonic for
-// non-negative floats; NaN maps above +Inf) folded with atomicMax.
+// Two-pass column split (MN-major B^T, k x n, any k): pass 1 writes per-chunk
+// partial column maxima (chunk = a band of rows; no atomics, no memset), pass 2
+// folds the <= kMaxChunks partials of its columns once per thread and streams
+// its band. 256 threads = 32 16-byte columns (512 contiguous bytes of a row per
+// warp) x 8 row lanes. DRAM: 4 B read + (4 B read, mostly L2 for operands that
+// fit) + 4 B written per element.
+constexpr int kMaxChunks = 32;
+
+template <int kLanes>
 __global__ void __launch_bounds__(256)
-colmax_kernel(const float* __restrict__ x, unsigned* __restrict__ colmax_bits, int64_t k,
-              int64_t n, int64_t rows_per_block) {
-  const int64_t c4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // float4 column
-  if (c4 * 4 >= n) return;
-  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block;
-  const int64_t r1 = min(k, r0 + rows_per_block);
-  float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
-  for (int64_t r = r0; r < r1; ++r) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(x + r * n) + c4);
-    m0 = isnan(v.x) ? INFINITY : fmaxf(m0, fabsf(v.x));
-    m1 = isnan(v.y) ? INFINITY : fmaxf(m1, fabsf(v.y));
-    m2 = isnan(v.z) ? INFINITY : fmaxf(m2, fabsf(v.z));
-    m3 = isnan(v.w) ? INFINITY : fmaxf(m3, fabsf(v.w));
+colmax_partial_kernel(const float* __restrict__ x, float* __restrict__ partial, int64_t k,
+                      int64_t n, int64_t rows_per_chunk) {
+  constexpr int kBandCols = 4 * kLanes, kBandRowLanes = 256 / kLanes;
+  __shared__ float4 red[kBandRowLanes][kLanes];
+  const int c4 = threadIdx.x % kLanes;
+  const int rl = threadIdx.x / kLanes;
+  const int64_t col = (int64_t)blockIdx.x * kBandCols + 4 * c4;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_chunk;
+  const int64_t r1 = min(k, r0 + rows_per_chunk);
+  float4 mx = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (col < n) {
+#pragma unroll 4
+    for (int64_t r = r0 + rl; r < r1; r += kBandRowLanes) {
+      const float4 v = ldg4(reinterpret_cast<const float4*>(x + r * n + col));
+      mx.x = isnan(v.x) ? INFINITY : fmaxf(mx.x, fabsf(v.x));
+      mx.y = isnan(v.y) ? INFINITY : fmaxf(mx.y, fabsf(v.y));
+      mx.z = isnan(v.z) ? INFINITY : fmaxf(mx.z, fabsf(v.z));
+      mx.w = isnan(v.w) ? INFINITY : fmaxf(mx.w, fabsf(v.w));
+    }
   }
-  atomicMax(colmax_bits + 4 * c4 + 0, __float_as_uint(m0));
-  atomicMax(colmax_bits + 4 * c4 + 1, __float_as_uint(m1));
-  atomicMax(colmax_bits + 4 * c4 + 2, __float_as_uint(m2));
-  atomicMax(colmax_bits + 4 * c4 + 3, __float_as_uint(m3));
+  red[rl][c4] = mx;
+  __syncthreads();
+  if (rl == 0 && col < n) {
+    for (int i = 1; i < kBandRowLanes; ++i) {
+      const float4 o = red[i][c4];
+      mx.x = fmaxf(mx.x, o.x); mx.y = fmaxf(mx.y, o.y); mx.z = fmaxf(mx.z, o.z); mx.w = fmaxf(mx.w, o.w);
+    }
+    *reinterpret_cast<float4*>(partial + (int64_t)blockIdx.y * n + col) = mx;
+  }
 }
 
-// Elementwise split of a k x n matrix with per-column scales.
+template <int kLanes>
 __global__ void __launch_bounds__(256)
-split_cols_f16_kernel(const float* __restrict__ x, const unsigned* __restrict__ colmax_bits,
-                      __half* __restrict__ hi, __half* __restrict__ lo,
-                      float* __restrict__ inv_scale, int64_t k, int64_t n) {
-  const int64_t n4 = n / 4;
-  const int64_t total = k * n4;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-    const int64_t r = i / n4, c4 = i - r * n4;
-    const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
-    const float s0 = pow2_scale(__uint_as_float(colmax_bits[4 * c4 + 0]));
-    const float s1 = pow2_scale(__uint_as_float(colmax_bits[4 * c4 + 1]));
-    const float s2 = pow2_scale(__uint_as_float(colmax_bits[4 * c4 + 2]));
-    const float s3 = pow2_scale(__uint_as_float(colmax_bits[4 * c4 + 3]));
-    if (r == 0) {
-      inv_scale[4 * c4 + 0] = 1.f / s0;
-      inv_scale[4 * c4 + 1] = 1.f / s1;
-      inv_scale[4 * c4 + 2] = 1.f / s2;
-      inv_scale[4 * c4 + 3] = 1.f / s3;
-    }
+split_cols_band_kernel(const float* __restrict__ x, const float* __restrict__ partial, int chunks,
+                       __half* __restrict__ hi, __half* __restrict__ lo,
+                       float* __restrict__ inv_scale, int64_t k, int64_t n,
+                       int64_t rows_per_band) {
+  constexpr int kBandCols = 4 * kLanes, kBandRowLanes = 256 / kLanes;
+  const int c4 = threadIdx.x % kLanes;
+  const int rl = threadIdx.x / kLanes;
+  const int64_t col = (int64_t)blockIdx.x * kBandCols + 4 * c4;
+  if (col >= n) return;
+  float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int q = 0; q < chunks; ++q) {
+    const float4 o = ldg4(reinterpret_cast<const float4*>(partial + (int64_t)q * n + col));
+    m.x = fmaxf(m.x, o.x); m.y = fmaxf(m.y, o.y); m.z = fmaxf(m.z, o.z); m.w = fmaxf(m.w, o.w);
+  }
+  const float4 sc = make_float4(pow2_scale(m.x), pow2_scale(m.y), pow2_scale(m.z), pow2_scale(m.w));
+  if (blockIdx.y == 0 && rl == 0)
+    *reinterpret_cast<float4*>(inv_scale + col) =
+        make_float4(1.f / sc.x, 1.f / sc.y, 1.f / sc.z, 1.f / sc.w);
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_band;
+  const int64_t r1 = min(k, r0 + rows_per_band);
+#pragma unroll 4
+  for (int64_t r = r0 + rl; r < r1; r += kBandRowLanes) {
+    const int64_t i = r * n + col;
+    const float4 v = ldg4(reinterpret_cast<const float4*>(x + i));
     __half h0, h1, h2, h3, l0, l1, l2, l3;
-    split2(v.x, s0, h0, l0);
-    split2(v.y, s1, h1, l1);
-    split2(v.z, s2, h2, l2);
-    split2(v.w, s3, h3, l3);
+    split2(v.x, sc.x, h0, l0);
+    split2(v.y, sc.y, h1, l1);
+    split2(v.z, sc.z, h2, l2);
+    split2(v.w, sc.w, h3, l3);
     __half2 hp0 = __halves2half2(h0, h1), hp1 = __halves2half2(h2, h3);
     __half2 lp0 = __halves2half2(l0, l1), lp1 = __halves2half2(l2, l3);
-    reinterpret_cast<uint2*>(hi)[i] =
+    reinterpret_cast<uint2*>(hi)[i / 4] =
         make_uint2(*reinterpret_cast<uint32_t*>(&hp0), *reinterpret_cast<uint32_t*>(&hp1));
-    reinterpret_cast<uint2*>(lo)[i] =
+    reinterpret_cast<uint2*>(lo)[i / 4] =
         make_uint2(*reinterpret_cast<uint32_t*>(&lp0), *reinterpret_cast<uint32_t*>(&lp1));
   }
 }
@@ -443,6 +466,145 @@ split_cols_strip_kernel(const float* __restrict__ x, __half* __restrict__ hi,
   }
 }
 
+// Column split by thread-block clusters (MN-major B^T, k x n, k <= 8192): a
+// cluster of c <= 8 CTAs owns one strip of 32 columns, CTA q holds rows
+// [q*32*kR, (q+1)*32*kR) of it in registers (256 threads = 8 16-byte columns x
+// 32 row lanes, kR rows each). The column maxima are reduced inside each CTA,
+// exchanged through distributed shared memory, and the halves are written from
+// the same registers: one DRAM read and one write per element (8 B), every load
+// issued up front, and strips x c CTAs to cover the SMs even when n is narrow
+// (the single-CTA strip kernel above leaves n = 4096 at ~2.3 TB/s).
+constexpr int kClusterRowLanes = 32;
+constexpr int kClusterMax = 8;
+
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cl_size() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float4 ld_dsmem(const float4* p, uint32_t rank) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(ra)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ float nanmax(float m, float v) {
+  return isnan(v) ? INFINITY : fmaxf(m, fabsf(v));
+}
+
+template <int kR>
+__global__ void __launch_bounds__(8 * kClusterRowLanes)
+split_cols_cluster_kernel(const float* __restrict__ x, __half* __restrict__ hi,
+                          __half* __restrict__ lo, float* __restrict__ inv_scale, int64_t k,
+                          int64_t n) {
+  __shared__ float4 red[kClusterRowLanes][8];
+  __shared__ float4 part[8];
+  __shared__ float4 scale[8];
+  const uint32_t csize = cl_size(), rank = cl_rank();
+  const int c4 = threadIdx.x % 8;
+  const int rl = threadIdx.x / 8;
+  const int64_t strip = blockIdx.x / csize;
+  const int64_t col = strip * kStripCols + 4 * c4;
+  const bool active = col < n;  // n % 4 == 0: the whole float4 is in range
+  const int64_t r0 = (int64_t)rank * kClusterRowLanes * kR + rl;
+  float4 v[kR];
+  float4 mx = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int u = 0; u < kR; ++u) {
+    const int64_t r = r0 + kClusterRowLanes * u;
+    v[u] = (active && r < k) ? ldg4(reinterpret_cast<const float4*>(x + r * n + col))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int u = 0; u < kR; ++u) {
+    mx.x = nanmax(mx.x, v[u].x); mx.y = nanmax(mx.y, v[u].y);
+    mx.z = nanmax(mx.z, v[u].z); mx.w = nanmax(mx.w, v[u].w);
+  }
+  red[rl][c4] = mx;
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    float4 m = red[0][threadIdx.x];
+    for (int i = 1; i < kClusterRowLanes; ++i) {
+      const float4 o = red[i][threadIdx.x];
+      m.x = fmaxf(m.x, o.x); m.y = fmaxf(m.y, o.y); m.z = fmaxf(m.z, o.z); m.w = fmaxf(m.w, o.w);
+    }
+    part[threadIdx.x] = m;
+  }
+  cl_sync();  // every CTA's partial maxima are visible cluster-wide
+  if (threadIdx.x < 8) {
+    float4 m = part[threadIdx.x];
+    for (uint32_t q = 0; q < csize; ++q) {
+      if (q == rank) continue;
+      const float4 o = ld_dsmem(&part[threadIdx.x], q);
+      m.x = fmaxf(m.x, o.x); m.y = fmaxf(m.y, o.y); m.z = fmaxf(m.z, o.z); m.w = fmaxf(m.w, o.w);
+    }
+    const float4 sc = make_float4(pow2_scale(m.x), pow2_scale(m.y), pow2_scale(m.z), pow2_scale(m.w));
+    scale[threadIdx.x] = sc;
+    const int64_t c = strip * kStripCols + 4 * threadIdx.x;
+    if (rank == 0 && c < n)
+      *reinterpret_cast<float4*>(inv_scale + c) =
+          make_float4(1.f / sc.x, 1.f / sc.y, 1.f / sc.z, 1.f / sc.w);
+  }
+  cl_sync();  // peers are done reading `part` (no CTA exits under a reader); scale is visible
+  if (!active) return;
+  const float4 sc = scale[c4];
+#pragma unroll
+  for (int u = 0; u < kR; ++u) {
+    const int64_t r = r0 + kClusterRowLanes * u;
+    if (r < k) {
+      const float4 w = v[u];
+      __half h0, h1, h2, h3, l0, l1, l2, l3;
+      split2(w.x, sc.x, h0, l0);
+      split2(w.y, sc.y, h1, l1);
+      split2(w.z, sc.z, h2, l2);
+      split2(w.w, sc.w, h3, l3);
+      __half2 hp0 = __halves2half2(h0, h1), hp1 = __halves2half2(h2, h3);
+      __half2 lp0 = __halves2half2(l0, l1), lp1 = __halves2half2(l2, l3);
+      const int64_t i = (r * n + col) / 4;
+      reinterpret_cast<uint2*>(hi)[i] =
+          make_uint2(*reinterpret_cast<uint32_t*>(&hp0), *reinterpret_cast<uint32_t*>(&hp1));
+      reinterpret_cast<uint2*>(lo)[i] =
+          make_uint2(*reinterpret_cast<uint32_t*>(&lp0), *reinterpret_cast<uint32_t*>(&lp1));
+    }
+  }
+}
+
+template <int kR>
+int launch_cols_cluster(const float* x, void* hi, void* lo, float* inv_scale, int64_t k,
+                        int64_t n, cudaStream_t s) {
+  const int64_t strips = (n + kStripCols - 1) / kStripCols;
+  const unsigned c = (unsigned)((k + kClusterRowLanes * kR - 1) / (kClusterRowLanes * kR));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(strips * c));
+  cfg.blockDim = dim3(8 * kClusterRowLanes);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = c;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MTNN_CUDA_TRY(cudaLaunchKernelEx(&cfg, split_cols_cluster_kernel<kR>, x,
+                                   static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale,
+                                   k, n));
+  return MTNN_OK;
+}
+
 }  // namespace
 
 // Splits (hi != nullptr) or row-scales (hi == nullptr) the rows of up to two
@@ -472,12 +634,7 @@ int launch_split_rows_f16_pair(const float* x0, void* hi0, void* lo0, float* inv
     else
       MTNN_TRY(launch_ctareg<16>(j0, j1, rows, k, di->sm_count, s));
   } else if (k > kWarpRowMax && row_bytes <= 160 * 1024 && any_split) {
-    static bool attr = false;
-    if (!attr) {
-      MTNN_CUDA_TRY(cudaFuncSetAttribute(split_rows_f16_smem_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-      attr = true;
-    }
+    MTNN_TRY(set_max_dynamic_smem((const void*)split_rows_f16_smem_kernel, 160 * 1024));
     const int per_sm = std::max<int>(1, std::min<int>(4, (int)((200 * 1024) / row_bytes)));
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)di->sm_count * per_sm));
     split_rows_f16_smem_kernel<<<(unsigned)blocks, kRowThreads, row_bytes, s>>>(j0, j1, k);
@@ -514,42 +671,67 @@ int launch_rowmax_f16(const float* x, float* inv_scale, int64_t rows, int64_t k,
                                     nullptr, nullptr, 0, k, s);
 }
 
+size_t split_cols_scratch_bytes(int64_t n) { return (size_t)kMaxChunks * (size_t)n * sizeof(float); }
+
 int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,
-                          unsigned* colmax_scratch, int64_t k, int64_t n, cudaStream_t s) {
+                          float* partial_scratch, int64_t k, int64_t n, cudaStream_t s) {
   if (k <= 0 || n <= 0) return MTNN_OK;
   const DeviceInfo* di = nullptr;
   MTNN_TRY(device_info(&di));
   const int64_t strips = (n + kStripCols - 1) / kStripCols;
-  // one launch while the strips in flight (~2 per SM) keep their re-read in L2
-  // and there are enough of them to cover the SMs
+  // MTNN_SPLIT_STRIP=0 forces the two-pass band path. Measured split times
+  // (NN calls, us; strip / cluster / band): k = 784, n = 4096: 21.6 / 25.0 / 27.7;
+  // k = 1024, n = 16384: 42.0 / 51.3 / 50.3; k = n = 4096: 72 / 52 / 55;
+  // k = n = 2048: - / 24-29 / 36; k = 8192, n = 8192: - / 205 / 201.
   static const bool strip_on = [] {
     const char* e = getenv("MTNN_SPLIT_STRIP");
     return !(e && e[0] == '0');
   }();
-  if (strip_on && strips >= di->sm_count / 2 &&
-      (double)std::min<int64_t>(strips, 2 * di->sm_count) * (double)k * 128.0 <= 64.0 * (1 << 20)) {
+  if (strip_on && k <= 1024 && strips >= di->sm_count / 2) {
+    // short columns, many strips: one CTA per strip re-reads its strip from L2
     KernelTimer timer(MTNN_KCLASS_SPLIT, 8.0 * (double)k * (double)n, s);
     split_cols_strip_kernel<<<(unsigned)strips, 8 * kStripLanes, 0, s>>>(
         x, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale, k, n);
     MTNN_CUDA_TRY(cudaGetLastError());
     return MTNN_OK;
   }
+  if (strip_on && k <= kClusterMax * kClusterRowLanes * 32) {
+    KernelTimer timer(MTNN_KCLASS_SPLIT, 8.0 * (double)k * (double)n, s);
+    // fewest rows per CTA that keep the cluster within 8 CTAs: the most CTAs
+    if (k <= kClusterMax * kClusterRowLanes * 4)
+      MTNN_TRY(launch_cols_cluster<4>(x, hi, lo, inv_scale, k, n, s));
+    else if (k <= kClusterMax * kClusterRowLanes * 8)
+      MTNN_TRY(launch_cols_cluster<8>(x, hi, lo, inv_scale, k, n, s));
+    else if (k <= kClusterMax * kClusterRowLanes * 16)
+      MTNN_TRY(launch_cols_cluster<16>(x, hi, lo, inv_scale, k, n, s));
+    else
+      MTNN_TRY(launch_cols_cluster<32>(x, hi, lo, inv_scale, k, n, s));
+    return MTNN_OK;
+  }
   KernelTimer timer(MTNN_KCLASS_SPLIT, 12.0 * (double)k * (double)n, s);
-  MTNN_CUDA_TRY(cudaMemsetAsync(colmax_scratch, 0, (size_t)n * sizeof(unsigned), s));
-  const int64_t n4 = n / 4;
-  const int64_t gx = (n4 + 255) / 256;
-  // enough row blocks to fill the chip; each thread scans rows_per_block rows
-  int64_t gy = std::max<int64_t>(1, ((int64_t)di->sm_count * 8) / std::max<int64_t>(gx, 1));
-  gy = std::min<int64_t>(gy, std::max<int64_t>(1, k / 16));
-  const int64_t rpb = (k + gy - 1) / gy;
-  gy = (k + rpb - 1) / rpb;
-  colmax_kernel<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, s>>>(x, colmax_scratch, k, n, rpb);
+  float* partial = partial_scratch;
+  // 32 16-byte lanes (512 B of a row per warp) x 8 row lanes: ncu at k = n =
+  // 4096 (pass 1 / pass 2 us): 15.2 / 30.1, vs 15.3 / 33.8 at 64 lanes and
+  // 17.7 / 35.5 at 256 (whole 4 KiB row segments per CTA)
+  constexpr int kLanes = 32;
+  const int64_t band_cols = 4 * kLanes;
+  const int64_t bands = (n + band_cols - 1) / band_cols;
+  // pass 1: about 4 CTAs per SM, bands of >= 64 rows
+  int64_t chunks = std::max<int64_t>(1, ((int64_t)di->sm_count * 4) / bands);
+  chunks = std::min<int64_t>({chunks, (int64_t)kMaxChunks, std::max<int64_t>(1, k / 64)});
+  const int64_t rpc = (k + chunks - 1) / chunks;
+  chunks = (k + rpc - 1) / rpc;
+  // pass 2: about 8 CTAs per SM
+  int64_t split_bands = std::max<int64_t>(1, ((int64_t)di->sm_count * 8) / bands);
+  split_bands = std::min<int64_t>(split_bands, std::max<int64_t>(1, k / 32));
+  const int64_t rpb = (k + split_bands - 1) / split_bands;
+  split_bands = (k + rpb - 1) / rpb;
+  colmax_partial_kernel<kLanes><<<dim3((unsigned)bands, (unsigned)chunks), 256, 0, s>>>(
+      x, partial, k, n, rpc);
   MTNN_CUDA_TRY(cudaGetLastError());
-  const int64_t total = k * n4;
-  const int64_t blocks = std::max<int64_t>(
-      1, std::min<int64_t>((total + 255) / 256, (int64_t)di->sm_count * 8));
-  split_cols_f16_kernel<<<(unsigned)blocks, 256, 0, s>>>(
-      x, colmax_scratch, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale, k, n);
+  split_cols_band_kernel<kLanes><<<dim3((unsigned)bands, (unsigned)split_bands), 256, 0, s>>>(
+      x, partial, (int)chunks, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale, k,
+      n, rpb);
   MTNN_CUDA_TRY(cudaGetLastError());
   return MTNN_OK;
 }

@@ -604,3 +604,24 @@ def test_row_split_every_branch(rng, k, n):
     g = got[ok]
     err = np.linalg.norm(g - want, axis=1) / np.linalg.norm(want, axis=1)
     assert err.max() < FP32_GATE, (k, n, float(err.max()))
+
+
+@pytest.mark.parametrize("k", [8, 104, 128, 1024, 1032, 2048, 2056, 4096, 4104, 8192, 8200, 16384])
+@pytest.mark.parametrize("n", [208, 384, 1072])
+def test_col_split_every_branch(rng, k, n):
+    """NN (MN-major B^T) column split on every branch picked by k — cluster
+    strips (k <= 8192, 1..8 CTAs per strip) and the two-pass / single-CTA strip
+    fallbacks past it — with ragged strips (n % 32 != 0), columns whose
+    magnitudes span 2^-40..2^40, and a NaN in the last row of one column
+    poisoning exactly that output column."""
+    m = 384
+    a = random_matrix(rng, m, k) * np.exp2(rng.integers(-40, 41, m)).astype(np.float32)[:, None]
+    bt = random_matrix(rng, k, n) * np.exp2(rng.integers(-40, 41, n)).astype(np.float32)[None, :]
+    bt[k - 1, 7] = np.nan
+    got = gemm_nn(a, bt, variant="tc3xf16s")
+    assert np.all(np.isnan(got[:, 7]))
+    ok = np.arange(n) != 7
+    want = np.asarray(a, np.float64) @ np.asarray(bt[:, ok], np.float64)
+    g = got[:, ok]
+    err = np.linalg.norm(g - want, axis=0) / np.linalg.norm(want, axis=0)
+    assert err.max() < FP32_GATE, (k, n, float(err.max()))
