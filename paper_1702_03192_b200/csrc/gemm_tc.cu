@@ -37,6 +37,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <utility>
 #include <atomic>
 #include <cmath>
 #include <mutex>
@@ -215,6 +216,16 @@ __device__ __forceinline__ void tc_fence_before() {
 }
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// Programmatic dependent launch: the GEMMs are launched with programmatic stream
+// serialization, so their prologue (barrier init, TMEM allocation, descriptor
+// prefetch) overlaps the tail of the operand split that precedes them on the
+// stream; every thread then waits for that grid's completion (and its memory)
+// before anything reads an operand. Kernels that trigger early: the splits.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -430,6 +441,7 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
 
   const int kb_per = p.kblocks_per_split;
 
@@ -733,6 +745,7 @@ __global__ void split_tf32_kernel(const float4* __restrict__ a, float4* __restri
                                   float4* __restrict__ a_lo, int64_t na4,
                                   const float4* __restrict__ b, float4* __restrict__ b_hi,
                                   float4* __restrict__ b_lo, int64_t nb4) {
+  pdl_trigger();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t total = na4 + nb4;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
@@ -798,6 +811,33 @@ static int encode(CUtensorMap* map, const void* base, int rank, const uint64_t* 
   return MTNN_OK;
 }
 
+// Launches a GEMM kernel with programmatic stream serialization (see pdl_wait);
+// MTNN_PDL=0 launches it fully serialised.
+static bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MTNN_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <class Kern, class... Args>
+static int launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                      Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  MTNN_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+  return MTNN_OK;
+}
+
 template <int BN, bool B_MN, class Kind, int kConv = 0>
 static int launch_impl(const void* ahi, const void* alo, const void* bhi,
                        const void* blo, float* out, const Params& p, int grid,
@@ -857,7 +897,7 @@ static int launch_impl(const void* ahi, const void* alo, const void* bhi,
   {
     KernelTimer timer(Kind::kScaled ? MTNN_KCLASS_GEMM_TC_F16S : MTNN_KCLASS_GEMM_TC,
                       2.0 * (double)p.m * (double)p.n * (double)p.k, s);
-    kern<<<grid, kNumThreads, S::kTotal, s>>>(mah, mal, mbh, mbl, mc, p);
+    MTNN_TRY(launch_pdl(kern, dim3(grid), dim3(kNumThreads), S::kTotal, s, mah, mal, mbh, mbl, mc, p));
   }
   MTNN_CUDA_TRY(cudaGetLastError());
   return MTNN_OK;
@@ -1033,6 +1073,7 @@ gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
   const int kb_per = p.kblocks_per_split;
 
   if (warp == 0) {
@@ -1255,7 +1296,8 @@ static int launch_pair_impl(const void* ahi, const void* alo, const void* bhi, c
   {
     KernelTimer timer(Kind::kScaled ? MTNN_KCLASS_GEMM_TC_F16S : MTNN_KCLASS_GEMM_TC,
                       2.0 * (double)p.m * (double)p.n * (double)p.k, s);
-    kern<<<2 * clusters, kThreads, S::kTotal, s>>>(mah, mal, mbh, mbl, mc, p, peers);
+    MTNN_TRY(launch_pdl(kern, dim3(2 * clusters), dim3(kThreads), S::kTotal, s, mah, mal, mbh, mbl,
+                        mc, p, peers));
   }
   MTNN_CUDA_TRY(cudaGetLastError());
   return MTNN_OK;
@@ -1452,6 +1494,7 @@ static int choose_splits(int tiles, int kblocks, int64_t m, int64_t n, int sms) 
   constexpr double kKblockSeconds = 0.5e-6;  // ~6 MMAs x 128 clk at ~1.6 GHz
   constexpr double kUnitOverheadKb = 2.0;    // prologue + epilogue drain, in k-blocks
   constexpr double kHbm = 5.0e12;
+  constexpr double kReduceLaunchSeconds = 4.0e-6;
   if (tiles >= 4 * sms || kblocks < 8) return 1;
   const double mn = (double)m * (double)n;
   int best = 1;
@@ -1462,7 +1505,9 @@ static int choose_splits(int tiles, int kblocks, int64_t m, int64_t n, int sms) 
     if (real_s != s) continue;
     const double waves = std::ceil((double)tiles * s / sms);
     double t = waves * (per + kUnitOverheadKb) * kKblockSeconds;
-    if (s > 1) t += 4.0 * (2.0 * s + 1.0) * mn / kHbm;
+    // split-K: partial write + re-read + the reduce kernel's launch and ramp
+    // (~4 us measured on tiny outputs, where it used to be worth the split)
+    if (s > 1) t += 4.0 * (2.0 * s + 1.0) * mn / kHbm + kReduceLaunchSeconds;
     if (t < best_t * 0.98) {  // prefer fewer splits unless clearly better
       best_t = t;
       best = s;

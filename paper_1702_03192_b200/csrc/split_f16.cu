@@ -38,6 +38,13 @@ __device__ __forceinline__ float pow2_scale(float mx) {
   return ldexpf(1.f, min(14 - c, 126));
 }
 
+// Lets the GEMM launched next on the stream (programmatic stream serialization)
+// start its prologue while this grid finishes; it waits for our completion
+// before reading any output (gemm_tc.cu pdl_wait).
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void split2(float v, float s, __half& h, __half& l) {
   const float xs = v * s;
   h = __float2half_rn(xs);
@@ -88,6 +95,7 @@ __device__ __forceinline__ const RowJob& pick(const RowJob& j0, const RowJob& j1
 // row from L1/L2 (a row is at most 8 KiB here).
 __global__ void __launch_bounds__(256)
 split_rows_f16_kernel(const RowJob j0, const RowJob j1, int64_t k) {
+  pdl_trigger();
   const int lane = threadIdx.x % 32;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / 32;
@@ -143,6 +151,7 @@ split_rows_f16_kernel(const RowJob j0, const RowJob j1, int64_t k) {
 template <int kR>
 __global__ void __launch_bounds__(256)
 split_rows_f16_reg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
+  pdl_trigger();
   const int lane = threadIdx.x % 32;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / 32;
@@ -191,6 +200,7 @@ constexpr int kRowThreads = 512;
 
 __global__ void __launch_bounds__(kRowThreads)
 split_rows_f16_smem_kernel(const RowJob j0, const RowJob j1, int64_t k) {
+  pdl_trigger();
   extern __shared__ float4 row_s[];
   __shared__ float red[kRowThreads / 32];
   const int64_t k4 = k / 4;
@@ -255,6 +265,7 @@ constexpr int kCtaRowThreads = 256;
 template <int kV>
 __global__ void __launch_bounds__(kCtaRowThreads)
 split_rows_f16_ctareg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
+  pdl_trigger();
   __shared__ float red[2][kCtaRowThreads / 32];
   const int64_t k4 = k / 4;
   const int t = threadIdx.x;
@@ -366,6 +377,7 @@ split_cols_band_kernel(const float* __restrict__ x, const float* __restrict__ pa
                        __half* __restrict__ hi, __half* __restrict__ lo,
                        float* __restrict__ inv_scale, int64_t k, int64_t n,
                        int64_t rows_per_band) {
+  pdl_trigger();
   constexpr int kBandCols = 4 * kLanes, kBandRowLanes = 256 / kLanes;
   const int c4 = threadIdx.x % kLanes;
   const int rl = threadIdx.x / kLanes;
@@ -413,6 +425,7 @@ __global__ void __launch_bounds__(8 * kStripLanes)
 split_cols_strip_kernel(const float* __restrict__ x, __half* __restrict__ hi,
                         __half* __restrict__ lo, float* __restrict__ inv_scale, int64_t k,
                         int64_t n) {
+  pdl_trigger();
   __shared__ float4 red[kStripLanes][8];
   __shared__ float4 scale[8];
   const int c4 = threadIdx.x % 8;
@@ -510,6 +523,7 @@ __global__ void __launch_bounds__(8 * kClusterRowLanes)
 split_cols_cluster_kernel(const float* __restrict__ x, __half* __restrict__ hi,
                           __half* __restrict__ lo, float* __restrict__ inv_scale, int64_t k,
                           int64_t n) {
+  pdl_trigger();
   __shared__ float4 red[kClusterRowLanes][8];
   __shared__ float4 part[8];
   __shared__ float4 scale[8];
