@@ -67,6 +67,11 @@ struct KernelTimer {
 // Kernel launchers (implemented in the .cu files). All asynchronous on `s`.
 int launch_transpose(const float* in, float* out, int64_t rows, int64_t cols,
                      cudaStream_t s);
+// SIMT NT for outputs with a side <= 16 (k % 4 == 0, 16-byte aligned operands).
+// ENOTSUP otherwise.
+bool skinny_eligible(const float* A, const float* B, int64_t m, int64_t n, int64_t k);
+int launch_gemm_skinny(const float* A, const float* B, float* C, int64_t m, int64_t n, int64_t k,
+                       cudaStream_t s);
 int launch_gemm_ffma(const float* A, const float* B, float* C, int64_t m, int64_t n,
                      int64_t k, bool b_is_nk, cudaStream_t s);
 // Tensor-core FP32-accurate GEMMs (three MMAs per product on hi/lo operand halves).

@@ -137,6 +137,15 @@ static int auto_variant(const float* A, const float* B, const float* C, int64_t 
   return MTNN_VARIANT_FFMA;
 }
 
+// MTNN_SKINNY=0 keeps outputs with a side <= 16 on the tile kernels (A/B runs).
+static bool skinny_auto() {
+  static const bool on = [] {
+    const char* e = getenv("MTNN_SKINNY");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static int gemm_dispatch(const float* A, const float* B, float* C, int64_t m, int64_t n,
                          int64_t k, int variant, bool b_is_nk, cudaStream_t s) {
   MTNN_TRY(check_dims(m, n, k));
@@ -148,6 +157,8 @@ static int gemm_dispatch(const float* A, const float* B, float* C, int64_t m, in
     MTNN_CUDA_TRY(cudaMemsetAsync(C, 0, (size_t)m * n * sizeof(float), s));
     return MTNN_OK;
   }
+  if (variant == MTNN_VARIANT_AUTO && b_is_nk && skinny_auto() && skinny_eligible(A, B, m, n, k))
+    return launch_gemm_skinny(A, B, C, m, n, k, s);  // output side <= 16: GEMV-class SIMT
   if (variant == MTNN_VARIANT_AUTO) variant = auto_variant(A, B, C, m, n, k, b_is_nk);
   if (variant == MTNN_VARIANT_TC3XF16S)
     return launch_gemm_tc(A, B, C, m, n, k, b_is_nk, TcKind::F16S, s);
@@ -426,6 +437,15 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
   return MTNN_OK;
 }
 
+static int64_t blocked_pipeline_max_k() {
+  static const int64_t v = [] {
+    const char* e = getenv("MTNN_PIPE_BLOCKED_MAXK");
+    const long long x = e ? atoll(e) : 0;
+    return (int64_t)(x > 0 ? x : 4096);
+  }();
+  return v;
+}
+
 static int host_gemm(const float* A, const float* B, float* C, int64_t m, int64_t n,
                      int64_t k, HostPath path, int variant) {
   MTNN_TRY(check_dims(m, n, k));
@@ -435,7 +455,7 @@ static int host_gemm(const float* A, const float* B, float* C, int64_t m, int64_
   // interleaved per case) it gains 3-14% there and loses 2-7% at k = 16384,
   // where the row chunks' H2D already dominates
   if (path == HostPath::NT && bytes >= pipe_min_bytes() && n >= 1024 && m > 0 && k > 0 &&
-      k <= 4096 && blocked_pipeline_enabled()) {
+      k <= blocked_pipeline_max_k() && blocked_pipeline_enabled()) {
     // eligibility of the tensor-core F16S path is a property of shapes/alignment
     // only; 16-byte aligned stand-ins decide it before any device allocation
     const float* al = reinterpret_cast<const float*>(uintptr_t(256));

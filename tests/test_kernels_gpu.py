@@ -625,3 +625,31 @@ def test_col_split_every_branch(rng, k, n):
     g = got[:, ok]
     err = np.linalg.norm(g - want, axis=0) / np.linalg.norm(want, axis=0)
     assert err.max() < FP32_GATE, (k, n, float(err.max()))
+
+
+@pytest.mark.parametrize("shape", [(1024, 10, 4096), (10, 4096, 1024), (1, 1, 4), (13, 13, 4096),
+                                   (7, 300, 1000), (3000, 16, 3200), (16, 5000, 12800),
+                                   (20000, 3, 64), (2, 70000, 8)])
+def test_skinny_outputs(rng, shape):
+    """Outputs with a side <= 16 (the FCN's 10-class layer, GEMV-like products):
+    the shared-memory SIMT kernel (or, past its 200 KiB short operand, the tile
+    kernels) through the device and host entry points, against the oracle; NaN
+    in a long-operand row poisons exactly that output line."""
+    import torch
+
+    m, n, k = shape
+    a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+    want = oracle.oracle_nt_blas(a, b)
+    assert rel_frobenius(gemm_nt(a, b), want) < FP32_GATE
+    dev = gemm_nt(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy()
+    assert rel_frobenius(dev, want) < FP32_GATE
+    if m >= n:
+        a[m // 2, k - 1] = np.nan
+        got = gemm_nt(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy()
+        assert np.all(np.isnan(got[m // 2]))
+        assert np.isfinite(np.delete(got, m // 2, axis=0)).all()
+    else:
+        b[n // 2, k - 1] = np.nan
+        got = gemm_nt(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy()
+        assert np.all(np.isnan(got[:, n // 2]))
+        assert np.isfinite(np.delete(got, n // 2, axis=1)).all()

@@ -4,7 +4,9 @@ sys.path.insert(0, ".")
 from paper_1702_03192_b200 import _lib
 L = _lib.lib
 E = [2 ** e for e in range(7, 15)]
-shapes = [(m, n, k) for m in E for n in E for k in E if n >= 1024 and 4 * (m * k + n * k + m * n) >= 8 << 20]
+import os
+KS = [int(x) for x in os.environ.get("KS", "").split(",") if x] or E
+shapes = [(m, n, k) for m in E for n in E for k in KS if n >= 1024 and 4 * (m * k + n * k + m * n) >= 8 << 20]
 ha = torch.empty(16384 * 16384, dtype=torch.float32).pin_memory().uniform_(-1, 1)
 hb = torch.empty(16384 * 16384, dtype=torch.float32).pin_memory().uniform_(-1, 1)
 hc = torch.empty(16384 * 16384, dtype=torch.float32).pin_memory()
