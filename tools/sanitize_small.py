@@ -18,4 +18,16 @@ for (m, n, k) in [(128, 2048, 256), (2048, 128, 256), (300, 1100, 520), (256, 38
         got = gemm_nn(a, np.ascontiguousarray(b.T))
         assert oracle.rel_frobenius(got, want) < 1e-5
     assert np.array_equal(transpose_oop(b), b.T)
+# session-3 kernels: row split by k branch (reg / looped / CTA-register / smem),
+# column split (strip / cluster / band), skinny NT
+for (m, n, k) in [(384, 384, 256), (384, 384, 1024), (384, 384, 4104), (384, 384, 16392), (384, 384, 20000)]:
+    a = rng.uniform(-1, 1, (m, k)).astype(np.float32); b = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    assert oracle.rel_frobenius(gemm_nt(a, b, variant="tc3xf16s"), oracle.oracle_nt_blas(a, b)) < 1e-5
+for (m, n, k) in [(384, 4096, 512), (384, 208, 1032), (384, 1072, 4104), (256, 384, 8200)]:
+    a = rng.uniform(-1, 1, (m, k)).astype(np.float32); bt = rng.uniform(-1, 1, (k, n)).astype(np.float32)
+    want = a.astype(np.float64) @ bt.astype(np.float64)
+    assert oracle.rel_frobenius(gemm_nn(a, bt, variant="tc3xf16s"), want) < 1e-5
+for (m, n, k) in [(1024, 10, 4096), (10, 4096, 1024), (300, 3, 64), (5, 7, 4)]:
+    a = rng.uniform(-1, 1, (m, k)).astype(np.float32); b = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    assert oracle.rel_frobenius(gemm_nt(a, b), oracle.oracle_nt_blas(a, b)) < 1e-5
 print("sanitize run ok")
