@@ -102,7 +102,7 @@ int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* w
  *   MTNN_F16S_INKERNEL=0 disables). The halves equal the split pass's; only
  *   the output tiling (and so the split-K order) may differ.
  * "tc_pair": 1 (default; env MTNN_TC_PAIR=0 turns it off): NT problems with
- *   >= 74 256x256 output tiles and k <= 4096 run on CTA pairs (tcgen05 cta_group::2, M = 256,
+ *   >= 74 256x256 output tiles run on CTA pairs (tcgen05 cta_group::2, M = 256,
  *   each CTA loading half of B); 2 forces it whenever structurally possible
  *   (tests), 0 keeps the single-CTA 128x256 tiles. Bit-identical results at the
  *   same split-K.

@@ -1523,6 +1523,17 @@ constexpr int kPairMnCols = 16;
 // CTA-pair kernel switch: mtnn_config_set("tc_pair", 0/1), env MTNN_TC_PAIR=0.
 static std::atomic<int> g_tc_pair{-1};
 // 0 = off, 1 = on for large problems (default), 2 = whenever structurally possible (tests)
+// Longest k that takes CTA pairs under tc_pair mode 1 (MTNN_PAIR_MAXK; default
+// no limit).
+static int64_t pair_max_k() {
+  static const int64_t v = [] {
+    const char* e = getenv("MTNN_PAIR_MAXK");
+    const long long x = e ? atoll(e) : 0;
+    return (int64_t)(x > 0 ? x : INT64_MAX);
+  }();
+  return v;
+}
+
 int tc_pair_mode() {
   int v = g_tc_pair.load(std::memory_order_relaxed);
   if (v < 0) {
@@ -1551,7 +1562,11 @@ static int tc_run_pair(const TcOperand& a, const TcOperand& b, float* C, int64_t
   p.inv_scale_b = b.inv_scale;
   p.tiles_m = (int)((m + tc::BM - 1) / tc::BM);
   p.tiles_mp = (p.tiles_m + 1) / 2;
-  p.group_m = tc::kGroupM;  // 16 pairs = 32 m-tiles per raster group: least DRAM traffic of 2..37
+  static const int group_env = [] {
+    const char* e = getenv("MTNN_PAIR_GROUP");  // m-tile pairs per raster group (testing)
+    return e ? atoi(e) : 0;
+  }();
+  p.group_m = group_env > 0 ? group_env : tc::kGroupM;  // 16 pairs = 32 m-tiles per raster group: least DRAM traffic of 2..37
   p.tiles_n = (int)((n + tc::kPairBN - 1) / tc::kPairBN);
   p.total_kblocks = (int)((k + bk - 1) / bk);
   const int pairs = di->sm_count / 2;
@@ -1654,15 +1669,18 @@ int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t 
     return fail(MTNN_EINVAL, "in-kernel operand split needs one prepared operand");
   if (conv && kind == TcKind::F16S && (conv == 1 ? a.inv_scale : b.inv_scale) == nullptr)
     return fail(MTNN_EINVAL, "in-kernel F16S split needs the operand's row scales");
-  // CTA pairs for NT problems with enough 256 x 256 tiles to fill the chip's 74
-  // TPCs at least once (split-K would otherwise be needed for occupancy) and
-  // k <= 4096. Back-to-back at the power cap (tools/probe_pair_sustained.py)
-  // pairs win 20% at k = 1024, 11% at 2048, tie at 4096 and lose 5% at 8192:
-  // their DRAM traffic is ~1.6x the single-CTA kernel's (ncu), which at long k
-  // costs more energy than the third of L2->SM traffic they save.
+  // CTA pairs for problems with enough 256 x 256 tiles to fill the chip's 74
+  // TPCs at least once (split-K would otherwise be needed for occupancy).
+  // Back-to-back at the power cap (tools/probe_pair_sustained.py, interleaved
+  // blocks) pairs win 20% at k = 1024, 11% at 2048 and, with the current
+  // kernels, 2-6% at k = 8192-16384 (65536x8192x8192: 23.7 vs 25.1 ms, 16384^3:
+  // 22.7 vs 24.1 ms) although their DRAM traffic is ~1.6x the single-CTA
+  // kernel's: the third of L2->SM and smem operand traffic they save is the
+  // larger energy term. (An earlier build measured a 5% loss at 8192, hence
+  // the MTNN_PAIR_MAXK knob.)
   const int pair = tc_pair_mode();
   if (conv == 0 && n > 128 && m > 128 && (b_is_nk || n % kPairMnCols == 0) &&
-      (pair == 2 || (pair == 1 && k <= 4096 && ((m + 255) / 256) * ((n + 255) / 256) >= 74)))
+      (pair == 2 || (pair == 1 && k <= pair_max_k() && ((m + 255) / 256) * ((n + 255) / 256) >= 74)))
     return tc_run_pair(a, b, C, m, n, k, ldc < n ? n : ldc, b_is_nk, kind, s);
   // F16S in-kernel split: 128-wide N tile (raw slot + 4-stage ring fit the smem)
   if (n <= 128 || (conv && kind == TcKind::F16S))

@@ -21,7 +21,7 @@ th = threading.Thread(target=sampler); th.start()
 res = {0: [], 1: []}
 for blk in range(8):
     mode = blk % 2
-    _lib.config_set("tc_pair", mode)
+    _lib.config_set("tc_pair", 2 * mode)  # 0 = single-CTA tiles, 2 = pairs forced
     _lib.check(L.mtnn_gemm_nt(A.data_ptr(), B.data_ptr(), C.data_ptr(), m, n, k, 0, s)); torch.cuda.synchronize()
     t0 = time.time()
     ev = []

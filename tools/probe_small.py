@@ -6,10 +6,14 @@ from paper_1702_03192_b200 import _lib
 L = _lib.lib
 dev = torch.device("cuda:0"); s = torch.cuda.current_stream().cuda_stream
 flush = torch.ones(64 * 2**20, device=dev)
-A = torch.rand(4096 * 4096, device=dev); B = torch.rand(4096 * 4096, device=dev); C = torch.empty(4096 * 4096, device=dev)
+import os
+N2 = 16384 * 16384 if os.environ.get('LONGSKINNY') else 4096 * 4096
+A = torch.rand(N2, device=dev); B = torch.rand(N2, device=dev); C = torch.empty(N2, device=dev)
 import os
 shapes = [(128, 128, 128), (256, 128, 128), (128, 1024, 256), (512, 512, 512), (1024, 1024, 256), (256, 2048, 512),
           (1024, 1024, 1024), (2048, 2048, 512), (512, 4096, 1024), (2048, 2048, 2048)]
+if os.environ.get("LONGSKINNY"):
+    shapes = [(128, 16384, 16384), (16384, 128, 16384), (256, 16384, 16384), (128, 16384, 4096), (256, 8192, 8192), (512, 16384, 16384), (128, 4096, 16384)]
 if os.environ.get("SKINNY"):
     shapes = [(m, n, k) for m in (128, 256, 512) for n in (128, 256, 512, 2048) for k in (128, 512, 2048)]
 names = {0: "auto", 1: "tf32", 2: "ffma", 3: "f16s"}
