@@ -1534,6 +1534,19 @@ static int64_t pair_max_k() {
   return v;
 }
 
+// Fewest 256 x 256 tiles that take CTA pairs under mode 1 (MTNN_PAIR_MIN_TILES).
+// Per-case A/B (cases with 16-73 tiles) showed 8192 x 512 x k gaining 7-10% on
+// pairs, but interleaved whole-sweep runs put 74 ahead of 32 by ~1%
+// (379.7-380.5 vs 373.9-378.2 TFLOP/s), so the default stays at 74.
+static int64_t pair_min_tiles() {
+  static const int64_t v = [] {
+    const char* e = getenv("MTNN_PAIR_MIN_TILES");
+    const long long x = e ? atoll(e) : 0;
+    return (int64_t)(x > 0 ? x : 74);
+  }();
+  return v;
+}
+
 int tc_pair_mode() {
   int v = g_tc_pair.load(std::memory_order_relaxed);
   if (v < 0) {
@@ -1680,7 +1693,7 @@ int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t 
   // the MTNN_PAIR_MAXK knob.)
   const int pair = tc_pair_mode();
   if (conv == 0 && n > 128 && m > 128 && (b_is_nk || n % kPairMnCols == 0) &&
-      (pair == 2 || (pair == 1 && k <= pair_max_k() && ((m + 255) / 256) * ((n + 255) / 256) >= 74)))
+      (pair == 2 || (pair == 1 && k <= pair_max_k() && ((m + 255) / 256) * ((n + 255) / 256) >= pair_min_tiles())))
     return tc_run_pair(a, b, C, m, n, k, ldc < n ? n : ldc, b_is_nk, kind, s);
   // F16S in-kernel split: 128-wide N tile (raw slot + 4-stage ring fit the smem)
   if (n <= 128 || (conv && kind == TcKind::F16S))
