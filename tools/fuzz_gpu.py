@@ -10,8 +10,11 @@ rng = np.random.default_rng(seed)
 picks = [1, 2, 3, 4, 7, 8, 9, 16, 31, 32, 33, 64, 96, 127, 128, 129, 192, 255, 256, 257, 384, 500, 512,
          513, 768, 1000, 1023, 1024, 1025, 1536, 2047, 2048, 2049, 3000, 4100]
 bad = 0
+longk = [4104, 6000, 8192, 8200, 12000, 16384, 16392, 20000]
 for it in range(N):
     m, n, k = (int(rng.choice(picks)) if rng.random() < 0.7 else int(rng.integers(1, 4200)) for _ in range(3))
+    if it % 4 == 3:  # long-k branches of the row / column splits (register, cluster, band, smem)
+        m, n, k = int(rng.choice(picks[:24])), int(rng.choice(picks[:24])), int(rng.choice(longk))
     knobs = {"tc_pair": int(rng.integers(0, 3)), "f16s_inkernel_max_short": int(rng.choice([0, 256, 1 << 20])),
              "host_pipeline_blocked": int(rng.integers(0, 2))}
     for kk, vv in knobs.items():
