@@ -653,3 +653,22 @@ def test_skinny_outputs(rng, shape):
         got = gemm_nt(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy()
         assert np.all(np.isnan(got[:, n // 2]))
         assert np.isfinite(np.delete(got, n // 2, axis=1)).all()
+
+
+@pytest.mark.parametrize("shape", [(1024, 4096, 10), (1, 1, 1), (7, 13, 3), (513, 1001, 16),
+                                   (4096, 10, 12), (3, 70000, 5)])
+def test_short_k(rng, shape):
+    """k <= 16 (the FCN's backward NN through the 10-class layer) through NT,
+    NN, TNN, host and device entry points."""
+    import torch
+
+    m, n, k = shape
+    a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+    want = oracle.oracle_nt_blas(a, b)
+    assert rel_frobenius(gemm_nt(a, b), want) < FP32_GATE
+    assert rel_frobenius(gemm_nt(a, b, variant="ffma"), want) < FP32_GATE
+    bt = np.ascontiguousarray(b.T)
+    assert rel_frobenius(gemm_nn(a, bt), want) < FP32_GATE
+    assert rel_frobenius(gemm_tnn(a, b), want) < FP32_GATE
+    dev = kernels.gemm_nn(torch.from_numpy(a).cuda(), torch.from_numpy(bt).cuda()).cpu().numpy()
+    assert rel_frobenius(dev, want) < FP32_GATE
