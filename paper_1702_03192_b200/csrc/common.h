@@ -50,7 +50,8 @@ int device_info(const DeviceInfo** out);
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
 // the attribute belongs to the device's context, so a process driving several
-// GPUs must set it on each.
+// GPUs must set it on each. Pass the kernel's largest launch size (later calls
+// for the same kernel are no-ops).
 int set_max_dynamic_smem(const void* kernel, int bytes);
 
 // Kernel timing instrumentation (mtnn_profile_*): a scope records a CUDA event
