@@ -310,12 +310,15 @@ split_rows_f16_ctareg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
 template <int kV>
 int launch_ctareg(const RowJob& j0, const RowJob& j1, int64_t rows, int64_t k, int sm_count,
                   cudaStream_t s) {
-  static int per_sm = 0;
-  if (per_sm == 0) {
-    MTNN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, split_rows_f16_ctareg_kernel<kV>, kCtaRowThreads, 0));
-    per_sm = std::max(per_sm, 1);
-  }
+  static const int per_sm = [] {  // same on every device of a node (B200 only)
+    int v = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, split_rows_f16_ctareg_kernel<kV>,
+                                                      kCtaRowThreads, 0) != cudaSuccess) {
+      (void)cudaGetLastError();
+      v = 1;
+    }
+    return std::max(v, 1);
+  }();
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)sm_count * per_sm));
   split_rows_f16_ctareg_kernel<kV><<<(unsigned)blocks, kCtaRowThreads, 0, s>>>(j0, j1, k);
   return MTNN_OK;
