@@ -518,6 +518,7 @@ def main():
         "traffic": ncu_traffic.get("traffic"),
         "traffic_launch": ncu_traffic.get("launch"),
         "traffic_algorithmic_bytes": ncu_traffic.get("algorithmic_bytes"),
+        "traffic_wave_floor_bytes": ncu_traffic.get("wave_floor_bytes"),
         "peak_basis": (f"FP32-accurate roof = measured bf16 dense {bf16} TFLOP/s (MEASURED_PEAKS.json, "
                        f"burst) / 3 MMAs per product (fp16 = bf16 rate)" if f16s else
                        f"3xTF32 FP32-accurate roof = measured bf16 dense {bf16} TFLOP/s "
