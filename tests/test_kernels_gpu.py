@@ -672,3 +672,45 @@ def test_short_k(rng, shape):
     assert rel_frobenius(gemm_tnn(a, b), want) < FP32_GATE
     dev = kernels.gemm_nn(torch.from_numpy(a).cuda(), torch.from_numpy(bt).cuda()).cpu().numpy()
     assert rel_frobenius(dev, want) < FP32_GATE
+
+
+@pytest.mark.parametrize("switch", ["MTNN_PDL=0", "MTNN_SPLIT_CTAREG=0", "MTNN_SPLIT_STRIP=0",
+                                    "MTNN_SKINNY=0", "MTNN_PAIR_MAXK=4096"])
+def test_env_switches_keep_results(tmp_path, switch):
+    """Every A/B environment switch (read once per process) keeps results within
+    the FP32 gate on the shapes it affects, and the switches that change only
+    scheduling or the split kernel (not the arithmetic) keep them bit-identical
+    to the default process."""
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    code = (
+        "import sys, numpy as np, oracle\n"
+        "from paper_1702_03192_b200 import gemm_nt, gemm_nn\n"
+        "rng = np.random.default_rng(11)\n"
+        "outs = []\n"
+        "for m, n, k in ((1024, 10, 4096), (384, 384, 4104), (512, 1072, 3000), (2048, 2048, 8192)):\n"
+        "    k -= k % 8\n"
+        "    a = rng.uniform(-1, 1, (m, k)).astype(np.float32)\n"
+        "    b = rng.uniform(-1, 1, (n, k)).astype(np.float32)\n"
+        "    want = oracle.oracle_nt_blas(a, b)\n"
+        "    c1 = gemm_nt(a, b)\n"
+        "    c2 = gemm_nn(a, np.ascontiguousarray(b.T)) if n % 16 == 0 else c1\n"
+        "    assert oracle.rel_frobenius(c1, want) < 1e-5 and oracle.rel_frobenius(c2, want) < 1e-5\n"
+        "    outs += [c1, c2]\n"
+        "np.savez(sys.argv[1], *outs)\n"
+        "print('ok')\n")
+    base = dict(__import__("os").environ, PYTHONPATH=str(ROOT))
+    key, val = switch.split("=")
+    res = {}
+    for name, env in (("default", base), ("switch", dict(base, **{key: val}))):
+        path = tmp_path / f"{name}.npz"
+        out = subprocess.run([sys.executable, "-c", code, str(path)], capture_output=True,
+                             text=True, env=env, cwd=str(ROOT), timeout=300)
+        assert out.returncode == 0 and "ok" in out.stdout, out.stderr
+        res[name] = np.load(path)
+    if key in ("MTNN_PDL", "MTNN_SPLIT_CTAREG", "MTNN_SPLIT_STRIP"):
+        for f in res["default"].files:
+            assert np.array_equal(res["default"][f], res["switch"][f]), (switch, f)
