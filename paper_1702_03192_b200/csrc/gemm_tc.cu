@@ -442,6 +442,7 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();
+  pdl_trigger();  // the next call's split may be scheduled (it waits for us)
 
   const int kb_per = p.kblocks_per_split;
 
@@ -1074,6 +1075,7 @@ gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();
+  pdl_trigger();  // the next call's split may be scheduled (it waits for us)
   const int kb_per = p.kblocks_per_split;
 
   if (warp == 0) {

@@ -44,6 +44,36 @@ __device__ __forceinline__ float pow2_scale(float mx) {
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// The split kernels are themselves launched with programmatic serialization
+// (launch_chained), so they can be scheduled while the previous GEMM drains;
+// they wait for it before reading anything.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Launch with programmatic stream serialization (MTNN_PDL=0: plain launch).
+bool chain_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MTNN_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <class Kern, class... Args>
+int launch_chained(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = chain_enabled() ? 1 : 0;
+  MTNN_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args...));
+  return MTNN_OK;
+}
+
 
 __device__ __forceinline__ void split2(float v, float s, __half& h, __half& l) {
   const float xs = v * s;
@@ -96,6 +126,7 @@ __device__ __forceinline__ const RowJob& pick(const RowJob& j0, const RowJob& j1
 __global__ void __launch_bounds__(256)
 split_rows_f16_kernel(const RowJob j0, const RowJob j1, int64_t k) {
   pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x % 32;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / 32;
@@ -152,6 +183,7 @@ template <int kR>
 __global__ void __launch_bounds__(256)
 split_rows_f16_reg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
   pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x % 32;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / 32;
@@ -201,6 +233,7 @@ constexpr int kRowThreads = 512;
 __global__ void __launch_bounds__(kRowThreads)
 split_rows_f16_smem_kernel(const RowJob j0, const RowJob j1, int64_t k) {
   pdl_trigger();
+  pdl_wait();
   extern __shared__ float4 row_s[];
   __shared__ float red[kRowThreads / 32];
   const int64_t k4 = k / 4;
@@ -266,6 +299,7 @@ template <int kV>
 __global__ void __launch_bounds__(kCtaRowThreads)
 split_rows_f16_ctareg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
   pdl_trigger();
+  pdl_wait();
   __shared__ float red[2][kCtaRowThreads / 32];
   const int64_t k4 = k / 4;
   const int t = threadIdx.x;
@@ -320,7 +354,8 @@ int launch_ctareg(const RowJob& j0, const RowJob& j1, int64_t rows, int64_t k, i
     return std::max(v, 1);
   }();
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)sm_count * per_sm));
-  split_rows_f16_ctareg_kernel<kV><<<(unsigned)blocks, kCtaRowThreads, 0, s>>>(j0, j1, k);
+  MTNN_TRY(launch_chained(split_rows_f16_ctareg_kernel<kV>, dim3((unsigned)blocks), dim3(kCtaRowThreads),
+                           0, s, j0, j1, k));
   return MTNN_OK;
 }
 
@@ -345,6 +380,7 @@ template <int kLanes>
 __global__ void __launch_bounds__(256)
 colmax_partial_kernel(const float* __restrict__ x, float* __restrict__ partial, int64_t k,
                       int64_t n, int64_t rows_per_chunk) {
+  pdl_wait();
   constexpr int kBandCols = 4 * kLanes, kBandRowLanes = 256 / kLanes;
   __shared__ float4 red[kBandRowLanes][kLanes];
   const int c4 = threadIdx.x % kLanes;
@@ -381,6 +417,7 @@ split_cols_band_kernel(const float* __restrict__ x, const float* __restrict__ pa
                        float* __restrict__ inv_scale, int64_t k, int64_t n,
                        int64_t rows_per_band) {
   pdl_trigger();
+  pdl_wait();
   constexpr int kBandCols = 4 * kLanes, kBandRowLanes = 256 / kLanes;
   const int c4 = threadIdx.x % kLanes;
   const int rl = threadIdx.x / kLanes;
@@ -429,6 +466,7 @@ split_cols_strip_kernel(const float* __restrict__ x, __half* __restrict__ hi,
                         __half* __restrict__ lo, float* __restrict__ inv_scale, int64_t k,
                         int64_t n) {
   pdl_trigger();
+  pdl_wait();
   __shared__ float4 red[kStripLanes][8];
   __shared__ float4 scale[8];
   const int c4 = threadIdx.x % 8;
@@ -527,6 +565,7 @@ split_cols_cluster_kernel(const float* __restrict__ x, __half* __restrict__ hi,
                           __half* __restrict__ lo, float* __restrict__ inv_scale, int64_t k,
                           int64_t n) {
   pdl_trigger();
+  pdl_wait();
   __shared__ float4 red[kClusterRowLanes][8];
   __shared__ float4 part[8];
   __shared__ float4 scale[8];
@@ -609,13 +648,15 @@ int launch_cols_cluster(const float* x, void* hi, void* lo, float* inv_scale, in
   cfg.blockDim = dim3(8 * kClusterRowLanes);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = c;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = chain_enabled() ? 2 : 1;
   MTNN_CUDA_TRY(cudaLaunchKernelEx(&cfg, split_cols_cluster_kernel<kR>, x,
                                    static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale,
                                    k, n));
@@ -654,7 +695,8 @@ int launch_split_rows_f16_pair(const float* x0, void* hi0, void* lo0, float* inv
     MTNN_TRY(set_max_dynamic_smem((const void*)split_rows_f16_smem_kernel, 160 * 1024));
     const int per_sm = std::max<int>(1, std::min<int>(4, (int)((200 * 1024) / row_bytes)));
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t)di->sm_count * per_sm));
-    split_rows_f16_smem_kernel<<<(unsigned)blocks, kRowThreads, row_bytes, s>>>(j0, j1, k);
+    MTNN_TRY(launch_chained(split_rows_f16_smem_kernel, dim3((unsigned)blocks), dim3(kRowThreads),
+                            row_bytes, s, j0, j1, k));
   } else {
     int64_t blocks = (rows + 7) / 8;
     // rows of <= 512 and 1024 < k <= 2048: whole row in registers, every load
@@ -664,13 +706,13 @@ int launch_split_rows_f16_pair(const float* x0, void* hi0, void* lo0, float* inv
     const bool reg = k <= 512 || (k > 1024 && k <= 2048);  // (longer rows: past the smem limit)
     blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)di->sm_count * (reg && k <= 512 ? 8 : 16)));
     if (k <= 256)
-      split_rows_f16_reg_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(j0, j1, k);
+      MTNN_TRY(launch_chained(split_rows_f16_reg_kernel<2>, dim3((unsigned)blocks), dim3(256), 0, s, j0, j1, k));
     else if (k <= 512)
-      split_rows_f16_reg_kernel<4><<<(unsigned)blocks, 256, 0, s>>>(j0, j1, k);
+      MTNN_TRY(launch_chained(split_rows_f16_reg_kernel<4>, dim3((unsigned)blocks), dim3(256), 0, s, j0, j1, k));
     else if (reg)
-      split_rows_f16_reg_kernel<16><<<(unsigned)blocks, 256, 0, s>>>(j0, j1, k);
+      MTNN_TRY(launch_chained(split_rows_f16_reg_kernel<16>, dim3((unsigned)blocks), dim3(256), 0, s, j0, j1, k));
     else
-      split_rows_f16_kernel<<<(unsigned)blocks, 256, 0, s>>>(j0, j1, k);
+      MTNN_TRY(launch_chained(split_rows_f16_kernel, dim3((unsigned)blocks), dim3(256), 0, s, j0, j1, k));
   }
   MTNN_CUDA_TRY(cudaGetLastError());
   return MTNN_OK;
@@ -707,8 +749,9 @@ int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,
   if (strip_on && k <= 1024 && strips >= di->sm_count / 2) {
     // short columns, many strips: one CTA per strip re-reads its strip from L2
     KernelTimer timer(MTNN_KCLASS_SPLIT, 8.0 * (double)k * (double)n, s);
-    split_cols_strip_kernel<<<(unsigned)strips, 8 * kStripLanes, 0, s>>>(
-        x, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale, k, n);
+    MTNN_TRY(launch_chained(split_cols_strip_kernel, dim3((unsigned)strips), dim3(8 * kStripLanes), 0,
+                            s, x, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale, k,
+                            n));
     MTNN_CUDA_TRY(cudaGetLastError());
     return MTNN_OK;
   }
@@ -743,8 +786,8 @@ int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,
   split_bands = std::min<int64_t>(split_bands, std::max<int64_t>(1, k / 32));
   const int64_t rpb = (k + split_bands - 1) / split_bands;
   split_bands = (k + rpb - 1) / rpb;
-  colmax_partial_kernel<kLanes><<<dim3((unsigned)bands, (unsigned)chunks), 256, 0, s>>>(
-      x, partial, k, n, rpc);
+  MTNN_TRY(launch_chained(colmax_partial_kernel<kLanes>, dim3((unsigned)bands, (unsigned)chunks),
+                          dim3(256), 0, s, x, partial, k, n, rpc));
   MTNN_CUDA_TRY(cudaGetLastError());
   split_cols_band_kernel<kLanes><<<dim3((unsigned)bands, (unsigned)split_bands), 256, 0, s>>>(
       x, partial, (int)chunks, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale, k,
