@@ -20,6 +20,7 @@
 #include <algorithm>
 
 #include "common.h"
+#include "pdl.h"
 #include "workspace.h"
 
 namespace mtnn {
@@ -33,6 +34,7 @@ __global__ void __launch_bounds__(256)
 sgemm_kernel(const float* __restrict__ A, const float* __restrict__ B,
              float* __restrict__ C, int64_t m, int64_t n, int64_t k, int64_t k_chunk,
              int64_t split_stride) {
+  pdl_enter();
   __shared__ __align__(16) float As[2][BK][BM];
   __shared__ __align__(16) float Bs[2][BK][BN];
 
@@ -176,6 +178,7 @@ template <int SMAX>
 __global__ void __launch_bounds__(256, 2)
 gemm_skinny_kernel(const float* __restrict__ big, const float* __restrict__ small,
                    float* __restrict__ C, int64_t L, int s, int64_t k, bool small_is_b, int W) {
+  pdl_enter();
   constexpr int R = 32 / SMAX;  // long rows per warp: R x SMAX <= 32 partial sums
   __shared__ float red[8][32];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -232,6 +235,7 @@ gemm_skinny_kernel(const float* __restrict__ big, const float* __restrict__ smal
 // Deterministic split-K reduction: C[i] = sum_s part[s][i], s ascending.
 __global__ void splitk_reduce_kernel(const float* __restrict__ part, float* __restrict__ C,
                                      int64_t count, int splits) {
+  pdl_enter();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
     float s = part[i];
@@ -247,8 +251,8 @@ int launch_splitk_reduce(const float* part, float* C, int64_t count, int splits,
   int64_t blocks = (count + 255) / 256;
   blocks = std::min<int64_t>(blocks, (int64_t)di->sm_count * 8);
   KernelTimer timer(MTNN_KCLASS_REDUCE, 4.0 * (double)(splits + 1) * (double)count, s);
-  splitk_reduce_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(part, C, count,
-                                                                            splits);
+  MTNN_TRY(launch_chained(splitk_reduce_kernel, dim3((unsigned)std::max<int64_t>(blocks, 1)),
+                          dim3(256), 0, s, part, C, count, splits));
   MTNN_CUDA_TRY(cudaGetLastError());
   return MTNN_OK;
 }
@@ -281,9 +285,11 @@ int launch_gemm_ffma(const float* A, const float* B, float* C, int64_t m, int64_
   {
   KernelTimer timer(MTNN_KCLASS_GEMM_FFMA, 2.0 * (double)m * (double)n * (double)k, s);
   if (b_is_nk)
-    sgemm_kernel<true><<<grid, 256, 0, s>>>(A, B, out, m, n, k, k_chunk, m * n);
+    MTNN_TRY(launch_chained(sgemm_kernel<true>, grid, dim3(256), 0, s, A, B, out, m, n, k, k_chunk,
+                            m * n));
   else
-    sgemm_kernel<false><<<grid, 256, 0, s>>>(A, B, out, m, n, k, k_chunk, m * n);
+    MTNN_TRY(launch_chained(sgemm_kernel<false>, grid, dim3(256), 0, s, A, B, out, m, n, k, k_chunk,
+                            m * n));
   }
   MTNN_CUDA_TRY(cudaGetLastError());
   if (splits > 1) MTNN_TRY(launch_splitk_reduce(out, C, m * n, splits, s));
@@ -320,11 +326,11 @@ int launch_gemm_skinny(const float* A, const float* B, float* C, int64_t m, int6
   const float* sml = small_is_b ? B : A;
   const unsigned g = (unsigned)blocks;
   switch (smax) {
-    case 4: gemm_skinny_kernel<4><<<g, 256, 0, s>>>(big, sml, C, L, sm_rows, k, small_is_b, W); break;
-    case 8: gemm_skinny_kernel<8><<<g, 256, 0, s>>>(big, sml, C, L, sm_rows, k, small_is_b, W); break;
-    case 10: gemm_skinny_kernel<10><<<g, 256, 0, s>>>(big, sml, C, L, sm_rows, k, small_is_b, W); break;
-    case 12: gemm_skinny_kernel<12><<<g, 256, 0, s>>>(big, sml, C, L, sm_rows, k, small_is_b, W); break;
-    default: gemm_skinny_kernel<16><<<g, 256, 0, s>>>(big, sml, C, L, sm_rows, k, small_is_b, W); break;
+    case 4: MTNN_TRY(launch_chained(gemm_skinny_kernel<4>, dim3(g), dim3(256), 0, s, big, sml, C, L, sm_rows, k, small_is_b, W)); break;
+    case 8: MTNN_TRY(launch_chained(gemm_skinny_kernel<8>, dim3(g), dim3(256), 0, s, big, sml, C, L, sm_rows, k, small_is_b, W)); break;
+    case 10: MTNN_TRY(launch_chained(gemm_skinny_kernel<10>, dim3(g), dim3(256), 0, s, big, sml, C, L, sm_rows, k, small_is_b, W)); break;
+    case 12: MTNN_TRY(launch_chained(gemm_skinny_kernel<12>, dim3(g), dim3(256), 0, s, big, sml, C, L, sm_rows, k, small_is_b, W)); break;
+    default: MTNN_TRY(launch_chained(gemm_skinny_kernel<16>, dim3(g), dim3(256), 0, s, big, sml, C, L, sm_rows, k, small_is_b, W)); break;
   }
   MTNN_CUDA_TRY(cudaGetLastError());
   return MTNN_OK;

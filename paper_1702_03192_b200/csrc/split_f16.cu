@@ -22,6 +22,7 @@
 #include <algorithm>
 
 #include "common.h"
+#include "pdl.h"
 
 namespace mtnn {
 namespace {
@@ -49,30 +50,6 @@ __device__ __forceinline__ void pdl_trigger() {
 // they wait for it before reading anything.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-// Launch with programmatic stream serialization (MTNN_PDL=0: plain launch).
-bool chain_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("MTNN_PDL");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
-template <class Kern, class... Args>
-int launch_chained(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = chain_enabled() ? 1 : 0;
-  MTNN_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args...));
-  return MTNN_OK;
-}
 
 
 __device__ __forceinline__ void split2(float v, float s, __half& h, __half& l) {

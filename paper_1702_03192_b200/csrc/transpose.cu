@@ -23,6 +23,7 @@
 #include <stdint.h>
 
 #include "common.h"
+#include "pdl.h"
 
 namespace mtnn {
 namespace {
@@ -49,6 +50,7 @@ __device__ __forceinline__ void stg_stream(uint4* p, const uint4& v) {
 __global__ void __launch_bounds__(kThreads)
 transpose_vec4_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
                       int64_t rows, int64_t cols, int64_t tiles_c) {
+  pdl_enter();
   // smem[r][v]: output-tile row r (= input column), 16-byte column v^swz(r).
   __shared__ uint4 smem[kTile][kVecPerRow];
 
@@ -102,6 +104,7 @@ transpose_vec4_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ ou
 __global__ void __launch_bounds__(256)
 transpose_scalar_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
                         int64_t rows, int64_t cols, int64_t tiles_c) {
+  pdl_enter();
   __shared__ uint32_t smem[32][33];
   const int64_t tile = blockIdx.x;
   const int64_t tr = tile / tiles_c;
@@ -128,6 +131,7 @@ transpose_scalar_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ 
 __global__ void __launch_bounds__(256)
 transpose_scalar64_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
                           int64_t rows, int64_t cols, int64_t tiles_c) {
+  pdl_enter();
   __shared__ uint32_t smem[64][65];
   const int64_t tile = blockIdx.x;
   const int64_t tr = tile / tiles_c;
@@ -170,25 +174,25 @@ int launch_transpose(const float* in, float* out, int64_t rows, int64_t cols,
     const int64_t tiles_c = (cols + kTile - 1) / kTile;
     const int64_t tiles = tiles_r * tiles_c;
     if (tiles > 0x7fffffffLL) return fail(MTNN_EINVAL, "transpose: matrix too large");
-    transpose_vec4_kernel<<<(unsigned)tiles, kThreads, 0, s>>>(
-        reinterpret_cast<const uint32_t*>(in), reinterpret_cast<uint32_t*>(out), rows,
-        cols, tiles_c);
+    MTNN_TRY(launch_chained(transpose_vec4_kernel, dim3((unsigned)tiles), dim3(kThreads), 0, s,
+                            reinterpret_cast<const uint32_t*>(in), reinterpret_cast<uint32_t*>(out),
+                            rows, cols, tiles_c));
   } else if (rows >= 64 && cols >= 64) {
     const int64_t tiles_r = (rows + 63) / 64;
     const int64_t tiles_c = (cols + 63) / 64;
     const int64_t tiles = tiles_r * tiles_c;
     if (tiles > 0x7fffffffLL) return fail(MTNN_EINVAL, "transpose: matrix too large");
-    transpose_scalar64_kernel<<<(unsigned)tiles, 256, 0, s>>>(
-        reinterpret_cast<const uint32_t*>(in), reinterpret_cast<uint32_t*>(out), rows,
-        cols, tiles_c);
+    MTNN_TRY(launch_chained(transpose_scalar64_kernel, dim3((unsigned)tiles), dim3(256), 0, s,
+                            reinterpret_cast<const uint32_t*>(in), reinterpret_cast<uint32_t*>(out),
+                            rows, cols, tiles_c));
   } else {
     const int64_t tiles_r = (rows + 31) / 32;
     const int64_t tiles_c = (cols + 31) / 32;
     const int64_t tiles = tiles_r * tiles_c;
     if (tiles > 0x7fffffffLL) return fail(MTNN_EINVAL, "transpose: matrix too large");
-    transpose_scalar_kernel<<<(unsigned)tiles, 256, 0, s>>>(
-        reinterpret_cast<const uint32_t*>(in), reinterpret_cast<uint32_t*>(out), rows,
-        cols, tiles_c);
+    MTNN_TRY(launch_chained(transpose_scalar_kernel, dim3((unsigned)tiles), dim3(256), 0, s,
+                            reinterpret_cast<const uint32_t*>(in), reinterpret_cast<uint32_t*>(out),
+                            rows, cols, tiles_c));
   }
   MTNN_CUDA_TRY(cudaGetLastError());
   return MTNN_OK;
