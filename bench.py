@@ -102,6 +102,62 @@ class ClockSampler:
                 "samples": len(rows), "samples_under_load": len(loaded)}
 
 
+class NvmlClockSampler:
+    """NVML sampled every 2 ms during the timed region (short workloads — the FCN
+    step is ~1 ms — finish between nvidia-smi samples); ClockSampler otherwise."""
+
+    # NVML clocks-event-reason bits: sw power cap, hw slowdown, sw / hw thermal
+    BITS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+            ("sw_power_cap", 0x4))
+
+    def __init__(self, index: int):
+        import pynvml
+
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        self.rows = []
+        self.stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                mhz = float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                util = float(nv.nvmlDeviceGetUtilizationRates(self.h).gpu)
+                self.rows.append((mhz, bits, util))
+            except Exception:  # noqa: BLE001  (a failed sample is skipped)
+                pass
+            self.stop.wait(0.002)
+
+    def __enter__(self):
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        self.stop.set()
+        self.thread.join(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        loaded = [r for r in self.rows if r[2] > 0] or self.rows
+        reasons = sorted({name for r in loaded for name, bit in self.BITS if r[1] & bit})
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.rows), "samples_under_load": len(loaded),
+                "sampler": "nvml 2 ms"}
+
+
+def clock_sampler(index: int):
+    try:
+        return NvmlClockSampler(index)
+    except Exception:  # noqa: BLE001  (no NVML: nvidia-smi at 100 ms)
+        return ClockSampler(index)
+
+
 # ----------------------------------------------------------------- CPU legs
 def cpu_sample_run(shapes, threads, seed=0):
     """Reference CPU path (oracle port of the numba kernels) over `shapes`:
@@ -426,7 +482,7 @@ def main():
     L.mtnn_profile_enable_classes((1 << _lib.KCLASS_GEMM_TC) | (1 << _lib.KCLASS_GEMM_TC_F16S)
                                   | (1 << _lib.KCLASS_GEMM_FFMA))
     events = []
-    with ClockSampler(local_rank) as clocks:
+    with clock_sampler(local_rank) as clocks:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
