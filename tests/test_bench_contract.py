@@ -10,6 +10,8 @@ import socket
 import subprocess
 import sys
 
+import pytest
+
 from conftest import ROOT
 
 BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
@@ -59,3 +61,31 @@ def test_reference_arm_under_torchrun():
     lines = _json_lines(out.stdout)
     assert len(lines) == 1  # rank 0 alone prints
     _check_reference_line(lines[0], 2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("workload", ["sweep", "fcn"])
+def test_gpu_arm_line(workload):
+    """The GPU arm's JSON line on a reduced sweep (m,n,k <= 512) and the FCN
+    step: roofline, cpu_baseline (sweep), e2e with host copies, launches and
+    sampled clocks are all present and consistent."""
+    args = [sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--workload", workload]
+    if workload == "sweep":
+        args += ["--exp-max", "9"]
+    out = subprocess.run(args, capture_output=True, text=True, cwd=str(ROOT), timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = _json_lines(out.stdout)
+    assert len(lines) == 1
+    d = lines[0]
+    assert BASE_KEYS <= set(d), BASE_KEYS - set(d)
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["steps"] == 3 and d["warmup"] == 3
+    r = d["roofline"]
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r)
+    assert r["bound"] == "tensor" and 0 < r["frac"] == pytest.approx(r["achieved"] / r["peak"])
+    e2e = d["e2e"]
+    assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    if workload == "sweep":
+        cb = d["cpu_baseline"]
+        assert {"value", "unit", "cores", "kind", "sample"} <= set(cb) and cb["value"] > 0
