@@ -473,14 +473,18 @@ def main():
     torch.cuda.synchronize()
 
     # ---------------- timed region: K steps
-    # Only the GEMM launches carry timing events here (the roofline kernel): a
-    # timestamp event pair serialises the stream around its launch, which costs
-    # ~4% of a sweep step when every split/reduce launch is bracketed too. All
-    # launches are still counted. The per-class breakdown comes from one extra
-    # fully instrumented step after the timed region.
+    # Only the large GEMM launches carry timing events here (the roofline kernel,
+    # calls of >= 2^35 flop, or the largest call if none is that big): a
+    # timestamp event pair serialises the stream around its launch and breaks
+    # the programmatic launch chain, which costs ~4% of a sweep step when every
+    # launch is bracketed (3% with every GEMM bracketed). All launches are still
+    # counted. The per-class breakdown comes from one extra fully instrumented
+    # step after the timed region.
+    min_work = min(float(2 ** 35), max((2.0 * m * n * k for _, m, n, k, _ in calls), default=0.0))
     L.mtnn_profile_reset()
     L.mtnn_profile_enable_classes((1 << _lib.KCLASS_GEMM_TC) | (1 << _lib.KCLASS_GEMM_TC_F16S)
                                   | (1 << _lib.KCLASS_GEMM_FFMA))
+    L.mtnn_profile_min_work(ctypes.c_double(min_work))
     events = []
     with clock_sampler(local_rank) as clocks:
         if world > 1:
@@ -503,7 +507,9 @@ def main():
     step_s = device_s / args.steps
     value = total_flops / step_s / 1e12
     prof = {c: _lib.profile_read(c) for c in _lib.KCLASS_NAMES}
+    prof_t = {c: _lib.profile_read_timed(c) for c in _lib.KCLASS_NAMES}
     launches = int(sum(v[1] for v in prof.values()))
+    L.mtnn_profile_min_work(ctypes.c_double(0.0))
     # per-class breakdown: one extra step with every launch timed
     L.mtnn_profile_reset()
     L.mtnn_profile_enable(1)
@@ -558,8 +564,9 @@ def main():
     # burst figure bounds it; the sustained fraction is listed beside it
     bf16_sus = peaks.get("bf16_tflops_sustained", bf16)
     hbm = peaks.get("hbm_gbs", 6650.0)
-    tc_class = max((_lib.KCLASS_GEMM_TC_F16S, _lib.KCLASS_GEMM_TC), key=lambda c: prof[c][0])
-    tc_ms, tc_n, tc_work = prof[tc_class]
+    tc_class = max((_lib.KCLASS_GEMM_TC_F16S, _lib.KCLASS_GEMM_TC), key=lambda c: prof_t[c][0])
+    tc_ms, tc_n, tc_work = prof_t[tc_class]
+    tc_all_n, tc_all_work = prof[tc_class][1], prof[tc_class][2]
     f16s = tc_class == _lib.KCLASS_GEMM_TC_F16S
     roof = bf16 / 3.0 if f16s else bf16 / 6.0
     roof_sus = bf16_sus / 3.0 if f16s else bf16_sus / 6.0
@@ -581,6 +588,9 @@ def main():
                        f"(MEASURED_PEAKS.json, burst) / 2 (tf32 rate) / 3 (MMAs per product)"),
         "peak_sustained": roof_sus, "frac_of_sustained": achieved / roof_sus if achieved else None,
         "launches": tc_n, "avg_launch_ms": tc_ms / tc_n if tc_n else None,
+        "timed_launches_note": (f"event-timed launches of >= {min_work:.3g} flop: {tc_n} of {tc_all_n} "
+                                f"launches of the class, {tc_work / tc_all_work:.1%} of its flops"
+                                if tc_all_work else None),
         "share_of_step": tc_ms / 1e3 / (device_s * 1.0) if device_s else None,
         "dominant_kernel_by_time": _lib.KCLASS_NAMES[dominant],
     }

@@ -90,6 +90,11 @@ int mtnn_profile_enable(int on);
  * While profiling is on (either call), launches and work of EVERY class are
  * counted; mtnn_profile_read's total_ms covers the timed classes only. */
 int mtnn_profile_enable_classes(unsigned mask);
+/* Time only launches whose work (flops or bytes) is at least `work`; the rest
+ * are still counted. mtnn_profile_read_timed returns the timed subset: its
+ * milliseconds, launch count and work (so rate = work / ms is consistent). */
+int mtnn_profile_min_work(double work);
+int mtnn_profile_read_timed(int kclass, double* total_ms, int64_t* launches, double* work);
 int mtnn_profile_reset(void);
 int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* work);
 

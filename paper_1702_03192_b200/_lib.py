@@ -69,6 +69,8 @@ def _load():
         "mtnn_profile_enable_classes": (c_int, [ctypes.c_uint]),
         "mtnn_profile_reset": (c_int, []),
         "mtnn_profile_read": (c_int, [c_int, _DP, _I64P, _DP]),
+        "mtnn_profile_read_timed": (c_int, [c_int, _DP, _I64P, _DP]),
+        "mtnn_profile_min_work": (c_int, [ctypes.c_double]),
         "mtnn_config_set": (c_int, [c_char_p, c_int64]),
         "mtnn_config_get": (c_int, [c_char_p, _I64P]),
         "mtnn_gemm_nt_allgather": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(c_void_p), c_int,
@@ -135,6 +137,14 @@ def profile_read(kclass: int):
     """(total_ms, launches, work) accumulated for one kernel class."""
     ms, n, w = ctypes.c_double(), c_int64(), ctypes.c_double()
     check(lib.mtnn_profile_read(kclass, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(w)))
+    return ms.value, n.value, w.value
+
+
+def profile_read_timed(kclass: int):
+    """(total_ms, launches, work) of the timed launches of one kernel class (those
+    with work >= the mtnn_profile_min_work threshold)."""
+    ms, n, w = ctypes.c_double(), c_int64(), ctypes.c_double()
+    check(lib.mtnn_profile_read_timed(kclass, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(w)))
     return ms.value, n.value, w.value
 
 

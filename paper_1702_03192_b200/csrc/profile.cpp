@@ -21,12 +21,15 @@ struct Pending {
 
 std::atomic<unsigned> g_mask{0};  // bit c: time kernel class c
 std::atomic<bool> g_counting{false};  // count launches and work of every class
+std::atomic<double> g_min_work{0.0};  // time only launches with at least this much work
 std::mutex g_mu;
 std::vector<Pending> g_pending;
 std::vector<cudaEvent_t> g_free_events;
 double g_ms[MTNN_KCLASS_COUNT];
 int64_t g_launches[MTNN_KCLASS_COUNT];
 double g_work[MTNN_KCLASS_COUNT];
+int64_t g_timed_launches[MTNN_KCLASS_COUNT];  // the launches behind g_ms
+double g_timed_work[MTNN_KCLASS_COUNT];
 
 cudaEvent_t take_event() {
   {
@@ -55,6 +58,7 @@ KernelTimer::KernelTimer(int kc, double w, cudaStream_t s) : kclass(kc), work(w)
     g_work[kc] += w;
   }
   if (!((g_mask.load(std::memory_order_relaxed) >> kc) & 1u)) return;
+  if (w < g_min_work.load(std::memory_order_relaxed)) return;
   start = take_event();
   if (start && cudaEventRecord(start, stream) != cudaSuccess) {
     (void)cudaGetLastError();
@@ -91,6 +95,20 @@ int mtnn_profile_enable_classes(unsigned mask) {
   return MTNN_OK;
 }
 
+int mtnn_profile_min_work(double work) {
+  g_min_work.store(work > 0.0 ? work : 0.0);
+  return MTNN_OK;
+}
+
+int mtnn_profile_read_timed(int kclass, double* total_ms, int64_t* launches, double* work) {
+  MTNN_TRY(mtnn_profile_read(kclass, nullptr, nullptr, nullptr));  // resolves pending events
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (total_ms) *total_ms = g_ms[kclass];
+  if (launches) *launches = g_timed_launches[kclass];
+  if (work) *work = g_timed_work[kclass];
+  return MTNN_OK;
+}
+
 int mtnn_profile_reset(void) {
   std::lock_guard<std::mutex> lk(g_mu);
   for (auto& p : g_pending) {
@@ -99,7 +117,10 @@ int mtnn_profile_reset(void) {
     g_free_events.push_back(p.stop);
   }
   g_pending.clear();
-  for (int i = 0; i < MTNN_KCLASS_COUNT; ++i) g_ms[i] = g_work[i] = 0.0, g_launches[i] = 0;
+  for (int i = 0; i < MTNN_KCLASS_COUNT; ++i) {
+    g_ms[i] = g_work[i] = g_timed_work[i] = 0.0;
+    g_launches[i] = g_timed_launches[i] = 0;
+  }
   (void)cudaGetLastError();
   return MTNN_OK;
 }
@@ -117,6 +138,8 @@ int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* w
       return fail(MTNN_ECUDA, "profile event: %s", cudaGetErrorString(e));
     }
     g_ms[p.kclass] += ms;
+    g_timed_launches[p.kclass] += 1;
+    g_timed_work[p.kclass] += p.work;
     g_free_events.push_back(p.start);
     g_free_events.push_back(p.stop);
   }
