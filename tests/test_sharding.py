@@ -136,7 +136,7 @@ def _fused_worker(rank, world, port, m, n, k, q):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m,n,k", [(1024, 768, 512), (600, 300, 264)])
+@pytest.mark.parametrize("m,n,k", [(1024, 768, 512), (600, 300, 264), (2048, 1024, 8192)])
 def test_fused_allgather_two_processes_one_gpu(m, n, k):
     """Two ranks (processes) share the GPU; each computes its row block with
     the all-gather fused into the GEMM epilogue (stores into the other rank's
@@ -157,7 +157,8 @@ def test_fused_allgather_two_processes_one_gpu(m, n, k):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m,n,k,row0,mloc", [(2048, 1024, 512, 512, 1024), (256, 300, 64, 100, 64)])
+@pytest.mark.parametrize("m,n,k,row0,mloc", [(2048, 1024, 512, 512, 1024), (256, 300, 64, 100, 64),
+                                             (4096, 2048, 8192, 1024, 2048)])
 def test_fused_allgather_local_destinations(m, n, k, row0, mloc):
     """The multi-destination epilogue on one process: peers are other local C
     buffers; the row block lands identically in all of them, other rows untouched
