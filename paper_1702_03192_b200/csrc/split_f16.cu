@@ -11,9 +11,15 @@
 // TF32 but runs at twice the tensor-core rate, and the per-row scale removes its
 // range limit (subnormal tails sit ~2^-38 below the row maximum).
 //
-// Traffic: row-split (K-major operands) reads each row twice from L2 but DRAM
-// once — 4 B read + 4 B written per element; column-split (MN-major B^T) makes a
-// max pass then a split pass — 8 B read + 4 B written per element.
+// Traffic: the row splits (K-major operands) read each element from DRAM once
+// and write its halves once — 4 B + 4 B; the column splits (MN-major B^T) do the
+// same (strip kernel: the second read hits L2; cluster kernel: registers),
+// except the two-pass band kernel for k > 8192 — 8 B read + 4 B written.
+//
+// Kernels by shape: rows — register warp (k <= 512, 1024 < k <= 2048), looped
+// warp (k = 1024), register CTA (2048 < k <= 16384), smem CTA (longer rows);
+// columns — single-CTA strip (k <= 1024, many strips), cluster strip with a
+// DSMEM max exchange (k <= 8192), two-pass band (beyond).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -434,7 +440,7 @@ split_cols_band_kernel(const float* __restrict__ x, const float* __restrict__ pa
 // row lanes. Pass 1 reads the strip for the column maxima (reduced through
 // shared memory), pass 2 re-reads it — from L2 while the strips in flight fit
 // there — and writes the halves: 8 B of DRAM traffic per element instead of the
-// two-kernel path's 12, and no scratch or memset.
+// two-pass band path's 12, and no scratch. Used for k <= 1024 with >= 74 strips.
 constexpr int kStripCols = 32;
 constexpr int kStripLanes = 64;
 
