@@ -606,6 +606,17 @@ def main():
     if args.workload in ("large", "fcn") and world > 1:
         extra["collective_ms_per_step"] = {
             k: statistics.mean(s.elapsed_time(e) for s, e in v) for k, v in comm.items() if v}
+        # compute-only view (§8e): the step without its separate collective
+        # windows (this rank's); with the fused gather the C stores stay inside
+        # the GEMM window, so only the broadcast of B is removed
+        comm_ms = sum(extra["collective_ms_per_step"].values())
+        comp_ms = step_s * 1e3 - comm_ms
+        if comp_ms > 0:
+            extra["compute_only"] = {
+                "value": total_flops / (comp_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                "ms_per_step": comp_ms,
+                "excludes": sorted(extra["collective_ms_per_step"]),
+            }
     if gather_mode is not None:
         extra["gather"] = gather_mode
     if world == 1:
