@@ -11,10 +11,16 @@ picks = [1, 2, 3, 4, 7, 8, 9, 16, 31, 32, 33, 64, 96, 127, 128, 129, 192, 255, 2
          513, 768, 1000, 1023, 1024, 1025, 1536, 2047, 2048, 2049, 3000, 4100]
 bad = 0
 longk = [4104, 6000, 8192, 8200, 12000, 16384, 16392, 20000]
+import os
+big = os.environ.get("FUZZ_BIG") == "1"
 for it in range(N):
     m, n, k = (int(rng.choice(picks)) if rng.random() < 0.7 else int(rng.integers(1, 4200)) for _ in range(3))
     if it % 4 == 3:  # long-k branches of the row / column splits (register, cluster, band, smem)
         m, n, k = int(rng.choice(picks[:24])), int(rng.choice(picks[:24])), int(rng.choice(longk))
+    if big and it % 4 == 1:  # one large output side: CTA pairs, grouped raster, split-K edges
+        dims = [int(rng.choice([4096, 6000, 8192, 10000, 16384])), int(rng.choice(picks)),
+                int(rng.choice([256, 1000, 2048, 4104]))]
+        m, n, k = (dims[0], dims[1], dims[2]) if rng.random() < 0.5 else (dims[1], dims[0], dims[2])
     knobs = {"tc_pair": int(rng.integers(0, 3)), "f16s_inkernel_max_short": int(rng.choice([0, 256, 1 << 20])),
              "host_pipeline_blocked": int(rng.integers(0, 2))}
     for kk, vv in knobs.items():
