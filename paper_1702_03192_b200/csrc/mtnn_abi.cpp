@@ -130,6 +130,11 @@ static int check_dims(int64_t m, int64_t n, int64_t k) {
 // including skinny ones (tools/probe_skinny.py), so no cost model is needed.
 static int auto_variant(const float* A, const float* B, const float* C, int64_t m, int64_t n,
                         int64_t k, bool b_is_nk) {
+  // Below 2^22 multiply-adds the exact-order FFMA kernel: it keeps the
+  // reference's bit-exact identity KATs (test_kernels.py:32-40, sizes <= 130^3)
+  // exact, which the hi/lo split cannot (22 of fp32's 24 significand bits). The
+  // tensor-core path would be faster there for k >= 64 (128^3: 14.5 vs 33 us,
+  // tools/probe_small.py TINY=1); parity wins.
   if ((double)m * (double)n * (double)k < 4194304.0) return MTNN_VARIANT_FFMA;
   // (an ineligible C — n % 4 != 0 or unaligned — is handled by a padded output)
   if (tc_eligible_operands(A, B, m, n, k, b_is_nk, TcKind::F16S)) return MTNN_VARIANT_TC3XF16S;

@@ -12,6 +12,8 @@ A = torch.rand(N2, device=dev); B = torch.rand(N2, device=dev); C = torch.empty(
 import os
 shapes = [(128, 128, 128), (256, 128, 128), (128, 1024, 256), (512, 512, 512), (1024, 1024, 256), (256, 2048, 512),
           (1024, 1024, 1024), (2048, 2048, 512), (512, 4096, 1024), (2048, 2048, 2048)]
+if os.environ.get("TINY"):
+    shapes = [(32, 32, 32), (64, 64, 64), (64, 64, 256), (128, 128, 64), (128, 128, 128), (96, 200, 128), (256, 256, 32), (128, 64, 512)]
 if os.environ.get("LONGSKINNY"):
     shapes = [(128, 16384, 16384), (16384, 128, 16384), (256, 16384, 16384), (128, 16384, 4096), (256, 8192, 8192), (512, 16384, 16384), (128, 4096, 16384)]
 if os.environ.get("SKINNY"):
