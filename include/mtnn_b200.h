@@ -74,7 +74,9 @@ int mtnn_device_features(double out5[5]);
  * class 0 = tc3xtf32 GEMM (2mnk flops), 1 = FFMA GEMM (2mnk flops),
  * 2 = transpose (8*rows*cols bytes), 3 = operand split (bytes moved: 8 per
  * element; 12 for the column-scaled fp16 split), 4 = split-K reduction
- * (4*(splits+1) bytes per output), 5 = tc3xf16s GEMM (2mnk flops).
+ * (4*(splits+1) bytes per output), 5 = tc3xf16s GEMM (2mnk flops),
+ * 6 = residual fix-up after a split tensor-core GEMM (work = 0: its cost is
+ * the time it adds).
  * mtnn_profile_read synchronizes the recorded events and returns the totals. */
 #define MTNN_KCLASS_GEMM_TC 0
 #define MTNN_KCLASS_GEMM_FFMA 1
@@ -82,7 +84,8 @@ int mtnn_device_features(double out5[5]);
 #define MTNN_KCLASS_SPLIT 3
 #define MTNN_KCLASS_REDUCE 4
 #define MTNN_KCLASS_GEMM_TC_F16S 5
-#define MTNN_KCLASS_COUNT 6
+#define MTNN_KCLASS_FIXUP 6
+#define MTNN_KCLASS_COUNT 7
 int mtnn_profile_enable(int on);
 /* Time only the classes whose bit (1 << class) is set: every timed launch is
  * bracketed by two timestamp events, which serialise the stream around it, so
@@ -115,6 +118,11 @@ int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* w
  *   host-buffer NT calls on the tc3xf16s path with n >= 1024, k <= 4096 stream B in row
  *   blocks against A's first row block so C leaves while B arrives; 0 = copy B
  *   first, then pipeline A/C row chunks.
+ * "fixup": 1 (default; env MTNN_FIXUP=0 turns it off): the split tensor-core
+ *   paths list every operand element their two-piece representation misses by
+ *   more than 2^-19 (tc3xf16s: entries far below their row's max; tc3xtf32:
+ *   FP32-subnormal parts) and add those terms to C exactly after the GEMM, so
+ *   accuracy does not depend on the range inside a row; 0 skips it (A/B only).
  * Unknown keys -> MTNN_EINVAL. */
 int mtnn_config_set(const char* key, int64_t value);
 int mtnn_config_get(const char* key, int64_t* value);

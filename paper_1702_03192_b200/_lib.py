@@ -33,8 +33,9 @@ KCLASS_TRANSPOSE = 2
 KCLASS_SPLIT = 3
 KCLASS_REDUCE = 4
 KCLASS_GEMM_TC_F16S = 5
+KCLASS_FIXUP = 6
 KCLASS_NAMES = {0: "gemm_tc3xtf32", 1: "gemm_ffma", 2: "transpose", 3: "operand_split",
-                4: "splitk_reduce", 5: "gemm_tc3xf16s"}
+                4: "splitk_reduce", 5: "gemm_tc3xf16s", 6: "residual_fixup"}
 
 CHOICE_NT = 0
 CHOICE_TNN = 1

@@ -8,6 +8,7 @@
 #include <string>
 
 #include "../../include/mtnn_b200.h"
+#include "fix.h"
 
 namespace mtnn {
 
@@ -92,16 +93,20 @@ struct TcOperand {
   const void* hi = nullptr;
   const void* lo = nullptr;
   const float* inv_scale = nullptr;
+  FixList fix;  // residual entries of this operand (fix.h)
 };
 struct ScratchBuffer;
 // inkernel: the operand is split inside the GEMM from its raw rows (hi = X,
 // lo = nullptr); F16S then only computes the row scales (read-only pass).
+// fh: receives the operand's residual list (fix.h; nullptr = no tracking); it
+// must live until the fix-up (launch_fixup) that consumes it is enqueued.
+struct FixHandle;
 int tc_prepare(const float* X, int64_t rows, int64_t k, bool mn_major, TcKind kind,
-               bool inkernel, ScratchBuffer& ws, TcOperand* out, cudaStream_t s);
+               bool inkernel, ScratchBuffer& ws, FixHandle* fh, TcOperand* out, cudaStream_t s);
 // Both operands of one GEMM; F16S with K-major B runs a single split launch.
 int tc_prepare_pair(const float* A, int64_t m, const float* B, int64_t n, int64_t k,
                     bool b_mn_major, TcKind kind, int conv, ScratchBuffer& wa, ScratchBuffer& wb,
-                    TcOperand* a, TcOperand* b, cudaStream_t s);
+                    FixHandle* fa, FixHandle* fb, TcOperand* a, TcOperand* b, cudaStream_t s);
 // Which operand (1 = A, 2 = B, 0 = none) the GEMM splits in-kernel for this shape.
 int tc_inkernel_operand(int64_t m, int64_t n, bool b_is_nk, TcKind kind);
 // Run-time knob (mtnn_config_set): largest output short side split in-kernel.
@@ -120,18 +125,71 @@ int gemm_nt_allgather(const float* A, const float* B, float* C_local, float* con
 // The library's AUTO NT dispatch (mtnn_abi.cpp), for internal fallbacks.
 int gemm_dispatch_nt(const float* A, const float* B, float* C, int64_t m, int64_t n, int64_t k,
                      cudaStream_t s);
+// F16S operand splits. `fix` receives the operand's residual entries (fix.h;
+// FixList{} = none). hiN == nullptr -> row scales (and residual check) only.
 int launch_split_rows_f16(const float* x, void* hi, void* lo, float* inv_scale, int64_t rows,
-                          int64_t k, cudaStream_t s);
-// Both K-major operands of one GEMM in one launch: rows of x0 then x1 (same k);
-// hiN == nullptr -> row scales only for that operand.
+                          int64_t k, const FixList& fix, cudaStream_t s);
+// Both K-major operands of one GEMM in one launch: rows of x0 then x1 (same k).
 int launch_split_rows_f16_pair(const float* x0, void* hi0, void* lo0, float* inv0, int64_t rows0,
-                               const float* x1, void* hi1, void* lo1, float* inv1, int64_t rows1,
-                               int64_t k, cudaStream_t s);
+                               const FixList& fix0, const float* x1, void* hi1, void* lo1,
+                               float* inv1, int64_t rows1, const FixList& fix1, int64_t k,
+                               cudaStream_t s);
 // 1/s per row (s = split_rows_f16's power-of-two row scale), reading x only.
-int launch_rowmax_f16(const float* x, float* inv_scale, int64_t rows, int64_t k, cudaStream_t s);
+int launch_rowmax_f16(const float* x, float* inv_scale, int64_t rows, int64_t k,
+                      const FixList& fix, cudaStream_t s);
 // Scratch (device bytes) launch_split_cols_f16 needs for an n-column operand.
 size_t split_cols_scratch_bytes(int64_t n);
 int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,
-                          float* partial_scratch, int64_t k, int64_t n, cudaStream_t s);
+                          float* partial_scratch, int64_t k, int64_t n, const FixList& fl,
+                          cudaStream_t s);
+
+// ------------------------------------------------------------ residual fix-up
+// Residual list of one split operand (fix.h): a ring counter pair plus entries
+// carved from the caller's workspace. Releasing an unconsumed list (error exit)
+// resets its counter on the stream.
+struct FixHandle {
+  FixList list;
+  cudaStream_t stream = nullptr;
+  bool consumed = false;
+  FixHandle() = default;
+  FixHandle(const FixHandle&) = delete;
+  FixHandle& operator=(const FixHandle&) = delete;
+  ~FixHandle();
+};
+// Whether split operands track residuals (mtnn_config_set("fixup", 0/1); env MTNN_FIXUP=0).
+bool fixup_enabled();
+void set_fixup_enabled(bool on);
+// Entries to reserve for an operand of `elems` elements, and their bytes.
+unsigned fix_capacity(int64_t elems);
+inline size_t fix_entry_bytes(unsigned cap) { return ((size_t)cap * sizeof(FixEntry) + 255) & ~size_t(255); }
+// Takes a zeroed counter pair from the device ring and points the list at
+// `entries` (cap entries). row0: global row of the operand's row 0.
+int fix_attach(FixHandle* h, void* entries, unsigned cap, int32_t row0, cudaStream_t s);
+
+enum class FixRep { F16S = 0, TF32_TRUNC = 1, TF32_RNA = 2 };
+// Adds the listed residual terms to C (ndst copies: C and up to 7 peer
+// buffers, same layout), or recomputes C with the exact-order FFMA tile loop
+// if a list overflowed. A: m x k raw rows (global rows a_row0.. of its list),
+// inv_a: its F16S row scales; B: n x k (b_is_nk) or k x n (ldb) raw; C rows of
+// ldc. reset_*: this is the list's last consumer (its counter is reset).
+struct FixupArgs {
+  const float* A = nullptr;
+  const float* inv_a = nullptr;  // F16S row scales of A (and of B): bound the
+  const float* inv_b = nullptr;  // corrections so negligible ones are skipped
+  const float* B = nullptr;
+  int64_t ldb = 0;
+  float* C[8] = {};
+  int ndst = 1;
+  int64_t ldc = 0;
+  int64_t m = 0, n = 0, k = 0;
+  bool b_is_nk = true;
+  FixRep rep = FixRep::F16S;
+  FixList fa, fb;
+  int32_t a_row0 = 0, b_row0 = 0;
+  bool reset_a = true, reset_b = true;
+};
+int launch_fixup(const FixupArgs& args, cudaStream_t s);
+// How the tensor-core kind represents an operand element (the fix-up recomputes it).
+FixRep tc_fix_rep(TcKind kind);
 
 }  // namespace mtnn

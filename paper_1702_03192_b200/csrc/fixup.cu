@@ -1,0 +1,398 @@
+// Residual fix-up of the split tensor-core GEMMs (see fix.h for the scheme).
+//
+// Runs after the GEMM (and its split-K reduction) on the same stream, chained
+// by programmatic launch. Three outcomes, decided on the device from the two
+// operands' list counters:
+//   * no entries (the usual case): every CTA reads two counters and exits;
+//   * entries within capacity: C[i, :] += r * B[:, p] per A entry and
+//     C[:, j] += rep(A[:, p]) * r per B entry, one output per thread, float
+//     atomics (entries meeting in one output add in any order);
+//   * a list overflowed: the whole output is recomputed by the exact-order FFMA
+//     tile loop (sgemm_tile.cuh), every destination overwritten.
+// Reference bar: the FP32 row-dot of _numba_impl.py:139-152 — every product
+// term carried to FP32 accuracy whatever the range inside a row.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <atomic>
+#include <mutex>
+
+#include "common.h"
+#include "fix.h"
+#include "pdl.h"
+#include "sgemm_tile.cuh"
+
+namespace mtnn {
+
+// ----------------------------------------------------------- counter ring
+namespace {
+constexpr unsigned kFixRing = 1u << 16;
+constexpr int kMaxDev = 64;
+FixCounter* g_ring[kMaxDev];
+std::atomic<unsigned> g_ring_next[kMaxDev];
+std::once_flag g_ring_once[kMaxDev];
+cudaError_t g_ring_err[kMaxDev];
+std::atomic<int> g_fixup{-1};
+}  // namespace
+
+bool fixup_enabled() {
+  int v = g_fixup.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = getenv("MTNN_FIXUP");
+    v = (e && e[0] == '0') ? 0 : 1;
+    g_fixup.store(v, std::memory_order_relaxed);
+  }
+  return v != 0;
+}
+void set_fixup_enabled(bool on) { g_fixup.store(on ? 1 : 0, std::memory_order_relaxed); }
+
+unsigned fix_capacity(int64_t elems) {
+  const int64_t c = 4096 + std::max<int64_t>(0, elems) / 4096;
+  return (unsigned)std::min<int64_t>(c, 1 << 24);
+}
+
+static int fix_counter(FixCounter** out) {
+  int dev = 0;
+  MTNN_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDev) return fail(MTNN_EINVAL, "device index %d out of range", dev);
+  std::call_once(g_ring_once[dev], [dev] {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, kFixRing * sizeof(FixCounter));
+    if (e == cudaSuccess) e = cudaMemset(p, 0, kFixRing * sizeof(FixCounter));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) (void)cudaGetLastError();
+    g_ring_err[dev] = e;
+    g_ring[dev] = e == cudaSuccess ? static_cast<FixCounter*>(p) : nullptr;
+  });
+  if (g_ring[dev] == nullptr)
+    return fail(MTNN_ECUDA, "residual counter ring: %s", cudaGetErrorString(g_ring_err[dev]));
+  const unsigned slot = g_ring_next[dev].fetch_add(1, std::memory_order_relaxed) % kFixRing;
+  *out = g_ring[dev] + slot;
+  return MTNN_OK;
+}
+
+int fix_attach(FixHandle* h, void* entries, unsigned cap, int32_t row0, cudaStream_t s) {
+  FixCounter* c = nullptr;
+  MTNN_TRY(fix_counter(&c));
+  h->list.ctr = c;
+  h->list.e = static_cast<FixEntry*>(entries);
+  h->list.cap = cap;
+  h->list.row0 = row0;
+  h->stream = s;
+  h->consumed = false;
+  return MTNN_OK;
+}
+
+FixHandle::~FixHandle() {
+  // a list whose fix-up never ran (error exit) leaves its counter dirty
+  if (list.ctr != nullptr && !consumed) {
+    (void)cudaMemsetAsync(list.ctr, 0, sizeof(FixCounter), stream);
+    (void)cudaGetLastError();
+  }
+}
+
+// ------------------------------------------------------------------ kernel
+namespace {
+
+struct FixupDev {
+  const float* A;
+  const float* inv_a;
+  const float* inv_b;
+  const float* B;
+  int64_t ldb;
+  float* C[8];
+  int ndst;
+  int64_t ldc;
+  int64_t m, n, k;
+  int rep;
+  FixList fa, fb;
+  int32_t a_row0, b_row0;
+  int reset_a, reset_b;
+  int smem_entries;
+};
+
+constexpr int kFixThreads = 256;
+constexpr int64_t kFixChunk = 256;  // k per FFMA chain in the overflow recompute
+// Entries (A + B, each padded to a power of two) the deterministic path sorts in
+// shared memory: 8192 x (8 B key + 4 B value) = 96 KiB (uniform data lists
+// ~2^-20 of its elements: ~1000 for two 16384^2 operands).
+constexpr int kFixSmemEntries = 8192;
+constexpr size_t kFixSmemBytes = (size_t)kFixSmemEntries * 12;
+
+__device__ __forceinline__ float rep_a(const FixupDev& p, int64_t i, float a) {
+  if (p.rep == (int)FixRep::F16S) return f16s_represented(a, p.inv_a[i]);
+  if (p.rep == (int)FixRep::TF32_RNA) return tf32_represented<true>(a);
+  return tf32_represented<false>(a);
+}
+
+// Counter reset protocol: every CTA, after reading a non-zero count, bumps
+// `done`; the last one zeroes the pair for the ring's next user.
+__device__ __forceinline__ void release(const FixList& fl, unsigned count, bool reset) {
+  if (fl.ctr == nullptr || count == 0 || !reset) return;
+  __threadfence();
+  if (atomicAdd(&fl.ctr->done, 1u) == gridDim.x - 1) {
+    fl.ctr->count = 0;
+    fl.ctr->done = 0;
+  }
+}
+
+__device__ __forceinline__ unsigned pow2_at_least(unsigned x) {
+  unsigned p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// Loads `cnt` entries as (row << 32 | col) keys + residuals, pads to `np` with
+// +inf keys and sorts them (bitonic; every CTA gets the same order).
+__device__ void load_sorted(const FixEntry* __restrict__ e, unsigned cnt, unsigned np,
+                            unsigned long long* key, float* val) {
+  for (unsigned i = threadIdx.x; i < np; i += blockDim.x) {
+    if (i < cnt) {
+      const FixEntry x = e[i];
+      key[i] = ((unsigned long long)(uint32_t)x.row << 32) | (uint32_t)x.col;
+      val[i] = x.r;
+    } else {
+      key[i] = ~0ull;
+      val[i] = 0.f;
+    }
+  }
+  __syncthreads();
+  for (unsigned size = 2; size <= np; size <<= 1) {
+    for (unsigned stride = size >> 1; stride > 0; stride >>= 1) {
+      for (unsigned i = threadIdx.x; i < np; i += blockDim.x) {
+        const unsigned j = i ^ stride;
+        if (j > i) {
+          const bool up = (i & size) == 0;
+          const unsigned long long ki = key[i], kj = key[j];
+          if ((ki > kj) == up) {
+            key[i] = kj;
+            key[j] = ki;
+            const float t = val[i];
+            val[i] = val[j];
+            val[j] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// First index in key[0, cnt) whose row is >= row.
+__device__ __forceinline__ unsigned lower_row(const unsigned long long* key, unsigned cnt,
+                                              uint32_t row) {
+  const unsigned long long want = (unsigned long long)row << 32;
+  unsigned lo = 0, hi = cnt;
+  while (lo < hi) {
+    const unsigned mid = (lo + hi) >> 1;
+    if (key[mid] < want) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint32_t key_row(unsigned long long k) { return (uint32_t)(k >> 32); }
+__device__ __forceinline__ uint32_t key_col(unsigned long long k) { return (uint32_t)k; }
+
+template <bool B_NK>
+__device__ __forceinline__ float b_at(const FixupDev& p, int64_t j, int64_t col) {
+  return B_NK ? __ldg(p.B + j * p.k + col) : __ldg(p.B + col * p.ldb + j);
+}
+
+template <bool B_NK>
+__global__ void __launch_bounds__(kFixThreads, 2) fixup_kernel(const FixupDev p) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  extern __shared__ __align__(16) unsigned char fix_smem[];
+  __shared__ unsigned s_na, s_nb;
+  // The counters are final before this grid can start: the split kernels that
+  // append to them completed before the GEMM passed its griddepcontrol.wait,
+  // and the GEMM triggers its dependents only after that wait. Reading them
+  // here overlaps the load with the GEMM's tail.
+  if (threadIdx.x == 0) {
+    s_na = p.fa.ctr ? *reinterpret_cast<volatile unsigned*>(&p.fa.ctr->count) : 0u;
+    s_nb = p.fb.ctr ? *reinterpret_cast<volatile unsigned*>(&p.fb.ctr->count) : 0u;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  __syncthreads();
+  const unsigned na = s_na, nb = s_nb;
+  if (na + nb == 0) return;  // the usual case: nothing listed, counters already zero
+  if (threadIdx.x == 0) {
+    release(p.fa, na, p.reset_a != 0);
+    release(p.fb, nb, p.reset_b != 0);
+  }
+  if (na > p.fa.cap || nb > p.fb.cap) {
+    // a list overflowed: recompute every output with FFMA chains of kFixChunk k,
+    // each chain added to the output in memory by the thread that owns it (the
+    // rounding error grows with ~k/kFixChunk + kFixChunk terms instead of k:
+    // one k = 40960 chain is ~1e-5 off; no running total in registers keeps
+    // this kernel at the SIMT GEMM's register count, so the next kernel's CTAs
+    // fit beside it)
+    auto& As = *reinterpret_cast<float(*)[2][sgemm::BK][sgemm::BM]>(fix_smem);
+    auto& Bs = *reinterpret_cast<float(*)[2][sgemm::BK][sgemm::BN]>(fix_smem + sizeof(As));
+    const int64_t tm = (p.m + sgemm::BM - 1) / sgemm::BM, tn = (p.n + sgemm::BN - 1) / sgemm::BN;
+    for (int64_t t = blockIdx.x; t < tm * tn; t += gridDim.x) {
+      const int64_t bm0 = (t / tn) * sgemm::BM, bn0 = (t % tn) * sgemm::BN;
+      for (int64_t k0 = 0; k0 < p.k; k0 += kFixChunk) {
+        float acc[8][8];
+        sgemm::tile<B_NK>(p.A, p.B, p.ldb, p.m, p.n, p.k, bm0, bn0, k0, min(p.k, k0 + kFixChunk),
+                          As, Bs, acc);
+        for (int d = 0; d < p.ndst; ++d) sgemm::store_acc(acc, p.C[d], p.ldc, p.m, p.n, bm0, bn0, k0 > 0);
+        __syncthreads();  // the next chunk refills the staging buffers
+      }
+    }
+    return;
+  }
+  const int64_t cn = (p.n + kFixThreads - 1) / kFixThreads;
+  const int64_t cm = (p.m + kFixThreads - 1) / kFixThreads;
+  const unsigned npa = na ? pow2_at_least(na) : 0, npb = nb ? pow2_at_least(nb) : 0;
+  if (npa + npb > (unsigned)p.smem_entries) {
+    // too many entries to sort on chip (operands of ~2^32 elements): float
+    // atomics, entries meeting in one output add in arrival order
+    const int64_t items_a = (int64_t)na * cn;
+    const int64_t total = items_a + (int64_t)nb * cm;
+    for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+      if (it < items_a) {
+        const FixEntry e = p.fa.e[it / cn];
+        const int64_t i = (int64_t)e.row - p.a_row0;
+        const int64_t j = (it % cn) * kFixThreads + threadIdx.x;
+        if (i < 0 || i >= p.m || j >= p.n) continue;
+        const float v = e.r * b_at<B_NK>(p, j, e.col);
+        if (v != 0.f)
+          for (int d = 0; d < p.ndst; ++d) atomicAdd(p.C[d] + i * p.ldc + j, v);
+      } else {
+        const int64_t q = it - items_a;
+        const FixEntry e = p.fb.e[q / cm];
+        const int64_t j = (int64_t)e.row - p.b_row0;
+        const int64_t i = (q % cm) * kFixThreads + threadIdx.x;
+        if (j < 0 || j >= p.n || i >= p.m) continue;
+        const float v = rep_a(p, i, __ldg(p.A + i * p.k + e.col)) * e.r;
+        if (v != 0.f)
+          for (int d = 0; d < p.ndst; ++d) atomicAdd(p.C[d] + i * p.ldc + j, v);
+      }
+    }
+    return;
+  }
+  // Deterministic path: every CTA sorts both lists by (row, k index); each
+  // affected output is then updated by exactly one thread, which adds its A
+  // terms (k ascending) and its B terms (k ascending) and stores once.
+  // F16S: a term is bounded by |r| * (max of the other operand's row) = |r| *
+  // 2^14 * its 1/s; an output whose corrections are provably below 2^-26 of its
+  // value (uniform data: all of them) is left as it is, so it costs one read of
+  // C and of the row scales instead of the strided gathers of B's column / A's
+  // column.
+  unsigned long long* ka = reinterpret_cast<unsigned long long*>(fix_smem);
+  unsigned long long* kb = ka + npa;
+  float* va = reinterpret_cast<float*>(kb + npb);
+  float* vb = va + npa;
+  if (na) load_sorted(p.fa.e, na, npa, ka, va);
+  if (nb) load_sorted(p.fb.e, nb, npb, kb, vb);
+  const bool bounded = p.rep == (int)FixRep::F16S && p.inv_a != nullptr && p.inv_b != nullptr;
+  constexpr float kRowMax = 16384.f;      // max |x| of a row <= 2^14 / s
+  constexpr float kNegligible = 0x1p-26f;  // of |C|: below a quarter ulp
+  // work items: (leading entry of a row of A entries, chunk of n) then
+  // (leading entry of a column of B entries, chunk of m)
+  const int64_t items_a = (int64_t)na * cn;
+  const int64_t total = items_a + (int64_t)nb * cm;
+  for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+    if (it < items_a) {
+      const unsigned e0 = (unsigned)(it / cn);
+      const uint32_t grow = key_row(ka[e0]);
+      if (e0 > 0 && key_row(ka[e0 - 1]) == grow) continue;  // not the row's first entry
+      const int64_t i = (int64_t)grow - p.a_row0;
+      const int64_t j = (it % cn) * kFixThreads + threadIdx.x;
+      if (i < 0 || i >= p.m || j >= p.n) continue;
+      unsigned e1 = e0;
+      float ra = 0.f;
+      while (e1 < na && key_row(ka[e1]) == grow) ra += fabsf(va[e1++]);
+      const uint32_t gcol = (uint32_t)(j + p.b_row0);
+      const unsigned b0 = nb ? lower_row(kb, nb, gcol) : 0u;
+      unsigned b1 = b0;
+      float rb = 0.f;
+      while (b1 < nb && key_row(kb[b1]) == gcol) rb += fabsf(vb[b1++]);
+      const float c = p.C[0][i * p.ldc + j];
+      if (bounded &&
+          ra * kRowMax * p.inv_b[j] + rb * kRowMax * p.inv_a[i] <= kNegligible * fabsf(c))
+        continue;
+      float s = 0.f;
+      for (unsigned e = e0; e < e1; ++e) s = fmaf(va[e], b_at<B_NK>(p, j, key_col(ka[e])), s);
+      for (unsigned e = b0; e < b1; ++e)
+        s = fmaf(rep_a(p, i, __ldg(p.A + i * p.k + key_col(kb[e]))), vb[e], s);
+      if (s != 0.f || isnan(s))
+        for (int d = 0; d < p.ndst; ++d) p.C[d][i * p.ldc + j] += s;
+    } else {
+      const int64_t q = it - items_a;
+      const unsigned e0 = (unsigned)(q / cm);
+      const uint32_t gcol = key_row(kb[e0]);
+      if (e0 > 0 && key_row(kb[e0 - 1]) == gcol) continue;
+      const int64_t j = (int64_t)gcol - p.b_row0;
+      const int64_t i = (q % cm) * kFixThreads + threadIdx.x;
+      if (j < 0 || j >= p.n || i >= p.m) continue;
+      // rows carrying A entries take their B terms in the A pass above
+      if (na) {
+        const uint32_t grow = (uint32_t)(i + p.a_row0);
+        const unsigned lb = lower_row(ka, na, grow);
+        if (lb < na && key_row(ka[lb]) == grow) continue;
+      }
+      unsigned e1 = e0;
+      float rb = 0.f;
+      while (e1 < nb && key_row(kb[e1]) == gcol) rb += fabsf(vb[e1++]);
+      if (bounded && rb * kRowMax * p.inv_a[i] <= kNegligible * fabsf(p.C[0][i * p.ldc + j]))
+        continue;
+      float s = 0.f;
+      for (unsigned e = e0; e < e1; ++e)
+        s = fmaf(rep_a(p, i, __ldg(p.A + i * p.k + key_col(kb[e]))), vb[e], s);
+      if (s != 0.f || isnan(s))
+        for (int d = 0; d < p.ndst; ++d) p.C[d][i * p.ldc + j] += s;
+    }
+  }
+}
+
+}  // namespace
+
+int launch_fixup(const FixupArgs& a, cudaStream_t s) {
+  if (a.fa.ctr == nullptr && a.fb.ctr == nullptr) return MTNN_OK;  // nothing tracked
+  if (a.m <= 0 || a.n <= 0 || a.k <= 0) return MTNN_OK;
+  if (a.ndst < 1 || a.ndst > 8) return fail(MTNN_EINVAL, "fix-up: %d destinations", a.ndst);
+  const DeviceInfo* di = nullptr;
+  MTNN_TRY(device_info(&di));
+  FixupDev p{};
+  p.A = a.A;
+  p.inv_a = a.inv_a;
+  p.inv_b = a.inv_b;
+  p.B = a.B;
+  p.ldb = a.ldb > 0 ? a.ldb : a.n;
+  for (int d = 0; d < a.ndst; ++d) p.C[d] = a.C[d];
+  p.ndst = a.ndst;
+  p.ldc = a.ldc > 0 ? a.ldc : a.n;
+  p.m = a.m;
+  p.n = a.n;
+  p.k = a.k;
+  p.rep = (int)a.rep;
+  p.fa = a.fa;
+  p.fb = a.fb;
+  p.a_row0 = a.a_row0;
+  p.b_row0 = a.b_row0;
+  p.reset_a = a.reset_a ? 1 : 0;
+  p.reset_b = a.reset_b ? 1 : 0;
+  if (p.rep == (int)FixRep::F16S && p.inv_a == nullptr && a.fb.ctr != nullptr)
+    return fail(MTNN_EINVAL, "fix-up: F16S B entries need A's row scales");
+  // one CTA per SM: the entry work of random data is small, and the overflow
+  // recompute walks its tiles with it (measured: 32 CTAs or a max-shared
+  // carveout change nothing; the kernel's cost is the chain step it adds)
+  const unsigned grid = (unsigned)di->sm_count;
+  p.smem_entries = kFixSmemEntries;
+  KernelTimer timer(MTNN_KCLASS_FIXUP, 0.0, s);
+  if (a.b_is_nk) {
+    MTNN_TRY(set_max_dynamic_smem((const void*)fixup_kernel<true>, (int)kFixSmemBytes));
+    MTNN_TRY(launch_chained(fixup_kernel<true>, dim3(grid), dim3(kFixThreads), kFixSmemBytes, s, p));
+  } else {
+    MTNN_TRY(set_max_dynamic_smem((const void*)fixup_kernel<false>, (int)kFixSmemBytes));
+    MTNN_TRY(launch_chained(fixup_kernel<false>, dim3(grid), dim3(kFixThreads), kFixSmemBytes, s, p));
+  }
+  MTNN_CUDA_TRY(cudaGetLastError());
+  return MTNN_OK;
+}
+
+}  // namespace mtnn

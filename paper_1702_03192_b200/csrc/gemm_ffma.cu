@@ -21,12 +21,11 @@
 
 #include "common.h"
 #include "pdl.h"
+#include "sgemm_tile.cuh"
 #include "workspace.h"
 
 namespace mtnn {
 namespace {
-
-constexpr int BM = 128, BN = 128, BK = 8;
 
 // B_NK: B stored n x k (NT). Else B^T stored k x n (NN).
 template <bool B_NK>
@@ -35,115 +34,15 @@ sgemm_kernel(const float* __restrict__ A, const float* __restrict__ B,
              float* __restrict__ C, int64_t m, int64_t n, int64_t k, int64_t k_chunk,
              int64_t split_stride) {
   pdl_enter();
-  __shared__ __align__(16) float As[2][BK][BM];
-  __shared__ __align__(16) float Bs[2][BK][BN];
-
-  const int tid = threadIdx.x;
-  const int64_t bm0 = (int64_t)blockIdx.y * BM;
-  const int64_t bn0 = (int64_t)blockIdx.x * BN;
+  __shared__ __align__(16) float As[2][sgemm::BK][sgemm::BM];
+  __shared__ __align__(16) float Bs[2][sgemm::BK][sgemm::BN];
+  const int64_t bm0 = (int64_t)blockIdx.y * sgemm::BM;
+  const int64_t bn0 = (int64_t)blockIdx.x * sgemm::BN;
   const int64_t kbeg = (int64_t)blockIdx.z * k_chunk;
   const int64_t kend = min(k, kbeg + k_chunk);
-
-  // global->register load mapping
-  const int a_row = tid >> 1, a_k = (tid & 1) * 4;  // A: 128 rows x 8 k
-  const int bt_k = tid >> 5, bt_c = (tid & 31) * 4;  // B^T: 8 k x 128 cols
-
-  float ra[4], rb[4];
-  auto load_tile = [&](int64_t k0) {
-    {
-      const int64_t r = bm0 + a_row;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t kk = k0 + a_k + j;
-        ra[j] = (r < m && kk < kend) ? __ldg(A + r * k + kk) : 0.f;
-      }
-    }
-    if (B_NK) {
-      const int64_t r = bn0 + a_row;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t kk = k0 + a_k + j;
-        rb[j] = (r < n && kk < kend) ? __ldg(B + r * k + kk) : 0.f;
-      }
-    } else {
-      const int64_t kk = k0 + bt_k;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t c = bn0 + bt_c + j;
-        rb[j] = (kk < kend && c < n) ? __ldg(B + kk * n + c) : 0.f;
-      }
-    }
-  };
-  auto store_tile = [&](int buf) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) As[buf][a_k + j][a_row] = ra[j];
-    if (B_NK) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) Bs[buf][a_k + j][a_row] = rb[j];
-    } else {
-      *reinterpret_cast<float4*>(&Bs[buf][bt_k][bt_c]) =
-          make_float4(rb[0], rb[1], rb[2], rb[3]);
-    }
-  };
-
-  const int tx = tid & 15, ty = tid >> 4;
   float acc[8][8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-
-  int buf = 0;
-  if (kbeg < kend) {
-    load_tile(kbeg);
-    store_tile(0);
-  }
-  __syncthreads();
-  for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
-    const bool has_next = k0 + BK < kend;
-    if (has_next) load_tile(k0 + BK);
-#pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      float a[8], b[8];
-      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
-      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][64 + ty * 4]);
-      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
-      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 + tx * 4]);
-      a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
-      a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
-      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
-      b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-    }
-    if (has_next) {
-      store_tile(buf ^ 1);
-      __syncthreads();
-      buf ^= 1;
-    }
-  }
-
-  float* out = C + (int64_t)blockIdx.z * split_stride;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t r = bm0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
-    if (r >= m) continue;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t c = bn0 + h * 64 + tx * 4;
-      float* dst = out + r * n + c;
-      if (c + 3 < n && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-        *reinterpret_cast<float4*>(dst) = make_float4(
-            acc[i][h * 4 + 0], acc[i][h * 4 + 1], acc[i][h * 4 + 2], acc[i][h * 4 + 3]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (c + j < n) dst[j] = acc[i][h * 4 + j];
-      }
-    }
-  }
+  sgemm::tile<B_NK>(A, B, n, m, n, k, bm0, bn0, kbeg, kend, As, Bs, acc);
+  sgemm::store(acc, C + (int64_t)blockIdx.z * split_stride, n, m, n, bm0, bn0);
 }
 
 // Skinny NT (GEMV-class): one side of the output <= kSkinnyMax (the FCN's
@@ -262,7 +161,7 @@ int launch_gemm_ffma(const float* A, const float* B, float* C, int64_t m, int64_
   if (m <= 0 || n <= 0) return MTNN_OK;
   const DeviceInfo* di = nullptr;
   MTNN_TRY(device_info(&di));
-  const int64_t tiles_m = (m + BM - 1) / BM, tiles_n = (n + BN - 1) / BN;
+  const int64_t tiles_m = (m + sgemm::BM - 1) / sgemm::BM, tiles_n = (n + sgemm::BN - 1) / sgemm::BN;
   if (tiles_m > 65535) return fail(MTNN_EINVAL, "ffma gemm: m=%lld too large", (long long)m);
   // Split K when the tile grid cannot fill the chip and k is long enough.
   int splits = 1;
@@ -272,7 +171,7 @@ int launch_gemm_ffma(const float* A, const float* B, float* C, int64_t m, int64_
     splits = std::max(1, std::min(splits, 64));
   }
   int64_t k_chunk = (k + splits - 1) / splits;
-  k_chunk = (k_chunk + BK - 1) / BK * BK;
+  k_chunk = (k_chunk + sgemm::BK - 1) / sgemm::BK * sgemm::BK;
   splits = (int)((k + k_chunk - 1) / std::max<int64_t>(k_chunk, 1));
   if (k <= 0) { splits = 1; k_chunk = 0; }
   float* out = C;

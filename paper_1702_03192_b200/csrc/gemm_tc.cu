@@ -745,7 +745,8 @@ template <bool kHiCopy>
 __global__ void split_tf32_kernel(const float4* __restrict__ a, float4* __restrict__ a_hi,
                                   float4* __restrict__ a_lo, int64_t na4,
                                   const float4* __restrict__ b, float4* __restrict__ b_hi,
-                                  float4* __restrict__ b_lo, int64_t nb4) {
+                                  float4* __restrict__ b_lo, int64_t nb4, int64_t row_len,
+                                  bool mn_major, const FixList fa, const FixList fb) {
   pdl_trigger();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t total = na4 + nb4;
@@ -754,17 +755,19 @@ __global__ void split_tf32_kernel(const float4* __restrict__ a, float4* __restri
     const int64_t j = is_a ? i : i - na4;
     const float4 v = __ldg((is_a ? a : b) + j);
     float4 h, l;
-#define MTNN_SPLIT(c)                                                          \
+    // residual vs what the tensor core multiplies (ftz(trunc_tf32) of hi and lo;
+    // fix.h): only FP32-subnormal hi/lo parts miss it by more than 2^-20
+#define MTNN_SPLIT(c, q)                                                       \
   {                                                                            \
-    uint32_t t;                                                                \
-    if (kHiCopy)                                                               \
-      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(v.c));                    \
-    else                                                                       \
-      t = __float_as_uint(v.c) & 0xFFFFE000u;                                  \
-    h.c = __uint_as_float(t);                                                  \
+    h.c = tf32_hi<kHiCopy>(v.c);                                               \
     l.c = v.c - h.c;                                                           \
+    const float r = v.c - tf32_represented<kHiCopy>(v.c);                      \
+    if (fabsf(r) > kFixRelTF32 * fabsf(v.c)) {                                 \
+      const int64_t e = 4 * j + q, u = e / row_len, w = e % row_len;           \
+      fix_push(is_a ? fa : fb, mn_major ? w : u, mn_major ? u : w, r);         \
+    }                                                                          \
   }
-    MTNN_SPLIT(x) MTNN_SPLIT(y) MTNN_SPLIT(z) MTNN_SPLIT(w)
+    MTNN_SPLIT(x, 0) MTNN_SPLIT(y, 1) MTNN_SPLIT(z, 2) MTNN_SPLIT(w, 3)
 #undef MTNN_SPLIT
     if (kHiCopy) (is_a ? a_hi : b_hi)[j] = h;
     (is_a ? a_lo : b_lo)[j] = l;
@@ -1402,10 +1405,23 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // Split one operand into its hi/lo halves (+ per-row scales for F16S).
 // K-major (rows x k: A, or B of NT) or MN-major (k x cols: B^T of NN).
 int tc_prepare(const float* X, int64_t rows, int64_t k, bool mn_major, TcKind kind,
-               bool inkernel, ScratchBuffer& ws, TcOperand* out, cudaStream_t s) {
+               bool inkernel, ScratchBuffer& ws, FixHandle* fh, TcOperand* out, cudaStream_t s) {
   const DeviceInfo* di = nullptr;
   MTNN_TRY(device_info(&di));
   const int64_t count = rows * k;  // MN-major: k x rows (rows = n)
+  // residual list (fix.h), carved from the end of the workspace
+  const bool track = fh != nullptr && fixup_enabled() && !(inkernel && kind == TcKind::TF32);
+  const unsigned cap = track ? fix_capacity(count) : 0;
+  const size_t fix_bytes = track ? fix_entry_bytes(cap) : 0;
+  auto attach = [&](uint8_t* entries) -> int {
+    if (!track) {
+      out->fix = FixList{};
+      return MTNN_OK;
+    }
+    MTNN_TRY(fix_attach(fh, entries, cap, 0, s));
+    out->fix = fh->list;
+    return MTNN_OK;
+  };
   if (inkernel) {
     // split in-kernel from the raw rows (K-major only); F16S needs the row scales
     if (mn_major && kind == TcKind::F16S)
@@ -1413,48 +1429,59 @@ int tc_prepare(const float* X, int64_t rows, int64_t k, bool mn_major, TcKind ki
     out->hi = X;
     out->lo = nullptr;
     out->inv_scale = nullptr;
+    out->fix = FixList{};
     if (kind == TcKind::F16S) {
-      MTNN_TRY(ws.alloc((size_t)rows * sizeof(float), s));
+      const size_t osc = align256((size_t)rows * sizeof(float));
+      MTNN_TRY(ws.alloc(osc + fix_bytes, s));
       float* inv = static_cast<float*>(ws.ptr);
-      MTNN_TRY(launch_rowmax_f16(X, inv, rows, k, s));
+      MTNN_TRY(attach(static_cast<uint8_t*>(ws.ptr) + osc));
+      MTNN_TRY(launch_rowmax_f16(X, inv, rows, k, out->fix, s));
       out->inv_scale = inv;
     }
     return MTNN_OK;
   }
   if (kind == TcKind::TF32) {
     const bool hi_copy = split_mode_hi_copy();
-    MTNN_TRY(ws.alloc((size_t)((hi_copy ? 2 : 1) * count) * sizeof(float), s));
+    const size_t olo = align256((size_t)((hi_copy ? 2 : 1) * count) * sizeof(float));
+    MTNN_TRY(ws.alloc(olo + fix_bytes, s));
     float* lo = static_cast<float*>(ws.ptr);
     float* hi = hi_copy ? lo + count : nullptr;
+    MTNN_TRY(attach(static_cast<uint8_t*>(ws.ptr) + olo));
     const int64_t total4 = count / 4;
     const int64_t blocks =
         std::max<int64_t>(1, std::min<int64_t>((total4 + 255) / 256, (int64_t)di->sm_count * 8));
     KernelTimer timer(MTNN_KCLASS_SPLIT, (hi_copy ? 12.0 : 8.0) * (double)count, s);
     auto x4 = reinterpret_cast<const float4*>(X);
+    // entries are (operand row, k index): for MN-major B^T (k x n) element
+    // p * n + j is operand row j, k index p
+    const int64_t row_len = mn_major ? rows : k;
     if (hi_copy)
       tc::split_tf32_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(
           x4, reinterpret_cast<float4*>(hi), reinterpret_cast<float4*>(lo), total4, nullptr,
-          nullptr, nullptr, 0);
+          nullptr, nullptr, 0, row_len, mn_major, out->fix, FixList{});
     else
       tc::split_tf32_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(
-          x4, nullptr, reinterpret_cast<float4*>(lo), total4, nullptr, nullptr, nullptr, 0);
+          x4, nullptr, reinterpret_cast<float4*>(lo), total4, nullptr, nullptr, nullptr, 0,
+          row_len, mn_major, out->fix, FixList{});
     MTNN_CUDA_TRY(cudaGetLastError());
     out->hi = hi_copy ? static_cast<const void*>(hi) : X;
     out->lo = lo;
     out->inv_scale = nullptr;
     return MTNN_OK;
   }
-  // F16S: [h | l | 1/s (+ partial column maxima)]
+  // F16S: [h | l | 1/s (+ partial column maxima) | residual entries]
   const size_t oh = align256((size_t)count * 2);
   const size_t osc = align256((size_t)rows * 4);
-  MTNN_TRY(ws.alloc(2 * oh + osc + (mn_major ? align256(split_cols_scratch_bytes(rows)) : 0), s));
+  const size_t ocm = mn_major ? align256(split_cols_scratch_bytes(rows)) : 0;
+  MTNN_TRY(ws.alloc(2 * oh + osc + ocm + fix_bytes, s));
   uint8_t* base = static_cast<uint8_t*>(ws.ptr);
   float* inv = reinterpret_cast<float*>(base + 2 * oh);
+  MTNN_TRY(attach(base + 2 * oh + osc + ocm));
   if (!mn_major) {
-    MTNN_TRY(launch_split_rows_f16(X, base, base + oh, inv, rows, k, s));
+    MTNN_TRY(launch_split_rows_f16(X, base, base + oh, inv, rows, k, out->fix, s));
   } else {
     float* cm = reinterpret_cast<float*>(base + 2 * oh + osc);
-    MTNN_TRY(launch_split_cols_f16(X, base, base + oh, inv, cm, k, rows, s));
+    MTNN_TRY(launch_split_cols_f16(X, base, base + oh, inv, cm, k, rows, out->fix, s));
   }
   out->hi = base;
   out->lo = base + oh;
@@ -1464,27 +1491,37 @@ int tc_prepare(const float* X, int64_t rows, int64_t k, bool mn_major, TcKind ki
 
 int tc_prepare_pair(const float* A, int64_t m, const float* B, int64_t n, int64_t k,
                     bool b_mn_major, TcKind kind, int conv, ScratchBuffer& wa, ScratchBuffer& wb,
-                    TcOperand* a, TcOperand* b, cudaStream_t s) {
+                    FixHandle* fa, FixHandle* fb, TcOperand* a, TcOperand* b, cudaStream_t s) {
   if (kind != TcKind::F16S || b_mn_major) {
-    MTNN_TRY(tc_prepare(A, m, k, false, kind, conv == 1, wa, a, s));
-    return tc_prepare(B, n, k, b_mn_major, kind, conv == 2, wb, b, s);
+    MTNN_TRY(tc_prepare(A, m, k, false, kind, conv == 1, wa, fa, a, s));
+    return tc_prepare(B, n, k, b_mn_major, kind, conv == 2, wb, fb, b, s);
   }
-  // F16S, both K-major: [h | l | 1/s] per split operand, [1/s] per in-kernel one
-  auto layout = [&](const float* X, int64_t rows, bool ink, ScratchBuffer& ws, TcOperand* o) {
+  // F16S, both K-major: [h | l | 1/s | entries] per split operand, [1/s | entries] per in-kernel one
+  const bool track = fixup_enabled();
+  auto layout = [&](const float* X, int64_t rows, bool ink, ScratchBuffer& ws, FixHandle* fh,
+                    TcOperand* o) {
     const size_t oh = ink ? 0 : align256((size_t)rows * k * 2);
-    MTNN_TRY(ws.alloc(2 * oh + align256((size_t)rows * 4), s));
+    const size_t osc = align256((size_t)rows * 4);
+    const bool t = track && fh != nullptr;
+    const unsigned cap = t ? fix_capacity(rows * k) : 0;
+    MTNN_TRY(ws.alloc(2 * oh + osc + (t ? fix_entry_bytes(cap) : 0), s));
     uint8_t* base = static_cast<uint8_t*>(ws.ptr);
     o->hi = ink ? static_cast<const void*>(X) : base;
     o->lo = ink ? nullptr : base + oh;
     o->inv_scale = reinterpret_cast<float*>(base + 2 * oh);
+    o->fix = FixList{};
+    if (t) {
+      MTNN_TRY(fix_attach(fh, base + 2 * oh + osc, cap, 0, s));
+      o->fix = fh->list;
+    }
     return MTNN_OK;
   };
-  MTNN_TRY(layout(A, m, conv == 1, wa, a));
-  MTNN_TRY(layout(B, n, conv == 2, wb, b));
+  MTNN_TRY(layout(A, m, conv == 1, wa, fa, a));
+  MTNN_TRY(layout(B, n, conv == 2, wb, fb, b));
   return launch_split_rows_f16_pair(
       A, conv == 1 ? nullptr : const_cast<void*>(a->hi), const_cast<void*>(a->lo),
-      const_cast<float*>(a->inv_scale), m, B, conv == 2 ? nullptr : const_cast<void*>(b->hi),
-      const_cast<void*>(b->lo), const_cast<float*>(b->inv_scale), n, k, s);
+      const_cast<float*>(a->inv_scale), m, a->fix, B, conv == 2 ? nullptr : const_cast<void*>(b->hi),
+      const_cast<void*>(b->lo), const_cast<float*>(b->inv_scale), n, b->fix, k, s);
 }
 
 // Split-K factor: minimise (waves of units) x (k-blocks per unit + per-unit
@@ -1708,6 +1745,43 @@ int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t 
 // into each peer pointer (the same rows of the peers' C). CTA-pair tc3xf16s
 // kernel with the peer stores; shapes it cannot take are computed locally and
 // pushed to the peers by device-to-device copies on the same stream.
+FixRep tc_fix_rep(TcKind kind) {
+  if (kind == TcKind::F16S) return FixRep::F16S;
+  return split_mode_hi_copy() ? FixRep::TF32_RNA : FixRep::TF32_TRUNC;
+}
+
+// Fix-up of one finished GEMM whose operands were prepared whole (fix.h).
+static int tc_fixup(const float* A, const TcOperand& a, const float* B, const TcOperand& b,
+                    float* const* dsts, int ndst, int64_t m, int64_t n, int64_t k, int64_t ldc,
+                    bool b_is_nk, TcKind kind, FixHandle& fa, FixHandle& fb, cudaStream_t s) {
+  if (a.fix.ctr == nullptr && b.fix.ctr == nullptr) return MTNN_OK;
+  FixupArgs f;
+  f.A = A;
+  f.inv_a = a.inv_scale;
+  f.inv_b = b.inv_scale;
+  f.B = B;
+  f.ldb = n;
+  for (int d = 0; d < ndst; ++d) f.C[d] = dsts[d];
+  f.ndst = ndst;
+  f.ldc = ldc;
+  f.m = m;
+  f.n = n;
+  f.k = k;
+  f.b_is_nk = b_is_nk;
+  f.rep = tc_fix_rep(kind);
+  f.fa = a.fix;
+  f.fb = b.fix;
+  MTNN_TRY(launch_fixup(f, s));
+  fa.consumed = fb.consumed = true;  // the fix-up resets their counters
+  return MTNN_OK;
+}
+
+// Row block of a row-sharded NT with the all-gather fused into the epilogue:
+// C_local = A_local x B^T (m_local x n, row stride n) is stored into C_local and
+// into each peer pointer (the same rows of the peers' C). CTA-pair tc3xf16s
+// kernel with the peer stores (the residual fix-up then adds to every copy);
+// shapes it cannot take are computed locally and pushed to the peers by
+// device-to-device copies on the same stream.
 int gemm_nt_allgather(const float* A, const float* B, float* C_local, float* const* peers,
                       int npeers, int64_t m, int64_t n, int64_t k, cudaStream_t s) {
   if (npeers < 0 || npeers > tc::kMaxPeers)
@@ -1718,9 +1792,13 @@ int gemm_nt_allgather(const float* A, const float* B, float* C_local, float* con
   for (int d = 0; d < npeers; ++d) peers_ok = peers_ok && (reinterpret_cast<uintptr_t>(peers[d]) & 15) == 0;
   if (pair_ok && peers_ok) {
     ScratchBuffer wa, wb;
+    FixHandle fa, fb;
     TcOperand a{}, b{};
-    MTNN_TRY(tc_prepare_pair(A, m, B, n, k, false, TcKind::F16S, 0, wa, wb, &a, &b, s));
-    return tc_run_pair(a, b, C_local, m, n, k, n, true, TcKind::F16S, s, peers, npeers);
+    MTNN_TRY(tc_prepare_pair(A, m, B, n, k, false, TcKind::F16S, 0, wa, wb, &fa, &fb, &a, &b, s));
+    MTNN_TRY(tc_run_pair(a, b, C_local, m, n, k, n, true, TcKind::F16S, s, peers, npeers));
+    float* dsts[8] = {C_local};
+    for (int d = 0; d < npeers; ++d) dsts[1 + d] = peers[d];
+    return tc_fixup(A, a, B, b, dsts, 1 + npeers, m, n, k, n, true, TcKind::F16S, fa, fb, s);
   }
   MTNN_TRY(gemm_dispatch_nt(A, B, C_local, m, n, k, s));
   for (int d = 0; d < npeers; ++d)
@@ -1736,20 +1814,25 @@ int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t 
     return fail(MTNN_ENOTSUP, "%s: shape/alignment not eligible (m=%lld n=%lld k=%lld)", name,
                 (long long)m, (long long)n, (long long)k);
   ScratchBuffer wa, wb, wc;
+  FixHandle fa, fb;
   TcOperand a{}, b{};
   const int conv = tc_inkernel_operand(m, n, b_is_nk, kind);
-  MTNN_TRY(tc_prepare_pair(A, m, B, n, k, !b_is_nk, kind, conv, wa, wb, &a, &b, s));
-  if (tc_eligible(A, B, C, m, n, k, b_is_nk, kind)) return tc_run(a, b, C, m, n, k, b_is_nk, kind, s);
-  // C cannot be a TMA store target (n % 4 != 0, e.g. a 10-class output layer, or
-  // an unaligned base): compute into a row-padded buffer and copy the n columns
-  // out (B's missing rows are TMA zero fill, so the padding columns are zeros)
-  const int64_t np = (n + 3) / 4 * 4;
-  MTNN_TRY(wc.alloc((size_t)(m * np) * sizeof(float), s));
-  float* cp = static_cast<float*>(wc.ptr);
-  MTNN_TRY(tc_run(a, b, cp, m, n, k, b_is_nk, kind, s, np));
-  MTNN_CUDA_TRY(cudaMemcpy2DAsync(C, (size_t)n * 4, cp, (size_t)np * 4, (size_t)n * 4, (size_t)m,
-                                  cudaMemcpyDeviceToDevice, s));
-  return MTNN_OK;
+  MTNN_TRY(tc_prepare_pair(A, m, B, n, k, !b_is_nk, kind, conv, wa, wb, &fa, &fb, &a, &b, s));
+  if (tc_eligible(A, B, C, m, n, k, b_is_nk, kind)) {
+    MTNN_TRY(tc_run(a, b, C, m, n, k, b_is_nk, kind, s));
+  } else {
+    // C cannot be a TMA store target (n % 4 != 0, e.g. a 10-class output layer, or
+    // an unaligned base): compute into a row-padded buffer and copy the n columns
+    // out (B's missing rows are TMA zero fill, so the padding columns are zeros)
+    const int64_t np = (n + 3) / 4 * 4;
+    MTNN_TRY(wc.alloc((size_t)(m * np) * sizeof(float), s));
+    float* cp = static_cast<float*>(wc.ptr);
+    MTNN_TRY(tc_run(a, b, cp, m, n, k, b_is_nk, kind, s, np));
+    MTNN_CUDA_TRY(cudaMemcpy2DAsync(C, (size_t)n * 4, cp, (size_t)np * 4, (size_t)n * 4, (size_t)m,
+                                    cudaMemcpyDeviceToDevice, s));
+  }
+  float* dsts[1] = {C};
+  return tc_fixup(A, a, B, b, dsts, 1, m, n, k, n, b_is_nk, kind, fa, fb, s);
 }
 
 }  // namespace mtnn

@@ -351,20 +351,26 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
   float* dbp = static_cast<float*>(db.ptr);
   float* dcp = static_cast<float*>(dc.ptr);
   // split operands: [h | l | 1/s] (A always; B unless conv == 2: 1/s only)
+  // one residual list per operand (fix.h), entries tagged with global rows
+  FixHandle fha, fhb;
+  const bool track = fixup_enabled();
   auto carve = [&](ScratchBuffer& w, int64_t rows, bool halves, __half_raw** h, __half_raw** l,
-                   float** inv) {
+                   float** inv, FixHandle* fh) {
     const size_t oh = halves ? (((size_t)(rows * k) * 2 + 255) & ~size_t(255)) : 0;
-    MTNN_TRY(w.alloc(2 * oh + (size_t)rows * 4 + 256, ps->in));
+    const size_t osc = (((size_t)rows * 4) + 255) & ~size_t(255);
+    const unsigned cap = track ? fix_capacity(rows * k) : 0;
+    MTNN_TRY(w.alloc(2 * oh + osc + (track ? fix_entry_bytes(cap) : 0), ps->in));
     uint8_t* base = static_cast<uint8_t*>(w.ptr);
     *h = halves ? reinterpret_cast<__half_raw*>(base) : nullptr;
     *l = halves ? reinterpret_cast<__half_raw*>(base + oh) : nullptr;
     *inv = reinterpret_cast<float*>(base + 2 * oh);
+    if (track) MTNN_TRY(fix_attach(fh, base + 2 * oh + osc, cap, 0, ps->comp));
     return MTNN_OK;
   };
   __half_raw *ah, *al, *bh, *bl;
   float *ainv, *binv;
-  MTNN_TRY(carve(wa, m, true, &ah, &al, &ainv));
-  MTNN_TRY(carve(wb, n, conv != 2, &bh, &bl, &binv));
+  MTNN_TRY(carve(wa, m, true, &ah, &al, &ainv, &fha));
+  MTNN_TRY(carve(wb, n, conv != 2, &bh, &bl, &binv, &fhb));
   auto a_rows = [&](int64_t i0) {
     TcOperand o{};
     o.hi = ah + i0 * k;
@@ -397,9 +403,38 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
     MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->comp, e, 0));
     const TcOperand o = is_a ? a_rows(r0) : b_rows(r0);
     const bool halves = is_a || conv != 2;
+    FixList fl = (is_a ? fha : fhb).list;  // this block's rows start at global row r0
+    fl.row0 = (int32_t)r0;
     return launch_split_rows_f16_pair(dst, halves ? const_cast<void*>(o.hi) : nullptr,
                                       const_cast<void*>(o.lo), const_cast<float*>(o.inv_scale),
-                                      rows, nullptr, nullptr, nullptr, nullptr, 0, k, ps->comp);
+                                      rows, fl, nullptr, nullptr, nullptr, nullptr, 0, FixList{},
+                                      k, ps->comp);
+  };
+  // residual fix-up of C rows i0.. (mi) x B rows j0.. (nj), rows of ldc; the
+  // last one resets both lists
+  int64_t fixups_left = (QA > 1 ? QA - 1 : 0) + QB;
+  auto fixup = [&](int64_t i0, int64_t mi, int64_t j0, int64_t nj, float* cblk, int64_t ldc) {
+    if (!track) return MTNN_OK;
+    FixupArgs f;
+    f.A = dap + i0 * k;
+    f.inv_a = ainv + i0;
+    f.inv_b = binv + j0;
+    f.B = dbp + j0 * k;
+    f.C[0] = cblk;
+    f.ldc = ldc;
+    f.m = mi;
+    f.n = nj;
+    f.k = k;
+    f.b_is_nk = true;
+    f.rep = FixRep::F16S;
+    f.fa = fha.list;
+    f.fb = fhb.list;
+    f.a_row0 = (int32_t)i0;
+    f.b_row0 = (int32_t)j0;
+    f.reset_a = f.reset_b = (--fixups_left == 0);
+    MTNN_TRY(launch_fixup(f, ps->comp));
+    if (f.reset_a) fha.consumed = fhb.consumed = true;
+    return MTNN_OK;
   };
   // multiply C block (i, j) and send it out
   auto block = [&](int64_t i, int64_t j) {
@@ -407,6 +442,7 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
     const int64_t mi = std::min(mb, m - i0), nj = std::min(nb, n - j0);
     float* cij = dcp + i0 * n + mi * j0;  // rows i0.. of C, block j: mi x nj contiguous
     MTNN_TRY(tc_run(a_rows(i0), b_rows(j0), cij, mi, nj, k, true, TcKind::F16S, ps->comp));
+    MTNN_TRY(fixup(i0, mi, j0, nj, cij, nj));
     cudaEvent_t e;
     MTNN_TRY(evs.make(&e));
     MTNN_CUDA_TRY(cudaEventRecord(e, ps->comp));
@@ -425,6 +461,7 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
     const int64_t i0 = i * mb, mi = std::min(mb, m - i0);
     float* ci = dcp + i0 * n;
     MTNN_TRY(tc_run(a_rows(i0), b_rows(0), ci, mi, n, k, true, TcKind::F16S, ps->comp));
+    MTNN_TRY(fixup(i0, mi, 0, n, ci, n));
     MTNN_TRY(evs.make(&ev));
     MTNN_CUDA_TRY(cudaEventRecord(ev, ps->comp));
     MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->out, ev, 0));
@@ -524,9 +561,10 @@ static int host_gemm(const float* A, const float* B, float* C, int64_t m, int64_
     return fail(MTNN_ENOTSUP, "tensor-core variant not eligible for (%lld, %lld, %lld)",
                 (long long)m, (long long)n, (long long)k);
   TcOperand bp{};
+  FixHandle fhb;  // B's residual list serves every chunk; the last one resets it
   // in-kernel split choice for the whole problem (chunks keep its operand roles)
   const int conv = tc ? tc_inkernel_operand(m, n, b_is_nk, kind) : 0;
-  if (tc) MTNN_TRY(tc_prepare(bop, n, k, !b_is_nk, kind, conv == 2, wb, &bp, ps->comp));
+  if (tc) MTNN_TRY(tc_prepare(bop, n, k, !b_is_nk, kind, conv == 2, wb, &fhb, &bp, ps->comp));
 
   // row chunks: 2..8 chunks of >= 16 MiB of A+C, multiples of 128 rows
   const double row_bytes = 4.0 * ((double)k + (double)n);
@@ -547,9 +585,32 @@ static int host_gemm(const float* A, const float* B, float* C, int64_t m, int64_
     MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->comp, ev_in, 0));
     if (tc) {
       ScratchBuffer wa;
+      FixHandle fha;
       TcOperand ap{};
-      MTNN_TRY(tc_prepare(a_c, mr, k, false, kind, conv == 1, wa, &ap, ps->comp));
+      MTNN_TRY(tc_prepare(a_c, mr, k, false, kind, conv == 1, wa, &fha, &ap, ps->comp));
       MTNN_TRY(tc_run(ap, bp, c_c, mr, n, k, b_is_nk, kind, ps->comp));
+      if (ap.fix.ctr != nullptr || bp.fix.ctr != nullptr) {
+        FixupArgs f;
+        f.A = a_c;
+        f.inv_a = ap.inv_scale;
+        f.inv_b = bp.inv_scale;
+        f.B = bop;
+        f.ldb = n;
+        f.C[0] = c_c;
+        f.ldc = n;
+        f.m = mr;
+        f.n = n;
+        f.k = k;
+        f.b_is_nk = b_is_nk;
+        f.rep = tc_fix_rep(kind);
+        f.fa = ap.fix;
+        f.fb = bp.fix;
+        f.reset_a = true;
+        f.reset_b = c == chunks - 1;
+        MTNN_TRY(launch_fixup(f, ps->comp));
+        fha.consumed = true;
+        if (f.reset_b) fhb.consumed = true;
+      }
     } else {
       MTNN_TRY(gemm_dispatch(a_c, bop, c_c, mr, n, k, v, b_is_nk, ps->comp));
     }
@@ -644,6 +705,11 @@ int mtnn_config_set(const char* key, int64_t value) {
     g_pipe_blocked.store((int)value, std::memory_order_relaxed);
     return MTNN_OK;
   }
+  if (strcmp(key, "fixup") == 0) {
+    if (value != 0 && value != 1) return fail(MTNN_EINVAL, "fixup must be 0 or 1");
+    set_fixup_enabled(value != 0);
+    return MTNN_OK;
+  }
   return fail(MTNN_EINVAL, "unknown config key '%s'", key);
 }
 
@@ -659,6 +725,10 @@ int mtnn_config_get(const char* key, int64_t* value) {
   }
   if (strcmp(key, "host_pipeline_blocked") == 0) {
     *value = blocked_pipeline_enabled() ? 1 : 0;
+    return MTNN_OK;
+  }
+  if (strcmp(key, "fixup") == 0) {
+    *value = fixup_enabled() ? 1 : 0;
     return MTNN_OK;
   }
   return fail(MTNN_EINVAL, "unknown config key '%s'", key);

@@ -28,6 +28,7 @@
 #include <algorithm>
 
 #include "common.h"
+#include "fix.h"
 #include "pdl.h"
 
 namespace mtnn {
@@ -58,12 +59,6 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 
 
 
-__device__ __forceinline__ void split2(float v, float s, __half& h, __half& l) {
-  const float xs = v * s;
-  h = __float2half_rn(xs);
-  l = __float2half_rn(xs - __half2float(h));
-}
-
 constexpr int kUnroll = 4;  // independent 16-byte loads per lane in flight
 
 __device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
@@ -73,16 +68,47 @@ __device__ __forceinline__ float absmax4(const float4& v) {
   return fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
 }
 
-__device__ __forceinline__ void split4(const float4& v, float s, uint2& hw, uint2& lw) {
+// split4 with residual tracking (fix.h): elements whose halves miss them by
+// more than 2^-19 are listed for the fix-up; col0 = k index of v.x.
+__device__ __forceinline__ void split4c(const float4& v, float s, float inv_s, uint2& hw,
+                                        uint2& lw, const FixList& fl, int64_t row, int64_t col0) {
   __half h0, h1, h2, h3, l0, l1, l2, l3;
-  split2(v.x, s, h0, l0);
-  split2(v.y, s, h1, l1);
-  split2(v.z, s, h2, l2);
-  split2(v.w, s, h3, l3);
+  f16s_split_checked(v.x, s, inv_s, h0, l0, fl, row, col0);
+  f16s_split_checked(v.y, s, inv_s, h1, l1, fl, row, col0 + 1);
+  f16s_split_checked(v.z, s, inv_s, h2, l2, fl, row, col0 + 2);
+  f16s_split_checked(v.w, s, inv_s, h3, l3, fl, row, col0 + 3);
   __half2 hp0 = __halves2half2(h0, h1), hp1 = __halves2half2(h2, h3);
   __half2 lp0 = __halves2half2(l0, l1), lp1 = __halves2half2(l2, l3);
   hw = make_uint2(*reinterpret_cast<uint32_t*>(&hp0), *reinterpret_cast<uint32_t*>(&hp1));
   lw = make_uint2(*reinterpret_cast<uint32_t*>(&lp0), *reinterpret_cast<uint32_t*>(&lp1));
+}
+// Residual check only (operands the GEMM splits in-kernel from raw rows: the
+// halves it builds are bit-identical to these).
+__device__ __forceinline__ void check4(const float4& v, float s, float inv_s, const FixList& fl,
+                                       int64_t row, int64_t col0) {
+  uint2 hw, lw;
+  split4c(v, s, inv_s, hw, lw, fl, row, col0);
+}
+__device__ __forceinline__ void split_col4(const float4& v, const float4& sc, const float4& inv,
+                                           uint2& hw, uint2& lw, const FixList& fl, int64_t col,
+                                           int64_t krow) {
+  __half h0, h1, h2, h3, l0, l1, l2, l3;
+  f16s_split_checked(v.x, sc.x, inv.x, h0, l0, fl, col, krow);
+  f16s_split_checked(v.y, sc.y, inv.y, h1, l1, fl, col + 1, krow);
+  f16s_split_checked(v.z, sc.z, inv.z, h2, l2, fl, col + 2, krow);
+  f16s_split_checked(v.w, sc.w, inv.w, h3, l3, fl, col + 3, krow);
+  __half2 hp0 = __halves2half2(h0, h1), hp1 = __halves2half2(h2, h3);
+  __half2 lp0 = __halves2half2(l0, l1), lp1 = __halves2half2(l2, l3);
+  hw = make_uint2(*reinterpret_cast<uint32_t*>(&hp0), *reinterpret_cast<uint32_t*>(&hp1));
+  lw = make_uint2(*reinterpret_cast<uint32_t*>(&lp0), *reinterpret_cast<uint32_t*>(&lp1));
+}
+// 1/s for the residual check, 0 (= untracked, fix.h) for a row or column whose
+// max is Inf/NaN: its output is non-finite anyway and its scale (1) says
+// nothing about the other entries' range.
+__device__ __forceinline__ float track_inv(float mx, float inv) { return mx <= 3.402823466e38f ? inv : 0.f; }
+__device__ __forceinline__ float4 track_inv4(const float4& m, const float4& sc) {
+  return make_float4(track_inv(m.x, 1.f / sc.x), track_inv(m.y, 1.f / sc.y),
+                     track_inv(m.z, 1.f / sc.z), track_inv(m.w, 1.f / sc.w));
 }
 
 // A launch serves up to two K-major operands (A and B of one GEMM, same k):
@@ -94,13 +120,24 @@ struct RowJob {
   __half* lo;
   float* inv_scale;
   int64_t rows;
+  FixList fix;  // residual list (fix.h); ctr == nullptr: none
 };
 
-__device__ __forceinline__ const RowJob& pick(const RowJob& j0, const RowJob& j1, int64_t v,
-                                              int64_t& r) {
-  if (v < j0.rows) { r = v; return j0; }
-  r = v - j0.rows;
-  return j1;
+__device__ __forceinline__ RowJob pick(const RowJob& j0, const RowJob& j1, int64_t v, int64_t& r) {
+  // field-wise select (a reference to either parameter would force both into local memory)
+  const bool first = v < j0.rows;
+  r = first ? v : v - j0.rows;
+  RowJob j;
+  j.x = first ? j0.x : j1.x;
+  j.hi = first ? j0.hi : j1.hi;
+  j.lo = first ? j0.lo : j1.lo;
+  j.inv_scale = first ? j0.inv_scale : j1.inv_scale;
+  j.rows = first ? j0.rows : j1.rows;
+  j.fix.ctr = first ? j0.fix.ctr : j1.fix.ctr;
+  j.fix.e = first ? j0.fix.e : j1.fix.e;
+  j.fix.cap = first ? j0.fix.cap : j1.fix.cap;
+  j.fix.row0 = first ? j0.fix.row0 : j1.fix.row0;
+  return j;
 }
 
 // One warp per row: max, then (split jobs) split. Both passes keep kUnroll
@@ -117,7 +154,7 @@ split_rows_f16_kernel(const RowJob j0, const RowJob j1, int64_t k) {
   constexpr int kStep = 32 * kUnroll;
   for (int64_t v = warp; v < j0.rows + j1.rows; v += nwarps) {
     int64_t r;
-    const RowJob& j = pick(j0, j1, v, r);
+    const RowJob j = pick(j0, j1, v, r);
     const float4* row = reinterpret_cast<const float4*>(j.x + r * k);
     float mx = 0.f;
     int64_t i = lane;
@@ -132,8 +169,14 @@ split_rows_f16_kernel(const RowJob j0, const RowJob j1, int64_t k) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     const float s = pow2_scale(mx);
-    if (lane == 0) j.inv_scale[r] = 1.f / s;
-    if (j.hi == nullptr) continue;  // row scales only
+    const float inv = 1.f / s;
+    const float tinv = track_inv(mx, inv);
+    if (lane == 0) j.inv_scale[r] = inv;
+    if (j.hi == nullptr) {  // row scales only (+ the residual check, from L1/L2)
+      if (j.fix.ctr != nullptr)
+        for (i = lane; i < k4; i += 32) check4(ldg4(row + i), s, tinv, j.fix, r, 4 * i);
+      continue;
+    }
     uint2* hrow = reinterpret_cast<uint2*>(j.hi + r * k);
     uint2* lrow = reinterpret_cast<uint2*>(j.lo + r * k);
     i = lane;
@@ -144,14 +187,14 @@ split_rows_f16_kernel(const RowJob j0, const RowJob j1, int64_t k) {
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         uint2 hw, lw;
-        split4(x[u], s, hw, lw);
+        split4c(x[u], s, tinv, hw, lw, j.fix, r, 4 * (i + 32 * u));
         hrow[i + 32 * u] = hw;
         lrow[i + 32 * u] = lw;
       }
     }
     for (; i < k4; i += 32) {
       uint2 hw, lw;
-      split4(ldg4(row + i), s, hw, lw);
+      split4c(ldg4(row + i), s, tinv, hw, lw, j.fix, r, 4 * i);
       hrow[i] = hw;
       lrow[i] = lw;
     }
@@ -173,7 +216,7 @@ split_rows_f16_reg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
   const int64_t k4 = k / 4;
   for (int64_t v = warp; v < j0.rows + j1.rows; v += nwarps) {
     int64_t r;
-    const RowJob& j = pick(j0, j1, v, r);
+    const RowJob j = pick(j0, j1, v, r);
     const float4* row = reinterpret_cast<const float4*>(j.x + r * k);
     float4 x[kR];
 #pragma unroll
@@ -187,8 +230,19 @@ split_rows_f16_reg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     const float s = pow2_scale(mx);
-    if (lane == 0) j.inv_scale[r] = 1.f / s;
-    if (j.hi == nullptr) continue;  // row scales only
+    const float inv = 1.f / s;
+    const float tinv = track_inv(mx, inv);
+    if (lane == 0) j.inv_scale[r] = inv;
+    if (j.hi == nullptr) {  // row scales only (+ the residual check)
+      if (j.fix.ctr != nullptr) {
+#pragma unroll
+        for (int u = 0; u < kR; ++u) {
+          const int64_t i = lane + 32 * u;
+          if (i < k4) check4(x[u], s, tinv, j.fix, r, 4 * i);
+        }
+      }
+      continue;
+    }
     uint2* hrow = reinterpret_cast<uint2*>(j.hi + r * k);
     uint2* lrow = reinterpret_cast<uint2*>(j.lo + r * k);
 #pragma unroll
@@ -196,7 +250,7 @@ split_rows_f16_reg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
       const int64_t i = lane + 32 * u;
       if (i < k4) {
         uint2 hw, lw;
-        split4(x[u], s, hw, lw);
+        split4c(x[u], s, tinv, hw, lw, j.fix, r, 4 * i);
         hrow[i] = hw;
         lrow[i] = lw;
       }
@@ -223,8 +277,8 @@ split_rows_f16_smem_kernel(const RowJob j0, const RowJob j1, int64_t k) {
   const int t = threadIdx.x;
   for (int64_t v = blockIdx.x; v < j0.rows + j1.rows; v += gridDim.x) {
     int64_t r;
-    const RowJob& j = pick(j0, j1, v, r);
-    const bool stage = j.hi != nullptr;
+    const RowJob j = pick(j0, j1, v, r);
+    const bool stage = j.hi != nullptr || j.fix.ctr != nullptr;
     const float4* row = reinterpret_cast<const float4*>(j.x + r * k);
     float mx = 0.f;
     int64_t i = t;
@@ -255,16 +309,20 @@ split_rows_f16_smem_kernel(const RowJob j0, const RowJob j1, int64_t k) {
     }
     __syncthreads();
     const float s = pow2_scale(red[0]);
-    if (t == 0) j.inv_scale[r] = 1.f / s;
-    if (stage) {
+    const float inv = 1.f / s;
+    const float tinv = track_inv(red[0], inv);
+    if (t == 0) j.inv_scale[r] = inv;
+    if (stage && j.hi != nullptr) {
       uint2* hrow = reinterpret_cast<uint2*>(j.hi + r * k);
       uint2* lrow = reinterpret_cast<uint2*>(j.lo + r * k);
       for (int64_t q = t; q < k4; q += kRowThreads) {
         uint2 hw, lw;
-        split4(row_s[q], s, hw, lw);
+        split4c(row_s[q], s, tinv, hw, lw, j.fix, r, 4 * q);
         hrow[q] = hw;
         lrow[q] = lw;
       }
+    } else if (stage) {
+      for (int64_t q = t; q < k4; q += kRowThreads) check4(row_s[q], s, tinv, j.fix, r, 4 * q);
     }
     __syncthreads();  // row_s and red are reused by the next row
   }
@@ -289,7 +347,7 @@ split_rows_f16_ctareg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
   int parity = 0;
   for (int64_t v = blockIdx.x; v < j0.rows + j1.rows; v += gridDim.x, parity ^= 1) {
     int64_t r;
-    const RowJob& j = pick(j0, j1, v, r);
+    const RowJob j = pick(j0, j1, v, r);
     const float4* row = reinterpret_cast<const float4*>(j.x + r * k);
     float4 x[kV];
 #pragma unroll
@@ -307,8 +365,19 @@ split_rows_f16_ctareg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
 #pragma unroll
     for (int w = 0; w < kCtaRowThreads / 32; ++w) mx = fmaxf(mx, red[parity][w]);
     const float s = pow2_scale(mx);
-    if (t == 0) j.inv_scale[r] = 1.f / s;
-    if (j.hi == nullptr) continue;  // row scales only
+    const float inv = 1.f / s;
+    const float tinv = track_inv(mx, inv);
+    if (t == 0) j.inv_scale[r] = inv;
+    if (j.hi == nullptr) {  // row scales only (+ the residual check)
+      if (j.fix.ctr != nullptr) {
+#pragma unroll
+        for (int u = 0; u < kV; ++u) {
+          const int64_t i = t + kCtaRowThreads * u;
+          if (i < k4) check4(x[u], s, tinv, j.fix, r, 4 * i);
+        }
+      }
+      continue;
+    }
     uint2* hrow = reinterpret_cast<uint2*>(j.hi + r * k);
     uint2* lrow = reinterpret_cast<uint2*>(j.lo + r * k);
 #pragma unroll
@@ -316,7 +385,7 @@ split_rows_f16_ctareg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
       const int64_t i = t + kCtaRowThreads * u;
       if (i < k4) {
         uint2 hw, lw;
-        split4(x[u], s, hw, lw);
+        split4c(x[u], s, tinv, hw, lw, j.fix, r, 4 * i);
         hrow[i] = hw;
         lrow[i] = lw;
       }
@@ -398,7 +467,7 @@ __global__ void __launch_bounds__(256)
 split_cols_band_kernel(const float* __restrict__ x, const float* __restrict__ partial, int chunks,
                        __half* __restrict__ hi, __half* __restrict__ lo,
                        float* __restrict__ inv_scale, int64_t k, int64_t n,
-                       int64_t rows_per_band) {
+                       int64_t rows_per_band, const FixList fl) {
   pdl_trigger();
   pdl_wait();
   constexpr int kBandCols = 4 * kLanes, kBandRowLanes = 256 / kLanes;
@@ -412,6 +481,7 @@ split_cols_band_kernel(const float* __restrict__ x, const float* __restrict__ pa
     m.x = fmaxf(m.x, o.x); m.y = fmaxf(m.y, o.y); m.z = fmaxf(m.z, o.z); m.w = fmaxf(m.w, o.w);
   }
   const float4 sc = make_float4(pow2_scale(m.x), pow2_scale(m.y), pow2_scale(m.z), pow2_scale(m.w));
+  const float4 inv = track_inv4(m, sc);
   if (blockIdx.y == 0 && rl == 0)
     *reinterpret_cast<float4*>(inv_scale + col) =
         make_float4(1.f / sc.x, 1.f / sc.y, 1.f / sc.z, 1.f / sc.w);
@@ -421,17 +491,10 @@ split_cols_band_kernel(const float* __restrict__ x, const float* __restrict__ pa
   for (int64_t r = r0 + rl; r < r1; r += kBandRowLanes) {
     const int64_t i = r * n + col;
     const float4 v = ldg4(reinterpret_cast<const float4*>(x + i));
-    __half h0, h1, h2, h3, l0, l1, l2, l3;
-    split2(v.x, sc.x, h0, l0);
-    split2(v.y, sc.y, h1, l1);
-    split2(v.z, sc.z, h2, l2);
-    split2(v.w, sc.w, h3, l3);
-    __half2 hp0 = __halves2half2(h0, h1), hp1 = __halves2half2(h2, h3);
-    __half2 lp0 = __halves2half2(l0, l1), lp1 = __halves2half2(l2, l3);
-    reinterpret_cast<uint2*>(hi)[i / 4] =
-        make_uint2(*reinterpret_cast<uint32_t*>(&hp0), *reinterpret_cast<uint32_t*>(&hp1));
-    reinterpret_cast<uint2*>(lo)[i / 4] =
-        make_uint2(*reinterpret_cast<uint32_t*>(&lp0), *reinterpret_cast<uint32_t*>(&lp1));
+    uint2 hw, lw;
+    split_col4(v, sc, inv, hw, lw, fl, col, r);
+    reinterpret_cast<uint2*>(hi)[i / 4] = hw;
+    reinterpret_cast<uint2*>(lo)[i / 4] = lw;
   }
 }
 
@@ -447,11 +510,12 @@ constexpr int kStripLanes = 64;
 __global__ void __launch_bounds__(8 * kStripLanes)
 split_cols_strip_kernel(const float* __restrict__ x, __half* __restrict__ hi,
                         __half* __restrict__ lo, float* __restrict__ inv_scale, int64_t k,
-                        int64_t n) {
+                        int64_t n, const FixList fl) {
   pdl_trigger();
   pdl_wait();
   __shared__ float4 red[kStripLanes][8];
   __shared__ float4 scale[8];
+  __shared__ float4 tinv_s[8];
   const int c4 = threadIdx.x % 8;
   const int rl = threadIdx.x / 8;
   const int64_t col = (int64_t)blockIdx.x * kStripCols + 4 * c4;
@@ -477,6 +541,7 @@ split_cols_strip_kernel(const float* __restrict__ x, __half* __restrict__ hi,
     }
     const float4 sc = make_float4(pow2_scale(m.x), pow2_scale(m.y), pow2_scale(m.z), pow2_scale(m.w));
     scale[threadIdx.x] = sc;
+    tinv_s[threadIdx.x] = track_inv4(m, sc);
     const int64_t c = (int64_t)blockIdx.x * kStripCols + 4 * threadIdx.x;
     if (c < n)
       *reinterpret_cast<float4*>(inv_scale + c) =
@@ -485,21 +550,15 @@ split_cols_strip_kernel(const float* __restrict__ x, __half* __restrict__ hi,
   __syncthreads();
   if (!active) return;
   const float4 sc = scale[c4];
+  const float4 inv = tinv_s[c4];
 #pragma unroll 4
   for (int64_t r = rl; r < k; r += kStripLanes) {
     const int64_t i = r * n + col;
-    const float4 v = __ldg(reinterpret_cast<const float4*>(x + i));
-    __half h0, h1, h2, h3, l0, l1, l2, l3;
-    split2(v.x, sc.x, h0, l0);
-    split2(v.y, sc.y, h1, l1);
-    split2(v.z, sc.z, h2, l2);
-    split2(v.w, sc.w, h3, l3);
-    __half2 hp0 = __halves2half2(h0, h1), hp1 = __halves2half2(h2, h3);
-    __half2 lp0 = __halves2half2(l0, l1), lp1 = __halves2half2(l2, l3);
-    reinterpret_cast<uint2*>(hi)[i / 4] =
-        make_uint2(*reinterpret_cast<uint32_t*>(&hp0), *reinterpret_cast<uint32_t*>(&hp1));
-    reinterpret_cast<uint2*>(lo)[i / 4] =
-        make_uint2(*reinterpret_cast<uint32_t*>(&lp0), *reinterpret_cast<uint32_t*>(&lp1));
+    const float4 v = ldg4(reinterpret_cast<const float4*>(x + i));
+    uint2 hw, lw;
+    split_col4(v, sc, inv, hw, lw, fl, col, r);
+    reinterpret_cast<uint2*>(hi)[i / 4] = hw;
+    reinterpret_cast<uint2*>(lo)[i / 4] = lw;
   }
 }
 
@@ -546,12 +605,13 @@ template <int kR>
 __global__ void __launch_bounds__(8 * kClusterRowLanes)
 split_cols_cluster_kernel(const float* __restrict__ x, __half* __restrict__ hi,
                           __half* __restrict__ lo, float* __restrict__ inv_scale, int64_t k,
-                          int64_t n) {
+                          int64_t n, const FixList fl) {
   pdl_trigger();
   pdl_wait();
   __shared__ float4 red[kClusterRowLanes][8];
   __shared__ float4 part[8];
   __shared__ float4 scale[8];
+  __shared__ float4 tinv_s[8];
   const uint32_t csize = cl_size(), rank = cl_rank();
   const int c4 = threadIdx.x % 8;
   const int rl = threadIdx.x / 8;
@@ -592,6 +652,7 @@ split_cols_cluster_kernel(const float* __restrict__ x, __half* __restrict__ hi,
     }
     const float4 sc = make_float4(pow2_scale(m.x), pow2_scale(m.y), pow2_scale(m.z), pow2_scale(m.w));
     scale[threadIdx.x] = sc;
+    tinv_s[threadIdx.x] = track_inv4(m, sc);
     const int64_t c = strip * kStripCols + 4 * threadIdx.x;
     if (rank == 0 && c < n)
       *reinterpret_cast<float4*>(inv_scale + c) =
@@ -600,30 +661,23 @@ split_cols_cluster_kernel(const float* __restrict__ x, __half* __restrict__ hi,
   cl_sync();  // peers are done reading `part` (no CTA exits under a reader); scale is visible
   if (!active) return;
   const float4 sc = scale[c4];
+  const float4 inv = tinv_s[c4];
 #pragma unroll
   for (int u = 0; u < kR; ++u) {
     const int64_t r = r0 + kClusterRowLanes * u;
     if (r < k) {
-      const float4 w = v[u];
-      __half h0, h1, h2, h3, l0, l1, l2, l3;
-      split2(w.x, sc.x, h0, l0);
-      split2(w.y, sc.y, h1, l1);
-      split2(w.z, sc.z, h2, l2);
-      split2(w.w, sc.w, h3, l3);
-      __half2 hp0 = __halves2half2(h0, h1), hp1 = __halves2half2(h2, h3);
-      __half2 lp0 = __halves2half2(l0, l1), lp1 = __halves2half2(l2, l3);
+      uint2 hw, lw;
+      split_col4(v[u], sc, inv, hw, lw, fl, col, r);
       const int64_t i = (r * n + col) / 4;
-      reinterpret_cast<uint2*>(hi)[i] =
-          make_uint2(*reinterpret_cast<uint32_t*>(&hp0), *reinterpret_cast<uint32_t*>(&hp1));
-      reinterpret_cast<uint2*>(lo)[i] =
-          make_uint2(*reinterpret_cast<uint32_t*>(&lp0), *reinterpret_cast<uint32_t*>(&lp1));
+      reinterpret_cast<uint2*>(hi)[i] = hw;
+      reinterpret_cast<uint2*>(lo)[i] = lw;
     }
   }
 }
 
 template <int kR>
 int launch_cols_cluster(const float* x, void* hi, void* lo, float* inv_scale, int64_t k,
-                        int64_t n, cudaStream_t s) {
+                        int64_t n, const FixList& fl, cudaStream_t s) {
   const int64_t strips = (n + kStripCols - 1) / kStripCols;
   const unsigned c = (unsigned)((k + kClusterRowLanes * kR - 1) / (kClusterRowLanes * kR));
   cudaLaunchConfig_t cfg = {};
@@ -642,7 +696,7 @@ int launch_cols_cluster(const float* x, void* hi, void* lo, float* inv_scale, in
   cfg.numAttrs = chain_enabled() ? 2 : 1;
   MTNN_CUDA_TRY(cudaLaunchKernelEx(&cfg, split_cols_cluster_kernel<kR>, x,
                                    static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale,
-                                   k, n));
+                                   k, n, fl));
   return MTNN_OK;
 }
 
@@ -651,21 +705,22 @@ int launch_cols_cluster(const float* x, void* hi, void* lo, float* inv_scale, in
 // Splits (hi != nullptr) or row-scales (hi == nullptr) the rows of up to two
 // K-major operands sharing k, in one launch.
 int launch_split_rows_f16_pair(const float* x0, void* hi0, void* lo0, float* inv0, int64_t rows0,
-                               const float* x1, void* hi1, void* lo1, float* inv1, int64_t rows1,
-                               int64_t k, cudaStream_t s) {
+                               const FixList& fix0, const float* x1, void* hi1, void* lo1,
+                               float* inv1, int64_t rows1, const FixList& fix1, int64_t k,
+                               cudaStream_t s) {
   if (rows0 < 0) rows0 = 0;
   if (rows1 < 0) rows1 = 0;
   if (rows0 + rows1 == 0) return MTNN_OK;
   const DeviceInfo* di = nullptr;
   MTNN_TRY(device_info(&di));
-  const RowJob j0{x0, static_cast<__half*>(hi0), static_cast<__half*>(lo0), inv0, rows0};
-  const RowJob j1{x1, static_cast<__half*>(hi1), static_cast<__half*>(lo1), inv1, rows1};
+  const RowJob j0{x0, static_cast<__half*>(hi0), static_cast<__half*>(lo0), inv0, rows0, fix0};
+  const RowJob j1{x1, static_cast<__half*>(hi1), static_cast<__half*>(lo1), inv1, rows1, fix1};
   const int64_t rows = rows0 + rows1;
   KernelTimer timer(MTNN_KCLASS_SPLIT,
                     ((hi0 ? 8.0 : 4.0) * (double)rows0 + (hi1 ? 8.0 : 4.0) * (double)rows1) * (double)k,
                     s);
   const size_t row_bytes = (size_t)k * sizeof(float);
-  const bool any_split = (hi0 && rows0) || (hi1 && rows1);
+  const bool any_split = ((hi0 || fix0.ctr) && rows0) || ((hi1 || fix1.ctr) && rows1);
   if (k > kWarpRowMax && k <= 16384 && ctareg_enabled()) {
     // measured (16384 x 8192 rows of 8192): 384 -> 280 us; 4096^2 x 4096: 101 -> 51 us
     if (k <= 4096)
@@ -702,21 +757,22 @@ int launch_split_rows_f16_pair(const float* x0, void* hi0, void* lo0, float* inv
 }
 
 int launch_split_rows_f16(const float* x, void* hi, void* lo, float* inv_scale, int64_t rows,
-                          int64_t k, cudaStream_t s) {
-  return launch_split_rows_f16_pair(x, hi, lo, inv_scale, rows, nullptr, nullptr, nullptr, nullptr,
-                                    0, k, s);
+                          int64_t k, const FixList& fix, cudaStream_t s) {
+  return launch_split_rows_f16_pair(x, hi, lo, inv_scale, rows, fix, nullptr, nullptr, nullptr,
+                                    nullptr, 0, FixList{}, k, s);
 }
 
 int launch_rowmax_f16(const float* x, float* inv_scale, int64_t rows, int64_t k,
-                      cudaStream_t s) {
-  return launch_split_rows_f16_pair(x, nullptr, nullptr, inv_scale, rows, nullptr, nullptr,
-                                    nullptr, nullptr, 0, k, s);
+                      const FixList& fix, cudaStream_t s) {
+  return launch_split_rows_f16_pair(x, nullptr, nullptr, inv_scale, rows, fix, nullptr, nullptr,
+                                    nullptr, nullptr, 0, FixList{}, k, s);
 }
 
 size_t split_cols_scratch_bytes(int64_t n) { return (size_t)kMaxChunks * (size_t)n * sizeof(float); }
 
 int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,
-                          float* partial_scratch, int64_t k, int64_t n, cudaStream_t s) {
+                          float* partial_scratch, int64_t k, int64_t n, const FixList& fl,
+                          cudaStream_t s) {
   if (k <= 0 || n <= 0) return MTNN_OK;
   const DeviceInfo* di = nullptr;
   MTNN_TRY(device_info(&di));
@@ -734,7 +790,7 @@ int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,
     KernelTimer timer(MTNN_KCLASS_SPLIT, 8.0 * (double)k * (double)n, s);
     MTNN_TRY(launch_chained(split_cols_strip_kernel, dim3((unsigned)strips), dim3(8 * kStripLanes), 0,
                             s, x, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale, k,
-                            n));
+                            n, fl));
     MTNN_CUDA_TRY(cudaGetLastError());
     return MTNN_OK;
   }
@@ -742,13 +798,13 @@ int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,
     KernelTimer timer(MTNN_KCLASS_SPLIT, 8.0 * (double)k * (double)n, s);
     // fewest rows per CTA that keep the cluster within 8 CTAs: the most CTAs
     if (k <= kClusterMax * kClusterRowLanes * 4)
-      MTNN_TRY(launch_cols_cluster<4>(x, hi, lo, inv_scale, k, n, s));
+      MTNN_TRY(launch_cols_cluster<4>(x, hi, lo, inv_scale, k, n, fl, s));
     else if (k <= kClusterMax * kClusterRowLanes * 8)
-      MTNN_TRY(launch_cols_cluster<8>(x, hi, lo, inv_scale, k, n, s));
+      MTNN_TRY(launch_cols_cluster<8>(x, hi, lo, inv_scale, k, n, fl, s));
     else if (k <= kClusterMax * kClusterRowLanes * 16)
-      MTNN_TRY(launch_cols_cluster<16>(x, hi, lo, inv_scale, k, n, s));
+      MTNN_TRY(launch_cols_cluster<16>(x, hi, lo, inv_scale, k, n, fl, s));
     else
-      MTNN_TRY(launch_cols_cluster<32>(x, hi, lo, inv_scale, k, n, s));
+      MTNN_TRY(launch_cols_cluster<32>(x, hi, lo, inv_scale, k, n, fl, s));
     return MTNN_OK;
   }
   KernelTimer timer(MTNN_KCLASS_SPLIT, 12.0 * (double)k * (double)n, s);
@@ -774,7 +830,7 @@ int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,
   MTNN_CUDA_TRY(cudaGetLastError());
   split_cols_band_kernel<kLanes><<<dim3((unsigned)bands, (unsigned)split_bands), 256, 0, s>>>(
       x, partial, (int)chunks, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale, k,
-      n, rpb);
+      n, rpb, fl);
   MTNN_CUDA_TRY(cudaGetLastError());
   return MTNN_OK;
 }
