@@ -69,16 +69,31 @@ __device__ __forceinline__ void fix_push(const FixList& fl, int64_t row, int64_t
 }
 
 // tc3xf16s: h = fp16(x s), l = fp16(x s - h); residual (x s - h - l) / s.
-// inv_s == 0: the row is not tracked (its max is Inf/NaN).
-__device__ __forceinline__ void f16s_split_checked(float v, float s, float inv_s, __half& h,
-                                                   __half& l, const FixList& fl, int64_t row,
-                                                   int64_t col) {
+// Only elements with |x s| < 2^-6 can miss by more than 2^-19 (the residual
+// is <= 2^-23 |x s| while l is normal and <= 2^-25 once it is subnormal), so
+// the exact check runs behind the one-compare filter |x| < cand = 2^-6 / s.
+// cand == 0: the row is not tracked (no list, or its max is Inf/NaN).
+__device__ __forceinline__ float f16s_candidate_bound(float inv_s) { return 0x1p-6f * inv_s; }
+__device__ __forceinline__ void f16s_check(float v, float s, float inv_s, float cand,
+                                           const FixList& fl, int64_t row, int64_t col) {
+  if (!(fabsf(v) < cand) || v == 0.f) return;
+  const float xs = v * s;
+  const float h = __half2float(__float2half_rn(xs));
+  const float d = xs - h;
+  const float rem = d - __half2float(__float2half_rn(d));
+  if (fabsf(rem) > kFixRelF16S * fabsf(xs)) fix_push(fl, row, col, rem * inv_s);
+}
+__device__ __forceinline__ void f16s_split_checked(float v, float s, float inv_s, float cand,
+                                                   __half& h, __half& l, const FixList& fl,
+                                                   int64_t row, int64_t col) {
   const float xs = v * s;
   h = __float2half_rn(xs);
   const float d = xs - __half2float(h);
   l = __float2half_rn(d);
-  const float rem = d - __half2float(l);
-  if (inv_s != 0.f && fabsf(rem) > kFixRelF16S * fabsf(xs)) fix_push(fl, row, col, rem * inv_s);
+  if (fabsf(v) < cand && v != 0.f) {
+    const float rem = d - __half2float(l);
+    if (fabsf(rem) > kFixRelF16S * fabsf(xs)) fix_push(fl, row, col, rem * inv_s);
+  }
 }
 
 // The value the f16s GEMM multiplies for x (row scale s = 1 / inv_s).

@@ -351,13 +351,10 @@ __global__ void __launch_bounds__(kFixThreads, 2) fixup_kernel(const FixupDev p)
 
 }  // namespace
 
-int launch_fixup(const FixupArgs& a, cudaStream_t s) {
-  if (a.fa.ctr == nullptr && a.fb.ctr == nullptr) return MTNN_OK;  // nothing tracked
-  if (a.m <= 0 || a.n <= 0 || a.k <= 0) return MTNN_OK;
+static int make_dev(const FixupArgs& a, FixupDev* out) {
   if (a.ndst < 1 || a.ndst > 8) return fail(MTNN_EINVAL, "fix-up: %d destinations", a.ndst);
-  const DeviceInfo* di = nullptr;
-  MTNN_TRY(device_info(&di));
-  FixupDev p{};
+  FixupDev& p = *out;
+  p = FixupDev{};
   p.A = a.A;
   p.inv_a = a.inv_a;
   p.inv_b = a.inv_b;
@@ -376,13 +373,23 @@ int launch_fixup(const FixupArgs& a, cudaStream_t s) {
   p.b_row0 = a.b_row0;
   p.reset_a = a.reset_a ? 1 : 0;
   p.reset_b = a.reset_b ? 1 : 0;
+  p.smem_entries = kFixSmemEntries;
   if (p.rep == (int)FixRep::F16S && p.inv_a == nullptr && a.fb.ctr != nullptr)
     return fail(MTNN_EINVAL, "fix-up: F16S B entries need A's row scales");
+  return MTNN_OK;
+}
+
+int launch_fixup(const FixupArgs& a, cudaStream_t s) {
+  if (a.fa.ctr == nullptr && a.fb.ctr == nullptr) return MTNN_OK;  // nothing tracked
+  if (a.m <= 0 || a.n <= 0 || a.k <= 0) return MTNN_OK;
+  const DeviceInfo* di = nullptr;
+  MTNN_TRY(device_info(&di));
+  FixupDev p;
+  MTNN_TRY(make_dev(a, &p));
   // one CTA per SM: the entry work of random data is small, and the overflow
   // recompute walks its tiles with it (measured: 32 CTAs or a max-shared
   // carveout change nothing; the kernel's cost is the chain step it adds)
   const unsigned grid = (unsigned)di->sm_count;
-  p.smem_entries = kFixSmemEntries;
   KernelTimer timer(MTNN_KCLASS_FIXUP, 0.0, s);
   if (a.b_is_nk) {
     MTNN_TRY(set_max_dynamic_smem((const void*)fixup_kernel<true>, (int)kFixSmemBytes));

@@ -761,7 +761,7 @@ __global__ void split_tf32_kernel(const float4* __restrict__ a, float4* __restri
   {                                                                            \
     h.c = tf32_hi<kHiCopy>(v.c);                                               \
     l.c = v.c - h.c;                                                           \
-    const float r = v.c - tf32_represented<kHiCopy>(v.c);                      \
+    const float r = fabsf(v.c) < 0x1p-100f ? v.c - tf32_represented<kHiCopy>(v.c) : 0.f; \
     if (fabsf(r) > kFixRelTF32 * fabsf(v.c)) {                                 \
       const int64_t e = 4 * j + q, u = e / row_len, w = e % row_len;           \
       fix_push(is_a ? fa : fb, mn_major ? w : u, mn_major ? u : w, r);         \
@@ -1740,21 +1740,15 @@ int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t 
   return tc_run_bn<256>(a, b, C, m, n, k, ldc < n ? n : ldc, b_is_nk, kind, conv, s);
 }
 
-// Row block of a row-sharded NT with the all-gather fused into the epilogue:
-// C_local = A_local x B^T (m_local x n, row stride n) is stored into C_local and
-// into each peer pointer (the same rows of the peers' C). CTA-pair tc3xf16s
-// kernel with the peer stores; shapes it cannot take are computed locally and
-// pushed to the peers by device-to-device copies on the same stream.
 FixRep tc_fix_rep(TcKind kind) {
   if (kind == TcKind::F16S) return FixRep::F16S;
   return split_mode_hi_copy() ? FixRep::TF32_RNA : FixRep::TF32_TRUNC;
 }
 
-// Fix-up of one finished GEMM whose operands were prepared whole (fix.h).
-static int tc_fixup(const float* A, const TcOperand& a, const float* B, const TcOperand& b,
-                    float* const* dsts, int ndst, int64_t m, int64_t n, int64_t k, int64_t ldc,
-                    bool b_is_nk, TcKind kind, FixHandle& fa, FixHandle& fb, cudaStream_t s) {
-  if (a.fix.ctr == nullptr && b.fix.ctr == nullptr) return MTNN_OK;
+// Fix-up arguments of one GEMM whose operands were prepared whole (fix.h).
+static FixupArgs tc_fix_args(const float* A, const TcOperand& a, const float* B,
+                             const TcOperand& b, float* const* dsts, int ndst, int64_t m, int64_t n,
+                             int64_t k, int64_t ldc, bool b_is_nk, TcKind kind) {
   FixupArgs f;
   f.A = A;
   f.inv_a = a.inv_scale;
@@ -1771,8 +1765,14 @@ static int tc_fixup(const float* A, const TcOperand& a, const float* B, const Tc
   f.rep = tc_fix_rep(kind);
   f.fa = a.fix;
   f.fb = b.fix;
+  return f;
+}
+
+// Launches the fix-up (it resets the lists' counters on the device).
+static int tc_fixup_finish(FixupArgs& f, FixHandle& fa, FixHandle& fb, cudaStream_t s) {
+  if (f.fa.ctr == nullptr && f.fb.ctr == nullptr) return MTNN_OK;
   MTNN_TRY(launch_fixup(f, s));
-  fa.consumed = fb.consumed = true;  // the fix-up resets their counters
+  fa.consumed = fb.consumed = true;
   return MTNN_OK;
 }
 
@@ -1798,7 +1798,8 @@ int gemm_nt_allgather(const float* A, const float* B, float* C_local, float* con
     MTNN_TRY(tc_run_pair(a, b, C_local, m, n, k, n, true, TcKind::F16S, s, peers, npeers));
     float* dsts[8] = {C_local};
     for (int d = 0; d < npeers; ++d) dsts[1 + d] = peers[d];
-    return tc_fixup(A, a, B, b, dsts, 1 + npeers, m, n, k, n, true, TcKind::F16S, fa, fb, s);
+    FixupArgs f = tc_fix_args(A, a, B, b, dsts, 1 + npeers, m, n, k, n, true, TcKind::F16S);
+    return tc_fixup_finish(f, fa, fb, s);
   }
   MTNN_TRY(gemm_dispatch_nt(A, B, C_local, m, n, k, s));
   for (int d = 0; d < npeers; ++d)
@@ -1819,20 +1820,25 @@ int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t 
   const int conv = tc_inkernel_operand(m, n, b_is_nk, kind);
   MTNN_TRY(tc_prepare_pair(A, m, B, n, k, !b_is_nk, kind, conv, wa, wb, &fa, &fb, &a, &b, s));
   if (tc_eligible(A, B, C, m, n, k, b_is_nk, kind)) {
+    float* dsts[1] = {C};
+    FixupArgs f = tc_fix_args(A, a, B, b, dsts, 1, m, n, k, n, b_is_nk, kind);
     MTNN_TRY(tc_run(a, b, C, m, n, k, b_is_nk, kind, s));
-  } else {
-    // C cannot be a TMA store target (n % 4 != 0, e.g. a 10-class output layer, or
-    // an unaligned base): compute into a row-padded buffer and copy the n columns
-    // out (B's missing rows are TMA zero fill, so the padding columns are zeros)
-    const int64_t np = (n + 3) / 4 * 4;
-    MTNN_TRY(wc.alloc((size_t)(m * np) * sizeof(float), s));
-    float* cp = static_cast<float*>(wc.ptr);
-    MTNN_TRY(tc_run(a, b, cp, m, n, k, b_is_nk, kind, s, np));
-    MTNN_CUDA_TRY(cudaMemcpy2DAsync(C, (size_t)n * 4, cp, (size_t)np * 4, (size_t)n * 4, (size_t)m,
-                                    cudaMemcpyDeviceToDevice, s));
+    return tc_fixup_finish(f, fa, fb, s);
   }
-  float* dsts[1] = {C};
-  return tc_fixup(A, a, B, b, dsts, 1, m, n, k, n, b_is_nk, kind, fa, fb, s);
+  // C cannot be a TMA store target (n % 4 != 0, e.g. a 10-class output layer, or
+  // an unaligned base): compute into a row-padded buffer (fixed up there) and
+  // copy the n columns out (B's missing rows are TMA zero fill, so the padding
+  // columns are zeros)
+  const int64_t np = (n + 3) / 4 * 4;
+  MTNN_TRY(wc.alloc((size_t)(m * np) * sizeof(float), s));
+  float* cp = static_cast<float*>(wc.ptr);
+  float* dsts[1] = {cp};
+  FixupArgs f = tc_fix_args(A, a, B, b, dsts, 1, m, n, k, np, b_is_nk, kind);
+  MTNN_TRY(tc_run(a, b, cp, m, n, k, b_is_nk, kind, s, np));
+  MTNN_TRY(tc_fixup_finish(f, fa, fb, s));
+  MTNN_CUDA_TRY(cudaMemcpy2DAsync(C, (size_t)n * 4, cp, (size_t)np * 4, (size_t)n * 4, (size_t)m,
+                                  cudaMemcpyDeviceToDevice, s));
+  return MTNN_OK;
 }
 
 }  // namespace mtnn

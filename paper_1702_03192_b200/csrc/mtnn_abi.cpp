@@ -410,11 +410,12 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
                                       rows, fl, nullptr, nullptr, nullptr, nullptr, 0, FixList{},
                                       k, ps->comp);
   };
-  // residual fix-up of C rows i0.. (mi) x B rows j0.. (nj), rows of ldc; the
-  // last one resets both lists
+  // GEMM + residual fix-up of C rows i0.. (mi) x B rows j0.. (nj), rows of ldc;
+  // the last fix-up resets both lists
   int64_t fixups_left = (QA > 1 ? QA - 1 : 0) + QB;
-  auto fixup = [&](int64_t i0, int64_t mi, int64_t j0, int64_t nj, float* cblk, int64_t ldc) {
-    if (!track) return MTNN_OK;
+  auto run_fixed = [&](const TcOperand& ao, const TcOperand& bo, int64_t i0, int64_t mi,
+                       int64_t j0, int64_t nj, float* cblk, int64_t ldc) {
+    if (!track) return tc_run(ao, bo, cblk, mi, nj, k, true, TcKind::F16S, ps->comp, ldc);
     FixupArgs f;
     f.A = dap + i0 * k;
     f.inv_a = ainv + i0;
@@ -432,6 +433,7 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
     f.a_row0 = (int32_t)i0;
     f.b_row0 = (int32_t)j0;
     f.reset_a = f.reset_b = (--fixups_left == 0);
+    MTNN_TRY(tc_run(ao, bo, cblk, mi, nj, k, true, TcKind::F16S, ps->comp, ldc));
     MTNN_TRY(launch_fixup(f, ps->comp));
     if (f.reset_a) fha.consumed = fhb.consumed = true;
     return MTNN_OK;
@@ -441,8 +443,7 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
     const int64_t i0 = i * mb, j0 = j * nb;
     const int64_t mi = std::min(mb, m - i0), nj = std::min(nb, n - j0);
     float* cij = dcp + i0 * n + mi * j0;  // rows i0.. of C, block j: mi x nj contiguous
-    MTNN_TRY(tc_run(a_rows(i0), b_rows(j0), cij, mi, nj, k, true, TcKind::F16S, ps->comp));
-    MTNN_TRY(fixup(i0, mi, j0, nj, cij, nj));
+    MTNN_TRY(run_fixed(a_rows(i0), b_rows(j0), i0, mi, j0, nj, cij, nj));
     cudaEvent_t e;
     MTNN_TRY(evs.make(&e));
     MTNN_CUDA_TRY(cudaEventRecord(e, ps->comp));
@@ -460,8 +461,7 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
     MTNN_TRY(bring(true, i));
     const int64_t i0 = i * mb, mi = std::min(mb, m - i0);
     float* ci = dcp + i0 * n;
-    MTNN_TRY(tc_run(a_rows(i0), b_rows(0), ci, mi, n, k, true, TcKind::F16S, ps->comp));
-    MTNN_TRY(fixup(i0, mi, 0, n, ci, n));
+    MTNN_TRY(run_fixed(a_rows(i0), b_rows(0), i0, mi, 0, n, ci, n));
     MTNN_TRY(evs.make(&ev));
     MTNN_CUDA_TRY(cudaEventRecord(ev, ps->comp));
     MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->out, ev, 0));
@@ -588,8 +588,9 @@ static int host_gemm(const float* A, const float* B, float* C, int64_t m, int64_
       FixHandle fha;
       TcOperand ap{};
       MTNN_TRY(tc_prepare(a_c, mr, k, false, kind, conv == 1, wa, &fha, &ap, ps->comp));
-      MTNN_TRY(tc_run(ap, bp, c_c, mr, n, k, b_is_nk, kind, ps->comp));
-      if (ap.fix.ctr != nullptr || bp.fix.ctr != nullptr) {
+      if (ap.fix.ctr == nullptr && bp.fix.ctr == nullptr) {
+        MTNN_TRY(tc_run(ap, bp, c_c, mr, n, k, b_is_nk, kind, ps->comp));
+      } else {
         FixupArgs f;
         f.A = a_c;
         f.inv_a = ap.inv_scale;
@@ -607,6 +608,7 @@ static int host_gemm(const float* A, const float* B, float* C, int64_t m, int64_
         f.fb = bp.fix;
         f.reset_a = true;
         f.reset_b = c == chunks - 1;
+        MTNN_TRY(tc_run(ap, bp, c_c, mr, n, k, b_is_nk, kind, ps->comp));
         MTNN_TRY(launch_fixup(f, ps->comp));
         fha.consumed = true;
         if (f.reset_b) fhb.consumed = true;

@@ -63,48 +63,99 @@ constexpr int kUnroll = 4;  // independent 16-byte loads per lane in flight
 
 __device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
 
+// Smallest non-zero magnitude of v (+inf if all zero): a thread whose elements
+// all sit at or above the row's residual candidate bound skips the check.
+__device__ __forceinline__ float absmin_nz4(const float4& v) {
+  const float ax = v.x != 0.f ? fabsf(v.x) : INFINITY, ay = v.y != 0.f ? fabsf(v.y) : INFINITY;
+  const float az = v.z != 0.f ? fabsf(v.z) : INFINITY, aw = v.w != 0.f ? fabsf(v.w) : INFINITY;
+  return fminf(fminf(ax, ay), fminf(az, aw));
+}
+
 __device__ __forceinline__ float absmax4(const float4& v) {
   if (isnan(v.x) || isnan(v.y) || isnan(v.z) || isnan(v.w)) return INFINITY;
   return fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
 }
 
 // split4 with residual tracking (fix.h): elements whose halves miss them by
-// more than 2^-19 are listed for the fix-up; col0 = k index of v.x.
-__device__ __forceinline__ void split4c(const float4& v, float s, float inv_s, uint2& hw,
-                                        uint2& lw, const FixList& fl, int64_t row, int64_t col0) {
+// more than 2^-19 are listed for the fix-up; col0 = k index of v.x; cand =
+// f16s_candidate_bound(1/s), or 0 for an untracked row.
+__device__ __forceinline__ void split4c(const float4& v, float s, float inv_s, float cand,
+                                        uint2& hw, uint2& lw, const FixList& fl, int64_t row,
+                                        int64_t col0) {
   __half h0, h1, h2, h3, l0, l1, l2, l3;
-  f16s_split_checked(v.x, s, inv_s, h0, l0, fl, row, col0);
-  f16s_split_checked(v.y, s, inv_s, h1, l1, fl, row, col0 + 1);
-  f16s_split_checked(v.z, s, inv_s, h2, l2, fl, row, col0 + 2);
-  f16s_split_checked(v.w, s, inv_s, h3, l3, fl, row, col0 + 3);
+  f16s_split_checked(v.x, s, inv_s, cand, h0, l0, fl, row, col0);
+  f16s_split_checked(v.y, s, inv_s, cand, h1, l1, fl, row, col0 + 1);
+  f16s_split_checked(v.z, s, inv_s, cand, h2, l2, fl, row, col0 + 2);
+  f16s_split_checked(v.w, s, inv_s, cand, h3, l3, fl, row, col0 + 3);
   __half2 hp0 = __halves2half2(h0, h1), hp1 = __halves2half2(h2, h3);
   __half2 lp0 = __halves2half2(l0, l1), lp1 = __halves2half2(l2, l3);
   hw = make_uint2(*reinterpret_cast<uint32_t*>(&hp0), *reinterpret_cast<uint32_t*>(&hp1));
   lw = make_uint2(*reinterpret_cast<uint32_t*>(&lp0), *reinterpret_cast<uint32_t*>(&lp1));
 }
+__device__ __forceinline__ void split4(const float4& v, float s, uint2& hw, uint2& lw) {
+  const __half2 h01 = __floats2half2_rn(v.x * s, v.y * s), h23 = __floats2half2_rn(v.z * s, v.w * s);
+  const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+  const __half2 l01 = __floats2half2_rn(v.x * s - f01.x, v.y * s - f01.y);
+  const __half2 l23 = __floats2half2_rn(v.z * s - f23.x, v.w * s - f23.y);
+  hw = make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+  lw = make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+}
+// chk: this thread holds a residual candidate (see absmin_nz4).
+__device__ __forceinline__ void split4x(bool chk, const float4& v, float s, float inv_s, float cand,
+                                        uint2& hw, uint2& lw, const FixList& fl, int64_t row,
+                                        int64_t col0) {
+  if (chk) split4c(v, s, inv_s, cand, hw, lw, fl, row, col0);
+  else split4(v, s, hw, lw);
+}
 // Residual check only (operands the GEMM splits in-kernel from raw rows: the
-// halves it builds are bit-identical to these).
-__device__ __forceinline__ void check4(const float4& v, float s, float inv_s, const FixList& fl,
-                                       int64_t row, int64_t col0) {
-  uint2 hw, lw;
-  split4c(v, s, inv_s, hw, lw, fl, row, col0);
+// halves it builds are bit-identical to these). One compare per element unless
+// an element is a candidate.
+__device__ __forceinline__ void check4(const float4& v, float s, float inv_s, float cand,
+                                       const FixList& fl, int64_t row, int64_t col0) {
+  f16s_check(v.x, s, inv_s, cand, fl, row, col0);
+  f16s_check(v.y, s, inv_s, cand, fl, row, col0 + 1);
+  f16s_check(v.z, s, inv_s, cand, fl, row, col0 + 2);
+  f16s_check(v.w, s, inv_s, cand, fl, row, col0 + 3);
 }
 __device__ __forceinline__ void split_col4(const float4& v, const float4& sc, const float4& inv,
                                            uint2& hw, uint2& lw, const FixList& fl, int64_t col,
                                            int64_t krow) {
   __half h0, h1, h2, h3, l0, l1, l2, l3;
-  f16s_split_checked(v.x, sc.x, inv.x, h0, l0, fl, col, krow);
-  f16s_split_checked(v.y, sc.y, inv.y, h1, l1, fl, col + 1, krow);
-  f16s_split_checked(v.z, sc.z, inv.z, h2, l2, fl, col + 2, krow);
-  f16s_split_checked(v.w, sc.w, inv.w, h3, l3, fl, col + 3, krow);
+  f16s_split_checked(v.x, sc.x, inv.x, f16s_candidate_bound(inv.x), h0, l0, fl, col, krow);
+  f16s_split_checked(v.y, sc.y, inv.y, f16s_candidate_bound(inv.y), h1, l1, fl, col + 1, krow);
+  f16s_split_checked(v.z, sc.z, inv.z, f16s_candidate_bound(inv.z), h2, l2, fl, col + 2, krow);
+  f16s_split_checked(v.w, sc.w, inv.w, f16s_candidate_bound(inv.w), h3, l3, fl, col + 3, krow);
   __half2 hp0 = __halves2half2(h0, h1), hp1 = __halves2half2(h2, h3);
   __half2 lp0 = __halves2half2(l0, l1), lp1 = __halves2half2(l2, l3);
   hw = make_uint2(*reinterpret_cast<uint32_t*>(&hp0), *reinterpret_cast<uint32_t*>(&hp1));
   lw = make_uint2(*reinterpret_cast<uint32_t*>(&lp0), *reinterpret_cast<uint32_t*>(&lp1));
 }
-// 1/s for the residual check, 0 (= untracked, fix.h) for a row or column whose
-// max is Inf/NaN: its output is non-finite anyway and its scale (1) says
-// nothing about the other entries' range.
+// Columns: per-component minimum of the non-zero magnitudes seen.
+__device__ __forceinline__ float4 absmin_nz_each(const float4& m, const float4& v) {
+  return make_float4(v.x != 0.f ? fminf(m.x, fabsf(v.x)) : m.x, v.y != 0.f ? fminf(m.y, fabsf(v.y)) : m.y,
+                     v.z != 0.f ? fminf(m.z, fabsf(v.z)) : m.z, v.w != 0.f ? fminf(m.w, fabsf(v.w)) : m.w);
+}
+__device__ __forceinline__ bool col_candidates(const float4& mn, const float4& inv) {
+  return mn.x < f16s_candidate_bound(inv.x) || mn.y < f16s_candidate_bound(inv.y) ||
+         mn.z < f16s_candidate_bound(inv.z) || mn.w < f16s_candidate_bound(inv.w);
+}
+__device__ __forceinline__ void split_col4x(bool chk, const float4& v, const float4& sc,
+                                            const float4& inv, uint2& hw, uint2& lw,
+                                            const FixList& fl, int64_t col, int64_t krow) {
+  if (chk) {
+    split_col4(v, sc, inv, hw, lw, fl, col, krow);
+    return;
+  }
+  const __half2 h01 = __floats2half2_rn(v.x * sc.x, v.y * sc.y), h23 = __floats2half2_rn(v.z * sc.z, v.w * sc.w);
+  const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+  const __half2 l01 = __floats2half2_rn(v.x * sc.x - f01.x, v.y * sc.y - f01.y);
+  const __half2 l23 = __floats2half2_rn(v.z * sc.z - f23.x, v.w * sc.w - f23.y);
+  hw = make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+  lw = make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+}
+// 1/s for the residual check, 0 (= untracked) for a row or column whose max is
+// Inf/NaN: its output is non-finite anyway and its scale (1) says nothing
+// about the other entries' range.
 __device__ __forceinline__ float track_inv(float mx, float inv) { return mx <= 3.402823466e38f ? inv : 0.f; }
 __device__ __forceinline__ float4 track_inv4(const float4& m, const float4& sc) {
   return make_float4(track_inv(m.x, 1.f / sc.x), track_inv(m.y, 1.f / sc.y),
@@ -156,25 +207,33 @@ split_rows_f16_kernel(const RowJob j0, const RowJob j1, int64_t k) {
     int64_t r;
     const RowJob j = pick(j0, j1, v, r);
     const float4* row = reinterpret_cast<const float4*>(j.x + r * k);
-    float mx = 0.f;
+    float mx = 0.f, mn = INFINITY;
     int64_t i = lane;
     for (; i + 32 * (kUnroll - 1) < k4; i += kStep) {
       float4 x[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) x[u] = ldg4(row + i + 32 * u);
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) mx = fmaxf(mx, absmax4(x[u]));
+      for (int u = 0; u < kUnroll; ++u) {
+        mx = fmaxf(mx, absmax4(x[u]));
+        mn = fminf(mn, absmin_nz4(x[u]));
+      }
     }
-    for (; i < k4; i += 32) mx = fmaxf(mx, absmax4(ldg4(row + i)));
+    for (; i < k4; i += 32) {
+      const float4 x = ldg4(row + i);
+      mx = fmaxf(mx, absmax4(x));
+      mn = fminf(mn, absmin_nz4(x));
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     const float s = pow2_scale(mx);
     const float inv = 1.f / s;
-    const float tinv = track_inv(mx, inv);
+    const float cand = j.fix.ctr ? f16s_candidate_bound(track_inv(mx, inv)) : 0.f;
+    const bool chk = mn < cand;  // this thread holds a residual candidate
     if (lane == 0) j.inv_scale[r] = inv;
     if (j.hi == nullptr) {  // row scales only (+ the residual check, from L1/L2)
-      if (j.fix.ctr != nullptr)
-        for (i = lane; i < k4; i += 32) check4(ldg4(row + i), s, tinv, j.fix, r, 4 * i);
+      if (chk)
+        for (i = lane; i < k4; i += 32) check4(ldg4(row + i), s, inv, cand, j.fix, r, 4 * i);
       continue;
     }
     uint2* hrow = reinterpret_cast<uint2*>(j.hi + r * k);
@@ -187,14 +246,14 @@ split_rows_f16_kernel(const RowJob j0, const RowJob j1, int64_t k) {
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         uint2 hw, lw;
-        split4c(x[u], s, tinv, hw, lw, j.fix, r, 4 * (i + 32 * u));
+        split4x(chk, x[u], s, inv, cand, hw, lw, j.fix, r, 4 * (i + 32 * u));
         hrow[i + 32 * u] = hw;
         lrow[i + 32 * u] = lw;
       }
     }
     for (; i < k4; i += 32) {
       uint2 hw, lw;
-      split4c(ldg4(row + i), s, tinv, hw, lw, j.fix, r, 4 * i);
+      split4x(chk, ldg4(row + i), s, inv, cand, hw, lw, j.fix, r, 4 * i);
       hrow[i] = hw;
       lrow[i] = lw;
     }
@@ -224,21 +283,25 @@ split_rows_f16_reg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
       const int64_t i = lane + 32 * u;
       x[u] = i < k4 ? ldg4(row + i) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    float mx = 0.f;
+    float mx = 0.f, mn = INFINITY;
 #pragma unroll
-    for (int u = 0; u < kR; ++u) mx = fmaxf(mx, absmax4(x[u]));
+    for (int u = 0; u < kR; ++u) {
+      mx = fmaxf(mx, absmax4(x[u]));
+      mn = fminf(mn, absmin_nz4(x[u]));
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     const float s = pow2_scale(mx);
     const float inv = 1.f / s;
-    const float tinv = track_inv(mx, inv);
+    const float cand = j.fix.ctr ? f16s_candidate_bound(track_inv(mx, inv)) : 0.f;
+    const bool chk = mn < cand;  // this thread holds a residual candidate
     if (lane == 0) j.inv_scale[r] = inv;
     if (j.hi == nullptr) {  // row scales only (+ the residual check)
-      if (j.fix.ctr != nullptr) {
+      if (chk) {
 #pragma unroll
         for (int u = 0; u < kR; ++u) {
           const int64_t i = lane + 32 * u;
-          if (i < k4) check4(x[u], s, tinv, j.fix, r, 4 * i);
+          if (i < k4) check4(x[u], s, inv, cand, j.fix, r, 4 * i);
         }
       }
       continue;
@@ -250,7 +313,7 @@ split_rows_f16_reg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
       const int64_t i = lane + 32 * u;
       if (i < k4) {
         uint2 hw, lw;
-        split4c(x[u], s, tinv, hw, lw, j.fix, r, 4 * i);
+        split4x(chk, x[u], s, inv, cand, hw, lw, j.fix, r, 4 * i);
         hrow[i] = hw;
         lrow[i] = lw;
       }
@@ -280,7 +343,7 @@ split_rows_f16_smem_kernel(const RowJob j0, const RowJob j1, int64_t k) {
     const RowJob j = pick(j0, j1, v, r);
     const bool stage = j.hi != nullptr || j.fix.ctr != nullptr;
     const float4* row = reinterpret_cast<const float4*>(j.x + r * k);
-    float mx = 0.f;
+    float mx = 0.f, mn = INFINITY;
     int64_t i = t;
     for (; i + kRowThreads * (kUnroll - 1) < k4; i += kRowThreads * kUnroll) {
       float4 x[kUnroll];
@@ -290,12 +353,14 @@ split_rows_f16_smem_kernel(const RowJob j0, const RowJob j1, int64_t k) {
       for (int u = 0; u < kUnroll; ++u) {
         if (stage) row_s[i + kRowThreads * u] = x[u];
         mx = fmaxf(mx, absmax4(x[u]));
+        mn = fminf(mn, absmin_nz4(x[u]));
       }
     }
     for (; i < k4; i += kRowThreads) {
       const float4 x = ldg4(row + i);
       if (stage) row_s[i] = x;
       mx = fmaxf(mx, absmax4(x));
+      mn = fminf(mn, absmin_nz4(x));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -310,19 +375,20 @@ split_rows_f16_smem_kernel(const RowJob j0, const RowJob j1, int64_t k) {
     __syncthreads();
     const float s = pow2_scale(red[0]);
     const float inv = 1.f / s;
-    const float tinv = track_inv(red[0], inv);
+    const float cand = j.fix.ctr ? f16s_candidate_bound(track_inv(red[0], inv)) : 0.f;
+    const bool chk = mn < cand;  // this thread holds a residual candidate
     if (t == 0) j.inv_scale[r] = inv;
     if (stage && j.hi != nullptr) {
       uint2* hrow = reinterpret_cast<uint2*>(j.hi + r * k);
       uint2* lrow = reinterpret_cast<uint2*>(j.lo + r * k);
       for (int64_t q = t; q < k4; q += kRowThreads) {
         uint2 hw, lw;
-        split4c(row_s[q], s, tinv, hw, lw, j.fix, r, 4 * q);
+        split4x(chk, row_s[q], s, inv, cand, hw, lw, j.fix, r, 4 * q);
         hrow[q] = hw;
         lrow[q] = lw;
       }
-    } else if (stage) {
-      for (int64_t q = t; q < k4; q += kRowThreads) check4(row_s[q], s, tinv, j.fix, r, 4 * q);
+    } else if (stage && chk) {
+      for (int64_t q = t; q < k4; q += kRowThreads) check4(row_s[q], s, inv, cand, j.fix, r, 4 * q);
     }
     __syncthreads();  // row_s and red are reused by the next row
   }
@@ -355,9 +421,12 @@ split_rows_f16_ctareg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
       const int64_t i = t + kCtaRowThreads * u;
       x[u] = i < k4 ? ldg4(row + i) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    float mx = 0.f;
+    float mx = 0.f, mn = INFINITY;
 #pragma unroll
-    for (int u = 0; u < kV; ++u) mx = fmaxf(mx, absmax4(x[u]));
+    for (int u = 0; u < kV; ++u) {
+      mx = fmaxf(mx, absmax4(x[u]));
+      mn = fminf(mn, absmin_nz4(x[u]));
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (t % 32 == 0) red[parity][t / 32] = mx;
@@ -366,14 +435,15 @@ split_rows_f16_ctareg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
     for (int w = 0; w < kCtaRowThreads / 32; ++w) mx = fmaxf(mx, red[parity][w]);
     const float s = pow2_scale(mx);
     const float inv = 1.f / s;
-    const float tinv = track_inv(mx, inv);
+    const float cand = j.fix.ctr ? f16s_candidate_bound(track_inv(mx, inv)) : 0.f;
+    const bool chk = mn < cand;  // this thread holds a residual candidate
     if (t == 0) j.inv_scale[r] = inv;
     if (j.hi == nullptr) {  // row scales only (+ the residual check)
-      if (j.fix.ctr != nullptr) {
+      if (chk) {
 #pragma unroll
         for (int u = 0; u < kV; ++u) {
           const int64_t i = t + kCtaRowThreads * u;
-          if (i < k4) check4(x[u], s, tinv, j.fix, r, 4 * i);
+          if (i < k4) check4(x[u], s, inv, cand, j.fix, r, 4 * i);
         }
       }
       continue;
@@ -385,7 +455,7 @@ split_rows_f16_ctareg_kernel(const RowJob j0, const RowJob j1, int64_t k) {
       const int64_t i = t + kCtaRowThreads * u;
       if (i < k4) {
         uint2 hw, lw;
-        split4c(x[u], s, tinv, hw, lw, j.fix, r, 4 * i);
+        split4x(chk, x[u], s, inv, cand, hw, lw, j.fix, r, 4 * i);
         hrow[i] = hw;
         lrow[i] = lw;
       }
@@ -521,10 +591,12 @@ split_cols_strip_kernel(const float* __restrict__ x, __half* __restrict__ hi,
   const int64_t col = (int64_t)blockIdx.x * kStripCols + 4 * c4;
   const bool active = col < n;  // n % 4 == 0: the whole float4 is in range
   float4 mx = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 mn = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
   if (active) {
 #pragma unroll 4
     for (int64_t r = rl; r < k; r += kStripLanes) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(x + r * n + col));
+      mn = absmin_nz_each(mn, v);
       mx.x = isnan(v.x) ? INFINITY : fmaxf(mx.x, fabsf(v.x));
       mx.y = isnan(v.y) ? INFINITY : fmaxf(mx.y, fabsf(v.y));
       mx.z = isnan(v.z) ? INFINITY : fmaxf(mx.z, fabsf(v.z));
@@ -551,12 +623,13 @@ split_cols_strip_kernel(const float* __restrict__ x, __half* __restrict__ hi,
   if (!active) return;
   const float4 sc = scale[c4];
   const float4 inv = tinv_s[c4];
+  const bool chk = fl.ctr != nullptr && col_candidates(mn, inv);
 #pragma unroll 4
   for (int64_t r = rl; r < k; r += kStripLanes) {
     const int64_t i = r * n + col;
     const float4 v = ldg4(reinterpret_cast<const float4*>(x + i));
     uint2 hw, lw;
-    split_col4(v, sc, inv, hw, lw, fl, col, r);
+    split_col4x(chk, v, sc, inv, hw, lw, fl, col, r);
     reinterpret_cast<uint2*>(hi)[i / 4] = hw;
     reinterpret_cast<uint2*>(lo)[i / 4] = lw;
   }
@@ -627,10 +700,12 @@ split_cols_cluster_kernel(const float* __restrict__ x, __half* __restrict__ hi,
     v[u] = (active && r < k) ? ldg4(reinterpret_cast<const float4*>(x + r * n + col))
                              : make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  float4 mn = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
 #pragma unroll
   for (int u = 0; u < kR; ++u) {
     mx.x = nanmax(mx.x, v[u].x); mx.y = nanmax(mx.y, v[u].y);
     mx.z = nanmax(mx.z, v[u].z); mx.w = nanmax(mx.w, v[u].w);
+    mn = absmin_nz_each(mn, v[u]);
   }
   red[rl][c4] = mx;
   __syncthreads();
@@ -662,12 +737,13 @@ split_cols_cluster_kernel(const float* __restrict__ x, __half* __restrict__ hi,
   if (!active) return;
   const float4 sc = scale[c4];
   const float4 inv = tinv_s[c4];
+  const bool chk = fl.ctr != nullptr && col_candidates(mn, inv);
 #pragma unroll
   for (int u = 0; u < kR; ++u) {
     const int64_t r = r0 + kClusterRowLanes * u;
     if (r < k) {
       uint2 hw, lw;
-      split_col4(v[u], sc, inv, hw, lw, fl, col, r);
+      split_col4x(chk, v[u], sc, inv, hw, lw, fl, col, r);
       const int64_t i = (r * n + col) / 4;
       reinterpret_cast<uint2*>(hi)[i] = hw;
       reinterpret_cast<uint2*>(lo)[i] = lw;
