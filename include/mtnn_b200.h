@@ -127,6 +127,17 @@ int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* w
 int mtnn_config_set(const char* key, int64_t value);
 int mtnn_config_get(const char* key, int64_t* value);
 
+/* ---- measurement support --------------------------------------------- */
+/* out[i] = float32(low + (high - low) * u_{skip+i}) for i < count, u_j the j-th
+ * double of numpy's PCG64 stream whose initial state is {state_lo, state_hi,
+ * inc_lo, inc_hi} (np.random.default_rng(seed).bit_generator.state): bit-identical
+ * to rng.uniform(low, high, count).astype(float32) after `skip` draws. With
+ * skip = 0 for A and skip = m*k for B this is the reference harness's
+ * make_operands(shape, seed) (pkg/src/mtnn/bench.py:104-114), generated on the
+ * device. Asynchronous on `stream`. */
+int mtnn_fill_uniform_pcg64(float* out, int64_t count, const uint64_t state[4], int64_t skip,
+                            double low, double high, void* stream);
+
 /* ---- device-resident kernels ----------------------------------------- */
 /* C = A x B^T directly. Replaces _impl.gemm_nt / gemm_nt_parallel
  * (_numba_impl.py:139-166; caller kernels/__init__.py:105-116). */

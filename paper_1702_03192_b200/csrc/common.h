@@ -143,6 +143,12 @@ int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,
                           float* partial_scratch, int64_t k, int64_t n, const FixList& fl,
                           cudaStream_t s);
 
+// Draws skip .. skip + count - 1 of numpy's PCG64 stream with initial
+// (state_lo, state_hi, inc_lo, inc_hi), as uniform(low, high) doubles rounded to
+// float32 (operands.cu; reference bench.py:104-114).
+int fill_uniform_pcg64(float* out, int64_t count, const uint64_t state[4], int64_t skip,
+                       double low, double high, cudaStream_t s);
+
 // ------------------------------------------------------------ residual fix-up
 // Residual list of one split operand (fix.h): a ring counter pair plus entries
 // carved from the caller's workspace. Releasing an unconsumed list (error exit)

@@ -750,6 +750,11 @@ int mtnn_gemm_nt_allgather(const float* A_local, const float* B, float* C, float
                            static_cast<cudaStream_t>(stream));
 }
 
+int mtnn_fill_uniform_pcg64(float* out, int64_t count, const uint64_t state[4], int64_t skip,
+                            double low, double high, void* stream) {
+  return fill_uniform_pcg64(out, count, state, skip, low, high, static_cast<cudaStream_t>(stream));
+}
+
 int mtnn_gemm_nt(const float* A, const float* B, float* C, int64_t m, int64_t n, int64_t k,
                  int variant, void* stream) {
   return gemm_dispatch(A, B, C, m, n, k, variant, true, static_cast<cudaStream_t>(stream));
