@@ -175,6 +175,17 @@ int mtnn_gemm_nt_allgather(const float* A_local, const float* B, float* C, float
 int mtnn_ipc_handle(const void* ptr, unsigned char handle[64], int64_t* offset);
 int mtnn_ipc_open(const unsigned char handle[64], int64_t offset, void** ptr);
 int mtnn_ipc_close(void* ptr);
+/* Device-side barrier of `world` ranks (<= 8) on `stream`: this rank stores
+ * `epoch` into slot `rank` of every peer's flag array (peer_flags[j], mapped
+ * with mtnn_ipc_open; release at system scope, cumulative over everything the
+ * stream did before) and waits until its own flags[i] >= epoch for every other
+ * rank i (acquire). Enqueued before and after mtnn_gemm_nt_allgather it keeps
+ * the exchange's completion on the device, inside the caller's event window.
+ * A peer silent for timeout_s (<= 0: 30 s) sets *status = 1 + its rank instead
+ * of hanging. Errors: MTNN_EINVAL. */
+int mtnn_peer_barrier(uint32_t* flags, uint32_t* const* peer_flags, int npeers, int rank,
+                      int world, uint32_t epoch, uint32_t* status, double timeout_s,
+                      void* stream);
 
 /* ---- host-buffer (drop-in) variants: synchronous, numpy semantics ------ */
 int mtnn_gemm_nt_host(const float* A, const float* B, float* C, int64_t m, int64_t n,

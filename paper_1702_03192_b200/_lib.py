@@ -81,6 +81,8 @@ def _load():
         "mtnn_ipc_handle": (c_int, [c_void_p, c_void_p, _I64P]),
         "mtnn_ipc_open": (c_int, [c_void_p, c_int64, POINTER(c_void_p)]),
         "mtnn_ipc_close": (c_int, [c_void_p]),
+        "mtnn_peer_barrier": (c_int, [c_void_p, POINTER(c_void_p), c_int, c_int, c_int,
+                                      ctypes.c_uint32, c_void_p, c_double, c_void_p]),
         "mtnn_gemm_nt": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p]),
         "mtnn_gemm_nn": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p]),
         "mtnn_transpose": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p]),

@@ -104,7 +104,11 @@ int prepare_mempool() {
   std::call_once(once[dev], [dev] {
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t threshold = UINT64_MAX;
+      // keep up to 8 GiB of freed workspace mapped between calls (operand
+      // halves + B^T of the largest configs[4] call fit), so steady-state calls
+      // never map memory; anything above is returned at the next sync.
+      // device_free_bytes_cached counts the pool's idle reserve as free.
+      uint64_t threshold = 8ull << 30;
       (void)cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
     }
     (void)cudaGetLastError();
@@ -120,9 +124,6 @@ static int check_dims(int64_t m, int64_t n, int64_t k) {
   return MTNN_OK;
 }
 
-// AUTO: the FP16x3-scaled tensor-core path once the problem is big enough to
-// amortise the operand split (else the TF32 path if only that is eligible);
-// tiny problems keep the exact-order FFMA chain (bit-exact identity KATs).
 // AUTO: the FP16x3-scaled tensor-core path once the problem is big enough to
 // amortise the operand split (else the TF32 path if only that is eligible);
 // tiny problems keep the exact-order FFMA chain (bit-exact identity KATs).
@@ -650,6 +651,16 @@ int device_free_bytes_cached(int64_t* out) {
   }
   size_t fr = 0, total = 0;
   MTNN_CUDA_TRY(cudaMemGetInfo(&fr, &total));
+  // freed-but-reserved bytes of our stream-ordered pool are allocatable too
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t reserved = 0, used = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
+        reserved > used)
+      fr += reserved - used;
+  }
+  (void)cudaGetLastError();
   if (dev >= 0 && dev < kMaxDevices) {
     g_free_stamp[dev] = now;
     g_free_value[dev] = (int64_t)fr;

@@ -162,35 +162,68 @@ class PeerGather:
     row0)`` then runs ``mtnn_gemm_nt_allgather``: the CTA-pair GEMM epilogue
     stores every C tile of this rank's row block into its own C and straight
     into each peer's C over NVLink, so the gather overlaps the MMAs instead of
-    following them as an ``ncclAllGather``. C is complete on every rank after
-    all ranks' calls finish; ``gemm`` synchronises the stream and the group.
+    following them as an ``ncclAllGather``. Completion is a device-side barrier
+    over IPC-mapped flag words (``mtnn_peer_barrier``) enqueued after the GEMM:
+    once it passes on a rank's stream, that rank's C holds every rank's rows.
     """
 
-    def __init__(self, c: torch.Tensor, *, group=None):
+    def __init__(self, c: torch.Tensor, *, group=None, timeout_s: float = 30.0):
         import ctypes
 
         from . import _lib
 
         if not (c.is_cuda and c.dtype == torch.float32 and c.is_contiguous() and c.dim() == 2):
             raise ValueError("c must be a contiguous 2-D float32 CUDA tensor")
-        self.c, self.group = c, group
+        self.c, self.group, self.timeout_s = c, group, float(timeout_s)
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
-        handle = (ctypes.c_char * 64)()
-        off = ctypes.c_int64()
-        _lib.check(_lib.lib.mtnn_ipc_handle(c.data_ptr(), ctypes.addressof(handle), ctypes.byref(off)))
+        if self.world > 8:
+            raise ValueError("PeerGather maps at most 8 ranks (one NVSwitch node)")
+        # per-rank flag words of the device-side barrier (slot i written by rank i)
+        self.flags = torch.zeros(8, dtype=torch.int32, device=c.device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=c.device)
+        self.epoch = 0
+        mine = []
+        for t in (c, self.flags):
+            handle = (ctypes.c_char * 64)()
+            off = ctypes.c_int64()
+            _lib.check(_lib.lib.mtnn_ipc_handle(t.data_ptr(), ctypes.addressof(handle),
+                                                ctypes.byref(off)))
+            mine.append((bytes(handle), off.value))
         infos = [None] * self.world
-        dist.all_gather_object(infos, (bytes(handle), off.value), group=group)
-        self.peers = []
-        for r, (h, o) in enumerate(infos):
+        dist.all_gather_object(infos, tuple(mine), group=group)
+        self.peers, self.peer_flags = [], []
+        for r, entries in enumerate(infos):
             if r == self.rank:
                 continue
-            buf = ctypes.create_string_buffer(h, 64)
-            p = ctypes.c_void_p()
-            _lib.check(_lib.lib.mtnn_ipc_open(ctypes.addressof(buf), o, ctypes.byref(p)))
-            self.peers.append(p.value)
+            for (h, o), dst in zip(entries, (self.peers, self.peer_flags)):
+                buf = ctypes.create_string_buffer(h, 64)
+                p = ctypes.c_void_p()
+                _lib.check(_lib.lib.mtnn_ipc_open(ctypes.addressof(buf), o, ctypes.byref(p)))
+                dst.append(p.value)
         self._peer_arr = (ctypes.c_void_p * max(1, len(self.peers)))(*self.peers)
+        self._flag_arr = (ctypes.c_void_p * max(1, len(self.peer_flags)))(*self.peer_flags)
+
+    def _barrier(self, stream):
+        from . import _lib
+
+        self.epoch += 1
+        _lib.check(_lib.lib.mtnn_peer_barrier(
+            self.flags.data_ptr(), self._flag_arr, len(self.peer_flags), self.rank, self.world,
+            self.epoch & 0xFFFFFFFF, self.status.data_ptr(), self.timeout_s, stream))
+
+    def check_status(self):
+        """Raise if a device-side barrier timed out waiting for a peer."""
+        bad = int(self.status.item())
+        if bad:
+            raise RuntimeError(f"PeerGather: rank {bad - 1} never reached the device barrier "
+                               f"(timeout {self.timeout_s} s)")
 
     def gemm(self, a_local: torch.Tensor, b: torch.Tensor, row0: int, *, sync: bool = True):
+        """Enqueue barrier -> fused GEMM + peer stores -> barrier on the current
+        stream. The first barrier keeps this rank from storing into a peer's C
+        while that peer's earlier work may still read it; the second makes C
+        complete on this rank's stream (everything after it sees all ranks'
+        tiles) without a host round trip. sync=True also waits on the host."""
         from . import _lib
 
         m, n = self.c.shape
@@ -198,18 +231,32 @@ class PeerGather:
         if tuple(b.shape) != (n, k) or row0 < 0 or row0 + mloc > m:
             raise ValueError(f"shapes: a_local {tuple(a_local.shape)}, b {tuple(b.shape)}, "
                              f"row0 {row0}, C {tuple(self.c.shape)}")
-        stream = torch.cuda.current_stream(self.c.device).cuda_stream
+        if a_local.device != self.c.device or b.device != self.c.device:
+            raise ValueError("a_local, b and c must be on the same device")
+        # bound for the duration of the (asynchronous) launch: a temporary made
+        # by .contiguous() must not return to the caching allocator before the
+        # kernel has read it
+        a_c, b_c = a_local.contiguous(), b.contiguous()
+        stream = torch.cuda.current_stream(self.c.device)
+        sp = stream.cuda_stream
+        self._barrier(sp)
         _lib.check(_lib.lib.mtnn_gemm_nt_allgather(
-            a_local.contiguous().data_ptr(), b.contiguous().data_ptr(), self.c.data_ptr(),
-            self._peer_arr, len(self.peers), row0, mloc, n, k, stream))
+            a_c.data_ptr(), b_c.data_ptr(), self.c.data_ptr(),
+            self._peer_arr, len(self.peers), row0, mloc, n, k, sp))
+        self._barrier(sp)
+        for t in (a_c, b_c):
+            if t is not a_local and t is not b:
+                t.record_stream(stream)
         if sync:
             torch.cuda.synchronize(self.c.device)
-            dist.barrier(group=self.group)
+            self.check_status()
         return self.c
 
     def close(self):
         from . import _lib
 
-        for p in self.peers:
+        torch.cuda.synchronize(self.c.device)
+        dist.barrier(group=self.group)  # no peer still stores into our buffers
+        for p in self.peers + self.peer_flags:
             _lib.check(_lib.lib.mtnn_ipc_close(p))
-        self.peers = []
+        self.peers, self.peer_flags = [], []

@@ -3,8 +3,6 @@ metrics.aggregate / render_report and its CSV wire formats (tests/golden/)."""
 
 import csv
 import io
-import importlib.util
-import os
 
 import numpy as np
 import pytest
@@ -99,9 +97,6 @@ def test_cli_errors_exit_1(tmp_path, capsys):
     assert rc == 1 and "error:" in capsys.readouterr().err
 
 
-@pytest.mark.skipif(importlib.util.find_spec("numba") is None
-                    or not os.path.isdir(os.environ.get("MTNN_REFERENCE_SRC", "/root/reference/pkg/src")),
-                    reason="train/cv use the reference learner")
 def test_cli_train_and_cv(tmp_path, capsys):
     model = tmp_path / "m.json"
     rc = cli.main(["train", "--samples", str(GOLDEN / "wire_s.csv"), "--model", str(model)])

@@ -714,3 +714,35 @@ def test_env_switches_keep_results(tmp_path, switch):
     if key in ("MTNN_PDL", "MTNN_SPLIT_CTAREG", "MTNN_SPLIT_STRIP"):
         for f in res["default"].files:
             assert np.array_equal(res["default"][f], res["switch"][f]), (switch, f)
+
+
+class TestDeviceValidation:
+    """device.* is called directly by sweep/evaluate/tools: shape and device
+    errors must raise before any pointer reaches the C ABI (a bad k would read
+    out of bounds and poison the context)."""
+
+    def test_inner_dimension_mismatch(self):
+        import torch
+
+        from paper_1702_03192_b200 import device
+
+        a = torch.zeros(64, 32, device="cuda")
+        b = torch.zeros(48, 40, device="cuda")
+        with pytest.raises(ValueError, match="share k"):
+            device.gemm_nt(a, b)
+        with pytest.raises(ValueError, match="share k"):
+            device.gemm_tnn(a, b)
+        with pytest.raises(ValueError, match="share k"):
+            device.gemm_nn(a, torch.zeros(40, 48, device="cuda"))
+        with pytest.raises(ValueError, match="shape"):
+            device.gemm_nt(a, torch.zeros(48, 32, device="cuda"), out=torch.zeros(64, 47, device="cuda"))
+        torch.cuda.synchronize()  # the context is still healthy
+        c = device.gemm_nt(a, torch.ones(48, 32, device="cuda"))
+        assert float(c.abs().sum()) == 0.0
+
+    def test_host_and_device_mix_rejected(self):
+        import torch
+
+        a = torch.zeros(8, 8, device="cuda")
+        with pytest.raises(TypeError):
+            gemm_nt(a, np.zeros((8, 8), np.float32))

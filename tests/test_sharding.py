@@ -110,7 +110,7 @@ def test_dp_weight_grad_world2_gloo(batch):
 
 
 # ---------------------------------------------------------------- GPU
-def _fused_worker(rank, world, port, m, n, k, q):
+def _fused_worker(rank, world, port, m, n, k, q, iters=1):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -125,7 +125,16 @@ def _fused_worker(rank, world, port, m, n, k, q):
         lo, hi = row_range(m, rank, world)
         c = torch.full((m, n), float("nan"), device="cuda")
         pg = PeerGather(c)
-        pg.gemm(a[lo:hi].cuda(), b.cuda(), lo)
+        bd = b.cuda()
+        for it in range(iters):
+            # device-side barriers only (sync=False): earlier iterations write
+            # scaled results that the last one must fully overwrite on every rank
+            scale = float(iters - it)
+            a_it = (a[lo:hi] * scale).cuda()
+            if it % 2:  # a non-contiguous view: the call's temporary must outlive the launch
+                a_it = a_it.t().contiguous().t()
+            pg.gemm(a_it, bd, lo, sync=(it == iters - 1))
+        pg.check_status()
         got = c.cpu().numpy()
         rows = np.unique(np.r_[0, m - 1, np.arange(0, m, 37)])
         want = oracle.oracle_nt_rows(a.numpy(), b.numpy(), rows, np.arange(n))
@@ -136,15 +145,17 @@ def _fused_worker(rank, world, port, m, n, k, q):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m,n,k", [(1024, 768, 512), (600, 300, 264), (2048, 1024, 8192)])
-def test_fused_allgather_two_processes_one_gpu(m, n, k):
+@pytest.mark.parametrize("m,n,k,iters", [(1024, 768, 512, 1), (600, 300, 264, 1), (2048, 1024, 8192, 1),
+                                         (2048, 1024, 1024, 4)])
+def test_fused_allgather_two_processes_one_gpu(m, n, k, iters):
     """Two ranks (processes) share the GPU; each computes its row block with
     the all-gather fused into the GEMM epilogue (stores into the other rank's
     IPC-mapped C). Both ranks then hold the full C (no NaN left, oracle match)."""
     world, port = 2, _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, m, n, k, q)) for r in range(world)]
+    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, m, n, k, q, iters))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
