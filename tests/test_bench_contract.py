@@ -42,7 +42,7 @@ def _check_reference_line(d, n):
 
 def test_reference_arm_single_process():
     out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1",
-                          "--warmup", "1"], capture_output=True, text=True, cwd=str(ROOT),
+                          "--warmup", "1", "--exp-max", "10"], capture_output=True, text=True, cwd=str(ROOT),
                          timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = _json_lines(out.stdout)
@@ -50,12 +50,24 @@ def test_reference_arm_single_process():
     _check_reference_line(lines[0], 1)
 
 
+def test_reference_arm_single_workload():
+    """configs[0]: the full 1024^3 op through both CPU reference paths."""
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1",
+                          "--warmup", "1", "--workload", "single", "--single", "256"],
+                         capture_output=True, text=True, cwd=str(ROOT), timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = _json_lines(out.stdout)
+    assert len(lines) == 1
+    _check_reference_line(lines[0], 1)
+    assert "configs[0]" in lines[0]["config"]["workload"]
+
+
 def test_reference_arm_under_torchrun():
     env = dict(os.environ, OMP_NUM_THREADS="1")
     out = subprocess.run(
         [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
          "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--impl",
-         "reference", "--gpus", "2", "--steps", "1", "--warmup", "1"],
+         "reference", "--gpus", "2", "--steps", "1", "--warmup", "1", "--exp-max", "10"],
         capture_output=True, text=True, cwd=str(ROOT), timeout=600, env=env)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = _json_lines(out.stdout)
@@ -64,7 +76,7 @@ def test_reference_arm_under_torchrun():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("workload", ["sweep", "fcn"])
+@pytest.mark.parametrize("workload", ["sweep", "fcn", "single"])
 def test_gpu_arm_line(workload):
     """The GPU arm's JSON line on a reduced sweep (m,n,k <= 512) and the FCN
     step: roofline, cpu_baseline (sweep), e2e with host copies, launches and
@@ -86,6 +98,15 @@ def test_gpu_arm_line(workload):
     assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
-    if workload == "sweep":
+    assert d["verify"]["failed"] == 0 and d["verify"]["worst_rel_frobenius"] < 1e-5
+    if workload in ("sweep", "single"):
         cb = d["cpu_baseline"]
         assert {"value", "unit", "cores", "kind", "sample"} <= set(cb) and cb["value"] > 0
+        # the reference arm reports the same config (same workload, same cases)
+        ref = subprocess.run(args + ["--impl", "reference", "--steps", "1", "--warmup", "1"],
+                             capture_output=True, text=True, cwd=str(ROOT), timeout=900)
+        assert ref.returncode == 0, ref.stderr[-2000:]
+        assert _json_lines(ref.stdout)[0]["config"] == d["config"]
+    if workload == "sweep":
+        mb = d["mtnn_vs_best_of_both"]
+        assert 0 < mb["mean_per_case_ratio"] <= 1.05 and mb["aggregate_ratio"] <= 1.02

@@ -2,12 +2,13 @@
 fix-up on / off (interleaved blocks), CUDA events around each block."""
 import sys, torch
 sys.path.insert(0, ".")
-from paper_1702_03192_b200 import device, _lib
+from paper_1702_03192_b200 import device, _lib, operands
 
-shapes = [(128, 1024, 256), (256, 256, 4096), (1024, 1024, 1024), (2048, 2048, 2048), (4096, 4096, 4096), (16384, 16384, 1024)]
+shapes = [(128, 1024, 256), (256, 256, 4096), (1024, 1024, 1024), (2048, 2048, 2048), (4096, 4096, 4096),
+          (16384, 16384, 1024), (16384, 128, 16384), (128, 16384, 16384), (8192, 8192, 8192),
+          (16384, 16384, 16384)]
 for (m, n, k) in shapes:
-    a = torch.rand(m, k, device="cuda") * 2 - 1
-    b = torch.rand(n, k, device="cuda") * 2 - 1
+    a, b = operands.make_operands(m, n, k, 0)  # the reference harness's operands
     c = torch.empty(m, n, device="cuda")
     reps = max(5, min(200, int(2e11 / (2 * m * n * k))))
     res = {0: [], 1: []}
