@@ -105,10 +105,13 @@ def measure_case(ops: Operands, m, n, k, reps=5, warmup=2, variant=_lib.VARIANT_
     return CaseTiming(m, n, k, t["nn"], t["nt"], t["tnn"])
 
 
-def sweep(exponents, reps=5, warmup=2, variant=_lib.VARIANT_AUTO, log=None):
-    shapes = grid_shapes(exponents)
-    mx = 2 ** max(exponents)
-    ops = Operands(mx, mx, mx)
+def sweep_shapes(shapes, reps=5, warmup=2, variant=_lib.VARIANT_AUTO, log=None):
+    """CaseTiming per (m, n, k) of `shapes`, in order, on the current device."""
+    shapes = [tuple(int(v) for v in s) for s in shapes]
+    if not shapes:
+        return []
+    ops = Operands(max(s[0] for s in shapes), max(s[1] for s in shapes),
+                   max(s[2] for s in shapes))
     out = []
     for (m, n, k) in shapes:
         ct = measure_case(ops, m, n, k, reps, warmup, variant)
@@ -117,6 +120,72 @@ def sweep(exponents, reps=5, warmup=2, variant=_lib.VARIANT_AUTO, log=None):
             log(f"{m} {n} {k}: nn {ct.t_nn*1e6:.1f}us nt {ct.t_nt*1e6:.1f}us "
                 f"tnn {ct.t_tnn*1e6:.1f}us  NT {2*m*n*k/ct.t_nt/1e12:.1f} TF")
     return out
+
+
+def sweep(exponents, reps=5, warmup=2, variant=_lib.VARIANT_AUTO, log=None, gpus=1, first=0):
+    """The grid sweep; gpus > 1 shards the cases over GPUs first..first+gpus-1."""
+    shapes = grid_shapes(exponents)
+    if gpus > 1:
+        return map_cases_on_gpus(_sweep_worker, shapes, gpus, (reps, warmup, variant), first)
+    return sweep_shapes(shapes, reps, warmup, variant, log)
+
+
+# --------------------------------------------------------- multi-GPU cases
+def lpt_shards(shapes, parts):
+    """Longest-processing-time-first assignment of cases (cost 2mnk) to parts."""
+    loads = [0.0] * parts
+    owner = [0] * len(shapes)
+    for i in sorted(range(len(shapes)), key=lambda j: -(shapes[j][0] * shapes[j][1] * shapes[j][2])):
+        r = min(range(parts), key=lambda q: loads[q])
+        owner[i] = r
+        loads[r] += float(shapes[i][0]) * shapes[i][1] * shapes[i][2]
+    return owner
+
+
+def _sweep_worker(dev, shapes, extra):
+    torch.cuda.set_device(dev)
+    return sweep_shapes(shapes, *extra)
+
+
+def _pool_entry(fn, slot_dev, shapes, extra, q):
+    try:
+        q.put((slot_dev, fn(slot_dev[1], shapes, extra), None))
+    except BaseException as exc:  # noqa: BLE001 - reported to the parent
+        q.put((slot_dev, None, f"{type(exc).__name__}: {exc}"))
+
+
+def map_cases_on_gpus(fn, shapes, gpus, extra, first=0, devices=None):
+    """Run fn(device, shapes_part, extra) -> list (one result per shape) in one
+    process per GPU (spawned; cases LPT-sharded, no collective) and return the
+    results in the order of `shapes`. Independent cases need no exchange.
+    `devices` (tests) overrides the device list first..first+gpus-1."""
+    import multiprocessing as mp
+
+    if devices is None:
+        have = torch.cuda.device_count()
+        if first < 0 or first + gpus > have:
+            raise ValueError(f"GPUs {first}..{first + gpus - 1} requested but {have} CUDA devices "
+                             f"are visible")
+        devices = list(range(first, first + gpus))
+    owner = lpt_shards([tuple(s) for s in shapes], len(devices))
+    parts = [[s for s, o in zip(shapes, owner) if o == d] for d in range(len(devices))]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_pool_entry, args=(fn, (slot, dev), parts[slot], extra, q))
+             for slot, dev in enumerate(devices)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in procs:
+        (slot, dev), res, err = q.get()
+        if err is not None:
+            for p in procs:
+                p.join(timeout=5)
+            raise RuntimeError(f"GPU {dev}: {err}")
+        got[slot] = iter(res)
+    for p in procs:
+        p.join()
+    return [next(got[o]) for o in owner]
 
 
 def write_timings_csv(path, rows):

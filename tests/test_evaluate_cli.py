@@ -128,3 +128,37 @@ def test_cli_demo_fcn_and_sweep_on_gpu(tmp_path, capsys):
                      "--records", str(tmp_path / "r.csv"), "--samples", str(tmp_path / "s.csv"),
                      "--timings", str(tmp_path / "t.csv")]) == 0
     assert len(open(tmp_path / "s.csv").read().splitlines()) == 9
+
+
+def test_lpt_shards_balance():
+    shapes = sweep.grid_shapes(range(7, 12))
+    owner = sweep.lpt_shards(shapes, 4)
+    loads = [sum(m * n * k for (m, n, k), o in zip(shapes, owner) if o == r) for r in range(4)]
+    assert set(owner) == {0, 1, 2, 3} and max(loads) / min(loads) < 1.05
+
+
+def test_cli_device_flags_parse():
+    p = cli.build_parser()
+    a = p.parse_args(["sweep", "--device", "1", "--gpus", "4", "--threads", "8", "--block", "64",
+                      "--tile", "16"])
+    assert (a.device, a.gpus, a.threads) == (1, 4, 8)
+    a = p.parse_args(["eval", "--gpus", "2"])
+    assert a.gpus == 2 and a.device == 0
+    assert p.parse_args(["predict", "--device", "3", "1", "2", "3"]).device == 3
+
+
+@pytest.mark.gpu
+def test_cases_sharded_over_processes_on_gpu():
+    """The --gpus path (one process per GPU, LPT shards, results in grid order),
+    exercised with two processes on GPU 0."""
+    shapes = sweep.grid_shapes(range(7, 9))
+    rows = sweep.map_cases_on_gpus(sweep._sweep_worker, shapes, 2, (2, 1, 0), devices=[0, 0])
+    assert [(r.m, r.n, r.k) for r in rows] == [tuple(s) for s in shapes]
+    assert all(r.t_nt > 0 and r.t_tnn > 0 and r.t_nn > 0 for r in rows)
+    from paper_1702_03192_b200.platform import probe_platform
+
+    d = Dispatcher(gbdt.deserialize_model(golden_model_text("const_pos")), probe_platform())
+    cases = sweep.map_cases_on_gpus(evaluate._eval_worker, [tuple(s) for s in shapes], 2,
+                                    (gbdt.serialize_model(d.model), tuple(d.platform.as_tuple()),
+                                     2, 1, "remeasured"), devices=[0, 0])
+    assert [tuple(c.shape) for c in cases] == [tuple(s) for s in shapes]
