@@ -20,8 +20,9 @@ N > 1 (torchrun, one rank per GPU, NCCL): sweep cases are assigned to ranks
 longest-first (no collective); `large` row-shards A with B broadcast and the
 all-gather of C fused into the GEMM epilogue; `fcn` is data parallel with an
 all-reduce of the weight gradients. `--impl reference` times the reference's
-CPU implementation of the path (the C restatement in oracle/, all host threads)
-on a bounded sample of the same workload and reports the same `config`.
+CPU implementation of the path (the reference itself from baseline/_ref when it
+is installed, else the C restatement in oracle/; all host threads) on a bounded
+sample of the same workload and reports the same `config`.
 """
 
 from __future__ import annotations
@@ -165,16 +166,74 @@ def clock_sampler(index: int):
 
 
 # ----------------------------------------------------------------- CPU legs
-# The reference's CPU path on a bounded sample of the SAME workload: every one of
-# the 512 sweep cases, each on its first r rows of A (r = m for small cases,
-# else enough rows for ~2^28 flop and at least 16 rows, so every host thread
-# gets rows on a 16-core box), at its full n and k. Both reference paths are per-row linear in m —
-# row-dot NT (_numba_impl.py:139-166) and TNN's blocked NN (:31-136) compute
-# each row of C from that row of A and all of B — so a case's time is the
-# sampled time x m/r; TNN also pays its full out-of-place transpose of B
-# (single-threaded, as the reference's gemm_tnn does), timed once per (n, k).
-# The case's CPU time is the faster of the two paths (an upper bound on the
-# reference MTNN, whose selector can only match or miss that choice).
+class CpuRef:
+    """The reference's CPU kernels for the CPU legs. Preferred: the reference
+    itself (baseline/_ref, installed unmodified by tools/install_reference.sh;
+    numba backend, its public kernels API: kernels.gemm_nt / gemm_nn /
+    transpose_oop / gemm_tnn with threads=) — kind "reference". Fallback when
+    it is absent or numba is not importable: the oracle/ C port of the same
+    loops — kind "port" (measured 0.97x the reference on NT and 0.69x on TNN
+    at 16 threads, profiles/ref_vs_port_r02.json). MTNN_BENCH_CPU=port forces
+    the port."""
+
+    def __init__(self):
+        self.kind, self.label = "port", "oracle/ C port of the reference numba kernels"
+        self._k = None
+        ref = ROOT / "baseline" / "_ref"
+        if os.environ.get("MTNN_BENCH_CPU") != "port" and (ref / "mtnn").is_dir():
+            try:
+                os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/mtnn_bench_numba")
+                os.environ["MTNN_BACKEND"] = "numba"
+                sys.path.insert(0, str(ref))
+                from mtnn import kernels as rk  # noqa: WPS433  (the unmodified reference)
+
+                if rk.active_backend() == "numba":
+                    self._k, self.kind = rk, "reference"
+                    self.label = "the reference (baseline/_ref, numba backend, mtnn.kernels API)"
+            except Exception as exc:  # noqa: BLE001 - fall back to the port, say why
+                self.label += f" (reference unavailable: {type(exc).__name__})"
+        if self._k is None:
+            import oracle
+
+            self._o = oracle
+
+    def gemm_nt(self, a, b, threads):
+        return (self._k.gemm_nt(a, b, threads=threads) if self._k else
+                self._o.gemm_nt(a, b, threads=threads))
+
+    def gemm_nn(self, a, bt, threads):
+        return (self._k.gemm_nn(a, bt, threads=threads) if self._k else
+                self._o.gemm_nn(a, bt, threads=threads))
+
+    def transpose(self, b):  # single-threaded in both (the reference has no parallel transpose)
+        return self._k.transpose_oop(b) if self._k else self._o.transpose(b, threads=1)
+
+    def gemm_tnn(self, a, b, threads):
+        return (self._k.gemm_tnn(a, b, threads=threads) if self._k else
+                self._o.gemm_tnn(a, b, threads=threads))
+
+    def warm(self, threads):
+        """JIT-compile / page in every kernel and thread-pool once (untimed)."""
+        rng = np.random.default_rng(1)
+        a = rng.uniform(-1, 1, (64, 48)).astype(np.float32)
+        b = rng.uniform(-1, 1, (40, 48)).astype(np.float32)
+        for t in sorted({1, threads}):
+            self.gemm_nt(a, b, t)
+            self.gemm_nn(a, np.ascontiguousarray(b.T), t)
+            self.gemm_tnn(a, b, t)
+        self.transpose(b)
+
+
+_CPU = None
+
+
+def cpu_ref():
+    global _CPU
+    if _CPU is None:
+        _CPU = CpuRef()
+    return _CPU
+
+
 CPU_ROW_FLOP_CAP = 2 ** 28
 CPU_MIN_ROWS = 16
 
@@ -187,8 +246,7 @@ def cpu_sweep_sample(shapes, threads):
     """(flops, seconds best-of-both, seconds NT, seconds TNN) extrapolated from
     row samples of `shapes`; operands are uniform[-1,1) (timing does not depend
     on the values)."""
-    import oracle
-
+    ref = cpu_ref()
     n_max = max(n for _, n, _ in shapes)
     k_max = max(k for _, _, k in shapes)
     rng = np.random.default_rng(0)
@@ -201,15 +259,15 @@ def cpu_sweep_sample(shapes, threads):
     for (n, k), ms in by_nk.items():
         b = b_buf[: n * k].reshape(n, k)
         t0 = time.perf_counter()
-        bt = oracle.transpose(b, threads=1)
+        bt = ref.transpose(b)
         t_tr = time.perf_counter() - t0
         for m in ms:
             r = cpu_rows(m, n, k)
             a = a_buf[: r * k].reshape(r, k)
             t0 = time.perf_counter()
-            oracle.gemm_nt(a, b, threads=threads)
+            ref.gemm_nt(a, b, threads)
             t1 = time.perf_counter()
-            oracle.gemm_nn(a, bt, threads=threads)
+            ref.gemm_nn(a, bt, threads)
             t2 = time.perf_counter()
             t_nt = (t1 - t0) * m / r
             t_tnn = t_tr + (t2 - t1) * m / r
@@ -222,24 +280,25 @@ def cpu_sweep_sample(shapes, threads):
 
 def cpu_single(m, n, k, threads, seed=0):
     """configs[0]: the full NT op through both reference paths on make_operands."""
-    import oracle
-
-    a, b, _ = oracle.make_operands(m, n, k, seed)
+    ref = cpu_ref()
+    rng = np.random.default_rng(seed)  # make_operands (reference bench.py:104-114)
+    a = rng.uniform(-1.0, 1.0, (m, k)).astype(np.float32)
+    b = rng.uniform(-1.0, 1.0, (n, k)).astype(np.float32)
     t0 = time.perf_counter()
-    oracle.gemm_nt(a, b, threads=threads)
+    ref.gemm_nt(a, b, threads)
     t1 = time.perf_counter()
-    oracle.gemm_tnn(a, b, threads=threads)
+    ref.gemm_tnn(a, b, threads)
     t2 = time.perf_counter()
     return 2.0 * m * n * k, min(t1 - t0, t2 - t1), t1 - t0, t2 - t1
 
 
 def cpu_sample_text(args, threads, per_step=False):
     if args.workload == "single":
-        return (f"the full {args.single}^3 NT op (make_operands seed 0), oracle/ C port of the "
-                f"reference numba kernels, faster of NT / TNN, {threads} threads")
+        return (f"the full {args.single}^3 NT op (make_operands seed 0), {cpu_ref().label}, "
+                f"faster of NT / TNN, {threads} threads")
     if args.workload == "fcn":
-        return (f"the full FCN step (12 products), oracle/ C port of the reference numba kernels, "
-                f"NT products: faster of NT / TNN, {threads} threads")
+        return (f"the full FCN step (12 products), {cpu_ref().label}, NT products: faster of "
+                f"NT / TNN, {threads} threads")
     if per_step:
         return (f"each step: every {CPU_PARTS}th case of the sweep (offset by the step; "
                 f"{CPU_PARTS} steps cover all {len(grid(args.exp_min, args.exp_max))}), "
@@ -247,7 +306,7 @@ def cpu_sample_text(args, threads, per_step=False):
     return (f"all {len(grid(args.exp_min, args.exp_max))} cases of the sweep, each on its first "
             f"min(m, max({CPU_MIN_ROWS}, 2^28 flop / 2nk)) rows of A at full n, k, time scaled by "
             f"m / rows (both reference paths are per-row linear; TNN adds its full single-thread "
-            f"transpose of B per (n, k)); oracle/ C port of the reference numba kernels, faster "
+            f"transpose of B per (n, k)); {cpu_ref().label}, faster "
             f"of NT / TNN per case, {threads} threads")
 
 
@@ -276,8 +335,7 @@ def cpu_fcn(threads):
     """configs[3] on the CPU reference: the FCN step's 12 products at full size
     (forward NT and backward weight-gradient NT: faster of the two reference
     paths; backward NN: the blocked NN kernel)."""
-    import oracle
-
+    ref = cpu_ref()
     rng = np.random.default_rng(0)
     widths = list(FCN_LAYERS)
     layers = list(zip(widths[:-1], widths[1:]))
@@ -291,16 +349,16 @@ def cpu_fcn(threads):
         flops += 2.0 * m * n * k
         if op == "nn":
             t0 = time.perf_counter()
-            oracle.gemm_nn(a, b, threads=threads)
+            ref.gemm_nn(a, b, threads)
             t = time.perf_counter() - t0
             s_best += t
             s_nt += t
             s_tnn += t
             continue
         t0 = time.perf_counter()
-        oracle.gemm_nt(a, b, threads=threads)
+        ref.gemm_nt(a, b, threads)
         t1 = time.perf_counter()
-        oracle.gemm_tnn(a, b, threads=threads)
+        ref.gemm_tnn(a, b, threads)
         t2 = time.perf_counter()
         s_nt += t1 - t0
         s_tnn += t2 - t1
@@ -318,9 +376,10 @@ def host_threads() -> int:
 
 
 def cpu_baseline(args, threads: int):
+    cpu_ref().warm(threads)
     flops, best, s_nt, s_tnn = cpu_run(args, threads)
     return {
-        "value": flops / best / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+        "value": flops / best / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": cpu_ref().kind,
         "sample": cpu_sample_text(args, threads)
                   + f"; always-NT {flops / s_nt / 1e12:.4f}, always-TNN {flops / s_tnn / 1e12:.4f} TFLOP/s",
         "seconds": best,
@@ -328,8 +387,8 @@ def cpu_baseline(args, threads: int):
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU implementation of the path (oracle
-    port), timed on the host cores, rank 0 only, on the same workload/config as
+    """--impl reference: the reference's CPU implementation of the path (CpuRef:
+    the reference itself, else the oracle port), timed on the host cores, rank 0 only, on the same workload/config as
     the GPU arm (a bounded sample of it; see cpu_sweep_sample)."""
     if rank != 0:
         return
@@ -340,7 +399,8 @@ def run_reference(args, rank, world):
                           "CPU reference"}), flush=True)
         return
     threads = host_threads()
-    for _ in range(args.warmup):  # warm caches / the OpenMP pool on a few cases
+    cpu_ref().warm(threads)
+    for _ in range(args.warmup):  # warm caches / the thread pool on a few cases
         if args.workload == "sweep":
             cpu_sweep_sample(grid(args.exp_min, min(args.exp_max, args.exp_min + 2)), threads)
         else:
@@ -361,7 +421,8 @@ def run_reference(args, rank, world):
         "ms_per_step": statistics.mean(walls) * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(args, world, workload_desc(args, world)),
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads,
+                         "kind": cpu_ref().kind,
                          "sample": cpu_sample_text(args, threads, per_step=True),
                          "cpu_seconds_per_step_of_the_covered_cases": statistics.mean(est)},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
