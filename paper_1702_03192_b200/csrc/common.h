@@ -92,6 +92,7 @@ bool tc_eligible(const float* A, const float* B, const float* C, int64_t m, int6
 struct TcOperand {
   const void* hi = nullptr;
   const void* lo = nullptr;
+  // F16S 1/s: per row (K-major), or [ceil(k / kScaleChunkK)][n] for MN-major B^T
   const float* inv_scale = nullptr;
   FixList fix;  // residual entries of this operand (fix.h)
 };
@@ -137,11 +138,12 @@ int launch_split_rows_f16_pair(const float* x0, void* hi0, void* lo0, float* inv
 // 1/s per row (s = split_rows_f16's power-of-two row scale), reading x only.
 int launch_rowmax_f16(const float* x, float* inv_scale, int64_t rows, int64_t k,
                       const FixList& fix, cudaStream_t s);
-// Scratch (device bytes) launch_split_cols_f16 needs for an n-column operand.
-size_t split_cols_scratch_bytes(int64_t n);
-int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,
-                          float* partial_scratch, int64_t k, int64_t n, const FixList& fl,
-                          cudaStream_t s);
+// Rows of an MN-major (k x n) F16S operand that share one column scale: the
+// column split writes inv_scale[ceil(k / kScaleChunkK)][n], and the GEMM applies
+// chunk c's scale to its FP32-promotion chunks covering k rows [256c, 256c+256).
+constexpr int kScaleChunkK = 256;
+int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale, int64_t k,
+                          int64_t n, const FixList& fl, cudaStream_t s);
 
 // Draws skip .. skip + count - 1 of numpy's PCG64 stream with initial
 // (state_lo, state_hi, inc_lo, inc_hi), as uniform(low, high) doubles rounded to

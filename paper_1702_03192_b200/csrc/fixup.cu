@@ -196,6 +196,13 @@ __device__ __forceinline__ unsigned lower_row(const unsigned long long* key, uns
 __device__ __forceinline__ uint32_t key_row(unsigned long long k) { return (uint32_t)(k >> 32); }
 __device__ __forceinline__ uint32_t key_col(unsigned long long k) { return (uint32_t)k; }
 
+// 1/s of B at (row j of B, k index kcol): per row for K-major B (NT), per
+// (kScaleChunkK chunk, column) for MN-major B^T (NN; split_f16.cu)
+template <bool B_NK>
+__device__ __forceinline__ float inv_b_at(const FixupDev& p, int64_t j, int64_t kcol) {
+  return B_NK ? p.inv_b[j] : p.inv_b[(kcol / kScaleChunkK) * p.n + j];
+}
+
 template <bool B_NK>
 __device__ __forceinline__ float b_at(const FixupDev& p, int64_t j, int64_t col) {
   return B_NK ? __ldg(p.B + j * p.k + col) : __ldg(p.B + col * p.ldb + j);
@@ -277,8 +284,8 @@ __global__ void __launch_bounds__(kFixThreads, 2) fixup_kernel(const FixupDev p)
   // Deterministic path: every CTA sorts both lists by (row, k index); each
   // affected output is then updated by exactly one thread, which adds its A
   // terms (k ascending) and its B terms (k ascending) and stores once.
-  // F16S: a term is bounded by |r| * (max of the other operand's row) = |r| *
-  // 2^14 * its 1/s; an output whose corrections are provably below 2^-26 of its
+  // F16S: a term is bounded by |r| * (max of the other operand's row, or of
+  // the MN-major B column's scale chunk) = |r| * 2^14 * its 1/s; an output whose corrections are provably below 2^-26 of its
   // value (uniform data: all of them) is left as it is, so it costs one read of
   // C and of the row scales instead of the strided gathers of B's column / A's
   // column.
@@ -303,17 +310,21 @@ __global__ void __launch_bounds__(kFixThreads, 2) fixup_kernel(const FixupDev p)
       const int64_t i = (int64_t)grow - p.a_row0;
       const int64_t j = (it % cn) * kFixThreads + threadIdx.x;
       if (i < 0 || i >= p.m || j >= p.n) continue;
+      // bound of the A terms: sum |r| * max|B[j, p]| (<= 2^14 / s of B's row j,
+      // or of column j's scale chunk holding p for an MN-major B)
       unsigned e1 = e0;
       float ra = 0.f;
-      while (e1 < na && key_row(ka[e1]) == grow) ra += fabsf(va[e1++]);
+      while (e1 < na && key_row(ka[e1]) == grow) {
+        ra += fabsf(va[e1]) * (bounded ? inv_b_at<B_NK>(p, j, key_col(ka[e1])) : 0.f);
+        ++e1;
+      }
       const uint32_t gcol = (uint32_t)(j + p.b_row0);
       const unsigned b0 = nb ? lower_row(kb, nb, gcol) : 0u;
       unsigned b1 = b0;
       float rb = 0.f;
       while (b1 < nb && key_row(kb[b1]) == gcol) rb += fabsf(vb[b1++]);
       const float c = p.C[0][i * p.ldc + j];
-      if (bounded &&
-          ra * kRowMax * p.inv_b[j] + rb * kRowMax * p.inv_a[i] <= kNegligible * fabsf(c))
+      if (bounded && ra * kRowMax + rb * kRowMax * p.inv_a[i] <= kNegligible * fabsf(c))
         continue;
       float s = 0.f;
       for (unsigned e = e0; e < e1; ++e) s = fmaf(va[e], b_at<B_NK>(p, j, key_col(ka[e])), s);

@@ -352,6 +352,35 @@ __device__ __forceinline__ void split8_f16(const float4& x0, const float4& x1, f
   lw = make_uint4(lp[0], lp[1], lp[2], lp[3]);
 }
 
+// MN-major F16S B: the exact column scales (powers of two) of one promotion
+// chunk for an epilogue warp's kCols columns, lane l holding columns l, 32 + l,
+// ... (coalesced loads, one per 32 columns; columns >= n get 0: never stored).
+template <int kCols>
+struct ChunkScales {
+  float v[kCols / 32];
+};
+template <int kCols>
+__device__ __forceinline__ ChunkScales<kCols> load_chunk_scales(const float* inv_b, int chunk,
+                                                                int64_t n, int64_t col0, int lane) {
+  const float* sc = inv_b + (int64_t)chunk * n + col0;
+  ChunkScales<kCols> c;
+#pragma unroll
+  for (int i = 0; i < kCols / 32; ++i) c.v[i] = col0 + 32 * i + lane < n ? __ldg(sc + 32 * i + lane) : 0.f;
+  return c;
+}
+// Adds 16 TMEM columns (the c16-th group of the warp's) of one chunk into the
+// FP32 sums, each scaled by its column's chunk scale (x * 2^e is exact, so the
+// sum rounds once per chunk exactly as the unscaled path does).
+template <int kCols>
+__device__ __forceinline__ void add_chunk_scaled(float* sum, const uint32_t (&r)[16],
+                                                 const ChunkScales<kCols>& cs, int c16) {
+  const float src = cs.v[c16 / 2];
+  const int base = (c16 & 1) * 16;
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    sum[j] += __uint_as_float(r[j]) * __shfl_sync(0xffffffffu, src, base + j);
+}
+
 // ------------------------------------------------------------------- kernel
 // kConv: 0 = both operands come split from the pre-pass; 1 / 2 = operand A / B
 // is read raw (fp32, 4 B per element from DRAM, no split pass) and split
@@ -378,6 +407,11 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
   using R = Roles<kF16Conv>;
   using S = Smem<BN, kF16Conv ? kF16ConvRows * 128 : 0, R::kEpi>;
   constexpr int kColsPerWarp = BN / (R::kEpi / 4);  // each epilogue warp: a column slice
+  // MN-major F16S B carries one scale per (kScaleChunkK rows, column): applied
+  // per promotion chunk (the host keeps chunks and k-splits aligned to it)
+  constexpr bool kChunkB = B_MN && Kind::kScaled;
+  constexpr int kScaleKb = kScaleChunkK / Kind::BK;
+  static_assert(kColsPerWarp % 32 == 0, "chunk scales: 32-column groups per epilogue warp");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -667,10 +701,15 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
       unit_coords(u, p, split, tm, tn);
       const int kb0 = split * kb_per;
       const int kb1 = min(p.total_kblocks, kb0 + kb_per);
+      const int64_t row = (int64_t)tm * BM + q * 32 + lane;
+      const int64_t col0 = (int64_t)tn * BN + h * kColsPerWarp;
       float sum[kColsPerWarp];
 #pragma unroll
       for (int j = 0; j < kColsPerWarp; ++j) sum[j] = 0.f;
       for (int kc = kb0; kc < kb1; kc += p.chunk_kb) {
+        // (the chunk's column scales load while the MMAs of the chunk finish)
+        ChunkScales<kColsPerWarp> cs{};
+        if (kChunkB) cs = load_chunk_scales<kColsPerWarp>(p.inv_scale_b, kc / kScaleKb, p.n, col0, lane);
         mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + h * kColsPerWarp;
@@ -679,8 +718,13 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
           uint32_t r[16];
           tmem_ld_32x32b_x16(taddr + c * 16, r);
           tmem_ld_wait();
+          if (kChunkB) {
+            // MN-major F16S B: this promotion chunk's exact column scales
+            add_chunk_scaled(sum + c * 16, r, cs, c);
+          } else {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) sum[c * 16 + j] += __uint_as_float(r[j]);
+            for (int j = 0; j < 16; ++j) sum[c * 16 + j] += __uint_as_float(r[j]);
+          }
         }
         tc_fence_before();
         __syncwarp();
@@ -688,9 +732,7 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
       // KindF16S: undo the exact power-of-two operand scales while storing,
-      // C = (acc * 1/s_a[row]) * 1/s_b[col]
-      const int64_t row = (int64_t)tm * BM + q * 32 + lane;
-      const int64_t col0 = (int64_t)tn * BN + h * kColsPerWarp;
+      // C = (acc * 1/s_a[row]) * 1/s_b[col] (MN-major B: applied per chunk above)
       const float sa = (Kind::kScaled && row < p.m) ? __ldg(p.inv_scale_a + row) : 1.f;
       // Store: 32 rows x kColsPerWarp through a 32x16 staging tile (64B swizzle).
 #pragma unroll
@@ -702,7 +744,9 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
           const int pj = j ^ ((lane >> 1) & 3);
           float4 v = make_float4(sum[c * 16 + 4 * j], sum[c * 16 + 4 * j + 1],
                                  sum[c * 16 + 4 * j + 2], sum[c * 16 + 4 * j + 3]);
-          if (Kind::kScaled) {
+          if (Kind::kScaled && kChunkB) {
+            v.x *= sa; v.y *= sa; v.z *= sa; v.w *= sa;
+          } else if (Kind::kScaled) {
             // the scale vector has n entries (n % 4 == 0): whole float4s are in range
             const int64_t cj = col0 + c * 16 + 4 * j;
             const float4 sb = cj < p.n ? __ldg(reinterpret_cast<const float4*>(p.inv_scale_b + cj))
@@ -1030,6 +1074,9 @@ gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
   using S = PairSmem;
   constexpr int BN = kPairBN;
   constexpr int kColsPerWarp = BN / 4;
+  constexpr bool kChunkB = B_MN && Kind::kScaled;  // see gemm_tc3x_kernel
+  constexpr int kScaleKb = kScaleChunkK / Kind::BK;
+  static_assert(kColsPerWarp % 32 == 0, "chunk scales: 32-column groups per epilogue warp");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1190,10 +1237,15 @@ gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
       const int tm = 2 * tmp + (int)rank;
       const int kb0 = split * kb_per;
       const int kb1 = min(p.total_kblocks, kb0 + kb_per);
+      const int64_t row = (int64_t)tm * BM + q * 32 + lane;
+      const int64_t col0 = (int64_t)tn * BN + h * kColsPerWarp;
       float sum[kColsPerWarp];
 #pragma unroll
       for (int j = 0; j < kColsPerWarp; ++j) sum[j] = 0.f;
       for (int kc = kb0; kc < kb1; kc += p.chunk_kb) {
+        // (the chunk's column scales load while the MMAs of the chunk finish)
+        ChunkScales<kColsPerWarp> cs{};
+        if (kChunkB) cs = load_chunk_scales<kColsPerWarp>(p.inv_scale_b, kc / kScaleKb, p.n, col0, lane);
         mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + h * kColsPerWarp;
@@ -1202,16 +1254,18 @@ gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
           uint32_t r[16];
           tmem_ld_32x32b_x16(taddr + c * 16, r);
           tmem_ld_wait();
+          if (kChunkB) {
+            add_chunk_scaled(sum + c * 16, r, cs, c);
+          } else {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) sum[c * 16 + j] += __uint_as_float(r[j]);
+            for (int j = 0; j < 16; ++j) sum[c * 16 + j] += __uint_as_float(r[j]);
+          }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cta(smem_u32(&tempty_bar[acc]), 0);  // the leader's
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
-      const int64_t row = (int64_t)tm * BM + q * 32 + lane;
-      const int64_t col0 = (int64_t)tn * BN + h * kColsPerWarp;
       const float sa = (Kind::kScaled && row < p.m) ? __ldg(p.inv_scale_a + row) : 1.f;
 #pragma unroll
       for (int c = 0; c < kColsPerWarp / 16; ++c) {
@@ -1222,7 +1276,9 @@ gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
           const int pj = j ^ ((lane >> 1) & 3);
           float4 v = make_float4(sum[c * 16 + 4 * j], sum[c * 16 + 4 * j + 1],
                                  sum[c * 16 + 4 * j + 2], sum[c * 16 + 4 * j + 3]);
-          if (Kind::kScaled) {
+          if (Kind::kScaled && kChunkB) {
+            v.x *= sa; v.y *= sa; v.z *= sa; v.w *= sa;
+          } else if (Kind::kScaled) {
             const int64_t cj = col0 + c * 16 + 4 * j;
             const float4 sb = cj < p.n ? __ldg(reinterpret_cast<const float4*>(p.inv_scale_b + cj))
                                        : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1329,6 +1385,19 @@ static int chunk_kblocks(TcKind) {
     return x > 0 ? x : 8;
   }();
   return v;
+}
+
+// MN-major F16S B has one scale per kScaleChunkK k-rows (split_f16.cu): every
+// promotion chunk and every k-split must then lie inside one scale chunk —
+// chunk_kb divides the scale chunk's k-blocks and k-splits start on its
+// boundaries (kblocks_per_split rounded up to a multiple of it).
+static void align_scale_chunks(tc::Params& p, TcKind kind, bool b_is_nk, int splits) {
+  p.kblocks_per_split = (p.total_kblocks + splits - 1) / splits;
+  if (kind == TcKind::F16S && !b_is_nk) {
+    constexpr int sk = kScaleChunkK / tc::KindF16S::BK;
+    if (sk % p.chunk_kb != 0) p.chunk_kb = sk;
+    p.kblocks_per_split = (p.kblocks_per_split + sk - 1) / sk * sk;
+  }
 }
 
 // TF32 kind, opt-in (MTNN_TF32_INKERNEL=1): the kernel computes the larger
@@ -1469,19 +1538,18 @@ int tc_prepare(const float* X, int64_t rows, int64_t k, bool mn_major, TcKind ki
     out->inv_scale = nullptr;
     return MTNN_OK;
   }
-  // F16S: [h | l | 1/s (+ partial column maxima) | residual entries]
+  // F16S: [h | l | 1/s | residual entries]; MN-major: 1/s per (256-row chunk, column)
   const size_t oh = align256((size_t)count * 2);
-  const size_t osc = align256((size_t)rows * 4);
-  const size_t ocm = mn_major ? align256(split_cols_scratch_bytes(rows)) : 0;
-  MTNN_TRY(ws.alloc(2 * oh + osc + ocm + fix_bytes, s));
+  const int64_t scale_rows = mn_major ? (k + kScaleChunkK - 1) / kScaleChunkK : 1;
+  const size_t osc = align256((size_t)(scale_rows * rows) * 4);
+  MTNN_TRY(ws.alloc(2 * oh + osc + fix_bytes, s));
   uint8_t* base = static_cast<uint8_t*>(ws.ptr);
   float* inv = reinterpret_cast<float*>(base + 2 * oh);
-  MTNN_TRY(attach(base + 2 * oh + osc + ocm));
+  MTNN_TRY(attach(base + 2 * oh + osc));
   if (!mn_major) {
     MTNN_TRY(launch_split_rows_f16(X, base, base + oh, inv, rows, k, out->fix, s));
   } else {
-    float* cm = reinterpret_cast<float*>(base + 2 * oh + osc);
-    MTNN_TRY(launch_split_cols_f16(X, base, base + oh, inv, cm, k, rows, out->fix, s));
+    MTNN_TRY(launch_split_cols_f16(X, base, base + oh, inv, k, rows, out->fix, s));
   }
   out->hi = base;
   out->lo = base + oh;
@@ -1626,7 +1694,7 @@ static int tc_run_pair(const TcOperand& a, const TcOperand& b, float* C, int64_t
   // peer stores go straight from the epilogue: no split-K partials
   int splits = npeers > 0 ? 1 : choose_splits(tiles, p.total_kblocks, m, n, pairs);
   p.npeers = npeers;
-  p.kblocks_per_split = (p.total_kblocks + splits - 1) / splits;
+  align_scale_chunks(p, kind, b_is_nk, splits);
   splits = (p.total_kblocks + p.kblocks_per_split - 1) / p.kblocks_per_split;
   p.splits = splits;
   p.units = tiles * splits;
@@ -1669,7 +1737,7 @@ static int tc_run_bn(const TcOperand& a, const TcOperand& b, float* C, int64_t m
   p.total_kblocks = (int)((k + bk - 1) / bk);
   const int tiles = p.tiles_m * p.tiles_n;
   int splits = choose_splits(tiles, p.total_kblocks, m, n, di->sm_count);
-  p.kblocks_per_split = (p.total_kblocks + splits - 1) / splits;
+  align_scale_chunks(p, kind, b_is_nk, splits);
   splits = (p.total_kblocks + p.kblocks_per_split - 1) / p.kblocks_per_split;
   p.splits = splits;
   p.units = tiles * splits;

@@ -11,15 +11,17 @@
 // TF32 but runs at twice the tensor-core rate, and the per-row scale removes its
 // range limit (subnormal tails sit ~2^-38 below the row maximum).
 //
+// MN-major operands (B^T of NN, k x n) get one scale per (256-row chunk,
+// column) instead of one per column: the GEMM's epilogue applies it to each
+// FP32-promotion chunk (gemm_tc.cu), which makes the column split a single
+// local pass.
+//
 // Traffic: the row splits (K-major operands) read each element from DRAM once
-// and write its halves once — 4 B + 4 B; the column splits (MN-major B^T) do the
-// same (strip kernel: the second read hits L2; cluster kernel: registers),
-// except the two-pass band kernel for k > 8192 — 8 B read + 4 B written.
+// and write its halves once — 4 B + 4 B; the column split does the same.
 //
 // Kernels by shape: rows — register warp (k <= 512, 1024 < k <= 2048), looped
 // warp (k = 1024), register CTA (2048 < k <= 16384), smem CTA (longer rows);
-// columns — single-CTA strip (k <= 1024, many strips), cluster strip with a
-// DSMEM max exchange (k <= 8192), two-pass band (beyond).
+// columns — one CTA per (256-row chunk, 32 columns).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -490,257 +492,88 @@ bool ctareg_enabled() {
   return on == 1;
 }
 
-// Two-pass column split (MN-major B^T, k x n, any k): pass 1 writes per-chunk
-// partial column maxima (chunk = a band of rows; no atomics, no memset), pass 2
-// folds the <= kMaxChunks partials of its columns once per thread and streams
-// its band. 256 threads = 32 16-byte columns (512 contiguous bytes of a row per
-// warp) x 8 row lanes. DRAM: 4 B read + (4 B read, mostly L2 for operands that
-// fit) + 4 B written per element.
-constexpr int kMaxChunks = 32;
-
-template <int kLanes>
-__global__ void __launch_bounds__(256)
-colmax_partial_kernel(const float* __restrict__ x, float* __restrict__ partial, int64_t k,
-                      int64_t n, int64_t rows_per_chunk) {
-  pdl_wait();
-  constexpr int kBandCols = 4 * kLanes, kBandRowLanes = 256 / kLanes;
-  __shared__ float4 red[kBandRowLanes][kLanes];
-  const int c4 = threadIdx.x % kLanes;
-  const int rl = threadIdx.x / kLanes;
-  const int64_t col = (int64_t)blockIdx.x * kBandCols + 4 * c4;
-  const int64_t r0 = (int64_t)blockIdx.y * rows_per_chunk;
-  const int64_t r1 = min(k, r0 + rows_per_chunk);
-  float4 mx = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (col < n) {
-#pragma unroll 4
-    for (int64_t r = r0 + rl; r < r1; r += kBandRowLanes) {
-      const float4 v = ldg4(reinterpret_cast<const float4*>(x + r * n + col));
-      mx.x = isnan(v.x) ? INFINITY : fmaxf(mx.x, fabsf(v.x));
-      mx.y = isnan(v.y) ? INFINITY : fmaxf(mx.y, fabsf(v.y));
-      mx.z = isnan(v.z) ? INFINITY : fmaxf(mx.z, fabsf(v.z));
-      mx.w = isnan(v.w) ? INFINITY : fmaxf(mx.w, fabsf(v.w));
-    }
-  }
-  red[rl][c4] = mx;
-  __syncthreads();
-  if (rl == 0 && col < n) {
-    for (int i = 1; i < kBandRowLanes; ++i) {
-      const float4 o = red[i][c4];
-      mx.x = fmaxf(mx.x, o.x); mx.y = fmaxf(mx.y, o.y); mx.z = fmaxf(mx.z, o.z); mx.w = fmaxf(mx.w, o.w);
-    }
-    *reinterpret_cast<float4*>(partial + (int64_t)blockIdx.y * n + col) = mx;
-  }
-}
-
-template <int kLanes>
-__global__ void __launch_bounds__(256)
-split_cols_band_kernel(const float* __restrict__ x, const float* __restrict__ partial, int chunks,
-                       __half* __restrict__ hi, __half* __restrict__ lo,
-                       float* __restrict__ inv_scale, int64_t k, int64_t n,
-                       int64_t rows_per_band, const FixList fl) {
-  pdl_trigger();
-  pdl_wait();
-  constexpr int kBandCols = 4 * kLanes, kBandRowLanes = 256 / kLanes;
-  const int c4 = threadIdx.x % kLanes;
-  const int rl = threadIdx.x / kLanes;
-  const int64_t col = (int64_t)blockIdx.x * kBandCols + 4 * c4;
-  if (col >= n) return;
-  float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int q = 0; q < chunks; ++q) {
-    const float4 o = ldg4(reinterpret_cast<const float4*>(partial + (int64_t)q * n + col));
-    m.x = fmaxf(m.x, o.x); m.y = fmaxf(m.y, o.y); m.z = fmaxf(m.z, o.z); m.w = fmaxf(m.w, o.w);
-  }
-  const float4 sc = make_float4(pow2_scale(m.x), pow2_scale(m.y), pow2_scale(m.z), pow2_scale(m.w));
-  const float4 inv = track_inv4(m, sc);
-  if (blockIdx.y == 0 && rl == 0)
-    *reinterpret_cast<float4*>(inv_scale + col) =
-        make_float4(1.f / sc.x, 1.f / sc.y, 1.f / sc.z, 1.f / sc.w);
-  const int64_t r0 = (int64_t)blockIdx.y * rows_per_band;
-  const int64_t r1 = min(k, r0 + rows_per_band);
-#pragma unroll 4
-  for (int64_t r = r0 + rl; r < r1; r += kBandRowLanes) {
-    const int64_t i = r * n + col;
-    const float4 v = ldg4(reinterpret_cast<const float4*>(x + i));
-    uint2 hw, lw;
-    split_col4(v, sc, inv, hw, lw, fl, col, r);
-    reinterpret_cast<uint2*>(hi)[i / 4] = hw;
-    reinterpret_cast<uint2*>(lo)[i / 4] = lw;
-  }
-}
-
-// Column split in one launch (MN-major B^T, k x n, n % 16 == 0): one CTA per
-// strip of 32 columns (128 bytes per row), 512 threads = 8 16-byte columns x 64
-// row lanes. Pass 1 reads the strip for the column maxima (reduced through
-// shared memory), pass 2 re-reads it — from L2 while the strips in flight fit
-// there — and writes the halves: 8 B of DRAM traffic per element instead of the
-// two-pass band path's 12, and no scratch. Used for k <= 1024 with >= 74 strips.
-constexpr int kStripCols = 32;
-constexpr int kStripLanes = 64;
-
-__global__ void __launch_bounds__(8 * kStripLanes)
-split_cols_strip_kernel(const float* __restrict__ x, __half* __restrict__ hi,
-                        __half* __restrict__ lo, float* __restrict__ inv_scale, int64_t k,
-                        int64_t n, const FixList fl) {
-  pdl_trigger();
-  pdl_wait();
-  __shared__ float4 red[kStripLanes][8];
-  __shared__ float4 scale[8];
-  __shared__ float4 tinv_s[8];
-  const int c4 = threadIdx.x % 8;
-  const int rl = threadIdx.x / 8;
-  const int64_t col = (int64_t)blockIdx.x * kStripCols + 4 * c4;
-  const bool active = col < n;  // n % 4 == 0: the whole float4 is in range
-  float4 mx = make_float4(0.f, 0.f, 0.f, 0.f);
-  float4 mn = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
-  if (active) {
-#pragma unroll 4
-    for (int64_t r = rl; r < k; r += kStripLanes) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(x + r * n + col));
-      mn = absmin_nz_each(mn, v);
-      mx.x = isnan(v.x) ? INFINITY : fmaxf(mx.x, fabsf(v.x));
-      mx.y = isnan(v.y) ? INFINITY : fmaxf(mx.y, fabsf(v.y));
-      mx.z = isnan(v.z) ? INFINITY : fmaxf(mx.z, fabsf(v.z));
-      mx.w = isnan(v.w) ? INFINITY : fmaxf(mx.w, fabsf(v.w));
-    }
-  }
-  red[rl][c4] = mx;
-  __syncthreads();
-  if (threadIdx.x < 8) {
-    float4 m = red[0][threadIdx.x];
-    for (int i = 1; i < kStripLanes; ++i) {
-      const float4 o = red[i][threadIdx.x];
-      m.x = fmaxf(m.x, o.x); m.y = fmaxf(m.y, o.y); m.z = fmaxf(m.z, o.z); m.w = fmaxf(m.w, o.w);
-    }
-    const float4 sc = make_float4(pow2_scale(m.x), pow2_scale(m.y), pow2_scale(m.z), pow2_scale(m.w));
-    scale[threadIdx.x] = sc;
-    tinv_s[threadIdx.x] = track_inv4(m, sc);
-    const int64_t c = (int64_t)blockIdx.x * kStripCols + 4 * threadIdx.x;
-    if (c < n)
-      *reinterpret_cast<float4*>(inv_scale + c) =
-          make_float4(1.f / sc.x, 1.f / sc.y, 1.f / sc.z, 1.f / sc.w);
-  }
-  __syncthreads();
-  if (!active) return;
-  const float4 sc = scale[c4];
-  const float4 inv = tinv_s[c4];
-  const bool chk = fl.ctr != nullptr && col_candidates(mn, inv);
-#pragma unroll 4
-  for (int64_t r = rl; r < k; r += kStripLanes) {
-    const int64_t i = r * n + col;
-    const float4 v = ldg4(reinterpret_cast<const float4*>(x + i));
-    uint2 hw, lw;
-    split_col4x(chk, v, sc, inv, hw, lw, fl, col, r);
-    reinterpret_cast<uint2*>(hi)[i / 4] = hw;
-    reinterpret_cast<uint2*>(lo)[i / 4] = lw;
-  }
-}
-
-// Column split by thread-block clusters (MN-major B^T, k x n, k <= 8192): a
-// cluster of c <= 8 CTAs owns one strip of 32 columns, CTA q holds rows
-// [q*32*kR, (q+1)*32*kR) of it in registers (256 threads = 8 16-byte columns x
-// 32 row lanes, kR rows each). The column maxima are reduced inside each CTA,
-// exchanged through distributed shared memory, and the halves are written from
-// the same registers: one DRAM read and one write per element (8 B), every load
-// issued up front, and strips x c CTAs to cover the SMs even when n is narrow
-// (the single-CTA strip kernel above leaves n = 4096 at ~2.3 TB/s).
-constexpr int kClusterRowLanes = 32;
-constexpr int kClusterMax = 8;
-
-__device__ __forceinline__ uint32_t cl_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t cl_size() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cl_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ float4 ld_dsmem(const float4* p, uint32_t rank) {
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
-  uint32_t ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(ra)
-               : "memory");
-  return v;
-}
+// Column split (MN-major B^T, k x n) with one scale per 256-row chunk of each
+// column (kScaleChunkK, the GEMM's FP32-promotion period): the GEMM epilogue
+// multiplies each TMEM chunk partial by its chunk's exact 1/s (gemm_tc.cu), so
+// a chunk's scale only needs that chunk's maximum. Every (chunk, 32-column)
+// block is then independent: one CTA reads its 256 x 32 block once (8 16-byte
+// loads per thread, all issued before the first use), reduces the column
+// maxima (shuffles + one shared-memory round), and writes the halves from
+// registers — 8 B of DRAM traffic per element, no cross-CTA exchange, no second
+// read, and (k/256) x (n/32) CTAs in flight instead of the cluster strips'
+// serialised load/reduce/store phases (k = n = 4096: 43 us at 1.6 TB/s of reads
+// -> this kernel). inv_scale is [ceil(k/256)][n].
 __device__ __forceinline__ float nanmax(float m, float v) {
   return isnan(v) ? INFINITY : fmaxf(m, fabsf(v));
 }
 
-template <int kR>
-__global__ void __launch_bounds__(8 * kClusterRowLanes)
-split_cols_cluster_kernel(const float* __restrict__ x, __half* __restrict__ hi,
-                          __half* __restrict__ lo, float* __restrict__ inv_scale, int64_t k,
-                          int64_t n, const FixList fl) {
+constexpr int kColBlockCols = 32;
+constexpr int kColRowLanes = 32;
+constexpr int kColRowsPerLane = kScaleChunkK / kColRowLanes;  // 8
+
+__global__ void __launch_bounds__(8 * kColRowLanes)
+split_cols_chunk_kernel(const float* __restrict__ x, __half* __restrict__ hi,
+                        __half* __restrict__ lo, float* __restrict__ inv_scale, int64_t k,
+                        int64_t n, const FixList fl) {
   pdl_trigger();
   pdl_wait();
-  __shared__ float4 red[kClusterRowLanes][8];
-  __shared__ float4 part[8];
+  __shared__ float4 wmax[8][8];  // [warp][16-byte column]
   __shared__ float4 scale[8];
   __shared__ float4 tinv_s[8];
-  const uint32_t csize = cl_size(), rank = cl_rank();
   const int c4 = threadIdx.x % 8;
-  const int rl = threadIdx.x / 8;
-  const int64_t strip = blockIdx.x / csize;
-  const int64_t col = strip * kStripCols + 4 * c4;
+  const int rl = threadIdx.x / 8;      // 0..31; a warp holds row lanes 4w..4w+3
+  const int warp = threadIdx.x / 32;
+  const int64_t col = (int64_t)blockIdx.x * kColBlockCols + 4 * c4;
   const bool active = col < n;  // n % 4 == 0: the whole float4 is in range
-  const int64_t r0 = (int64_t)rank * kClusterRowLanes * kR + rl;
-  float4 v[kR];
-  float4 mx = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int64_t r0 = (int64_t)blockIdx.y * kScaleChunkK + rl;
+  float4 v[kColRowsPerLane];
 #pragma unroll
-  for (int u = 0; u < kR; ++u) {
-    const int64_t r = r0 + kClusterRowLanes * u;
+  for (int u = 0; u < kColRowsPerLane; ++u) {
+    const int64_t r = r0 + kColRowLanes * u;
     v[u] = (active && r < k) ? ldg4(reinterpret_cast<const float4*>(x + r * n + col))
                              : make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  float4 mx = make_float4(0.f, 0.f, 0.f, 0.f);
   float4 mn = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
 #pragma unroll
-  for (int u = 0; u < kR; ++u) {
+  for (int u = 0; u < kColRowsPerLane; ++u) {
     mx.x = nanmax(mx.x, v[u].x); mx.y = nanmax(mx.y, v[u].y);
     mx.z = nanmax(mx.z, v[u].z); mx.w = nanmax(mx.w, v[u].w);
     mn = absmin_nz_each(mn, v[u]);
   }
-  red[rl][c4] = mx;
+  // lanes 8 and 16 apart hold the same columns
+#pragma unroll
+  for (int off = 8; off < 32; off <<= 1) {
+    mx.x = fmaxf(mx.x, __shfl_xor_sync(0xffffffffu, mx.x, off));
+    mx.y = fmaxf(mx.y, __shfl_xor_sync(0xffffffffu, mx.y, off));
+    mx.z = fmaxf(mx.z, __shfl_xor_sync(0xffffffffu, mx.z, off));
+    mx.w = fmaxf(mx.w, __shfl_xor_sync(0xffffffffu, mx.w, off));
+  }
+  if (threadIdx.x % 32 < 8) wmax[warp][c4] = mx;
   __syncthreads();
   if (threadIdx.x < 8) {
-    float4 m = red[0][threadIdx.x];
-    for (int i = 1; i < kClusterRowLanes; ++i) {
-      const float4 o = red[i][threadIdx.x];
-      m.x = fmaxf(m.x, o.x); m.y = fmaxf(m.y, o.y); m.z = fmaxf(m.z, o.z); m.w = fmaxf(m.w, o.w);
-    }
-    part[threadIdx.x] = m;
-  }
-  cl_sync();  // every CTA's partial maxima are visible cluster-wide
-  if (threadIdx.x < 8) {
-    float4 m = part[threadIdx.x];
-    for (uint32_t q = 0; q < csize; ++q) {
-      if (q == rank) continue;
-      const float4 o = ld_dsmem(&part[threadIdx.x], q);
+    float4 m = wmax[0][threadIdx.x];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+      const float4 o = wmax[w][threadIdx.x];
       m.x = fmaxf(m.x, o.x); m.y = fmaxf(m.y, o.y); m.z = fmaxf(m.z, o.z); m.w = fmaxf(m.w, o.w);
     }
     const float4 sc = make_float4(pow2_scale(m.x), pow2_scale(m.y), pow2_scale(m.z), pow2_scale(m.w));
     scale[threadIdx.x] = sc;
     tinv_s[threadIdx.x] = track_inv4(m, sc);
-    const int64_t c = strip * kStripCols + 4 * threadIdx.x;
-    if (rank == 0 && c < n)
-      *reinterpret_cast<float4*>(inv_scale + c) =
+    const int64_t c = (int64_t)blockIdx.x * kColBlockCols + 4 * threadIdx.x;
+    if (c < n)
+      *reinterpret_cast<float4*>(inv_scale + (int64_t)blockIdx.y * n + c) =
           make_float4(1.f / sc.x, 1.f / sc.y, 1.f / sc.z, 1.f / sc.w);
   }
-  cl_sync();  // peers are done reading `part` (no CTA exits under a reader); scale is visible
+  __syncthreads();
   if (!active) return;
   const float4 sc = scale[c4];
   const float4 inv = tinv_s[c4];
   const bool chk = fl.ctr != nullptr && col_candidates(mn, inv);
 #pragma unroll
-  for (int u = 0; u < kR; ++u) {
-    const int64_t r = r0 + kClusterRowLanes * u;
+  for (int u = 0; u < kColRowsPerLane; ++u) {
+    const int64_t r = r0 + kColRowLanes * u;
     if (r < k) {
       uint2 hw, lw;
       split_col4x(chk, v[u], sc, inv, hw, lw, fl, col, r);
@@ -749,31 +582,6 @@ split_cols_cluster_kernel(const float* __restrict__ x, __half* __restrict__ hi,
       reinterpret_cast<uint2*>(lo)[i] = lw;
     }
   }
-}
-
-template <int kR>
-int launch_cols_cluster(const float* x, void* hi, void* lo, float* inv_scale, int64_t k,
-                        int64_t n, const FixList& fl, cudaStream_t s) {
-  const int64_t strips = (n + kStripCols - 1) / kStripCols;
-  const unsigned c = (unsigned)((k + kClusterRowLanes * kR - 1) / (kClusterRowLanes * kR));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(strips * c));
-  cfg.blockDim = dim3(8 * kClusterRowLanes);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = c;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = chain_enabled() ? 2 : 1;
-  MTNN_CUDA_TRY(cudaLaunchKernelEx(&cfg, split_cols_cluster_kernel<kR>, x,
-                                   static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale,
-                                   k, n, fl));
-  return MTNN_OK;
 }
 
 }  // namespace
@@ -844,69 +652,16 @@ int launch_rowmax_f16(const float* x, float* inv_scale, int64_t rows, int64_t k,
                                     nullptr, nullptr, 0, FixList{}, k, s);
 }
 
-size_t split_cols_scratch_bytes(int64_t n) { return (size_t)kMaxChunks * (size_t)n * sizeof(float); }
-
-int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale,
-                          float* partial_scratch, int64_t k, int64_t n, const FixList& fl,
-                          cudaStream_t s) {
+int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale, int64_t k,
+                          int64_t n, const FixList& fl, cudaStream_t s) {
   if (k <= 0 || n <= 0) return MTNN_OK;
-  const DeviceInfo* di = nullptr;
-  MTNN_TRY(device_info(&di));
-  const int64_t strips = (n + kStripCols - 1) / kStripCols;
-  // MTNN_SPLIT_STRIP=0 forces the two-pass band path. Measured split times
-  // (NN calls, us; strip / cluster / band): k = 784, n = 4096: 21.6 / 25.0 / 27.7;
-  // k = 1024, n = 16384: 42.0 / 51.3 / 50.3; k = n = 4096: 72 / 52 / 55;
-  // k = n = 2048: - / 24-29 / 36; k = 8192, n = 8192: - / 205 / 201.
-  static const bool strip_on = [] {
-    const char* e = getenv("MTNN_SPLIT_STRIP");
-    return !(e && e[0] == '0');
-  }();
-  if (strip_on && k <= 1024 && strips >= di->sm_count / 2) {
-    // short columns, many strips: one CTA per strip re-reads its strip from L2
-    KernelTimer timer(MTNN_KCLASS_SPLIT, 8.0 * (double)k * (double)n, s);
-    MTNN_TRY(launch_chained(split_cols_strip_kernel, dim3((unsigned)strips), dim3(8 * kStripLanes), 0,
-                            s, x, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale, k,
-                            n, fl));
-    MTNN_CUDA_TRY(cudaGetLastError());
-    return MTNN_OK;
-  }
-  if (strip_on && k <= kClusterMax * kClusterRowLanes * 32) {
-    KernelTimer timer(MTNN_KCLASS_SPLIT, 8.0 * (double)k * (double)n, s);
-    // fewest rows per CTA that keep the cluster within 8 CTAs: the most CTAs
-    if (k <= kClusterMax * kClusterRowLanes * 4)
-      MTNN_TRY(launch_cols_cluster<4>(x, hi, lo, inv_scale, k, n, fl, s));
-    else if (k <= kClusterMax * kClusterRowLanes * 8)
-      MTNN_TRY(launch_cols_cluster<8>(x, hi, lo, inv_scale, k, n, fl, s));
-    else if (k <= kClusterMax * kClusterRowLanes * 16)
-      MTNN_TRY(launch_cols_cluster<16>(x, hi, lo, inv_scale, k, n, fl, s));
-    else
-      MTNN_TRY(launch_cols_cluster<32>(x, hi, lo, inv_scale, k, n, fl, s));
-    return MTNN_OK;
-  }
-  KernelTimer timer(MTNN_KCLASS_SPLIT, 12.0 * (double)k * (double)n, s);
-  float* partial = partial_scratch;
-  // 32 16-byte lanes (512 B of a row per warp) x 8 row lanes: ncu at k = n =
-  // 4096 (pass 1 / pass 2 us): 15.2 / 30.1, vs 15.3 / 33.8 at 64 lanes and
-  // 17.7 / 35.5 at 256 (whole 4 KiB row segments per CTA)
-  constexpr int kLanes = 32;
-  const int64_t band_cols = 4 * kLanes;
-  const int64_t bands = (n + band_cols - 1) / band_cols;
-  // pass 1: about 4 CTAs per SM, bands of >= 64 rows
-  int64_t chunks = std::max<int64_t>(1, ((int64_t)di->sm_count * 4) / bands);
-  chunks = std::min<int64_t>({chunks, (int64_t)kMaxChunks, std::max<int64_t>(1, k / 64)});
-  const int64_t rpc = (k + chunks - 1) / chunks;
-  chunks = (k + rpc - 1) / rpc;
-  // pass 2: about 8 CTAs per SM
-  int64_t split_bands = std::max<int64_t>(1, ((int64_t)di->sm_count * 8) / bands);
-  split_bands = std::min<int64_t>(split_bands, std::max<int64_t>(1, k / 32));
-  const int64_t rpb = (k + split_bands - 1) / split_bands;
-  split_bands = (k + rpb - 1) / rpb;
-  MTNN_TRY(launch_chained(colmax_partial_kernel<kLanes>, dim3((unsigned)bands, (unsigned)chunks),
-                          dim3(256), 0, s, x, partial, k, n, rpc));
-  MTNN_CUDA_TRY(cudaGetLastError());
-  split_cols_band_kernel<kLanes><<<dim3((unsigned)bands, (unsigned)split_bands), 256, 0, s>>>(
-      x, partial, (int)chunks, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale, k,
-      n, rpb, fl);
+  const int64_t chunks = (k + kScaleChunkK - 1) / kScaleChunkK;
+  if (chunks > 65535) return fail(MTNN_EINVAL, "column split: k = %lld too long", (long long)k);
+  KernelTimer timer(MTNN_KCLASS_SPLIT, 8.0 * (double)k * (double)n, s);
+  MTNN_TRY(launch_chained(split_cols_chunk_kernel,
+                          dim3((unsigned)((n + kColBlockCols - 1) / kColBlockCols), (unsigned)chunks),
+                          dim3(8 * kColRowLanes), 0, s, x, static_cast<__half*>(hi),
+                          static_cast<__half*>(lo), inv_scale, k, n, fl));
   MTNN_CUDA_TRY(cudaGetLastError());
   return MTNN_OK;
 }

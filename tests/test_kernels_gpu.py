@@ -606,17 +606,19 @@ def test_row_split_every_branch(rng, k, n):
     assert err.max() < FP32_GATE, (k, n, float(err.max()))
 
 
-@pytest.mark.parametrize("k", [8, 104, 128, 1024, 1032, 2048, 2056, 4096, 4104, 8192, 8200, 16384])
+@pytest.mark.parametrize("k", [8, 104, 128, 256, 264, 1024, 1032, 2048, 2056, 4096, 4104, 8192, 8200,
+                               16384])
 @pytest.mark.parametrize("n", [208, 384, 1072])
 def test_col_split_every_branch(rng, k, n):
-    """NN (MN-major B^T) column split on every branch picked by k — cluster
-    strips (k <= 8192, 1..8 CTAs per strip) and the two-pass / single-CTA strip
-    fallbacks past it — with ragged strips (n % 32 != 0), columns whose
-    magnitudes span 2^-40..2^40, and a NaN in the last row of one column
-    poisoning exactly that output column."""
+    """NN (MN-major B^T) column split — one scale per (256-row chunk, column) —
+    at chunk-ragged k (k % 256 != 0, k < 256), ragged 32-column blocks
+    (n % 32 != 0), columns whose magnitudes span 2^-40..2^40 AND change by up to
+    2^+-20 from one k-row to the next (every chunk gets its own scale), and a
+    NaN in the last row of one column poisoning exactly that output column."""
     m = 384
     a = random_matrix(rng, m, k) * np.exp2(rng.integers(-40, 41, m)).astype(np.float32)[:, None]
-    bt = random_matrix(rng, k, n) * np.exp2(rng.integers(-40, 41, n)).astype(np.float32)[None, :]
+    bt = (random_matrix(rng, k, n) * np.exp2(rng.integers(-40, 41, n)).astype(np.float32)[None, :]
+          * np.exp2(rng.integers(-20, 21, k)).astype(np.float32)[:, None])
     bt[k - 1, 7] = np.nan
     got = gemm_nn(a, bt, variant="tc3xf16s")
     assert np.all(np.isnan(got[:, 7]))
@@ -625,6 +627,28 @@ def test_col_split_every_branch(rng, k, n):
     g = got[:, ok]
     err = np.linalg.norm(g - want, axis=0) / np.linalg.norm(want, axis=0)
     assert err.max() < FP32_GATE, (k, n, float(err.max()))
+
+
+@pytest.mark.parametrize("m,n,k", [(256, 256, 4104), (128, 512, 8200), (256, 256, 16384),
+                                   (2304, 2304, 1000), (2304, 2304, 4360), (512, 4096, 2056)])
+def test_nn_chunk_scales_with_split_k_and_pairs(rng, m, n, k):
+    """MN-major chunk scales through split-K (k-splits start on 256-row chunk
+    boundaries) and the CTA-pair kernel (>= 74 pair tiles), with B^T rows whose
+    magnitudes change per k-row; NN, TNN and the host entry point agree with
+    float64 and NN == TNN bit for bit (same kernels on the same B^T)."""
+    k -= k % 8
+    a = random_matrix(rng, m, k)
+    bt = random_matrix(rng, k, n) * np.exp2(rng.integers(-12, 13, k)).astype(np.float32)[:, None]
+    want = np.asarray(a, np.float64) @ np.asarray(bt, np.float64)
+    nn = gemm_nn(a, bt, variant="tc3xf16s")
+    tnn = gemm_tnn(a, np.ascontiguousarray(bt.T), variant="tc3xf16s")
+    assert rel_frobenius(nn, want) < FP32_GATE
+    assert np.array_equal(nn, tnn)
+    import torch
+
+    dev = kernels.gemm_nn(torch.from_numpy(a).cuda(), torch.from_numpy(bt).cuda(),
+                          variant="tc3xf16s").cpu().numpy()
+    assert np.array_equal(dev, nn)
 
 
 @pytest.mark.parametrize("shape", [(1024, 10, 4096), (10, 4096, 1024), (1, 1, 4), (13, 13, 4096),
@@ -674,8 +698,8 @@ def test_short_k(rng, shape):
     assert rel_frobenius(dev, want) < FP32_GATE
 
 
-@pytest.mark.parametrize("switch", ["MTNN_PDL=0", "MTNN_SPLIT_CTAREG=0", "MTNN_SPLIT_STRIP=0",
-                                    "MTNN_SKINNY=0", "MTNN_PAIR_MAXK=4096"])
+@pytest.mark.parametrize("switch", ["MTNN_PDL=0", "MTNN_SPLIT_CTAREG=0", "MTNN_SKINNY=0",
+                                    "MTNN_PAIR_MAXK=4096"])
 def test_env_switches_keep_results(tmp_path, switch):
     """Every A/B environment switch (read once per process) keeps results within
     the FP32 gate on the shapes it affects, and the switches that change only
@@ -711,7 +735,7 @@ def test_env_switches_keep_results(tmp_path, switch):
                              text=True, env=env, cwd=str(ROOT), timeout=300)
         assert out.returncode == 0 and "ok" in out.stdout, out.stderr
         res[name] = np.load(path)
-    if key in ("MTNN_PDL", "MTNN_SPLIT_CTAREG", "MTNN_SPLIT_STRIP"):
+    if key in ("MTNN_PDL", "MTNN_SPLIT_CTAREG"):
         for f in res["default"].files:
             assert np.array_equal(res["default"][f], res["switch"][f]), (switch, f)
 
