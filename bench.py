@@ -749,10 +749,15 @@ def main():
     # counted. The per-class breakdown comes from one extra fully instrumented
     # step after the timed region.
     min_work = min(float(2 ** 35), max((2.0 * m * n * k for _, m, n, k, _ in calls), default=0.0))
+    # a step of several mid-size launches at that size (the FCN step: six GEMMs of
+    # 3.4e10 flop, each ~12 us slower when bracketed) times a rotating one of them
+    eligible = sum(1 for _, m, n, k, _ in calls if 2.0 * m * n * k >= min_work)
+    sample_every = eligible + 1 if args.workload == "fcn" and eligible > 1 else 1
     L.mtnn_profile_reset()
     L.mtnn_profile_enable_classes((1 << _lib.KCLASS_GEMM_TC) | (1 << _lib.KCLASS_GEMM_TC_F16S)
                                   | (1 << _lib.KCLASS_GEMM_FFMA))
     L.mtnn_profile_min_work(ctypes.c_double(min_work))
+    L.mtnn_profile_sample_every(sample_every)
     events = []
     with clock_sampler(local_rank) as clocks:
         if world > 1:
@@ -778,6 +783,7 @@ def main():
     prof_t = {c: _lib.profile_read_timed(c) for c in _lib.KCLASS_NAMES}
     launches = int(sum(v[1] for v in prof.values()))
     L.mtnn_profile_min_work(ctypes.c_double(0.0))
+    L.mtnn_profile_sample_every(1)
     # per-class breakdown: one extra step with every launch timed
     L.mtnn_profile_reset()
     L.mtnn_profile_enable(1)
@@ -864,8 +870,10 @@ def main():
                        f"(MEASURED_PEAKS.json, burst) / 2 (tf32 rate) / 3 (MMAs per product)"),
         "peak_sustained": roof_sus, "frac_of_sustained": achieved / roof_sus if achieved else None,
         "launches": tc_n, "avg_launch_ms": tc_ms / tc_n if tc_n else None,
-        "timed_launches_note": (f"event-timed launches of >= {min_work:.3g} flop: {tc_n} of {tc_all_n} "
-                                f"launches of the class, {tc_work / tc_all_work:.1%} of its flops"
+        "timed_launches_note": (f"event-timed launches of >= {min_work:.3g} flop"
+                                + (f", every {sample_every}th of those (rotating)" if sample_every > 1 else "")
+                                + f": {tc_n} of {tc_all_n} launches of the class, "
+                                f"{tc_work / tc_all_work:.1%} of its flops"
                                 if tc_all_work else None),
         "share_of_step": tc_ms / 1e3 / (device_s * 1.0) if device_s else None,
         "dominant_kernel_by_time": _lib.KCLASS_NAMES[dominant],
@@ -896,6 +904,9 @@ def main():
             }
     if gather_mode is not None:
         extra["gather"] = gather_mode
+    if args.workload == "fcn":
+        extra["per_call_us"] = {f"{op} ({m},{n},{k})#{i}": round(t * 1e6, 1)
+                                for i, ((op, m, n, k, _), t) in enumerate(zip(calls, per_call))}
     if world == 1 and args.workload == "sweep":
         # a short idle first: the pass measures single transposes, not the power
         # state the preceding back-to-back sweep passes leave behind

@@ -97,6 +97,11 @@ int mtnn_profile_enable_classes(unsigned mask);
  * are still counted. mtnn_profile_read_timed returns the timed subset: its
  * milliseconds, launch count and work (so rate = work / ms is consistent). */
 int mtnn_profile_min_work(double work);
+/* Of the launches that pass the class mask and the work filter, time every
+ * n-th (n >= 1; resets the counter): a rotating sample, so the event pairs
+ * (which serialise the stream around a launch and break the programmatic launch
+ * chain) stay a small part of a step of many mid-size launches. */
+int mtnn_profile_sample_every(int n);
 int mtnn_profile_read_timed(int kclass, double* total_ms, int64_t* launches, double* work);
 int mtnn_profile_reset(void);
 int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* work);

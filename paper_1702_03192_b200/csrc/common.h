@@ -142,8 +142,12 @@ int launch_rowmax_f16(const float* x, float* inv_scale, int64_t rows, int64_t k,
 // column split writes inv_scale[ceil(k / kScaleChunkK)][n], and the GEMM applies
 // chunk c's scale to its FP32-promotion chunks covering k rows [256c, 256c+256).
 constexpr int kScaleChunkK = 256;
+// Optionally also splits a K-major operand `a` (a_rows x k, per-row scales) in
+// the same launch (NN: A and B^T of one call).
 int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale, int64_t k,
-                          int64_t n, const FixList& fl, cudaStream_t s);
+                          int64_t n, const FixList& fl, cudaStream_t s, const float* a = nullptr,
+                          void* a_hi = nullptr, void* a_lo = nullptr, float* a_inv = nullptr,
+                          int64_t a_rows = 0, const FixList& a_fl = FixList{});
 
 // Draws skip .. skip + count - 1 of numpy's PCG64 stream with initial
 // (state_lo, state_hi, inc_lo, inc_hi), as uniform(low, high) doubles rounded to

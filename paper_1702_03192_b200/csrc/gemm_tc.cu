@@ -1560,16 +1560,17 @@ int tc_prepare(const float* X, int64_t rows, int64_t k, bool mn_major, TcKind ki
 int tc_prepare_pair(const float* A, int64_t m, const float* B, int64_t n, int64_t k,
                     bool b_mn_major, TcKind kind, int conv, ScratchBuffer& wa, ScratchBuffer& wb,
                     FixHandle* fa, FixHandle* fb, TcOperand* a, TcOperand* b, cudaStream_t s) {
-  if (kind != TcKind::F16S || b_mn_major) {
+  if (kind != TcKind::F16S || (b_mn_major && conv != 0)) {
     MTNN_TRY(tc_prepare(A, m, k, false, kind, conv == 1, wa, fa, a, s));
     return tc_prepare(B, n, k, b_mn_major, kind, conv == 2, wb, fb, b, s);
   }
-  // F16S, both K-major: [h | l | 1/s | entries] per split operand, [1/s | entries] per in-kernel one
+  // F16S: [h | l | 1/s | entries] per split operand, [1/s | entries] per in-kernel
+  // one; an MN-major B^T has 1/s per (256-row chunk, column)
   const bool track = fixup_enabled();
   auto layout = [&](const float* X, int64_t rows, bool ink, ScratchBuffer& ws, FixHandle* fh,
-                    TcOperand* o) {
+                    TcOperand* o, int64_t scale_rows = 1) {
     const size_t oh = ink ? 0 : align256((size_t)rows * k * 2);
-    const size_t osc = align256((size_t)rows * 4);
+    const size_t osc = align256((size_t)(scale_rows * rows) * 4);
     const bool t = track && fh != nullptr;
     const unsigned cap = t ? fix_capacity(rows * k) : 0;
     MTNN_TRY(ws.alloc(2 * oh + osc + (t ? fix_entry_bytes(cap) : 0), s));
@@ -1585,6 +1586,14 @@ int tc_prepare_pair(const float* A, int64_t m, const float* B, int64_t n, int64_
     return MTNN_OK;
   };
   MTNN_TRY(layout(A, m, conv == 1, wa, fa, a));
+  if (b_mn_major) {
+    // NN: B^T's column split and A's row split in one launch
+    MTNN_TRY(layout(B, n, false, wb, fb, b, (k + kScaleChunkK - 1) / kScaleChunkK));
+    return launch_split_cols_f16(B, const_cast<void*>(b->hi), const_cast<void*>(b->lo),
+                                 const_cast<float*>(b->inv_scale), k, n, b->fix, s, A,
+                                 const_cast<void*>(a->hi), const_cast<void*>(a->lo),
+                                 const_cast<float*>(a->inv_scale), m, a->fix);
+  }
   MTNN_TRY(layout(B, n, conv == 2, wb, fb, b));
   return launch_split_rows_f16_pair(
       A, conv == 1 ? nullptr : const_cast<void*>(a->hi), const_cast<void*>(a->lo),

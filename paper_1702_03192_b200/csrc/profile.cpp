@@ -22,6 +22,8 @@ struct Pending {
 std::atomic<unsigned> g_mask{0};  // bit c: time kernel class c
 std::atomic<bool> g_counting{false};  // count launches and work of every class
 std::atomic<double> g_min_work{0.0};  // time only launches with at least this much work
+std::atomic<int> g_sample_every{1};   // of those, time every n-th (a rotating sample)
+std::atomic<uint64_t> g_eligible{0};  // launches that passed the class and work filters
 std::mutex g_mu;
 std::vector<Pending> g_pending;
 std::vector<cudaEvent_t> g_free_events;
@@ -59,6 +61,9 @@ KernelTimer::KernelTimer(int kc, double w, cudaStream_t s) : kclass(kc), work(w)
   }
   if (!((g_mask.load(std::memory_order_relaxed) >> kc) & 1u)) return;
   if (w < g_min_work.load(std::memory_order_relaxed)) return;
+  const int every = g_sample_every.load(std::memory_order_relaxed);
+  if (g_eligible.fetch_add(1, std::memory_order_relaxed) % (uint64_t)(every > 0 ? every : 1) != 0)
+    return;
   start = take_event();
   if (start && cudaEventRecord(start, stream) != cudaSuccess) {
     (void)cudaGetLastError();
@@ -97,6 +102,13 @@ int mtnn_profile_enable_classes(unsigned mask) {
 
 int mtnn_profile_min_work(double work) {
   g_min_work.store(work > 0.0 ? work : 0.0);
+  return MTNN_OK;
+}
+
+int mtnn_profile_sample_every(int n) {
+  if (n < 1) return fail(MTNN_EINVAL, "sample period must be >= 1, got %d", n);
+  g_sample_every.store(n);
+  g_eligible.store(0);
   return MTNN_OK;
 }
 

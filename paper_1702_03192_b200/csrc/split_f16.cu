@@ -511,21 +511,66 @@ constexpr int kColBlockCols = 32;
 constexpr int kColRowLanes = 32;
 constexpr int kColRowsPerLane = kScaleChunkK / kColRowLanes;  // 8
 
+// The A rows of the same NN call (K-major, one scale per row) ride along in the
+// same launch (`rows`, blocks past the column grid: one CTA per row, max pass
+// then split from an L1/L2 re-read — the same per-element operations as the
+// row kernels, so the halves are identical), so the two splits overlap instead
+// of running as two chained launches.
+__device__ void split_row_cta(const RowJob& j, int64_t r, int64_t k, float* red) {
+  const float4* row = reinterpret_cast<const float4*>(j.x + r * k);
+  const int64_t k4 = k / 4;
+  const int t = threadIdx.x;
+  float mx = 0.f, mn = INFINITY;
+#pragma unroll 4
+  for (int64_t i = t; i < k4; i += 256) {
+    const float4 v = ldg4(row + i);
+    mx = fmaxf(mx, absmax4(v));
+    mn = fminf(mn, absmin_nz4(v));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (t % 32 == 0) red[t / 32] = mx;
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < 8; ++w) mx = fmaxf(mx, red[w]);
+  const float s = pow2_scale(mx);
+  const float inv = 1.f / s;
+  const float cand = j.fix.ctr ? f16s_candidate_bound(track_inv(mx, inv)) : 0.f;
+  const bool chk = mn < cand;
+  if (t == 0) j.inv_scale[r] = inv;
+  uint2* hrow = reinterpret_cast<uint2*>(j.hi + r * k);
+  uint2* lrow = reinterpret_cast<uint2*>(j.lo + r * k);
+#pragma unroll 4
+  for (int64_t i = t; i < k4; i += 256) {
+    uint2 hw, lw;
+    split4x(chk, ldg4(row + i), s, inv, cand, hw, lw, j.fix, r, 4 * i);
+    hrow[i] = hw;
+    lrow[i] = lw;
+  }
+}
+
 __global__ void __launch_bounds__(8 * kColRowLanes)
 split_cols_chunk_kernel(const float* __restrict__ x, __half* __restrict__ hi,
                         __half* __restrict__ lo, float* __restrict__ inv_scale, int64_t k,
-                        int64_t n, const FixList fl) {
+                        int64_t n, const FixList fl, const RowJob rows) {
   pdl_trigger();
   pdl_wait();
   __shared__ float4 wmax[8][8];  // [warp][16-byte column]
   __shared__ float4 scale[8];
   __shared__ float4 tinv_s[8];
+  const int64_t nbx = (n + kColBlockCols - 1) / kColBlockCols;
+  const int64_t ncol_blocks = nbx * ((k + kScaleChunkK - 1) / kScaleChunkK);
+  if ((int64_t)blockIdx.x >= ncol_blocks) {
+    split_row_cta(rows, (int64_t)blockIdx.x - ncol_blocks, k, reinterpret_cast<float*>(wmax));
+    return;
+  }
+  const int64_t bx = (int64_t)blockIdx.x % nbx, by = (int64_t)blockIdx.x / nbx;
   const int c4 = threadIdx.x % 8;
   const int rl = threadIdx.x / 8;      // 0..31; a warp holds row lanes 4w..4w+3
   const int warp = threadIdx.x / 32;
-  const int64_t col = (int64_t)blockIdx.x * kColBlockCols + 4 * c4;
+  const int64_t col = bx * kColBlockCols + 4 * c4;
   const bool active = col < n;  // n % 4 == 0: the whole float4 is in range
-  const int64_t r0 = (int64_t)blockIdx.y * kScaleChunkK + rl;
+  const int64_t r0 = by * kScaleChunkK + rl;
   float4 v[kColRowsPerLane];
 #pragma unroll
   for (int u = 0; u < kColRowsPerLane; ++u) {
@@ -561,9 +606,9 @@ split_cols_chunk_kernel(const float* __restrict__ x, __half* __restrict__ hi,
     const float4 sc = make_float4(pow2_scale(m.x), pow2_scale(m.y), pow2_scale(m.z), pow2_scale(m.w));
     scale[threadIdx.x] = sc;
     tinv_s[threadIdx.x] = track_inv4(m, sc);
-    const int64_t c = (int64_t)blockIdx.x * kColBlockCols + 4 * threadIdx.x;
+    const int64_t c = bx * kColBlockCols + 4 * threadIdx.x;
     if (c < n)
-      *reinterpret_cast<float4*>(inv_scale + (int64_t)blockIdx.y * n + c) =
+      *reinterpret_cast<float4*>(inv_scale + by * n + c) =
           make_float4(1.f / sc.x, 1.f / sc.y, 1.f / sc.z, 1.f / sc.w);
   }
   __syncthreads();
@@ -653,15 +698,20 @@ int launch_rowmax_f16(const float* x, float* inv_scale, int64_t rows, int64_t k,
 }
 
 int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale, int64_t k,
-                          int64_t n, const FixList& fl, cudaStream_t s) {
-  if (k <= 0 || n <= 0) return MTNN_OK;
+                          int64_t n, const FixList& fl, cudaStream_t s, const float* a,
+                          void* a_hi, void* a_lo, float* a_inv, int64_t a_rows,
+                          const FixList& a_fl) {
+  if (k <= 0 || (n <= 0 && a_rows <= 0)) return MTNN_OK;
+  if (n < 0) n = 0;
+  if (a_rows < 0 || a == nullptr) a_rows = 0;
   const int64_t chunks = (k + kScaleChunkK - 1) / kScaleChunkK;
-  if (chunks > 65535) return fail(MTNN_EINVAL, "column split: k = %lld too long", (long long)k);
-  KernelTimer timer(MTNN_KCLASS_SPLIT, 8.0 * (double)k * (double)n, s);
-  MTNN_TRY(launch_chained(split_cols_chunk_kernel,
-                          dim3((unsigned)((n + kColBlockCols - 1) / kColBlockCols), (unsigned)chunks),
-                          dim3(8 * kColRowLanes), 0, s, x, static_cast<__half*>(hi),
-                          static_cast<__half*>(lo), inv_scale, k, n, fl));
+  const int64_t blocks = (n + kColBlockCols - 1) / kColBlockCols * chunks + a_rows;
+  if (blocks > 0x7fffffff) return fail(MTNN_EINVAL, "column split: grid too large");
+  const RowJob rj{a, static_cast<__half*>(a_hi), static_cast<__half*>(a_lo), a_inv, a_rows, a_fl};
+  KernelTimer timer(MTNN_KCLASS_SPLIT, 8.0 * (double)k * (double)(n + a_rows), s);
+  MTNN_TRY(launch_chained(split_cols_chunk_kernel, dim3((unsigned)blocks), dim3(8 * kColRowLanes),
+                          0, s, x, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale,
+                          k, n, fl, rj));
   MTNN_CUDA_TRY(cudaGetLastError());
   return MTNN_OK;
 }
