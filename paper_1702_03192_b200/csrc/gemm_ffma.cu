@@ -46,89 +46,86 @@ sgemm_kernel(const float* __restrict__ A, const float* __restrict__ B,
 }
 
 // Skinny NT (GEMV-class): one side of the output <= kSkinnyMax (the FCN's
-// 10-class layer and its weight gradient, batch-1 products): the long operand
-// (L x k) is read from DRAM once and the product is bound by how much of it is
-// in flight. One CTA per SM (512 threads), each owning a contiguous block of
-// long rows; a row's k is split over the CTA's 16 warps when the block has few
-// rows (1024 x 4096: 7 rows, 2 warps per row), else each warp walks whole rows.
-// A lane issues U 16-byte long-operand loads before using any of them (U x 32
-// x 16 warps = 64 KiB in flight per SM), then runs s four-term FFMA chains per
-// piece against the short operand (L1/L2-resident, shared by the CTA's warps).
-// Sums fold across lanes by shuffles and across a row's warps through shared
-// memory in a fixed order (deterministic). Output (long row r, short row j)
-// goes to C[r * s + j] when the short side is B, C[j * L + r] when it is A.
-// (Round 1 ran one CTA per 3 rows: 1.16 waves of latency-bound CTAs, 15.8 us
-// for 1024 x 10 x 4096.)
+// 10-class layer, batch-1 products). A CTA (8 warps) owns rows of the long
+// operand in groups of R and splits k into W slices, one per warp (W = 8 for
+// k >= 4096; shorter k gives several row groups per CTA). Per 16-byte k-step a
+// lane first issues all its loads — R long-operand pieces (DRAM, read once) and
+// the s short-row pieces (L2-resident, reused across the R rows) — then runs
+// s x R FFMA chains. The R x SMAX = 32 partial sums are folded across the warp
+// by a butterfly that halves the values per lane each step (31 shuffles, lane l
+// ends with value l), then across the W slices through shared memory. Output
+// (long row r, short row j) goes to C[r * s + j] when the short side is B,
+// C[j * L + r] when it is A. No operand split and no 128-wide tensor-core tile
+// for a 10-wide output.
 constexpr int kSkinnyMax = 16;
-constexpr int kSkinnyWarps = 16;
-constexpr int kSkinnyU = 8;
+
+__device__ __forceinline__ void butterfly32(float* w, int lane) {
+  // w[0..32): afterwards w[0] of lane l holds the warp-wide sum of value l
+#pragma unroll
+  for (int o = 16, n = 32; o >= 1; o >>= 1, n >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const float send = upper ? w[i] : w[i + n / 2];
+      const float keep = upper ? w[i + n / 2] : w[i];
+      w[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+}
 
 template <int SMAX>
-__global__ void __launch_bounds__(32 * kSkinnyWarps, 1)
+__global__ void __launch_bounds__(256, 2)
 gemm_skinny_kernel(const float* __restrict__ big, const float* __restrict__ small,
-                   float* __restrict__ C, int64_t L, int s, int64_t k, int64_t rows_per_cta,
-                   bool small_is_b) {
+                   float* __restrict__ C, int64_t L, int s, int64_t k, bool small_is_b, int W) {
   pdl_enter();
-  __shared__ float part[kSkinnyWarps][SMAX];
+  constexpr int R = 32 / SMAX;  // long rows per warp: R x SMAX <= 32 partial sums
+  __shared__ float red[8][32];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int64_t row0 = (int64_t)blockIdx.x * rows_per_cta;
-  const int64_t rows = min(rows_per_cta, L - row0);
-  if (rows <= 0) return;
+  const int groups = 8 / W;
+  const int slice = warp % W, grp = warp / W;
   const int64_t k4 = k / 4;
-  // warps per row (k-parts) when the block is short, else rows per warp
-  const int wpr = rows >= kSkinnyWarps ? 1 : kSkinnyWarps / (int)rows;
-  const int64_t per = (k4 + wpr - 1) / wpr;  // 16-byte pieces per k-part
+  const int64_t per = (k4 + W - 1) / W;
+  const int64_t q_begin = (int64_t)slice * per, q_end = min(k4, q_begin + per);
+  const int64_t rows_per_cta = (int64_t)groups * R;
   const float4* big4 = reinterpret_cast<const float4*>(big);
   const float4* small4 = reinterpret_cast<const float4*>(small);
-  const int64_t task_count = rows * wpr;
-  const int tasks = task_count < kSkinnyWarps ? (int)task_count : kSkinnyWarps;
-  for (int64_t rbase = 0; rbase < rows; rbase += kSkinnyWarps / wpr) {
-    float acc[SMAX];
+  for (int64_t base = (int64_t)blockIdx.x * rows_per_cta; base < L;
+       base += (int64_t)gridDim.x * rows_per_cta) {
+    const int64_t r0 = base + (int64_t)grp * R;
+    float acc[32];
 #pragma unroll
-    for (int j = 0; j < SMAX; ++j) acc[j] = 0.f;
-    const int64_t rr = rbase + warp / wpr;  // this warp's row (block-relative)
-    const int part_k = warp % wpr;
-    const bool active = warp < tasks && rr < rows;
-    if (active) {
-      const int64_t qb0 = (int64_t)part_k * per, qb1 = min(k4, qb0 + per);
-      const float4* arow = big4 + (row0 + rr) * k4;
-      for (int64_t qb = qb0; qb < qb1; qb += 32 * kSkinnyU) {
-        float4 a[kSkinnyU];
+    for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+    for (int64_t q = q_begin + lane; q < q_end; q += 32) {
+      float4 a[R], b[SMAX];
 #pragma unroll
-        for (int u = 0; u < kSkinnyU; ++u) {
-          const int64_t q = qb + lane + 32 * u;
-          a[u] = q < qb1 ? __ldg(arow + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int r = 0; r < R; ++r)
+        a[r] = r0 + r < L ? __ldg(big4 + (r0 + r) * k4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < SMAX; ++j)
+        b[j] = j < s ? __ldg(small4 + (int64_t)j * k4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int j = 0; j < SMAX; ++j) {
+          float& c = acc[r * SMAX + j];  // (slots past R x SMAX stay 0)
+          c = fmaf(a[r].w, b[j].w, fmaf(a[r].z, b[j].z, fmaf(a[r].y, b[j].y, fmaf(a[r].x, b[j].x, c))));
         }
-#pragma unroll
-        for (int u = 0; u < kSkinnyU; ++u) {
-          const int64_t q = qb + lane + 32 * u;
-          if (q >= qb1) break;
-#pragma unroll
-          for (int j = 0; j < SMAX; ++j) {
-            if (j >= s) break;
-            const float4 b = __ldg(small4 + (int64_t)j * k4 + q);
-            acc[j] = fmaf(a[u].w, b.w, fmaf(a[u].z, b.z, fmaf(a[u].y, b.y, fmaf(a[u].x, b.x, acc[j]))));
-          }
-        }
+    }
+    butterfly32(acc, lane);
+    red[warp][lane] = acc[0];
+    __syncthreads();
+    // fold the W slices of each row group: thread t -> (group, value)
+    if (threadIdx.x < groups * 32) {
+      const int g2 = threadIdx.x / 32, val = threadIdx.x % 32;
+      const int r = val / SMAX, j = val % SMAX;
+      const int64_t row = base + (int64_t)g2 * R + r;
+      if (r < R && j < s && row < L) {
+        float sum = 0.f;
+        for (int w = 0; w < W; ++w) sum += red[g2 * W + w][val];
+        C[small_is_b ? row * s + j : (int64_t)j * L + row] = sum;
       }
     }
-#pragma unroll
-    for (int j = 0; j < SMAX; ++j)
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
-    if (lane == 0) {
-#pragma unroll
-      for (int j = 0; j < SMAX; ++j) part[warp][j] = acc[j];
-    }
-    __syncthreads();
-    // the first warp of each row adds its row's k-parts in order and stores
-    if (active && part_k == 0 && lane < s) {
-      float sum = part[warp][lane];
-      for (int w = 1; w < wpr; ++w) sum += part[warp + w][lane];
-      const int64_t row = row0 + rr;
-      C[small_is_b ? row * s + lane : (int64_t)lane * L + row] = sum;
-    }
-    __syncthreads();  // part is reused by the next rows
+    __syncthreads();  // red is reused by the next row block
   }
 }
 
@@ -214,20 +211,25 @@ int launch_gemm_skinny(const float* A, const float* B, float* C, int64_t m, int6
   const bool small_is_b = n <= m;
   const int sm_rows = (int)(small_is_b ? n : m);
   const int64_t L = small_is_b ? m : n;
-  // one CTA per SM, contiguous row blocks
-  const int64_t rows_per_cta = (L + di->sm_count - 1) / di->sm_count;
-  const int64_t blocks = (L + rows_per_cta - 1) / rows_per_cta;
+  // k slices per row group: 32 lanes x >= 4 k-steps of 16 bytes per slice
+  int W = (int)std::min<int64_t>(8, std::max<int64_t>(1, k / 512));
+  while (8 % W) --W;
+  // SMAX = short rows the kernel is compiled for (registers: SMAX + R float4
+  // loads and 32 sums per lane, <= 128 registers for 2 CTAs per SM)
+  const int smax = sm_rows <= 4 ? 4 : sm_rows <= 8 ? 8 : sm_rows <= 10 ? 10 : sm_rows <= 12 ? 12 : 16;
+  const int64_t rows_per_cta = (int64_t)(8 / W) * (32 / smax);
+  const int64_t blocks = std::max<int64_t>(
+      1, std::min<int64_t>((L + rows_per_cta - 1) / rows_per_cta, (int64_t)di->sm_count * 8));
   KernelTimer timer(MTNN_KCLASS_GEMM_FFMA, 2.0 * (double)m * (double)n * (double)k, s);
   const float* big = small_is_b ? A : B;
   const float* sml = small_is_b ? B : A;
-  const dim3 g((unsigned)blocks), blk(32 * kSkinnyWarps);
-  const int smax = sm_rows <= 4 ? 4 : sm_rows <= 8 ? 8 : sm_rows <= 10 ? 10 : sm_rows <= 12 ? 12 : 16;
+  const unsigned g = (unsigned)blocks;
   switch (smax) {
-    case 4: MTNN_TRY(launch_chained(gemm_skinny_kernel<4>, g, blk, 0, s, big, sml, C, L, sm_rows, k, rows_per_cta, small_is_b)); break;
-    case 8: MTNN_TRY(launch_chained(gemm_skinny_kernel<8>, g, blk, 0, s, big, sml, C, L, sm_rows, k, rows_per_cta, small_is_b)); break;
-    case 10: MTNN_TRY(launch_chained(gemm_skinny_kernel<10>, g, blk, 0, s, big, sml, C, L, sm_rows, k, rows_per_cta, small_is_b)); break;
-    case 12: MTNN_TRY(launch_chained(gemm_skinny_kernel<12>, g, blk, 0, s, big, sml, C, L, sm_rows, k, rows_per_cta, small_is_b)); break;
-    default: MTNN_TRY(launch_chained(gemm_skinny_kernel<16>, g, blk, 0, s, big, sml, C, L, sm_rows, k, rows_per_cta, small_is_b)); break;
+    case 4: MTNN_TRY(launch_chained(gemm_skinny_kernel<4>, dim3(g), dim3(256), 0, s, big, sml, C, L, sm_rows, k, small_is_b, W)); break;
+    case 8: MTNN_TRY(launch_chained(gemm_skinny_kernel<8>, dim3(g), dim3(256), 0, s, big, sml, C, L, sm_rows, k, small_is_b, W)); break;
+    case 10: MTNN_TRY(launch_chained(gemm_skinny_kernel<10>, dim3(g), dim3(256), 0, s, big, sml, C, L, sm_rows, k, small_is_b, W)); break;
+    case 12: MTNN_TRY(launch_chained(gemm_skinny_kernel<12>, dim3(g), dim3(256), 0, s, big, sml, C, L, sm_rows, k, small_is_b, W)); break;
+    default: MTNN_TRY(launch_chained(gemm_skinny_kernel<16>, dim3(g), dim3(256), 0, s, big, sml, C, L, sm_rows, k, small_is_b, W)); break;
   }
   MTNN_CUDA_TRY(cudaGetLastError());
   return MTNN_OK;
