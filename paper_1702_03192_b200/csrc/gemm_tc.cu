@@ -43,6 +43,8 @@
 #include <mutex>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
+#include <unistd.h>
 
 #include "common.h"
 #include "workspace.h"
@@ -218,6 +220,28 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
+// Warp-role register split (setmaxnreg): launch bounds give every thread of a
+// 640-thread CTA 96 registers; warpgroup 0 (TMA / MMA / TMEM warps) needs far
+// fewer, the epilogue (64 FP32 sums per thread) more — without the split its
+// spills go to local memory, which misses the tiny L1 (shared memory takes
+// 225 KB) and costs an L2 round trip per reload on the tile's exposed tail.
+// setmaxnreg.inc only draws on registers other warps of the CTA released, so
+// 128 * control + 512 * work <= 640 * 96 (the launch allocation).
+#ifndef MTNN_REGS_CONTROL  // (A/B builds: -DMTNN_REGS_CONTROL=0 disables the split)
+#define MTNN_REGS_CONTROL 0
+#define MTNN_REGS_WORK 0
+#endif
+constexpr int kRegsControl = MTNN_REGS_CONTROL, kRegsWork = MTNN_REGS_WORK;
+static_assert(4 * 32 * kRegsControl + 16 * 32 * kRegsWork <= 640 * 96, "launch register allocation");
+// (each called by all four warps of a warpgroup, at the top of that warpgroup's
+// own branch, so the compiler allocates each branch under its own limit)
+__device__ __forceinline__ void regs_control() {
+  if constexpr (kRegsControl > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsControl));
+}
+__device__ __forceinline__ void regs_work() {
+  if constexpr (kRegsControl > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsWork));
+}
+
 // Programmatic dependent launch: the GEMMs are launched with programmatic stream
 // serialization, so their prologue (barrier init, TMEM allocation, descriptor
 // prefetch) overlaps the tail of the operand split that precedes them on the
@@ -308,7 +332,17 @@ struct Params {
   int units;
   const float* inv_scale_a;  // KindF16S: 1/s per row of A (m) and of B (n)
   const float* inv_scale_b;
+  // Stream-K (sk != 0, single-CTA kernel, pre-split operands): the grid's G CTAs
+  // share the tile-major (tile, k-block) space evenly, see work_item().
+  int sk;
+  int sk_slots;                 // partial slots per tile (segments per tile - 1)
+  int64_t sk_work;              // tiles * total_kblocks
+  float4* sk_part;              // [tile][slot][epilogue warp][kCols/4][32 lanes]
+  unsigned long long* sk_flags; // [tile][slot][epilogue warp] = sk_token when posted
+  unsigned long long sk_token;  // unique per launch (flags are never reset)
+  unsigned long long* trace;    // mtnn_profile_trace: [CTA][kTracePoints] globaltimer ns
 };
+constexpr int kTracePoints = 16;
 
 // Work-unit order: units are (k-split, tile); within a split, tiles walk
 // groups of kGroupM m-tiles with the group's m-tiles fastest, so the ~148 units
@@ -328,6 +362,85 @@ __device__ __forceinline__ void unit_coords(int u, const Params& p, int& split, 
   const int r = t - group * per_group;
   tm = first_m + r % gm;
   tn = r / gm;
+}
+
+// One work item of a CTA: output tile (tm, tn), k-split index, k-block range.
+// Stream-K items also carry their segment index within the tile and whether
+// they hold the tile's last k-block (fin: that CTA adds the earlier segments'
+// partial sums and stores C; the others post partials).
+struct Work {
+  int tm, tn, split, kb0, kb1, tile, idx;
+  bool fin;
+};
+
+// Stream-K: CTA b owns k-blocks [b*W/G, (b+1)*W/G) of the tile-major space
+// (W = tiles * total_kblocks, G = gridDim.x <= W). Its range covers the tail of
+// one tile, whole tiles, and the head of a last tile; the head (the only
+// segment that is not its tile's last) is processed FIRST, so every posted
+// partial is produced without waiting and every waiting segment depends only on
+// partials that are — no cycle, given all G CTAs are resident (G <= SMs, one
+// CTA per SM). A tile's segments are numbered by CTA: idx = b - first CTA of it.
+__device__ __forceinline__ int64_t sk_first_cta(int64_t x, int64_t W, int64_t G) {
+  return ((x + 1) * G + W - 1) / W - 1;  // largest b with floor(b*W/G) <= x
+}
+__device__ __forceinline__ int work_count(const Params& p) {
+  if (p.sk) {
+    const int64_t W = p.sk_work, G = gridDim.x, KB = p.total_kblocks;
+    const int64_t s = (int64_t)blockIdx.x * W / G, e = ((int64_t)blockIdx.x + 1) * W / G;
+    return e > s ? (int)((e - 1) / KB - s / KB + 1) : 0;
+  }
+  return blockIdx.x < (unsigned)p.units ? (p.units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+}
+__device__ __forceinline__ Work work_item(const Params& p, int i) {
+  Work w;
+  if (p.sk) {
+    const int64_t W = p.sk_work, G = gridDim.x, KB = p.total_kblocks;
+    const int64_t s = (int64_t)blockIdx.x * W / G, e = ((int64_t)blockIdx.x + 1) * W / G;
+    const int t0 = (int)(s / KB), t1 = (int)((e - 1) / KB);
+    const bool head = (e % KB) != 0;
+    const int tile = head ? (i == 0 ? t1 : t0 + i - 1) : t0 + i;
+    int split;
+    unit_coords(tile, p, split, w.tm, w.tn);
+    w.split = 0;
+    w.tile = tile;
+    w.kb0 = (int)(max(s, (int64_t)tile * KB) - (int64_t)tile * KB);
+    w.kb1 = (int)(min(e, ((int64_t)tile + 1) * KB) - (int64_t)tile * KB);
+    w.fin = !(head && i == 0);
+    w.idx = (int)(blockIdx.x - sk_first_cta((int64_t)tile * KB, W, G));
+    return w;
+  }
+  const int u = blockIdx.x + i * gridDim.x;
+  unit_coords(u, p, w.split, w.tm, w.tn);
+  w.tile = u;
+  w.kb0 = w.split * p.kblocks_per_split;
+  w.kb1 = min(p.total_kblocks, w.kb0 + p.kblocks_per_split);
+  w.fin = true;
+  w.idx = 0;
+  return w;
+}
+// End of the promotion chunk starting at k-block kc. Stream-K segments start
+// anywhere, so their chunks follow the global chunk grid (an MN-major B's scale
+// chunks stay whole); split-K ranges start on it already where that matters.
+__device__ __forceinline__ int chunk_end(const Params& p, int kc, int kb1) {
+  return p.sk ? min(kb1, (kc / p.chunk_kb + 1) * p.chunk_kb) : min(kb1, kc + p.chunk_kb);
+}
+
+// Phase timestamps of one CTA (mtnn_profile_trace; off = null pointer).
+__device__ __forceinline__ void trace_mark(const Params& p, int point) {
+  if (p.trace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[(size_t)blockIdx.x * kTracePoints + point] = t;
+  }
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* a) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* a, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
 }
 
 // FP16 hi/lo of 8 consecutive k-values of one row with the row's exact
@@ -412,6 +525,7 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
   constexpr bool kChunkB = B_MN && Kind::kScaled;
   constexpr int kScaleKb = kScaleChunkK / Kind::BK;
   static_assert(kColsPerWarp % 32 == 0, "chunk scales: 32-column groups per epilogue warp");
+  static_assert(R::kEpi * kColsPerWarp * 32 * 4 <= S::kRingBytes, "last-tile staging fits the ring");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -440,6 +554,7 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) trace_mark(p, 0);
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ahi)) : "memory");
@@ -475,303 +590,374 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) trace_mark(p, 1);
   pdl_wait();
   pdl_trigger();  // the next call's split may be scheduled (it waits for us)
+  if (threadIdx.x == 0) trace_mark(p, 2);
 
-  const int kb_per = p.kblocks_per_split;
-
-  if (warp == 0) {
-    // ===================== TMA producer =====================
-    if (elect_one()) {
+  if (warp < kEpiWarp0) {
+    regs_control();  // warpgroup 0: TMA, MMA, TMEM and converter-feeding warps
+    if (warp == 0) {
+      // ===================== TMA producer =====================
+      if (elect_one()) {
+        int stage = 0;
+        uint32_t phase = 0;
+        const int nw = work_count(p);
+        for (int wi = 0; wi < nw; ++wi) {
+          const Work w = work_item(p, wi);
+          const int tm = w.tm, tn = w.tn;
+          if (wi == 0) trace_mark(p, 12);
+          for (int kb = w.kb0; kb < w.kb1; ++kb) {
+            mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+            const uint32_t fb = smem_u32(&full_bar[stage]);
+            mbar_expect_tx(fb, kExpectBytes);
+            uint8_t* st = ring + stage * S::kStageBytes;
+            const int kx = kb * Kind::BK;
+            if (!(kF16Conv && kConv == 1)) {  // (raw A: warp 3)
+              tma_load_2d(smem_u32(st), &map_ahi, fb, kx, tm * BM);
+              if (kConv != 1) tma_load_2d(smem_u32(st + S::kABytes), &map_alo, fb, kx, tm * BM);
+            }
+            if (kF16Conv && kConv == 2) {
+              // raw B: warp 3
+            } else if (!B_MN) {
+              tma_load_2d(smem_u32(st + 2 * S::kABytes), &map_bhi, fb, kx, tn * BN);
+              if (kConv != 2)
+                tma_load_2d(smem_u32(st + 2 * S::kABytes + S::kBBytes), &map_blo, fb, kx, tn * BN);
+            } else {
+              // BN/kMnBox boxes of [BK k-rows][kMnBox columns] (128-byte rows), each
+              // one MN group of the canonical MN-major layout, kMnLBO bytes apart
+  #pragma unroll
+              for (int g = 0; g < BN / Kind::kMnBox; ++g) {
+                tma_load_2d(smem_u32(st + 2 * S::kABytes + g * Kind::kMnLBO), &map_bhi, fb,
+                            tn * BN + g * Kind::kMnBox, kx);
+                if (kConv != 2)
+                  tma_load_2d(smem_u32(st + 2 * S::kABytes + S::kBBytes + g * Kind::kMnLBO),
+                              &map_blo, fb, tn * BN + g * Kind::kMnBox, kx);
+              }
+            }
+            if (wi == 0 && kb == w.kb0) trace_mark(p, 3);
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
+          }
+        }
+        trace_mark(p, 11);
+      }
+    } else if (warp == 1) {
+      // ===================== MMA issuer =====================
+      constexpr uint32_t idesc = make_idesc(BN, B_MN, Kind::kFmt);
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        int split, tm, tn;
-        unit_coords(u, p, split, tm, tn);
-        const int kb0 = split * kb_per;
-        const int kb1 = min(p.total_kblocks, kb0 + kb_per);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
-          const uint32_t fb = smem_u32(&full_bar[stage]);
-          mbar_expect_tx(fb, kExpectBytes);
-          uint8_t* st = ring + stage * S::kStageBytes;
-          const int kx = kb * Kind::BK;
-          if (!(kF16Conv && kConv == 1)) {  // (raw A: warp 3)
-            tma_load_2d(smem_u32(st), &map_ahi, fb, kx, tm * BM);
-            if (kConv != 1) tma_load_2d(smem_u32(st + S::kABytes), &map_alo, fb, kx, tm * BM);
-          }
-          if (kF16Conv && kConv == 2) {
-            // raw B: warp 3
-          } else if (!B_MN) {
-            tma_load_2d(smem_u32(st + 2 * S::kABytes), &map_bhi, fb, kx, tn * BN);
-            if (kConv != 2)
-              tma_load_2d(smem_u32(st + 2 * S::kABytes + S::kBBytes), &map_blo, fb, kx, tn * BN);
-          } else {
-            // BN/kMnBox boxes of [BK k-rows][kMnBox columns] (128-byte rows), each
-            // one MN group of the canonical MN-major layout, kMnLBO bytes apart
-#pragma unroll
-            for (int g = 0; g < BN / Kind::kMnBox; ++g) {
-              tma_load_2d(smem_u32(st + 2 * S::kABytes + g * Kind::kMnLBO), &map_bhi, fb,
-                          tn * BN + g * Kind::kMnBox, kx);
-              if (kConv != 2)
-                tma_load_2d(smem_u32(st + 2 * S::kABytes + S::kBBytes + g * Kind::kMnLBO),
-                            &map_blo, fb, tn * BN + g * Kind::kMnBox, kx);
-            }
-          }
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    constexpr uint32_t idesc = make_idesc(BN, B_MN, Kind::kFmt);
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const int split = u / (p.tiles_m * p.tiles_n);
-      const int kb0 = split * kb_per;
-      const int kb1 = min(p.total_kblocks, kb0 + kb_per);
-      for (int kc = kb0; kc < kb1; kc += p.chunk_kb) {
-        const int kce = min(kb1, kc + p.chunk_kb);
-        mbar_wait(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int kb = kc; kb < kce; ++kb) {
-          // TF32 conversion waits full_bar itself, so conv_bar implies it; the F16S
-          // converters do not (the raw tile has its own ring)
-          if (kConv == 0 || kF16Conv) mbar_wait(smem_u32(&full_bar[stage]), phase);
-          if (kConv != 0) mbar_wait(smem_u32(&conv_bar[stage]), phase);
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      const int nw = work_count(p);
+      for (int wi = 0; wi < nw; ++wi) {
+        const Work w = work_item(p, wi);
+        const int kb1 = w.kb1;
+        for (int kc = w.kb0, kce; kc < kb1; kc = kce) {
+          kce = chunk_end(p, kc, kb1);
+          mbar_wait(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
           tc_fence_after();
-          if (elect_one()) {
-            uint8_t* st = ring + stage * S::kStageBytes;
-            const uint32_t a_hi = smem_u32(st);
-            const uint32_t a_lo = a_hi + S::kABytes;
-            const uint32_t b_hi = a_hi + 2 * S::kABytes;
-            const uint32_t b_lo = b_hi + S::kBBytes;
-#pragma unroll
-            for (int ks = 0; ks < Kind::BK / Kind::UMMA_K; ++ks) {
-              // A: K-major SW64 — 64-byte rows, 8-row groups 512 B apart; k-step +32 B.
-              const uint64_t dah = make_sdesc(a_hi + ks * 32, 16, 512, kLayoutSW64);
-              const uint64_t dal = make_sdesc(a_lo + ks * 32, 16, 512, kLayoutSW64);
-              uint64_t dbh, dbl;
-              if (!B_MN) {
-                dbh = make_sdesc(b_hi + ks * 32, 16, 512, kLayoutSW64);
-                dbl = make_sdesc(b_lo + ks * 32, 16, 512, kLayoutSW64);
-              } else {
-                // B: MN-major — column groups kMnLBO apart, k-row groups kMnSBO apart
-                dbh = make_sdesc(b_hi + ks * Kind::kMnKStep, Kind::kMnLBO, Kind::kMnSBO,
-                                 Kind::kMnLayout);
-                dbl = make_sdesc(b_lo + ks * Kind::kMnKStep, Kind::kMnLBO, Kind::kMnSBO,
-                                 Kind::kMnLayout);
+          const uint32_t tmem_d = tmem_base + acc * BN;
+          for (int kb = kc; kb < kce; ++kb) {
+            // TF32 conversion waits full_bar itself, so conv_bar implies it; the F16S
+            // converters do not (the raw tile has its own ring)
+            if (kConv == 0 || kF16Conv) mbar_wait(smem_u32(&full_bar[stage]), phase);
+            if (kConv != 0) mbar_wait(smem_u32(&conv_bar[stage]), phase);
+            if (wi == 0 && kb == w.kb0 && lane == 0) trace_mark(p, 4);
+            tc_fence_after();
+            if (elect_one()) {
+              uint8_t* st = ring + stage * S::kStageBytes;
+              const uint32_t a_hi = smem_u32(st);
+              const uint32_t a_lo = a_hi + S::kABytes;
+              const uint32_t b_hi = a_hi + 2 * S::kABytes;
+              const uint32_t b_lo = b_hi + S::kBBytes;
+  #pragma unroll
+              for (int ks = 0; ks < Kind::BK / Kind::UMMA_K; ++ks) {
+                // A: K-major SW64 — 64-byte rows, 8-row groups 512 B apart; k-step +32 B.
+                const uint64_t dah = make_sdesc(a_hi + ks * 32, 16, 512, kLayoutSW64);
+                const uint64_t dal = make_sdesc(a_lo + ks * 32, 16, 512, kLayoutSW64);
+                uint64_t dbh, dbl;
+                if (!B_MN) {
+                  dbh = make_sdesc(b_hi + ks * 32, 16, 512, kLayoutSW64);
+                  dbl = make_sdesc(b_lo + ks * 32, 16, 512, kLayoutSW64);
+                } else {
+                  // B: MN-major — column groups kMnLBO apart, k-row groups kMnSBO apart
+                  dbh = make_sdesc(b_hi + ks * Kind::kMnKStep, Kind::kMnLBO, Kind::kMnSBO,
+                                   Kind::kMnLayout);
+                  dbl = make_sdesc(b_lo + ks * Kind::kMnKStep, Kind::kMnLBO, Kind::kMnSBO,
+                                   Kind::kMnLayout);
+                }
+                const uint32_t accum = (kb == kc && ks == 0) ? 0u : 1u;
+                tc_mma<Kind::kScaled>(tmem_d, dal, dbh, idesc, accum);
+                tc_mma<Kind::kScaled>(tmem_d, dah, dbl, idesc, 1u);
+                tc_mma<Kind::kScaled>(tmem_d, dah, dbh, idesc, 1u);
               }
-              const uint32_t accum = (kb == kc && ks == 0) ? 0u : 1u;
-              tc_mma<Kind::kScaled>(tmem_d, dal, dbh, idesc, accum);
-              tc_mma<Kind::kScaled>(tmem_d, dah, dbl, idesc, 1u);
-              tc_mma<Kind::kScaled>(tmem_d, dah, dbh, idesc, 1u);
+              tc_commit(smem_u32(&empty_bar[stage]));
+              if (kb == kce - 1) tc_commit(smem_u32(&tfull_bar[acc]));
             }
-            tc_commit(smem_u32(&empty_bar[stage]));
-            if (kb == kce - 1) tc_commit(smem_u32(&tfull_bar[acc]));
+            __syncwarp();
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
-          __syncwarp();
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
-        }
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      }
-    }
-  } else if (kF16Conv && warp == 3) {
-    // ===================== TMA producer of the raw (converted) operand =====================
-    if (elect_one()) {
-      int rs = 0;
-      uint32_t rphase = 0;
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        int split, tm, tn;
-        unit_coords(u, p, split, tm, tn);
-        const int kb0 = split * kb_per;
-        const int kb1 = min(p.total_kblocks, kb0 + kb_per);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(smem_u32(&rempty_bar[rs]), rphase ^ 1);
-          const uint32_t fb = smem_u32(&rfull_bar[rs]);
-          mbar_expect_tx(fb, kRawTileBytes);
-          const uint32_t dst = smem_u32(raw_ring + rs * kRawTileBytes);
-          if (kConv == 1) tma_load_2d(dst, &map_ahi, fb, kb * Kind::BK, tm * BM);
-          else tma_load_2d(dst, &map_bhi, fb, kb * Kind::BK, tn * BN);
-          if (++rs == kRawStages) { rs = 0; rphase ^= 1; }
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
       }
-    }
-  } else if (kF16Conv && warp >= R::kConv0) {
-    // ===================== in-kernel FP16 split (F16S, one operand) =====================
-    // Two groups of 4 warps take alternate k-blocks, so each group's serial
-    // chain (raw wait, LDS, convert, h/l-slot wait, STS, proxy fence, arrive)
-    // has two MMA k-blocks of time. Thread r of a group owns row r of the
-    // converted tile: reads its 128-byte raw row (SWIZZLE_128B: 16-byte chunk c at
-    // c ^ (r & 7)) and writes 64-byte h and l rows (SWIZZLE_64B: chunk c at
-    // c ^ ((r >> 1) & 3)); both patterns keep each warp's 16-byte accesses
-    // conflict-free.
-    const int t = threadIdx.x - 32 * R::kConv0;
-    const int r = t % kF16ConvRows;             // tile row
-    const int grp = t / kF16ConvRows;           // k-block parity this thread converts
-    const int sw128 = r & 7, sw64 = (r >> 1) & 3;
-    const float* inv = kConv == 1 ? p.inv_scale_a : p.inv_scale_b;
-    const int64_t nrows = kConv == 1 ? p.m : p.n;
-    int stage = 0, rs = 0, parity = 0;
-    uint32_t phase = 0, rphase = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      int split, tm, tn;
-      unit_coords(u, p, split, tm, tn);
-      const int64_t row = (int64_t)(kConv == 1 ? tm * BM : tn * BN) + r;
-      const float sc = row < nrows ? 1.f / __ldg(inv + row) : 1.f;  // exact: powers of two
-      const int kb0 = split * kb_per;
-      const int kb1 = min(p.total_kblocks, kb0 + kb_per);
-      for (int kb = kb0; kb < kb1; ++kb) {
-        if (parity == grp) {
-          // raw tile -> registers -> halves; the raw slot is released as soon as
-          // its values are consumed, before waiting for the h/l slot
-          mbar_wait(smem_u32(&rfull_bar[rs]), rphase);
-          const uint32_t raw = smem_u32(raw_ring + rs * kRawTileBytes) + r * 128;
-          float4 x[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) x[j] = lds128f(raw + ((j ^ sw128) << 4));
-          uint4 hw[4], lw[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) split8_f16(x[2 * j], x[2 * j + 1], sc, hw[j], lw[j]);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&rempty_bar[rs]));
-          mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);  // MMA done with the h/l slot
-          const uint32_t hrow = smem_u32(ring + stage * S::kStageBytes) +
-                                (kConv == 1 ? 0 : 2 * S::kABytes) + r * 64;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t off = (j ^ sw64) << 4;
-            sts128(hrow + off, hw[j]);
-            sts128(hrow + kConvBytes + off, lw[j]);
+      if (lane == 0) trace_mark(p, 5);
+    } else if (kF16Conv && warp == 3) {
+      // ===================== TMA producer of the raw (converted) operand =====================
+      if (elect_one()) {
+        int rs = 0;
+        uint32_t rphase = 0;
+        const int nw = work_count(p);
+        for (int wi = 0; wi < nw; ++wi) {
+          const Work w = work_item(p, wi);
+          const int tm = w.tm, tn = w.tn;
+          for (int kb = w.kb0; kb < w.kb1; ++kb) {
+            mbar_wait(smem_u32(&rempty_bar[rs]), rphase ^ 1);
+            const uint32_t fb = smem_u32(&rfull_bar[rs]);
+            mbar_expect_tx(fb, kRawTileBytes);
+            const uint32_t dst = smem_u32(raw_ring + rs * kRawTileBytes);
+            if (kConv == 1) tma_load_2d(dst, &map_ahi, fb, kb * Kind::BK, tm * BM);
+            else tma_load_2d(dst, &map_bhi, fb, kb * Kind::BK, tn * BN);
+            if (++rs == kRawStages) { rs = 0; rphase ^= 1; }
+          }
+        }
+      }
+    } else if (kConv != 0 && !Kind::kScaled && (warp == 2 || warp == 3)) {
+      // ===================== in-kernel lo split (TF32, one operand) =====================
+      const int t = threadIdx.x - 64;  // 0..63
+      int stage = 0;
+      uint32_t phase = 0;
+      const int nw = work_count(p);
+      for (int wi = 0; wi < nw; ++wi) {
+        const Work w = work_item(p, wi);
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          mbar_wait(smem_u32(&full_bar[stage]), phase);
+          uint8_t* raw = ring + stage * S::kStageBytes + (kConv == 1 ? 0 : 2 * S::kABytes);
+          uint8_t* lo = raw + kConvBytes;
+  #pragma unroll 4
+          for (int i = t; i < kConvBytes / 16; i += 64) {
+            float4 v = *reinterpret_cast<const float4*>(raw + 16 * i);
+            v.x -= __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+            v.y -= __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+            v.z -= __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+            v.w -= __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+            *reinterpret_cast<float4*>(lo + 16 * i) = v;
           }
           fence_proxy_async_smem();  // generic-proxy smem writes -> visible to UMMA
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&conv_bar[stage]));
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        parity ^= 1;
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
-        if (++rs == kRawStages) { rs = 0; rphase ^= 1; }
       }
     }
-  } else if (kConv != 0 && !Kind::kScaled && (warp == 2 || warp == 3)) {
-    // ===================== in-kernel lo split (TF32, one operand) =====================
-    const int t = threadIdx.x - 64;  // 0..63
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const int split = u / (p.tiles_m * p.tiles_n);
-      const int kb0 = split * kb_per;
-      const int kb1 = min(p.total_kblocks, kb0 + kb_per);
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(smem_u32(&full_bar[stage]), phase);
-        uint8_t* raw = ring + stage * S::kStageBytes + (kConv == 1 ? 0 : 2 * S::kABytes);
-        uint8_t* lo = raw + kConvBytes;
-#pragma unroll 4
-        for (int i = t; i < kConvBytes / 16; i += 64) {
-          float4 v = *reinterpret_cast<const float4*>(raw + 16 * i);
-          v.x -= __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-          v.y -= __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-          v.z -= __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-          v.w -= __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-          *reinterpret_cast<float4*>(lo + 16 * i) = v;
+  } else {
+    regs_work();  // epilogue (and F16S converter) warpgroups
+    if (kF16Conv && warp >= R::kConv0) {
+      // ===================== in-kernel FP16 split (F16S, one operand) =====================
+      // Two groups of 4 warps take alternate k-blocks, so each group's serial
+      // chain (raw wait, LDS, convert, h/l-slot wait, STS, proxy fence, arrive)
+      // has two MMA k-blocks of time. Thread r of a group owns row r of the
+      // converted tile: reads its 128-byte raw row (SWIZZLE_128B: 16-byte chunk c at
+      // c ^ (r & 7)) and writes 64-byte h and l rows (SWIZZLE_64B: chunk c at
+      // c ^ ((r >> 1) & 3)); both patterns keep each warp's 16-byte accesses
+      // conflict-free.
+      const int t = threadIdx.x - 32 * R::kConv0;
+      const int r = t % kF16ConvRows;             // tile row
+      const int grp = t / kF16ConvRows;           // k-block parity this thread converts
+      const int sw128 = r & 7, sw64 = (r >> 1) & 3;
+      const float* inv = kConv == 1 ? p.inv_scale_a : p.inv_scale_b;
+      const int64_t nrows = kConv == 1 ? p.m : p.n;
+      int stage = 0, rs = 0, parity = 0;
+      uint32_t phase = 0, rphase = 0;
+      const int nw = work_count(p);
+      for (int wi = 0; wi < nw; ++wi) {
+        const Work w = work_item(p, wi);
+        const int64_t row = (int64_t)(kConv == 1 ? w.tm * BM : w.tn * BN) + r;
+        const float sc = row < nrows ? 1.f / __ldg(inv + row) : 1.f;  // exact: powers of two
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          if (parity == grp) {
+            // raw tile -> registers -> halves; the raw slot is released as soon as
+            // its values are consumed, before waiting for the h/l slot
+            mbar_wait(smem_u32(&rfull_bar[rs]), rphase);
+            const uint32_t raw = smem_u32(raw_ring + rs * kRawTileBytes) + r * 128;
+            float4 x[8];
+  #pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = lds128f(raw + ((j ^ sw128) << 4));
+            uint4 hw[4], lw[4];
+  #pragma unroll
+            for (int j = 0; j < 4; ++j) split8_f16(x[2 * j], x[2 * j + 1], sc, hw[j], lw[j]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&rempty_bar[rs]));
+            mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);  // MMA done with the h/l slot
+            const uint32_t hrow = smem_u32(ring + stage * S::kStageBytes) +
+                                  (kConv == 1 ? 0 : 2 * S::kABytes) + r * 64;
+  #pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t off = (j ^ sw64) << 4;
+              sts128(hrow + off, hw[j]);
+              sts128(hrow + kConvBytes + off, lw[j]);
+            }
+            fence_proxy_async_smem();  // generic-proxy smem writes -> visible to UMMA
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&conv_bar[stage]));
+          }
+          parity ^= 1;
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          if (++rs == kRawStages) { rs = 0; rphase ^= 1; }
         }
-        fence_proxy_async_smem();  // generic-proxy smem writes -> visible to UMMA
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&conv_bar[stage]));
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
-    }
-  } else if (warp >= kEpiWarp0) {
-    // ===================== epilogue: FP32 promotion + store =====================
-    // The tensor core's accumulator truncates (measured bias ~ -0.5 ulp per MMA
-    // accumulation), so each TMEM accumulation covers only p.chunk_kb k-blocks; the
-    // chunk is then added into round-to-nearest FP32 register sums here.
-    const int e = warp - kEpiWarp0;
-    const int q = warp % 4;             // TMEM lane quarter this warp may access
-    const int h = e / 4;                // column slice
-    uint8_t* stg = epi + e * S::kStagingBytes;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      int split, tm, tn;
-      unit_coords(u, p, split, tm, tn);
-      const int kb0 = split * kb_per;
-      const int kb1 = min(p.total_kblocks, kb0 + kb_per);
-      const int64_t row = (int64_t)tm * BM + q * 32 + lane;
-      const int64_t col0 = (int64_t)tn * BN + h * kColsPerWarp;
-      float sum[kColsPerWarp];
-#pragma unroll
-      for (int j = 0; j < kColsPerWarp; ++j) sum[j] = 0.f;
-      for (int kc = kb0; kc < kb1; kc += p.chunk_kb) {
-        // (the chunk's column scales load while the MMAs of the chunk finish)
-        ChunkScales<kColsPerWarp> cs{};
-        if (kChunkB) cs = load_chunk_scales<kColsPerWarp>(p.inv_scale_b, kc / kScaleKb, p.n, col0, lane);
-        mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
-        tc_fence_after();
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + h * kColsPerWarp;
-#pragma unroll
+    } else {
+      // ===================== epilogue: FP32 promotion + store =====================
+      // The tensor core's accumulator truncates (measured bias ~ -0.5 ulp per MMA
+      // accumulation), so each TMEM accumulation covers only p.chunk_kb k-blocks; the
+      // chunk is then added into round-to-nearest FP32 register sums here.
+      const int e = warp - kEpiWarp0;
+      const int q = warp % 4;             // TMEM lane quarter this warp may access
+      const int h = e / 4;                // column slice
+      uint8_t* stg = epi + e * S::kStagingBytes;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      const int nw = work_count(p);
+      for (int wi = 0; wi < nw; ++wi) {
+        const Work w = work_item(p, wi);
+        const int tm = w.tm, tn = w.tn, split = w.split, kb1 = w.kb1;
+        const int64_t row = (int64_t)tm * BM + q * 32 + lane;
+        const int64_t col0 = (int64_t)tn * BN + h * kColsPerWarp;
+        float sum[kColsPerWarp];
+  #pragma unroll
+        for (int j = 0; j < kColsPerWarp; ++j) sum[j] = 0.f;
+        // output scales (F16S): the row's 1/s_a and, K-major B, the warp's column
+        // 1/s_b (lane l holding columns l, 32 + l, ...), loaded while the tile's
+        // last chunk is still in the tensor core so the store below does not wait
+        // on them
+        float sa = 1.f;
+        ChunkScales<kColsPerWarp> csb{};
+        for (int kc = w.kb0, kce; kc < kb1; kc = kce) {
+          kce = chunk_end(p, kc, kb1);
+          // (the chunk's column scales load while the MMAs of the chunk finish)
+          ChunkScales<kColsPerWarp> cs{};
+          if (kChunkB) cs = load_chunk_scales<kColsPerWarp>(p.inv_scale_b, kc / kScaleKb, p.n, col0, lane);
+          if (Kind::kScaled && kce >= kb1) {
+            if (row < p.m) sa = __ldg(p.inv_scale_a + row);
+            if (!kChunkB) csb = load_chunk_scales<kColsPerWarp>(p.inv_scale_b, 0, p.n, col0, lane);
+          }
+          mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
+          if (e == 0 && lane == 0) trace_mark(p, wi == 0 && kc == w.kb0 ? 6 : 7);
+          tc_fence_after();
+          const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + h * kColsPerWarp;
+  #pragma unroll
+          for (int c = 0; c < kColsPerWarp / 16; ++c) {
+            uint32_t r[16];
+            tmem_ld_32x32b_x16(taddr + c * 16, r);
+            tmem_ld_wait();
+            if (kChunkB) {
+              // MN-major F16S B: this promotion chunk's exact column scales
+              add_chunk_scaled(sum + c * 16, r, cs, c);
+            } else {
+  #pragma unroll
+              for (int j = 0; j < 16; ++j) sum[c * 16 + j] += __uint_as_float(r[j]);
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[acc]));
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+        if (p.sk) {
+          // Stream-K: sums (before the row/column scales) of an earlier segment go
+          // to this warp's slice of the tile's partial slot, lane-interleaved
+          // float4s (each store instruction writes 512 contiguous bytes), then the
+          // slice's flag is released; the tile's last segment adds the posted
+          // slices in segment order (deterministic) before storing C.
+          constexpr int kV = kColsPerWarp / 4;
+          const int64_t slot0 = (int64_t)w.tile * p.sk_slots;
+          if (!w.fin) {
+            float4* dst = p.sk_part + ((slot0 + w.idx) * R::kEpi + e) * (kV * 32) + lane;
+  #pragma unroll
+            for (int j = 0; j < kV; ++j)
+              __stcg(dst + j * 32, make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]));
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) st_release_u64(p.sk_flags + (slot0 + w.idx) * R::kEpi + e, p.sk_token);
+            continue;
+          }
+          for (int j0 = 0; j0 < w.idx; ++j0) {
+            if (lane == 0) {
+              const unsigned long long* f = p.sk_flags + (slot0 + j0) * R::kEpi + e;
+              while (ld_acquire_u64(f) != p.sk_token) __nanosleep(100);
+            }
+            __syncwarp();
+            const float4* src = p.sk_part + ((slot0 + j0) * R::kEpi + e) * (kV * 32) + lane;
+  #pragma unroll
+            for (int j = 0; j < kV; ++j) {
+              const float4 v = __ldcg(src + j * 32);
+              sum[4 * j] += v.x; sum[4 * j + 1] += v.y; sum[4 * j + 2] += v.z; sum[4 * j + 3] += v.w;
+            }
+          }
+        }
+        // KindF16S: undo the exact power-of-two operand scales while storing,
+        // C = (acc * 1/s_a[row]) * 1/s_b[col] (MN-major B: applied per chunk above)
+        // Store: 32 rows x kColsPerWarp as 32x16 tiles (64B swizzle) through this
+        // warp's staging tile, one TMA store at a time — except on the CTA's last
+        // work item, where the operand ring is idle (its last MMAs have completed)
+        // and holds all of the warp's tiles, so their stores issue back to back.
+        const bool ring_stage = wi == nw - 1;
+  #pragma unroll
         for (int c = 0; c < kColsPerWarp / 16; ++c) {
-          uint32_t r[16];
-          tmem_ld_32x32b_x16(taddr + c * 16, r);
-          tmem_ld_wait();
-          if (kChunkB) {
-            // MN-major F16S B: this promotion chunk's exact column scales
-            add_chunk_scaled(sum + c * 16, r, cs, c);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) sum[c * 16 + j] += __uint_as_float(r[j]);
+          uint8_t* tile = ring_stage ? ring + (e * (kColsPerWarp / 16) + c) * S::kStagingBytes : stg;
+          if (!ring_stage) {
+            if (lane == 0) tma_store_wait_read<0>();
+            __syncwarp();
+          }
+  #pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int pj = j ^ ((lane >> 1) & 3);
+            float4 v = make_float4(sum[c * 16 + 4 * j], sum[c * 16 + 4 * j + 1],
+                                   sum[c * 16 + 4 * j + 2], sum[c * 16 + 4 * j + 3]);
+            if (Kind::kScaled && kChunkB) {
+              v.x *= sa; v.y *= sa; v.z *= sa; v.w *= sa;
+            } else if (Kind::kScaled) {
+              // column c*16 + 4j + t of the warp's slice: lane (that % 32) of csb
+              const int cc = c * 16 + 4 * j;
+              const float src = csb.v[cc / 32];
+              v.x = (v.x * sa) * __shfl_sync(0xffffffffu, src, (cc + 0) % 32);
+              v.y = (v.y * sa) * __shfl_sync(0xffffffffu, src, (cc + 1) % 32);
+              v.z = (v.z * sa) * __shfl_sync(0xffffffffu, src, (cc + 2) % 32);
+              v.w = (v.w * sa) * __shfl_sync(0xffffffffu, src, (cc + 3) % 32);
+            }
+            *reinterpret_cast<float4*>(tile + lane * 64 + pj * 16) = v;
+          }
+          if (!ring_stage) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(&map_c, smem_u32(tile), tn * BN + h * kColsPerWarp + c * 16,
+                           tm * BM + q * 32, split);
+              tma_store_commit();
+            }
           }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[acc]));
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      }
-      // KindF16S: undo the exact power-of-two operand scales while storing,
-      // C = (acc * 1/s_a[row]) * 1/s_b[col] (MN-major B: applied per chunk above)
-      const float sa = (Kind::kScaled && row < p.m) ? __ldg(p.inv_scale_a + row) : 1.f;
-      // Store: 32 rows x kColsPerWarp through a 32x16 staging tile (64B swizzle).
-#pragma unroll
-      for (int c = 0; c < kColsPerWarp / 16; ++c) {
-        if (lane == 0) tma_store_wait_read<0>();
-        __syncwarp();
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int pj = j ^ ((lane >> 1) & 3);
-          float4 v = make_float4(sum[c * 16 + 4 * j], sum[c * 16 + 4 * j + 1],
-                                 sum[c * 16 + 4 * j + 2], sum[c * 16 + 4 * j + 3]);
-          if (Kind::kScaled && kChunkB) {
-            v.x *= sa; v.y *= sa; v.z *= sa; v.w *= sa;
-          } else if (Kind::kScaled) {
-            // the scale vector has n entries (n % 4 == 0): whole float4s are in range
-            const int64_t cj = col0 + c * 16 + 4 * j;
-            const float4 sb = cj < p.n ? __ldg(reinterpret_cast<const float4*>(p.inv_scale_b + cj))
-                                       : make_float4(0.f, 0.f, 0.f, 0.f);
-            v.x = (v.x * sa) * sb.x;
-            v.y = (v.y * sa) * sb.y;
-            v.z = (v.z * sa) * sb.z;
-            v.w = (v.w * sa) * sb.w;
+        if (ring_stage) {
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+  #pragma unroll
+            for (int c = 0; c < kColsPerWarp / 16; ++c)
+              tma_store_3d(&map_c, smem_u32(ring + (e * (kColsPerWarp / 16) + c) * S::kStagingBytes),
+                           tn * BN + h * kColsPerWarp + c * 16, tm * BM + q * 32, split);
+            tma_store_commit();
           }
-          *reinterpret_cast<float4*>(stg + lane * 64 + pj * 16) = v;
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_3d(&map_c, smem_u32(stg), tn * BN + h * kColsPerWarp + c * 16,
-                       tm * BM + q * 32, split);
-          tma_store_commit();
         }
       }
+      if (e == 0 && lane == 0) trace_mark(p, 8);
+      if (lane == 0) tma_store_wait_all();
+      if (e == 0 && lane == 0) trace_mark(p, 9);
     }
-    if (lane == 0) tma_store_wait_all();
   }
 
+  __syncwarp();  // reconverge the role branches: bar.sync is warp-aligned
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) trace_mark(p, 10);
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -1305,6 +1491,7 @@ gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
   }
 
   tc_fence_before();
+  __syncwarp();  // reconverge the role branches: the cluster barrier is warp-aligned
   cluster_sync_all();  // both CTAs done with the accumulator before it is freed
   if (warp == 2) {
     tc_fence_after();
@@ -1606,12 +1793,16 @@ int tc_prepare_pair(const float* A, int64_t m, const float* B, int64_t n, int64_
 // partial C's, the reduction reads them and writes C). Wave quantisation
 // matters: 64 tiles x 3 splits = 192 units is two waves on 148 SMs and slower
 // than 2 splits in one wave.
-static int choose_splits(int tiles, int kblocks, int64_t m, int64_t n, int sms) {
+static int choose_splits(int tiles, int kblocks, int64_t m, int64_t n, int sms,
+                         double* time_out = nullptr) {
   constexpr double kKblockSeconds = 0.5e-6;  // ~6 MMAs x 128 clk at ~1.6 GHz
   constexpr double kUnitOverheadKb = 2.0;    // prologue + epilogue drain, in k-blocks
   constexpr double kHbm = 5.0e12;
   constexpr double kReduceLaunchSeconds = 4.0e-6;
-  if (tiles >= 4 * sms || kblocks < 8) return 1;
+  if (tiles >= 4 * sms || kblocks < 8) {
+    if (time_out) *time_out = std::ceil((double)tiles / sms) * (kblocks + kUnitOverheadKb) * kKblockSeconds;
+    return 1;
+  }
   const double mn = (double)m * (double)n;
   int best = 1;
   double best_t = 1e300;
@@ -1629,7 +1820,59 @@ static int choose_splits(int tiles, int kblocks, int64_t m, int64_t n, int sms) 
       best = s;
     }
   }
+  if (time_out) *time_out = best_t;
   return best;
+}
+
+// Stream-K (single-CTA kernel, pre-split operands): the grid's CTAs share the
+// (tile, k-block) space evenly, so a problem of 128 or 256 tiles (1024 x 4096
+// and 4096 x 4096 outputs: 86.5% of 148 SMs' wave slots) runs as ~0.87 and
+// ~1.73 tiles per SM instead of 1 and 2. Cut tiles exchange unscaled FP32
+// partials through an L2-resident workspace (BM x BN floats per cut). The result
+// is deterministic (fixed cuts for a given SM count) but rounds the cut tiles'
+// sums in a different association than the uncut kernel (like split-K).
+// Measured on the B200 it does not pay: these GEMMs are power-bound (the SM
+// clock settles at ~1.4-1.55 GHz under dense MMAs with 128 SMs busy), so the
+// 20 idle SMs add no throughput — 1024 x 4096 x 4096: 108.9 vs 106.8 us per
+// call, the whole sweep 183.9 vs 182.4 ms (tools/probes/probe_streamk.py) —
+// hence off by default.
+// mtnn_config_set("tc_streamk", v) / MTNN_STREAMK: 0 off (default), 1 when it
+// shortens the predicted makespan, 2 whenever possible (tests).
+static std::atomic<int> g_tc_streamk{-1};
+int tc_streamk_mode() {
+  int v = g_tc_streamk.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = getenv("MTNN_STREAMK");
+    v = e ? std::min(2, std::max(0, atoi(e))) : 0;
+    g_tc_streamk.store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+void set_tc_streamk_mode(int v) { g_tc_streamk.store(v, std::memory_order_relaxed); }
+
+// Most segments any tile is cut into (CTA b owns [b*W/G, (b+1)*W/G)).
+static int streamk_segments(int tiles, int kblocks, int G) {
+  const int64_t W = (int64_t)tiles * kblocks;
+  auto first = [&](int64_t x) { return ((x + 1) * G + W - 1) / W - 1; };
+  int64_t most = 1;
+  for (int64_t t = 0; t < tiles; ++t)
+    most = std::max(most, first((t + 1) * kblocks - 1) - first(t * kblocks) + 1);
+  return (int)most;
+}
+
+// mtnn_profile_trace: phase timestamps of the single-CTA kernel's CTAs.
+static std::atomic<unsigned long long*> g_trace{nullptr};
+static std::atomic<int64_t> g_trace_ctas{0};
+void set_gemm_trace(void* buf, int64_t ctas) {
+  g_trace.store(static_cast<unsigned long long*>(buf));
+  g_trace_ctas.store(ctas);
+}
+
+// Unique per launch: flags are compared for equality with it and never reset.
+static unsigned long long next_streamk_token() {
+  static std::atomic<unsigned long long> ctr{
+      ((unsigned long long)time(nullptr) << 24) ^ ((unsigned long long)getpid() << 44) ^ 0x5bd1e995ull};
+  return ctr.fetch_add(1, std::memory_order_relaxed) + 1;
 }
 
 // MN-major B^T on CTA pairs: each CTA's 128 columns are whole 64-column TMA
@@ -1745,18 +1988,52 @@ static int tc_run_bn(const TcOperand& a, const TcOperand& b, float* C, int64_t m
   p.tiles_n = (int)((n + BN - 1) / BN);
   p.total_kblocks = (int)((k + bk - 1) / bk);
   const int tiles = p.tiles_m * p.tiles_n;
-  int splits = choose_splits(tiles, p.total_kblocks, m, n, di->sm_count);
+  double t_split = 0.0;
+  int splits = choose_splits(tiles, p.total_kblocks, m, n, di->sm_count, &t_split);
   align_scale_chunks(p, kind, b_is_nk, splits);
   splits = (p.total_kblocks + p.kblocks_per_split - 1) / p.kblocks_per_split;
   p.splits = splits;
   p.units = tiles * splits;
-  const int grid = std::min(p.units, di->sm_count);
+  int grid = std::min(p.units, di->sm_count);
 
+  // stream-K instead, when it is predicted clearly shorter (same cost model as
+  // choose_splits: 0.5 us per k-block, 2 k-blocks per unit of overhead, one more
+  // per cut for the partial exchange)
+  const int G = di->sm_count;
+  const int64_t W = (int64_t)tiles * p.total_kblocks;
+  const int sk_mode = conv == 0 ? tc_streamk_mode() : 0;
+  if (sk_mode != 0 && W >= 4 * (int64_t)G && tiles > 1) {
+    const int segs = streamk_segments(tiles, p.total_kblocks, G);
+    const double t_sk = ((double)((W + G - 1) / G) + 3.0) * 0.5e-6;
+    if (segs <= 8 && (sk_mode == 2 || t_sk < 0.97 * t_split)) {
+      p.sk = 1;
+      p.sk_slots = std::max(1, segs - 1);
+      p.sk_work = W;
+      p.splits = 1;
+      p.kblocks_per_split = p.total_kblocks;
+      p.units = tiles;
+      if (kind == TcKind::F16S && !b_is_nk) {
+        constexpr int sk = kScaleChunkK / tc::KindF16S::BK;  // chunks inside scale chunks
+        if (sk % p.chunk_kb != 0) p.chunk_kb = sk;
+      }
+      splits = 1;
+      grid = G;
+    }
+  }
+
+  if (g_trace.load() && grid <= g_trace_ctas.load()) p.trace = g_trace.load();
   float* out = C;
   ScratchBuffer part;
   if (splits > 1) {
     MTNN_TRY(part.alloc((size_t)splits * m * ldc * sizeof(float), s));
     out = static_cast<float*>(part.ptr);
+  } else if (p.sk) {
+    const size_t nslots = (size_t)tiles * p.sk_slots;
+    const size_t part_bytes = align256(nslots * tc::BM * BN * sizeof(float));
+    MTNN_TRY(part.alloc(part_bytes + nslots * tc::kEpiWarps * sizeof(unsigned long long), s));
+    p.sk_part = static_cast<float4*>(part.ptr);
+    p.sk_flags = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(part.ptr) + part_bytes);
+    p.sk_token = next_streamk_token();
   }
   int rc;
   if (kind == TcKind::F16S && conv == 0)

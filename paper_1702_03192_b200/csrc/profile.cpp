@@ -88,6 +88,12 @@ using namespace mtnn;
 
 extern "C" {
 
+int mtnn_profile_trace(void* buf, int64_t ctas) {
+  if (buf && ctas <= 0) return fail(MTNN_EINVAL, "trace buffer needs ctas > 0");
+  set_gemm_trace(buf, buf ? ctas : 0);
+  return MTNN_OK;
+}
+
 int mtnn_profile_enable(int on) {
   g_mask.store(on ? (1u << MTNN_KCLASS_COUNT) - 1u : 0u);
   g_counting.store(on != 0);

@@ -12,7 +12,8 @@ cases = {"nt8192": ("nt", 8192, 8192, 8192), "nt16384": ("nt", 16384, 16384, 163
          "nt4096": ("nt", 4096, 4096, 4096), "skinny_m128": ("nt", 128, 16384, 16384),
          "skinny_n128": ("nt", 16384, 128, 16384), "skinny_m256": ("nt", 256, 16384, 16384),
          "smallk256": ("nt", 16384, 16384, 256), "nn1024x4096x4096": ("nn", 1024, 4096, 4096),
-         "fcn10": ("nt", 1024, 10, 4096)}
+         "fcn10": ("nt", 1024, 10, 4096), "nt1024x4096x4096": ("nt", 1024, 4096, 4096),
+         "nt4096x4096x1024": ("nt", 4096, 4096, 1024)}
 op, m, n, k = cases[which]
 if op == "tr":
     b = torch.rand(m, n, device="cuda"); out = torch.empty(n, m, device="cuda")
