@@ -112,6 +112,7 @@ struct FixupDev {
   int32_t a_row0, b_row0;
   int reset_a, reset_b;
   int smem_entries;
+  int a_chunked, b_chunked;  // K-major A / B with per-(256-k chunk, row) scales (fused split)
 };
 
 constexpr int kFixThreads = 256;
@@ -122,8 +123,12 @@ constexpr int64_t kFixChunk = 256;  // k per FFMA chain in the overflow recomput
 constexpr int kFixSmemEntries = 8192;
 constexpr size_t kFixSmemBytes = (size_t)kFixSmemEntries * 12;
 
-__device__ __forceinline__ float rep_a(const FixupDev& p, int64_t i, float a) {
-  if (p.rep == (int)FixRep::F16S) return f16s_represented(a, p.inv_a[i]);
+// 1/s of A at (row i, k index kcol): per row, or per (chunk, row) (fused split)
+__device__ __forceinline__ float inv_a_at(const FixupDev& p, int64_t i, int64_t kcol) {
+  return p.a_chunked ? p.inv_a[(kcol / kScaleChunkK) * p.m + i] : p.inv_a[i];
+}
+__device__ __forceinline__ float rep_a(const FixupDev& p, int64_t i, int64_t kcol, float a) {
+  if (p.rep == (int)FixRep::F16S) return f16s_represented(a, inv_a_at(p, i, kcol));
   if (p.rep == (int)FixRep::TF32_RNA) return tf32_represented<true>(a);
   return tf32_represented<false>(a);
 }
@@ -197,10 +202,11 @@ __device__ __forceinline__ uint32_t key_row(unsigned long long k) { return (uint
 __device__ __forceinline__ uint32_t key_col(unsigned long long k) { return (uint32_t)k; }
 
 // 1/s of B at (row j of B, k index kcol): per row for K-major B (NT), per
-// (kScaleChunkK chunk, column) for MN-major B^T (NN; split_f16.cu)
+// (kScaleChunkK chunk, column) for MN-major B^T (NN; split_f16.cu) and for a
+// fused-split K-major B (split_seg.cuh)
 template <bool B_NK>
 __device__ __forceinline__ float inv_b_at(const FixupDev& p, int64_t j, int64_t kcol) {
-  return B_NK ? p.inv_b[j] : p.inv_b[(kcol / kScaleChunkK) * p.n + j];
+  return (B_NK && !p.b_chunked) ? p.inv_b[j] : p.inv_b[(kcol / kScaleChunkK) * p.n + j];
 }
 
 template <bool B_NK>
@@ -217,11 +223,17 @@ __global__ void __launch_bounds__(kFixThreads, 2) fixup_kernel(const FixupDev p)
   // append to them completed before the GEMM passed its griddepcontrol.wait,
   // and the GEMM triggers its dependents only after that wait. Reading them
   // here overlaps the load with the GEMM's tail.
-  if (threadIdx.x == 0) {
+  // (A fused-split GEMM appends entries itself: read them after its completion.)
+  const bool late = p.a_chunked || p.b_chunked;
+  if (threadIdx.x == 0 && !late) {
     s_na = p.fa.ctr ? *reinterpret_cast<volatile unsigned*>(&p.fa.ctr->count) : 0u;
     s_nb = p.fb.ctr ? *reinterpret_cast<volatile unsigned*>(&p.fb.ctr->count) : 0u;
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0 && late) {
+    s_na = p.fa.ctr ? *reinterpret_cast<volatile unsigned*>(&p.fa.ctr->count) : 0u;
+    s_nb = p.fb.ctr ? *reinterpret_cast<volatile unsigned*>(&p.fb.ctr->count) : 0u;
+  }
   __syncthreads();
   const unsigned na = s_na, nb = s_nb;
   if (na + nb == 0) return;  // the usual case: nothing listed, counters already zero
@@ -274,7 +286,7 @@ __global__ void __launch_bounds__(kFixThreads, 2) fixup_kernel(const FixupDev p)
         const int64_t j = (int64_t)e.row - p.b_row0;
         const int64_t i = (q % cm) * kFixThreads + threadIdx.x;
         if (j < 0 || j >= p.n || i >= p.m) continue;
-        const float v = rep_a(p, i, __ldg(p.A + i * p.k + e.col)) * e.r;
+        const float v = rep_a(p, i, e.col, __ldg(p.A + i * p.k + e.col)) * e.r;
         if (v != 0.f)
           for (int d = 0; d < p.ndst; ++d) atomicAdd(p.C[d] + i * p.ldc + j, v);
       }
@@ -321,15 +333,18 @@ __global__ void __launch_bounds__(kFixThreads, 2) fixup_kernel(const FixupDev p)
       const uint32_t gcol = (uint32_t)(j + p.b_row0);
       const unsigned b0 = nb ? lower_row(kb, nb, gcol) : 0u;
       unsigned b1 = b0;
-      float rb = 0.f;
-      while (b1 < nb && key_row(kb[b1]) == gcol) rb += fabsf(vb[b1++]);
+      float rb = 0.f;  // sum |r| * (1/s of A's row at the entry's k)
+      while (b1 < nb && key_row(kb[b1]) == gcol) {
+        rb += fabsf(vb[b1]) * (bounded ? inv_a_at(p, i, key_col(kb[b1])) : 0.f);
+        ++b1;
+      }
       const float c = p.C[0][i * p.ldc + j];
-      if (bounded && ra * kRowMax + rb * kRowMax * p.inv_a[i] <= kNegligible * fabsf(c))
+      if (bounded && ra * kRowMax + rb * kRowMax <= kNegligible * fabsf(c))
         continue;
       float s = 0.f;
       for (unsigned e = e0; e < e1; ++e) s = fmaf(va[e], b_at<B_NK>(p, j, key_col(ka[e])), s);
       for (unsigned e = b0; e < b1; ++e)
-        s = fmaf(rep_a(p, i, __ldg(p.A + i * p.k + key_col(kb[e]))), vb[e], s);
+        s = fmaf(rep_a(p, i, key_col(kb[e]), __ldg(p.A + i * p.k + key_col(kb[e]))), vb[e], s);
       if (s != 0.f || isnan(s))
         for (int d = 0; d < p.ndst; ++d) p.C[d][i * p.ldc + j] += s;
     } else {
@@ -348,12 +363,15 @@ __global__ void __launch_bounds__(kFixThreads, 2) fixup_kernel(const FixupDev p)
       }
       unsigned e1 = e0;
       float rb = 0.f;
-      while (e1 < nb && key_row(kb[e1]) == gcol) rb += fabsf(vb[e1++]);
-      if (bounded && rb * kRowMax * p.inv_a[i] <= kNegligible * fabsf(p.C[0][i * p.ldc + j]))
+      while (e1 < nb && key_row(kb[e1]) == gcol) {
+        rb += fabsf(vb[e1]) * (bounded ? inv_a_at(p, i, key_col(kb[e1])) : 0.f);
+        ++e1;
+      }
+      if (bounded && rb * kRowMax <= kNegligible * fabsf(p.C[0][i * p.ldc + j]))
         continue;
       float s = 0.f;
       for (unsigned e = e0; e < e1; ++e)
-        s = fmaf(rep_a(p, i, __ldg(p.A + i * p.k + key_col(kb[e]))), vb[e], s);
+        s = fmaf(rep_a(p, i, key_col(kb[e]), __ldg(p.A + i * p.k + key_col(kb[e]))), vb[e], s);
       if (s != 0.f || isnan(s))
         for (int d = 0; d < p.ndst; ++d) p.C[d][i * p.ldc + j] += s;
     }
@@ -385,6 +403,8 @@ static int make_dev(const FixupArgs& a, FixupDev* out) {
   p.reset_a = a.reset_a ? 1 : 0;
   p.reset_b = a.reset_b ? 1 : 0;
   p.smem_entries = kFixSmemEntries;
+  p.a_chunked = a.a_chunked ? 1 : 0;
+  p.b_chunked = a.b_chunked ? 1 : 0;
   if (p.rep == (int)FixRep::F16S && p.inv_a == nullptr && a.fb.ctr != nullptr)
     return fail(MTNN_EINVAL, "fix-up: F16S B entries need A's row scales");
   return MTNN_OK;

@@ -9,11 +9,14 @@ dev = torch.device("cuda:0"); s = torch.cuda.current_stream().cuda_stream
 _lib.config_set("tc_pair", 0)
 import os
 _lib.config_set("tc_streamk", int(os.environ.get("SK", "0")))
+_lib.config_set("fused_split", int(os.environ.get("FS", "0")))
 NAMES = ["entry", "prologue", "pdl_wait", "tma0", "stage0", "mma_last", "chunk0", "chunk_last",
-         "stores_issued", "stores_done", "exit", "tma_last", "producer_w0"]
+         "stores_issued", "stores_done", "exit", "tma_last", "producer_w0", "split_first", "split_last", "chunk_wait_last"]
 A = torch.rand(4096 * 16384, device=dev); B = torch.rand(4096 * 16384, device=dev); C = torch.empty(4096 * 4096, device=dev)
 tr = torch.zeros(148 * 16, dtype=torch.int64, device=dev)
 shapes = [(1024, 4096, k) for k in (512, 4096)] + [(2048, 2048, 1024), (4096, 4096, 4096), (256, 4096, 4096)]
+if os.environ.get("SHAPES"):
+    shapes = [tuple(int(x) for x in t.split("x")) for t in os.environ["SHAPES"].split(",")]
 for m, n, k in shapes:
     for _ in range(3):
         _lib.check(L.mtnn_gemm_nt(A.data_ptr(), B.data_ptr(), C.data_ptr(), m, n, k, 3, s))
