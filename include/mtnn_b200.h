@@ -108,7 +108,8 @@ int mtnn_profile_sample_every(int n);
  * dependency wait, 3 first TMA issued, 4 first stage landed (MMA warp), 5 last
  * MMA issued, 6 first accumulator chunk ready (epilogue), 7 last chunk ready,
  * 8 last C store issued, 9 C stores complete, 10 exit, 11 last TMA issued.
- * Diagnostics only; NULL turns it off. */
+ * Diagnostics only, compiled in with -DMTNN_TRACE (tools/build_variant.sh);
+ * other builds return MTNN_ENOTSUP for a non-NULL buffer. NULL turns it off. */
 int mtnn_profile_trace(void* buf, int64_t ctas);
 int mtnn_profile_read_timed(int kclass, double* total_ms, int64_t* launches, double* work);
 int mtnn_profile_reset(void);
@@ -127,14 +128,11 @@ int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* w
  *   each CTA loading half of B); 2 forces it whenever structurally possible
  *   (tests), 0 keeps the single-CTA 128x256 tiles. Bit-identical results at the
  *   same split-K.
- * "tc_streamk": 0 (default; env MTNN_STREAMK): 1 runs single-CTA tensor-core
- *   GEMMs on pre-split operands whose tile count leaves the last wave partly
- *   empty (e.g. 128 or 256 tiles on 148 SMs) as stream-K — the SMs share the
- *   (tile, k-block) space evenly and cut tiles add FP32 partials from an
- *   L2-resident workspace (deterministic; the cut tiles round like split-K) —
- *   when the predicted makespan is >= 3% shorter than the split-K choice; 2
- *   forces it whenever possible (tests). Off by default: on the B200 those
- *   GEMMs are power-bound, so the idle SMs add no throughput.
+ * "fused_split": 0 (default; env MTNN_FUSED_SPLIT): 1/2 split tc3xf16s NT
+ *   operands inside the GEMM (per-(256-k chunk, row) scales, chunk 0 by a
+ *   pre-pass, later chunks by two warps of every GEMM CTA ahead of its TMA
+ *   producer). Correct, but 2.5-4x slower on the B200 (the GEMM's own TMA
+ *   traffic saturates the SMs' L1TEX path; profiles/fused_split_r02.md).
  * "host_pipeline_blocked": 1 (default; env MTNN_PIPE_BLOCKED=0 turns it off):
  *   host-buffer NT calls on the tc3xf16s path with n >= 1024, k <= 4096 stream B in row
  *   blocks against A's first row block so C leaves while B arrives; 0 = copy B

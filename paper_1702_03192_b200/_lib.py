@@ -51,6 +51,10 @@ class MtnnError(RuntimeError):
     """A CUDA/runtime failure reported by libmtnn_b200."""
 
 
+# diagnostics-only entry points a library selected by MTNN_B200_LIB may lack
+_DIAGNOSTIC = {"mtnn_profile_trace"}
+
+
 def _load():
     path = os.environ.get("MTNN_B200_LIB", str(LIB_PATH))
     if not Path(path).exists():
@@ -112,6 +116,8 @@ def _load():
                                             c_int64, c_int64, c_int64, c_int, POINTER(c_int)]),
     }
     for name, (res, args) in sig.items():
+        if name in _DIAGNOSTIC and not hasattr(lib, name):
+            continue  # (an older library under MTNN_B200_LIB for A/B runs)
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

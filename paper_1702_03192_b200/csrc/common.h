@@ -116,14 +116,11 @@ void set_f16s_inkernel_max_short(int64_t v);
 // Run-time knob (mtnn_config_set "tc_pair"): 256 x 256 CTA-pair tiles for large NT.
 int tc_pair_mode();  // 0 off, 1 large problems (default), 2 always when possible
 void set_tc_pair_mode(int v);
-// Run-time knob (mtnn_config_set "tc_streamk"): stream-K for wave-quantised tile counts.
-int tc_streamk_mode();  // 0 off, 1 when predicted shorter (default), 2 always when possible
-void set_tc_streamk_mode(int v);
 // Run-time knob (mtnn_config_set "fused_split"): operand split overlapped with the NT GEMM.
 int fused_split_mode();  // 0 off, 1 measured-good shapes, 2 whenever eligible
 void set_fused_split_mode(int v);
 // mtnn_profile_trace: phase timestamps of the single-CTA tensor-core kernel.
-void set_gemm_trace(void* buf, int64_t ctas);
+int set_gemm_trace(void* buf, int64_t ctas);
 // ldc: C row stride in elements (-1 = n); a larger one pads each C row.
 int tc_run(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n, int64_t k,
            bool b_is_nk, TcKind kind, cudaStream_t s, int64_t ldc = -1);

@@ -224,28 +224,6 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-// Warp-role register split (setmaxnreg): launch bounds give every thread of a
-// 640-thread CTA 96 registers; warpgroup 0 (TMA / MMA / TMEM warps) needs far
-// fewer, the epilogue (64 FP32 sums per thread) more — without the split its
-// spills go to local memory, which misses the tiny L1 (shared memory takes
-// 225 KB) and costs an L2 round trip per reload on the tile's exposed tail.
-// setmaxnreg.inc only draws on registers other warps of the CTA released, so
-// 128 * control + 512 * work <= 640 * 96 (the launch allocation).
-#ifndef MTNN_REGS_CONTROL  // (A/B builds: -DMTNN_REGS_CONTROL=0 disables the split)
-#define MTNN_REGS_CONTROL 0
-#define MTNN_REGS_WORK 0
-#endif
-constexpr int kRegsControl = MTNN_REGS_CONTROL, kRegsWork = MTNN_REGS_WORK;
-static_assert(4 * 32 * kRegsControl + 16 * 32 * kRegsWork <= 640 * 96, "launch register allocation");
-// (each called by all four warps of a warpgroup, at the top of that warpgroup's
-// own branch, so the compiler allocates each branch under its own limit)
-__device__ __forceinline__ void regs_control() {
-  if constexpr (kRegsControl > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsControl));
-}
-__device__ __forceinline__ void regs_work() {
-  if constexpr (kRegsControl > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsWork));
-}
-
 // Programmatic dependent launch: the GEMMs are launched with programmatic stream
 // serialization, so their prologue (barrier init, TMEM allocation, descriptor
 // prefetch) overlaps the tail of the operand split that precedes them on the
@@ -336,14 +314,6 @@ struct Params {
   int units;
   const float* inv_scale_a;  // KindF16S: 1/s per row of A (m) and of B (n)
   const float* inv_scale_b;
-  // Stream-K (sk != 0, single-CTA kernel, pre-split operands): the grid's G CTAs
-  // share the tile-major (tile, k-block) space evenly, see work_item().
-  int sk;
-  int sk_slots;                 // partial slots per tile (segments per tile - 1)
-  int64_t sk_work;              // tiles * total_kblocks
-  float4* sk_part;              // [tile][slot][epilogue warp][kCols/4][32 lanes]
-  unsigned long long* sk_flags; // [tile][slot][epilogue warp] = sk_token when posted
-  unsigned long long sk_token;  // unique per launch (flags are never reset)
   unsigned long long* trace;    // mtnn_profile_trace: [CTA][kTracePoints] globaltimer ns
   // Fused split (kConv == 3): both K-major operands carry per-(256-k chunk,
   // row) scales (inv_scale_a/b = fs.op[0/1].inv, [chunk][rows]); chunks
@@ -375,74 +345,36 @@ __device__ __forceinline__ void unit_coords(int u, const Params& p, int& split, 
   tn = r / gm;
 }
 
-// One work item of a CTA: output tile (tm, tn), k-split index, k-block range.
-// Stream-K items also carry their segment index within the tile and whether
-// they hold the tile's last k-block (fin: that CTA adds the earlier segments'
-// partial sums and stores C; the others post partials).
+// One work item of a CTA: output tile (tm, tn), k-split index, k-block range
+// (units are (k-split, tile), strided over the grid).
 struct Work {
-  int tm, tn, split, kb0, kb1, tile, idx;
-  bool fin;
+  int tm, tn, split, kb0, kb1;
 };
-
-// Stream-K: CTA b owns k-blocks [b*W/G, (b+1)*W/G) of the tile-major space
-// (W = tiles * total_kblocks, G = gridDim.x <= W). Its range covers the tail of
-// one tile, whole tiles, and the head of a last tile; the head (the only
-// segment that is not its tile's last) is processed FIRST, so every posted
-// partial is produced without waiting and every waiting segment depends only on
-// partials that are — no cycle, given all G CTAs are resident (G <= SMs, one
-// CTA per SM). A tile's segments are numbered by CTA: idx = b - first CTA of it.
-__device__ __forceinline__ int64_t sk_first_cta(int64_t x, int64_t W, int64_t G) {
-  return ((x + 1) * G + W - 1) / W - 1;  // largest b with floor(b*W/G) <= x
-}
 __device__ __forceinline__ int work_count(const Params& p) {
-  if (p.sk) {
-    const int64_t W = p.sk_work, G = gridDim.x, KB = p.total_kblocks;
-    const int64_t s = (int64_t)blockIdx.x * W / G, e = ((int64_t)blockIdx.x + 1) * W / G;
-    return e > s ? (int)((e - 1) / KB - s / KB + 1) : 0;
-  }
   return blockIdx.x < (unsigned)p.units ? (p.units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 }
 __device__ __forceinline__ Work work_item(const Params& p, int i) {
   Work w;
-  if (p.sk) {
-    const int64_t W = p.sk_work, G = gridDim.x, KB = p.total_kblocks;
-    const int64_t s = (int64_t)blockIdx.x * W / G, e = ((int64_t)blockIdx.x + 1) * W / G;
-    const int t0 = (int)(s / KB), t1 = (int)((e - 1) / KB);
-    const bool head = (e % KB) != 0;
-    const int tile = head ? (i == 0 ? t1 : t0 + i - 1) : t0 + i;
-    int split;
-    unit_coords(tile, p, split, w.tm, w.tn);
-    w.split = 0;
-    w.tile = tile;
-    w.kb0 = (int)(max(s, (int64_t)tile * KB) - (int64_t)tile * KB);
-    w.kb1 = (int)(min(e, ((int64_t)tile + 1) * KB) - (int64_t)tile * KB);
-    w.fin = !(head && i == 0);
-    w.idx = (int)(blockIdx.x - sk_first_cta((int64_t)tile * KB, W, G));
-    return w;
-  }
-  const int u = blockIdx.x + i * gridDim.x;
-  unit_coords(u, p, w.split, w.tm, w.tn);
-  w.tile = u;
+  unit_coords(blockIdx.x + i * gridDim.x, p, w.split, w.tm, w.tn);
   w.kb0 = w.split * p.kblocks_per_split;
   w.kb1 = min(p.total_kblocks, w.kb0 + p.kblocks_per_split);
-  w.fin = true;
-  w.idx = 0;
   return w;
-}
-// End of the promotion chunk starting at k-block kc. Stream-K segments start
-// anywhere, so their chunks follow the global chunk grid (an MN-major B's scale
-// chunks stay whole); split-K ranges start on it already where that matters.
-__device__ __forceinline__ int chunk_end(const Params& p, int kc, int kb1) {
-  return p.sk ? min(kb1, (kc / p.chunk_kb + 1) * p.chunk_kb) : min(kb1, kc + p.chunk_kb);
 }
 
 // Phase timestamps of one CTA (mtnn_profile_trace; off = null pointer).
+// Compiled in only with -DMTNN_TRACE (tools/build_variant.sh NAME -DMTNN_TRACE):
+// even the untaken null check costs ~2 us per call on the one-wave GEMMs.
 __device__ __forceinline__ void trace_mark(const Params& p, int point) {
+#ifdef MTNN_TRACE
   if (p.trace) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     p.trace[(size_t)blockIdx.x * kTracePoints + point] = t;
   }
+#else
+  (void)p;
+  (void)point;
+#endif
 }
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
@@ -453,15 +385,6 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* a) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u64(unsigned long long* a, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
-}
-
 // FP16 hi/lo of 8 consecutive k-values of one row with the row's exact
 // power-of-two scale s — the same operations as split_f16.cu's split2, so the
 // halves (and every C bit) equal the pre-split path's.
@@ -622,7 +545,6 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
   if (threadIdx.x == 0) trace_mark(p, 2);
 
   if (warp < kEpiWarp0) {
-    regs_control();  // warpgroup 0: TMA, MMA, TMEM and converter-feeding warps
     if (warp == 0) {
       // ===================== TMA producer =====================
       if (elect_one()) {
@@ -688,7 +610,7 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
         const Work w = work_item(p, wi);
         const int kb1 = w.kb1;
         for (int kc = w.kb0, kce; kc < kb1; kc = kce) {
-          kce = chunk_end(p, kc, kb1);
+          kce = min(kb1, kc + p.chunk_kb);
           mbar_wait(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
           tc_fence_after();
           const uint32_t tmem_d = tmem_base + acc * BN;
@@ -859,7 +781,6 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
       }
     }
   } else {
-    regs_work();  // epilogue (and F16S converter) warpgroups
     if (kF16Conv && warp >= R::kConv0) {
       // ===================== in-kernel FP16 split (F16S, one operand) =====================
       // Two groups of 4 warps take alternate k-blocks, so each group's serial
@@ -935,7 +856,7 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
   #pragma unroll
         for (int j = 0; j < kColsPerWarp; ++j) sum[j] = 0.f;
         for (int kc = w.kb0, kce; kc < kb1; kc = kce) {
-          kce = chunk_end(p, kc, kb1);
+          kce = min(kb1, kc + p.chunk_kb);
           // (the chunk's column scales load while the MMAs of the chunk finish)
           ChunkScales<kColsPerWarp> cs{};
           if (kChunkB && !kFS) cs = load_chunk_scales<kColsPerWarp>(p.inv_scale_b, kc / kScaleKb, p.n, col0, lane);
@@ -973,38 +894,6 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[acc]));
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        }
-        if (p.sk) {
-          // Stream-K: sums (before the row/column scales) of an earlier segment go
-          // to this warp's slice of the tile's partial slot, lane-interleaved
-          // float4s (each store instruction writes 512 contiguous bytes), then the
-          // slice's flag is released; the tile's last segment adds the posted
-          // slices in segment order (deterministic) before storing C.
-          constexpr int kV = kColsPerWarp / 4;
-          const int64_t slot0 = (int64_t)w.tile * p.sk_slots;
-          if (!w.fin) {
-            float4* dst = p.sk_part + ((slot0 + w.idx) * R::kEpi + e) * (kV * 32) + lane;
-  #pragma unroll
-            for (int j = 0; j < kV; ++j)
-              __stcg(dst + j * 32, make_float4(sum[4 * j], sum[4 * j + 1], sum[4 * j + 2], sum[4 * j + 3]));
-            __threadfence();
-            __syncwarp();
-            if (lane == 0) st_release_u64(p.sk_flags + (slot0 + w.idx) * R::kEpi + e, p.sk_token);
-            continue;
-          }
-          for (int j0 = 0; j0 < w.idx; ++j0) {
-            if (lane == 0) {
-              const unsigned long long* f = p.sk_flags + (slot0 + j0) * R::kEpi + e;
-              while (ld_acquire_u64(f) != p.sk_token) __nanosleep(100);
-            }
-            __syncwarp();
-            const float4* src = p.sk_part + ((slot0 + j0) * R::kEpi + e) * (kV * 32) + lane;
-  #pragma unroll
-            for (int j = 0; j < kV; ++j) {
-              const float4 v = __ldcg(src + j * 32);
-              sum[4 * j] += v.x; sum[4 * j + 1] += v.y; sum[4 * j + 2] += v.z; sum[4 * j + 3] += v.w;
-            }
-          }
         }
         // KindF16S: undo the exact power-of-two operand scales while storing,
         // C = (acc * 1/s_a[row]) * 1/s_b[col] (MN-major B: applied per chunk
@@ -1922,55 +1811,19 @@ static int choose_splits(int tiles, int kblocks, int64_t m, int64_t n, int sms,
   return best;
 }
 
-// Stream-K (single-CTA kernel, pre-split operands): the grid's CTAs share the
-// (tile, k-block) space evenly, so a problem of 128 or 256 tiles (1024 x 4096
-// and 4096 x 4096 outputs: 86.5% of 148 SMs' wave slots) runs as ~0.87 and
-// ~1.73 tiles per SM instead of 1 and 2. Cut tiles exchange unscaled FP32
-// partials through an L2-resident workspace (BM x BN floats per cut). The result
-// is deterministic (fixed cuts for a given SM count) but rounds the cut tiles'
-// sums in a different association than the uncut kernel (like split-K).
-// Measured on the B200 it does not pay: these GEMMs are power-bound (the SM
-// clock settles at ~1.4-1.55 GHz under dense MMAs with 128 SMs busy), so the
-// 20 idle SMs add no throughput — 1024 x 4096 x 4096: 108.9 vs 106.8 us per
-// call, the whole sweep 183.9 vs 182.4 ms (tools/probes/probe_streamk.py) —
-// hence off by default.
-// mtnn_config_set("tc_streamk", v) / MTNN_STREAMK: 0 off (default), 1 when it
-// shortens the predicted makespan, 2 whenever possible (tests).
-static std::atomic<int> g_tc_streamk{-1};
-int tc_streamk_mode() {
-  int v = g_tc_streamk.load(std::memory_order_relaxed);
-  if (v < 0) {
-    const char* e = getenv("MTNN_STREAMK");
-    v = e ? std::min(2, std::max(0, atoi(e))) : 0;
-    g_tc_streamk.store(v, std::memory_order_relaxed);
-  }
-  return v;
-}
-void set_tc_streamk_mode(int v) { g_tc_streamk.store(v, std::memory_order_relaxed); }
-
-// Most segments any tile is cut into (CTA b owns [b*W/G, (b+1)*W/G)).
-static int streamk_segments(int tiles, int kblocks, int G) {
-  const int64_t W = (int64_t)tiles * kblocks;
-  auto first = [&](int64_t x) { return ((x + 1) * G + W - 1) / W - 1; };
-  int64_t most = 1;
-  for (int64_t t = 0; t < tiles; ++t)
-    most = std::max(most, first((t + 1) * kblocks - 1) - first(t * kblocks) + 1);
-  return (int)most;
-}
-
 // mtnn_profile_trace: phase timestamps of the single-CTA kernel's CTAs.
 static std::atomic<unsigned long long*> g_trace{nullptr};
 static std::atomic<int64_t> g_trace_ctas{0};
-void set_gemm_trace(void* buf, int64_t ctas) {
+int set_gemm_trace(void* buf, int64_t ctas) {
+#ifdef MTNN_TRACE
   g_trace.store(static_cast<unsigned long long*>(buf));
   g_trace_ctas.store(ctas);
-}
-
-// Unique per launch: flags are compared for equality with it and never reset.
-static unsigned long long next_streamk_token() {
-  static std::atomic<unsigned long long> ctr{
-      ((unsigned long long)time(nullptr) << 24) ^ ((unsigned long long)getpid() << 44) ^ 0x5bd1e995ull};
-  return ctr.fetch_add(1, std::memory_order_relaxed) + 1;
+  return MTNN_OK;
+#else
+  (void)ctas;
+  if (buf == nullptr) return MTNN_OK;
+  return fail(MTNN_ENOTSUP, "phase trace not compiled in (build with -DMTNN_TRACE: tools/build_variant.sh)");
+#endif
 }
 
 // MN-major B^T on CTA pairs: each CTA's 128 columns are whole 64-column TMA
@@ -2094,13 +1947,12 @@ static int tc_run_bn(const TcOperand& a, const TcOperand& b, float* C, int64_t m
   p.tiles_n = (int)((n + BN - 1) / BN);
   p.total_kblocks = (int)((k + bk - 1) / bk);
   const int tiles = p.tiles_m * p.tiles_n;
-  double t_split = 0.0;
-  int splits = choose_splits(tiles, p.total_kblocks, m, n, di->sm_count, &t_split);
+  int splits = choose_splits(tiles, p.total_kblocks, m, n, di->sm_count);
   align_scale_chunks(p, kind, b_is_nk, splits, fs != nullptr);
   splits = (p.total_kblocks + p.kblocks_per_split - 1) / p.kblocks_per_split;
   p.splits = splits;
   p.units = tiles * splits;
-  int grid = std::min(p.units, di->sm_count);
+  const int grid = std::min(p.units, di->sm_count);
   if (fs) {
     p.fs = fs->pr;
     p.fs_cnt = fs->cnt;
@@ -2110,44 +1962,12 @@ static int tc_run_bn(const TcOperand& a, const TcOperand& b, float* C, int64_t m
       return fail(MTNN_EINVAL, "fused split: F16S NT with conv 3 only");
   }
 
-  // stream-K instead, when it is predicted clearly shorter (same cost model as
-  // choose_splits: 0.5 us per k-block, 2 k-blocks per unit of overhead, one more
-  // per cut for the partial exchange)
-  const int G = di->sm_count;
-  const int64_t W = (int64_t)tiles * p.total_kblocks;
-  const int sk_mode = conv == 0 ? tc_streamk_mode() : 0;
-  if (sk_mode != 0 && W >= 4 * (int64_t)G && tiles > 1) {
-    const int segs = streamk_segments(tiles, p.total_kblocks, G);
-    const double t_sk = ((double)((W + G - 1) / G) + 3.0) * 0.5e-6;
-    if (segs <= 8 && (sk_mode == 2 || t_sk < 0.97 * t_split)) {
-      p.sk = 1;
-      p.sk_slots = std::max(1, segs - 1);
-      p.sk_work = W;
-      p.splits = 1;
-      p.kblocks_per_split = p.total_kblocks;
-      p.units = tiles;
-      if (kind == TcKind::F16S && !b_is_nk) {
-        constexpr int sk = kScaleChunkK / tc::KindF16S::BK;  // chunks inside scale chunks
-        if (sk % p.chunk_kb != 0) p.chunk_kb = sk;
-      }
-      splits = 1;
-      grid = G;
-    }
-  }
-
   if (g_trace.load() && grid <= g_trace_ctas.load()) p.trace = g_trace.load();
   float* out = C;
   ScratchBuffer part;
   if (splits > 1) {
     MTNN_TRY(part.alloc((size_t)splits * m * ldc * sizeof(float), s));
     out = static_cast<float*>(part.ptr);
-  } else if (p.sk) {
-    const size_t nslots = (size_t)tiles * p.sk_slots;
-    const size_t part_bytes = align256(nslots * tc::BM * BN * sizeof(float));
-    MTNN_TRY(part.alloc(part_bytes + nslots * tc::kEpiWarps * sizeof(unsigned long long), s));
-    p.sk_part = static_cast<float4*>(part.ptr);
-    p.sk_flags = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(part.ptr) + part_bytes);
-    p.sk_token = next_streamk_token();
   }
   int rc;
   if (kind == TcKind::F16S && conv == 0)

@@ -90,8 +90,7 @@ extern "C" {
 
 int mtnn_profile_trace(void* buf, int64_t ctas) {
   if (buf && ctas <= 0) return fail(MTNN_EINVAL, "trace buffer needs ctas > 0");
-  set_gemm_trace(buf, buf ? ctas : 0);
-  return MTNN_OK;
+  return set_gemm_trace(buf, buf ? ctas : 0);
 }
 
 int mtnn_profile_enable(int on) {

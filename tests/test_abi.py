@@ -124,7 +124,7 @@ def test_config_knobs_roundtrip_and_reject_unknown():
         _lib.config_set(key, old)
     with pytest.raises(ValueError, match="unknown config key"):
         _lib.config_set("no_such_knob", 1)
-    for key in ("tc_streamk", "fused_split"):
+    for key in ("fused_split",):
         old = _lib.config_get(key)
         try:
             for v in (0, 2, 1):
@@ -134,15 +134,6 @@ def test_config_knobs_roundtrip_and_reject_unknown():
                 _lib.config_set(key, 3)
         finally:
             _lib.config_set(key, old)
-    old = _lib.config_get("tc_streamk")
-    try:
-        for v in (0, 2, 1):
-            _lib.config_set("tc_streamk", v)
-            assert _lib.config_get("tc_streamk") == v
-        with pytest.raises(ValueError, match="0, 1 or 2"):
-            _lib.config_set("tc_streamk", 3)
-    finally:
-        _lib.config_set("tc_streamk", old)
 
 
 def test_ipc_and_allgather_fail_cleanly_without_a_gpu():

@@ -456,67 +456,6 @@ class TestCtaPairTiles:
             _lib.config_set("tc_pair", old)
 
 
-class TestStreamK:
-    """Stream-K on the single-CTA tensor-core kernel (knob tc_streamk = 2 forces it
-    wherever a tile is cut into <= 8 segments): the 148 CTAs share the (tile,
-    k-block) space evenly and a cut tile's last segment adds the earlier
-    segments' posted FP32 partials. Only the association of the cut tiles' sums
-    changes, so results stay within 1e-6 of the uncut kernel and within the FP32
-    gate of float64; two runs are bit-identical (fixed cuts)."""
-
-    @pytest.mark.parametrize("shape", [(1024, 4096, 4096), (1024, 4096, 784), (1024, 1024, 8192),
-                                       (300, 520, 1000), (4096, 4096, 1024), (8192, 128, 512)])
-    def test_streamk_matches_uncut(self, rng, shape):
-        import torch
-
-        from paper_1702_03192_b200 import _lib
-
-        m, n, k = shape
-        a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
-        ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
-        want = oracle.oracle_nt_blas(a, b)
-        old_sk, old_pair = _lib.config_get("tc_streamk"), _lib.config_get("tc_pair")
-        try:
-            _lib.config_set("tc_pair", 0)
-            for v in ("tc3xf16s", "tc3xtf32"):
-                calls = [("nt", tb)] + ([("nn", tb.t().contiguous())] if n % 16 == 0 else [])
-                for op, bb in calls:
-                    fn = gemm_nt if op == "nt" else gemm_nn
-                    _lib.config_set("tc_streamk", 0)
-                    uncut = fn(ta, bb, variant=v).cpu().numpy()
-                    _lib.config_set("tc_streamk", 2)
-                    sk = fn(ta, bb, variant=v).cpu().numpy()
-                    sk2 = fn(ta, bb, variant=v).cpu().numpy()
-                    assert np.array_equal(sk, sk2), (v, op)
-                    assert rel_frobenius(sk, want) < FP32_GATE, (v, op)
-                    assert rel_frobenius(sk, uncut) < 1e-6, (v, op)
-                    if shape == (1024, 4096, 4096):
-                        assert not np.array_equal(sk, uncut)  # the cut path did run
-        finally:
-            _lib.config_set("tc_streamk", old_sk)
-            _lib.config_set("tc_pair", old_pair)
-
-    def test_streamk_range_fixup(self, rng):
-        """Cut tiles still get the residual fix-up's exact terms (an outlier column
-        10^8 x the rest, partner column zero)."""
-        import torch
-
-        from paper_1702_03192_b200 import _lib
-
-        m, n, k = 1024, 4096, 2048
-        a, b = random_matrix(rng, m, k) * 1e-7, random_matrix(rng, n, k)
-        a[:, 0], b[:, 0] = 10.0, 0.0
-        want = oracle.oracle_nt_blas(a, b)
-        old = _lib.config_get("tc_streamk")
-        try:
-            _lib.config_set("tc_streamk", 2)
-            got = gemm_nt(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
-                          variant="tc3xf16s").cpu().numpy()
-        finally:
-            _lib.config_set("tc_streamk", old)
-        assert rel_frobenius(got, want) < FP32_GATE
-
-
 class TestFusedSplit:
     """tc3xf16s NT with the operand split overlapped with the GEMM (knob
     fused_split = 2 forces it): per-(256-k chunk, row) scales, chunk 0 split by a

@@ -2,8 +2,10 @@
 1024x4096x4096 NT (128 CTAs on 148 SMs) alone vs with an HBM-bound transpose
 stream on a second stream launched right after it; GEMM kernel time from
 mtnn_profile_trace (entry of its first CTA -> last C store complete)."""
-import statistics, sys, torch
+import os, statistics, sys, torch
 sys.path.insert(0, ".")
+# phase traces need a -DMTNN_TRACE build: tools/build_variant.sh trace -DMTNN_TRACE
+os.environ.setdefault("MTNN_B200_LIB", "build/variants/trace/libmtnn_b200.so")
 from paper_1702_03192_b200 import _lib
 L = _lib.lib
 dev = torch.device("cuda:0")

@@ -1,14 +1,15 @@
 """Phase timeline of the single-CTA tensor-core GEMM (mtnn_profile_trace): per
 phase, the median / max over CTAs of globaltimer ns since the first CTA's entry.
 Whole calls (split -> GEMM -> fix-up, chained), warm, one after another."""
-import statistics, sys, torch
+import os, statistics, sys, torch
 sys.path.insert(0, ".")
+# phase traces need a -DMTNN_TRACE build: tools/build_variant.sh trace -DMTNN_TRACE
+os.environ.setdefault("MTNN_B200_LIB", "build/variants/trace/libmtnn_b200.so")
 from paper_1702_03192_b200 import _lib
 L = _lib.lib
 dev = torch.device("cuda:0"); s = torch.cuda.current_stream().cuda_stream
 _lib.config_set("tc_pair", 0)
 import os
-_lib.config_set("tc_streamk", int(os.environ.get("SK", "0")))
 _lib.config_set("fused_split", int(os.environ.get("FS", "0")))
 NAMES = ["entry", "prologue", "pdl_wait", "tma0", "stage0", "mma_last", "chunk0", "chunk_last",
          "stores_issued", "stores_done", "exit", "tma_last", "producer_w0", "split_first", "split_last", "chunk_wait_last"]
