@@ -53,8 +53,13 @@ def main(prefix, specs):
         parts = shape.split(":")
         r = read(rep, parts[1] if len(parts) > 1 else None)
         r["traffic_bytes"] = r.get("dram_read", 0) + r.get("dram_write", 0)
-        dims = [int(x) for x in parts[0].split(",")]
-        if len(dims) == 3:
+        split = parts[0].startswith("s")
+        dims = [int(x) for x in parts[0].lstrip("s").split(",")]
+        if split:
+            # operand split: read x (4 B), write h + l (2 B + 2 B) per element
+            r["algorithmic_bytes"] = 8 * sum(dims[i] * dims[i + 1] for i in range(0, len(dims), 2))
+            r["achieved"] = f"{r['algorithmic_bytes'] / r['duration'] / 1e9:.0f} GB/s"
+        elif len(dims) == 3:
             m, n, k = dims
             # hi/lo halves of A and B (4 bytes per element in total for both the
             # TF32 lo-only and the FP16 h+l splits, plus the raw fp32 operand read as
@@ -65,8 +70,6 @@ def main(prefix, specs):
             rr, cc = dims
             r["algorithmic_bytes"] = 8 * rr * cc
             r["achieved"] = f"{8 * rr * cc / r['duration'] / 1e9:.0f} GB/s"
-        else:
-            rows_, k = dims[0], dims[1] if len(dims) > 1 else 0
         summary[name] = r
         md.append(f"| {name} | {r['kernel'][:40]} | {r['duration']*1e3:.3f} ms | "
                   f"{r['traffic_bytes']/1e9:.2f} GB | {r['algorithmic_bytes']/1e9:.2f} GB | "
