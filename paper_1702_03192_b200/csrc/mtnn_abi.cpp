@@ -344,7 +344,40 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
   int64_t R = (int64_t)(per_block / (4.0 * (double)k));
   R = std::max<int64_t>(1024, R / 128 * 128);
   const int64_t mb = std::min(R, m), nb = std::min(R, n);
-  const int64_t QA = (m + mb - 1) / mb, QB = (n + nb - 1) / nb;
+  const int64_t QB = (n + nb - 1) / nb;
+  // A's first block (the prefix multiplied against each arriving B block, its C
+  // blocks leaving while the next B block arrives): sized so the D2H engine has
+  // C to send while B streams in — with n >> k (wide C) all of A goes first.
+  // Modeled with the measured PCIe rates (55.5 GB/s one way, ~46.5 each way when
+  // both run): prefix in, then B in || C(prefix) out, then the other A rows in ||
+  // their C out. MTNN_PIPE_PREFIX=<rows> fixes it, < 0 keeps one mb block (A/B).
+  auto phase = [](double in, double out) {
+    const double lo = std::min(in, out), hi = std::max(in, out);
+    return lo > 0.25 * hi ? hi / 46.5e9 : std::max(in / 55.5e9, out / 54.2e9);
+  };
+  auto model = [&](int64_t rp) {
+    return 4.0 * rp * k / 55.5e9 + phase(4.0 * n * k, 4.0 * rp * n) +
+           phase(4.0 * (m - rp) * k, 4.0 * (m - rp) * n);
+  };
+  static const int64_t prefix_env = [] {
+    const char* e = getenv("MTNN_PIPE_PREFIX");
+    return e ? (int64_t)atoll(e) : (int64_t)0;
+  }();
+  int64_t rp = mb;  // (MTNN_PIPE_PREFIX < 0: always one mb block, the round-2 start)
+  if (prefix_env < 0) {
+  } else if (prefix_env > 0) {
+    rp = std::min(m, std::max<int64_t>(128, prefix_env / 128 * 128));
+  } else {
+    double best = model(mb);
+    for (int64_t r = mb + 128; r <= m; r += std::max<int64_t>(128, m / 64 / 128 * 128)) {
+      const double t = model(r);
+      if (t < best * 0.97) { best = t; rp = r; }
+    }
+    if (model(m) < best * 0.97) rp = m;
+  }
+  std::vector<int64_t> abeg{0, rp};  // A blocks: [0, rp), then mb rows each
+  while (abeg.back() < m) abeg.push_back(std::min(m, abeg.back() + mb));
+  const int64_t QA = (int64_t)abeg.size() - 1;
   MTNN_TRY(da.alloc((size_t)(m * k) * 4, ps->in));
   MTNN_TRY(db.alloc((size_t)(n * k) * 4, ps->in));
   MTNN_TRY(dc.alloc((size_t)(m * n) * 4, ps->in));  // C blocks, each contiguous
@@ -393,8 +426,8 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
   MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->out, ev, 0));
   // copy one operand block in, split it on the compute stream
   auto bring = [&](bool is_a, int64_t q) {
-    const int64_t r0 = q * (is_a ? mb : nb);
-    const int64_t rows = std::min(is_a ? mb : nb, (is_a ? m : n) - r0);
+    const int64_t r0 = is_a ? abeg[q] : q * nb;
+    const int64_t rows = is_a ? abeg[q + 1] - r0 : std::min(nb, n - r0);
     float* dst = (is_a ? dap : dbp) + r0 * k;
     MTNN_CUDA_TRY(cudaMemcpyAsync(dst, (is_a ? A : B) + r0 * k, (size_t)(rows * k) * 4,
                                   cudaMemcpyHostToDevice, ps->in));
@@ -441,8 +474,8 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
   };
   // multiply C block (i, j) and send it out
   auto block = [&](int64_t i, int64_t j) {
-    const int64_t i0 = i * mb, j0 = j * nb;
-    const int64_t mi = std::min(mb, m - i0), nj = std::min(nb, n - j0);
+    const int64_t i0 = abeg[i], j0 = j * nb;
+    const int64_t mi = abeg[i + 1] - i0, nj = std::min(nb, n - j0);
     float* cij = dcp + i0 * n + mi * j0;  // rows i0.. of C, block j: mi x nj contiguous
     MTNN_TRY(run_fixed(a_rows(i0), b_rows(j0), i0, mi, j0, nj, cij, nj));
     cudaEvent_t e;
@@ -458,9 +491,9 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
     MTNN_TRY(bring(false, j));
     MTNN_TRY(block(0, j));
   }
-  for (int64_t i = 1; i < QA; ++i) {  // rows i*mb.. against all of B, full width
+  for (int64_t i = 1; i < QA; ++i) {  // the other A blocks against all of B, full width
     MTNN_TRY(bring(true, i));
-    const int64_t i0 = i * mb, mi = std::min(mb, m - i0);
+    const int64_t i0 = abeg[i], mi = abeg[i + 1] - i0;
     float* ci = dcp + i0 * n;
     MTNN_TRY(run_fixed(a_rows(i0), b_rows(0), i0, mi, 0, n, ci, n));
     MTNN_TRY(evs.make(&ev));

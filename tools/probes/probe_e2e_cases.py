@@ -19,7 +19,8 @@ for (m, n, k) in shapes:
     h2d, d2h = 4 * (m * k + n * k), 4 * m * n
     floor = max(h2d / 55.5e9, d2h / 54.2e9)
     rows.append(dict(m=m, n=n, k=k, t=t, floor=floor, h2d=h2d, d2h=d2h))
-with open("gpurun_out/e2e_cases.csv", "w", newline="") as fh:
+import os
+with open(os.environ.get("OUT", "gpurun_out/e2e_cases.csv"), "w", newline="") as fh:
     w = csv.DictWriter(fh, fieldnames=list(rows[0])); w.writeheader(); w.writerows(rows)
 T = sum(r["t"] for r in rows); Fl = sum(r["floor"] for r in rows)
 print(f"total {T*1e3:.1f} ms floor {Fl*1e3:.1f} ms  TF/s {2*32640**3/T/1e12:.1f}")
