@@ -680,6 +680,8 @@ def main():
         return C[: m * n].view(m, n)
 
     comm = {"bcast": [], "gather": [], "allreduce": []}
+    gate_t = torch.zeros(1, dtype=torch.int32).pin_memory()  # mtnn_gate release flag
+    gate_np, gate_ptr, gate_seq = gate_t.numpy(), gate_t.data_ptr(), [0]
 
     from paper_1702_03192_b200.sharding import allreduce_weight_grad as allreduce_grad
 
@@ -697,17 +699,23 @@ def main():
         for i, (op, m, n, k, fl) in enumerate(calls):
             if fl:
                 flush_src.sum()
-            # keep the GPU busy while the host enqueues the timed call, so the
-            # event window holds device work only (no Python/ctypes gaps)
-            torch.cuda._sleep(SLEEP_CYCLES)
             if events is not None:
+                # hold the stream at a gate until the whole call is enqueued, so
+                # the event window holds device work only: a host stall while
+                # enqueueing (first-use allocation, GIL, page fault) would
+                # otherwise sit inside the open window as GPU idle time
+                # (tools/probes/probe_outliers.py)
+                gate_seq[0] += 1
+                _lib.check(L.mtnn_gate(gate_ptr, gate_seq[0], stream))
                 s = torch.cuda.Event(enable_timing=True)
                 e = torch.cuda.Event(enable_timing=True)
                 s.record()
                 run_call(i, grad_bufs.get(i))
                 e.record()
+                gate_np[0] = gate_seq[0]  # release
                 events.append((s, e))
             else:
+                torch.cuda._sleep(SLEEP_CYCLES)
                 run_call(i, grad_bufs.get(i))
             if op == "grad" and world > 1:
                 works.append(allreduce_grad(grad_bufs[i]))

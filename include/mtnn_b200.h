@@ -111,6 +111,11 @@ int mtnn_profile_sample_every(int n);
  * Diagnostics only, compiled in with -DMTNN_TRACE (tools/build_variant.sh);
  * other builds return MTNN_ENOTSUP for a non-NULL buffer. NULL turns it off. */
 int mtnn_profile_trace(void* buf, int64_t ctas);
+/* Stream gate for event-timed windows: enqueues a one-thread kernel that
+ * holds `stream` until *host_flag >= value (host_flag: pinned host memory the
+ * caller writes after enqueueing the work it times), so host stalls while
+ * enqueueing are not counted as device time. Bounded to 1 s. */
+int mtnn_gate(const int32_t* host_flag, int32_t value, void* stream);
 int mtnn_profile_read_timed(int kclass, double* total_ms, int64_t* launches, double* work);
 int mtnn_profile_reset(void);
 int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* work);

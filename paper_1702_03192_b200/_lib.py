@@ -52,7 +52,7 @@ class MtnnError(RuntimeError):
 
 
 # diagnostics-only entry points a library selected by MTNN_B200_LIB may lack
-_DIAGNOSTIC = {"mtnn_profile_trace"}
+_DIAGNOSTIC = {"mtnn_profile_trace", "mtnn_gate"}
 
 
 def _load():
@@ -78,6 +78,7 @@ def _load():
         "mtnn_profile_min_work": (c_int, [ctypes.c_double]),
         "mtnn_profile_sample_every": (c_int, [c_int]),
         "mtnn_profile_trace": (c_int, [ctypes.c_void_p, ctypes.c_int64]),
+        "mtnn_gate": (c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p]),
         "mtnn_config_set": (c_int, [c_char_p, c_int64]),
         "mtnn_fill_uniform_pcg64": (c_int, [c_void_p, c_int64, POINTER(ctypes.c_uint64), c_int64,
                                             c_double, c_double, c_void_p]),

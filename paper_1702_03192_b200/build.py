@@ -34,7 +34,7 @@ NVCC_FLAGS = ARCH + [
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall",
              f"-I{CUDA_HOME / 'include'}", f"-I{INCLUDE}"]
 
-SOURCES = ["transpose.cu", "gemm_ffma.cu", "gemm_tc.cu", "split_f16.cu", "fixup.cu", "operands.cu", "peer.cu", "mtnn_abi.cpp", "model.cpp", "profile.cpp",
+SOURCES = ["transpose.cu", "gemm_ffma.cu", "gemm_tc.cu", "split_f16.cu", "fixup.cu", "operands.cu", "peer.cu", "gate.cu", "mtnn_abi.cpp", "model.cpp", "profile.cpp",
            "ipc.cpp"]
 HEADERS = ["common.h", "workspace.h", "model.h", "fix.h", "sgemm_tile.cuh", "pdl.h"]
 

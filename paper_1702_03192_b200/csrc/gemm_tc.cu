@@ -544,400 +544,396 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
   pdl_trigger();  // the next call's split may be scheduled (it waits for us)
   if (threadIdx.x == 0) trace_mark(p, 2);
 
-  if (warp < kEpiWarp0) {
-    if (warp == 0) {
-      // ===================== TMA producer =====================
-      if (elect_one()) {
-        int stage = 0;
-        uint32_t phase = 0;
-        const int nw = work_count(p);
-        for (int wi = 0; wi < nw; ++wi) {
-          const Work w = work_item(p, wi);
-          const int tm = w.tm, tn = w.tn;
-          if (wi == 0) trace_mark(p, 12);
-          for (int kb = w.kb0; kb < w.kb1; ++kb) {
-            if (kFS && (kb == w.kb0 || kb % kScaleKb == 0) && kb / kScaleKb >= p.fs_c0) {
-              // chunk split inside this grid: wait until all of its splitter warps
-              // posted it, then order the TMA reads after their generic writes
-              const unsigned* cnt = p.fs_cnt + kb / kScaleKb;
-              const unsigned want = 2u * gridDim.x;
-              while (ld_acquire_u32(cnt) < want) __nanosleep(64);
-              fence_proxy_async_global();
-              trace_mark(p, 15);
-            }
-            mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
-            const uint32_t fb = smem_u32(&full_bar[stage]);
-            mbar_expect_tx(fb, kExpectBytes);
-            uint8_t* st = ring + stage * S::kStageBytes;
-            const int kx = kb * Kind::BK;
-            if (!(kF16Conv && kConv == 1)) {  // (raw A: warp 3)
-              tma_load_2d(smem_u32(st), &map_ahi, fb, kx, tm * BM);
-              if (kConv != 1) tma_load_2d(smem_u32(st + S::kABytes), &map_alo, fb, kx, tm * BM);
-            }
-            if (kF16Conv && kConv == 2) {
-              // raw B: warp 3
-            } else if (!B_MN) {
-              tma_load_2d(smem_u32(st + 2 * S::kABytes), &map_bhi, fb, kx, tn * BN);
-              if (kConv != 2)
-                tma_load_2d(smem_u32(st + 2 * S::kABytes + S::kBBytes), &map_blo, fb, kx, tn * BN);
-            } else {
-              // BN/kMnBox boxes of [BK k-rows][kMnBox columns] (128-byte rows), each
-              // one MN group of the canonical MN-major layout, kMnLBO bytes apart
-  #pragma unroll
-              for (int g = 0; g < BN / Kind::kMnBox; ++g) {
-                tma_load_2d(smem_u32(st + 2 * S::kABytes + g * Kind::kMnLBO), &map_bhi, fb,
-                            tn * BN + g * Kind::kMnBox, kx);
-                if (kConv != 2)
-                  tma_load_2d(smem_u32(st + 2 * S::kABytes + S::kBBytes + g * Kind::kMnLBO),
-                              &map_blo, fb, tn * BN + g * Kind::kMnBox, kx);
-              }
-            }
-            if (wi == 0 && kb == w.kb0) trace_mark(p, 3);
-            if (++stage == kStages) { stage = 0; phase ^= 1; }
-          }
-        }
-        trace_mark(p, 11);
-      }
-    } else if (warp == 1) {
-      // ===================== MMA issuer =====================
-      constexpr uint32_t idesc = make_idesc(BN, B_MN, Kind::kFmt);
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      const int nw = work_count(p);
-      for (int wi = 0; wi < nw; ++wi) {
-        const Work w = work_item(p, wi);
-        const int kb1 = w.kb1;
-        for (int kc = w.kb0, kce; kc < kb1; kc = kce) {
-          kce = min(kb1, kc + p.chunk_kb);
-          mbar_wait(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
-          tc_fence_after();
-          const uint32_t tmem_d = tmem_base + acc * BN;
-          for (int kb = kc; kb < kce; ++kb) {
-            // TF32 conversion waits full_bar itself, so conv_bar implies it; the F16S
-            // converters do not (the raw tile has its own ring)
-            if (kConv == 0 || kF16Conv || kFS) mbar_wait(smem_u32(&full_bar[stage]), phase);
-            if (kConv == 1 || kConv == 2) mbar_wait(smem_u32(&conv_bar[stage]), phase);
-            if (wi == 0 && kb == w.kb0 && lane == 0) trace_mark(p, 4);
-            tc_fence_after();
-            if (elect_one()) {
-              uint8_t* st = ring + stage * S::kStageBytes;
-              const uint32_t a_hi = smem_u32(st);
-              const uint32_t a_lo = a_hi + S::kABytes;
-              const uint32_t b_hi = a_hi + 2 * S::kABytes;
-              const uint32_t b_lo = b_hi + S::kBBytes;
-  #pragma unroll
-              for (int ks = 0; ks < Kind::BK / Kind::UMMA_K; ++ks) {
-                // A: K-major SW64 — 64-byte rows, 8-row groups 512 B apart; k-step +32 B.
-                const uint64_t dah = make_sdesc(a_hi + ks * 32, 16, 512, kLayoutSW64);
-                const uint64_t dal = make_sdesc(a_lo + ks * 32, 16, 512, kLayoutSW64);
-                uint64_t dbh, dbl;
-                if (!B_MN) {
-                  dbh = make_sdesc(b_hi + ks * 32, 16, 512, kLayoutSW64);
-                  dbl = make_sdesc(b_lo + ks * 32, 16, 512, kLayoutSW64);
-                } else {
-                  // B: MN-major — column groups kMnLBO apart, k-row groups kMnSBO apart
-                  dbh = make_sdesc(b_hi + ks * Kind::kMnKStep, Kind::kMnLBO, Kind::kMnSBO,
-                                   Kind::kMnLayout);
-                  dbl = make_sdesc(b_lo + ks * Kind::kMnKStep, Kind::kMnLBO, Kind::kMnSBO,
-                                   Kind::kMnLayout);
-                }
-                const uint32_t accum = (kb == kc && ks == 0) ? 0u : 1u;
-                tc_mma<Kind::kScaled>(tmem_d, dal, dbh, idesc, accum);
-                tc_mma<Kind::kScaled>(tmem_d, dah, dbl, idesc, 1u);
-                tc_mma<Kind::kScaled>(tmem_d, dah, dbh, idesc, 1u);
-              }
-              tc_commit(smem_u32(&empty_bar[stage]));
-              if (kb == kce - 1) tc_commit(smem_u32(&tfull_bar[acc]));
-            }
-            __syncwarp();
-            if (++stage == kStages) { stage = 0; phase ^= 1; }
-          }
-          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        }
-      }
-      if (lane == 0) trace_mark(p, 5);
-    } else if (kF16Conv && warp == 3) {
-      // ===================== TMA producer of the raw (converted) operand =====================
-      if (elect_one()) {
-        int rs = 0;
-        uint32_t rphase = 0;
-        const int nw = work_count(p);
-        for (int wi = 0; wi < nw; ++wi) {
-          const Work w = work_item(p, wi);
-          const int tm = w.tm, tn = w.tn;
-          for (int kb = w.kb0; kb < w.kb1; ++kb) {
-            mbar_wait(smem_u32(&rempty_bar[rs]), rphase ^ 1);
-            const uint32_t fb = smem_u32(&rfull_bar[rs]);
-            mbar_expect_tx(fb, kRawTileBytes);
-            const uint32_t dst = smem_u32(raw_ring + rs * kRawTileBytes);
-            if (kConv == 1) tma_load_2d(dst, &map_ahi, fb, kb * Kind::BK, tm * BM);
-            else tma_load_2d(dst, &map_bhi, fb, kb * Kind::BK, tn * BN);
-            if (++rs == kRawStages) { rs = 0; rphase ^= 1; }
-          }
-        }
-      }
-    } else if (kFS && (warp == 2 || warp == 3)) {
-      // ===================== fused split: chunks fs_c0.. of A and B =====================
-      // Global splitter warp g of 2G takes rows g, g + 2G, ... of the m + n
-      // rows, chunk by chunk in k order (the chunks the MMAs need first are
-      // posted first). Its segments stream through its own ring of 1 KiB smem
-      // slots by bulk copies issued kSegPerWarp ahead (24 KiB in flight per
-      // warp); after its share of a chunk the warp bumps fs_cnt[chunk].
-      const int sw = warp - 2;
-      uint8_t* slots = raw_ring + sw * kSegPerWarp * 1024;
-      uint64_t* sbar = seg_bar + sw * kSegPerWarp;
-      const int64_t nw2 = 2LL * gridDim.x;
-      const int64_t g = 2LL * blockIdx.x + sw;
-      const int64_t rows0 = p.fs.op[0].rows, rows = rows0 + p.fs.op[1].rows;
-      const int64_t per_chunk = g < rows ? (rows - 1 - g) / nw2 + 1 : 0;
-      const int64_t nseg = per_chunk * (p.fs_nchunks - p.fs_c0);
-      const int64_t k = p.fs.k;
-      // issue cursor (chunk ci, the warp's ji-th row of it), slot si
-      int ci = p.fs_c0, si = 0;
-      int64_t ji = 0;
-      auto issue = [&]() {  // lane 0
-        const int64_t v = g + ji * nw2;
-        const bool b = v >= rows0;
-        const int64_t r = b ? v - rows0 : v;
-        const int len = (int)min((int64_t)kScaleChunkK, k - (int64_t)ci * kScaleChunkK);
-        const float* src = (b ? p.fs.op[1].x : p.fs.op[0].x) + r * k + (int64_t)ci * kScaleChunkK;
-        const uint32_t bar = smem_u32(&sbar[si]);
-        mbar_expect_tx(bar, (uint32_t)len * 4);
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(slots + si * 1024)),
-            "l"(src), "r"(len * 4), "r"(bar)
-            : "memory");
-        if (++ji == per_chunk) { ji = 0; ++ci; }
-        if (++si == kSegPerWarp) si = 0;
-      };
-      if (per_chunk == 0) {
-        if (lane == 0)
-          for (int c = p.fs_c0; c < p.fs_nchunks; ++c) atomicAdd(p.fs_cnt + c, 1u);
-      } else {
-        int64_t issued = min(nseg, (int64_t)kSegPerWarp);
-        if (lane == 0)
-          for (int64_t i = 0; i < issued; ++i) issue();
-        int c = p.fs_c0, slot = 0;
-        uint32_t parity = 0;
-        int64_t j = 0;
-        const int len_full = kScaleChunkK;
-        for (int64_t i = 0; i < nseg; ++i) {
-          mbar_wait(smem_u32(&sbar[slot]), parity);
-          const int64_t v = g + j * nw2;
-          const int o = v >= rows0 ? 1 : 0;
-          const int64_t r = o ? v - rows0 : v;
-          const int len = (c + 1) * kScaleChunkK <= k ? len_full : (int)(k - (int64_t)c * kScaleChunkK);
-          seg::split_staged_segment(reinterpret_cast<const float*>(slots + slot * 1024), len,
-                                    seg::sel(p.fs, o), r, k, c, lane);
-          __syncwarp();  // every lane is done with the slot
-          if (issued < nseg) {
-            if (lane == 0) {
-              fence_proxy_async_smem();  // generic reads of the slot before the async refill
-              issue();
-            }
-            ++issued;
-          }
-          if (++slot == kSegPerWarp) { slot = 0; parity ^= 1; }
-          if (++j == per_chunk) {  // this warp's share of chunk c is written
-            __threadfence();
-            fence_proxy_async_global();
-            __syncwarp();
-            if (lane == 0) atomicAdd(p.fs_cnt + c, 1u);
-            if (sw == 0 && lane == 0) trace_mark(p, c == p.fs_c0 ? 13 : 14);
-            j = 0;
-            ++c;
-          }
-        }
-      }
-    } else if ((kConv == 1 || kConv == 2) && !Kind::kScaled && (warp == 2 || warp == 3)) {
-      // ===================== in-kernel lo split (TF32, one operand) =====================
-      const int t = threadIdx.x - 64;  // 0..63
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
       const int nw = work_count(p);
       for (int wi = 0; wi < nw; ++wi) {
         const Work w = work_item(p, wi);
+        const int tm = w.tm, tn = w.tn;
+        if (wi == 0) trace_mark(p, 12);
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
-          mbar_wait(smem_u32(&full_bar[stage]), phase);
-          uint8_t* raw = ring + stage * S::kStageBytes + (kConv == 1 ? 0 : 2 * S::kABytes);
-          uint8_t* lo = raw + kConvBytes;
-  #pragma unroll 4
-          for (int i = t; i < kConvBytes / 16; i += 64) {
-            float4 v = *reinterpret_cast<const float4*>(raw + 16 * i);
-            v.x -= __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-            v.y -= __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-            v.z -= __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-            v.w -= __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-            *reinterpret_cast<float4*>(lo + 16 * i) = v;
+          if (kFS && (kb == w.kb0 || kb % kScaleKb == 0) && kb / kScaleKb >= p.fs_c0) {
+            // chunk split inside this grid: wait until all of its splitter warps
+            // posted it, then order the TMA reads after their generic writes
+            const unsigned* cnt = p.fs_cnt + kb / kScaleKb;
+            const unsigned want = 2u * gridDim.x;
+            while (ld_acquire_u32(cnt) < want) __nanosleep(64);
+            fence_proxy_async_global();
+            trace_mark(p, 15);
+          }
+          mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+          const uint32_t fb = smem_u32(&full_bar[stage]);
+          mbar_expect_tx(fb, kExpectBytes);
+          uint8_t* st = ring + stage * S::kStageBytes;
+          const int kx = kb * Kind::BK;
+          if (!(kF16Conv && kConv == 1)) {  // (raw A: warp 3)
+            tma_load_2d(smem_u32(st), &map_ahi, fb, kx, tm * BM);
+            if (kConv != 1) tma_load_2d(smem_u32(st + S::kABytes), &map_alo, fb, kx, tm * BM);
+          }
+          if (kF16Conv && kConv == 2) {
+            // raw B: warp 3
+          } else if (!B_MN) {
+            tma_load_2d(smem_u32(st + 2 * S::kABytes), &map_bhi, fb, kx, tn * BN);
+            if (kConv != 2)
+              tma_load_2d(smem_u32(st + 2 * S::kABytes + S::kBBytes), &map_blo, fb, kx, tn * BN);
+          } else {
+            // BN/kMnBox boxes of [BK k-rows][kMnBox columns] (128-byte rows), each
+            // one MN group of the canonical MN-major layout, kMnLBO bytes apart
+#pragma unroll
+            for (int g = 0; g < BN / Kind::kMnBox; ++g) {
+              tma_load_2d(smem_u32(st + 2 * S::kABytes + g * Kind::kMnLBO), &map_bhi, fb,
+                          tn * BN + g * Kind::kMnBox, kx);
+              if (kConv != 2)
+                tma_load_2d(smem_u32(st + 2 * S::kABytes + S::kBBytes + g * Kind::kMnLBO),
+                            &map_blo, fb, tn * BN + g * Kind::kMnBox, kx);
+            }
+          }
+          if (wi == 0 && kb == w.kb0) trace_mark(p, 3);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+      trace_mark(p, 11);
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    constexpr uint32_t idesc = make_idesc(BN, B_MN, Kind::kFmt);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const int nw = work_count(p);
+    for (int wi = 0; wi < nw; ++wi) {
+      const Work w = work_item(p, wi);
+      const int kb1 = w.kb1;
+      for (int kc = w.kb0, kce; kc < kb1; kc = kce) {
+        kce = min(kb1, kc + p.chunk_kb);
+        mbar_wait(smem_u32(&tempty_bar[acc]), acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = kc; kb < kce; ++kb) {
+          // TF32 conversion waits full_bar itself, so conv_bar implies it; the F16S
+          // converters do not (the raw tile has its own ring)
+          if (kConv == 0 || kF16Conv || kFS) mbar_wait(smem_u32(&full_bar[stage]), phase);
+          if (kConv == 1 || kConv == 2) mbar_wait(smem_u32(&conv_bar[stage]), phase);
+          if (wi == 0 && kb == w.kb0 && lane == 0) trace_mark(p, 4);
+          tc_fence_after();
+          if (elect_one()) {
+            uint8_t* st = ring + stage * S::kStageBytes;
+            const uint32_t a_hi = smem_u32(st);
+            const uint32_t a_lo = a_hi + S::kABytes;
+            const uint32_t b_hi = a_hi + 2 * S::kABytes;
+            const uint32_t b_lo = b_hi + S::kBBytes;
+#pragma unroll
+            for (int ks = 0; ks < Kind::BK / Kind::UMMA_K; ++ks) {
+              // A: K-major SW64 — 64-byte rows, 8-row groups 512 B apart; k-step +32 B.
+              const uint64_t dah = make_sdesc(a_hi + ks * 32, 16, 512, kLayoutSW64);
+              const uint64_t dal = make_sdesc(a_lo + ks * 32, 16, 512, kLayoutSW64);
+              uint64_t dbh, dbl;
+              if (!B_MN) {
+                dbh = make_sdesc(b_hi + ks * 32, 16, 512, kLayoutSW64);
+                dbl = make_sdesc(b_lo + ks * 32, 16, 512, kLayoutSW64);
+              } else {
+                // B: MN-major — column groups kMnLBO apart, k-row groups kMnSBO apart
+                dbh = make_sdesc(b_hi + ks * Kind::kMnKStep, Kind::kMnLBO, Kind::kMnSBO,
+                                 Kind::kMnLayout);
+                dbl = make_sdesc(b_lo + ks * Kind::kMnKStep, Kind::kMnLBO, Kind::kMnSBO,
+                                 Kind::kMnLayout);
+              }
+              const uint32_t accum = (kb == kc && ks == 0) ? 0u : 1u;
+              tc_mma<Kind::kScaled>(tmem_d, dal, dbh, idesc, accum);
+              tc_mma<Kind::kScaled>(tmem_d, dah, dbl, idesc, 1u);
+              tc_mma<Kind::kScaled>(tmem_d, dah, dbh, idesc, 1u);
+            }
+            tc_commit(smem_u32(&empty_bar[stage]));
+            if (kb == kce - 1) tc_commit(smem_u32(&tfull_bar[acc]));
+          }
+          __syncwarp();
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+    if (lane == 0) trace_mark(p, 5);
+  } else if (kF16Conv && warp == 3) {
+    // ===================== TMA producer of the raw (converted) operand =====================
+    if (elect_one()) {
+      int rs = 0;
+      uint32_t rphase = 0;
+      const int nw = work_count(p);
+      for (int wi = 0; wi < nw; ++wi) {
+        const Work w = work_item(p, wi);
+        const int tm = w.tm, tn = w.tn;
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          mbar_wait(smem_u32(&rempty_bar[rs]), rphase ^ 1);
+          const uint32_t fb = smem_u32(&rfull_bar[rs]);
+          mbar_expect_tx(fb, kRawTileBytes);
+          const uint32_t dst = smem_u32(raw_ring + rs * kRawTileBytes);
+          if (kConv == 1) tma_load_2d(dst, &map_ahi, fb, kb * Kind::BK, tm * BM);
+          else tma_load_2d(dst, &map_bhi, fb, kb * Kind::BK, tn * BN);
+          if (++rs == kRawStages) { rs = 0; rphase ^= 1; }
+        }
+      }
+    }
+  } else if (kFS && (warp == 2 || warp == 3)) {
+    // ===================== fused split: chunks fs_c0.. of A and B =====================
+    // Global splitter warp g of 2G takes rows g, g + 2G, ... of the m + n
+    // rows, chunk by chunk in k order (the chunks the MMAs need first are
+    // posted first). Its segments stream through its own ring of 1 KiB smem
+    // slots by bulk copies issued kSegPerWarp ahead (24 KiB in flight per
+    // warp); after its share of a chunk the warp bumps fs_cnt[chunk].
+    const int sw = warp - 2;
+    uint8_t* slots = raw_ring + sw * kSegPerWarp * 1024;
+    uint64_t* sbar = seg_bar + sw * kSegPerWarp;
+    const int64_t nw2 = 2LL * gridDim.x;
+    const int64_t g = 2LL * blockIdx.x + sw;
+    const int64_t rows0 = p.fs.op[0].rows, rows = rows0 + p.fs.op[1].rows;
+    const int64_t per_chunk = g < rows ? (rows - 1 - g) / nw2 + 1 : 0;
+    const int64_t nseg = per_chunk * (p.fs_nchunks - p.fs_c0);
+    const int64_t k = p.fs.k;
+    // issue cursor (chunk ci, the warp's ji-th row of it), slot si
+    int ci = p.fs_c0, si = 0;
+    int64_t ji = 0;
+    auto issue = [&]() {  // lane 0
+      const int64_t v = g + ji * nw2;
+      const bool b = v >= rows0;
+      const int64_t r = b ? v - rows0 : v;
+      const int len = (int)min((int64_t)kScaleChunkK, k - (int64_t)ci * kScaleChunkK);
+      const float* src = (b ? p.fs.op[1].x : p.fs.op[0].x) + r * k + (int64_t)ci * kScaleChunkK;
+      const uint32_t bar = smem_u32(&sbar[si]);
+      mbar_expect_tx(bar, (uint32_t)len * 4);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(slots + si * 1024)),
+          "l"(src), "r"(len * 4), "r"(bar)
+          : "memory");
+      if (++ji == per_chunk) { ji = 0; ++ci; }
+      if (++si == kSegPerWarp) si = 0;
+    };
+    if (per_chunk == 0) {
+      if (lane == 0)
+        for (int c = p.fs_c0; c < p.fs_nchunks; ++c) atomicAdd(p.fs_cnt + c, 1u);
+    } else {
+      int64_t issued = min(nseg, (int64_t)kSegPerWarp);
+      if (lane == 0)
+        for (int64_t i = 0; i < issued; ++i) issue();
+      int c = p.fs_c0, slot = 0;
+      uint32_t parity = 0;
+      int64_t j = 0;
+      const int len_full = kScaleChunkK;
+      for (int64_t i = 0; i < nseg; ++i) {
+        mbar_wait(smem_u32(&sbar[slot]), parity);
+        const int64_t v = g + j * nw2;
+        const int o = v >= rows0 ? 1 : 0;
+        const int64_t r = o ? v - rows0 : v;
+        const int len = (c + 1) * kScaleChunkK <= k ? len_full : (int)(k - (int64_t)c * kScaleChunkK);
+        seg::split_staged_segment(reinterpret_cast<const float*>(slots + slot * 1024), len,
+                                  seg::sel(p.fs, o), r, k, c, lane);
+        __syncwarp();  // every lane is done with the slot
+        if (issued < nseg) {
+          if (lane == 0) {
+            fence_proxy_async_smem();  // generic reads of the slot before the async refill
+            issue();
+          }
+          ++issued;
+        }
+        if (++slot == kSegPerWarp) { slot = 0; parity ^= 1; }
+        if (++j == per_chunk) {  // this warp's share of chunk c is written
+          __threadfence();
+          fence_proxy_async_global();
+          __syncwarp();
+          if (lane == 0) atomicAdd(p.fs_cnt + c, 1u);
+          if (sw == 0 && lane == 0) trace_mark(p, c == p.fs_c0 ? 13 : 14);
+          j = 0;
+          ++c;
+        }
+      }
+    }
+  } else if ((kConv == 1 || kConv == 2) && !Kind::kScaled && (warp == 2 || warp == 3)) {
+    // ===================== in-kernel lo split (TF32, one operand) =====================
+    const int t = threadIdx.x - 64;  // 0..63
+    int stage = 0;
+    uint32_t phase = 0;
+    const int nw = work_count(p);
+    for (int wi = 0; wi < nw; ++wi) {
+      const Work w = work_item(p, wi);
+      for (int kb = w.kb0; kb < w.kb1; ++kb) {
+        mbar_wait(smem_u32(&full_bar[stage]), phase);
+        uint8_t* raw = ring + stage * S::kStageBytes + (kConv == 1 ? 0 : 2 * S::kABytes);
+        uint8_t* lo = raw + kConvBytes;
+#pragma unroll 4
+        for (int i = t; i < kConvBytes / 16; i += 64) {
+          float4 v = *reinterpret_cast<const float4*>(raw + 16 * i);
+          v.x -= __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+          v.y -= __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+          v.z -= __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+          v.w -= __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          *reinterpret_cast<float4*>(lo + 16 * i) = v;
+        }
+        fence_proxy_async_smem();  // generic-proxy smem writes -> visible to UMMA
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&conv_bar[stage]));
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (kF16Conv && warp >= R::kConv0) {
+    // ===================== in-kernel FP16 split (F16S, one operand) =====================
+    // Two groups of 4 warps take alternate k-blocks, so each group's serial
+    // chain (raw wait, LDS, convert, h/l-slot wait, STS, proxy fence, arrive)
+    // has two MMA k-blocks of time. Thread r of a group owns row r of the
+    // converted tile: reads its 128-byte raw row (SWIZZLE_128B: 16-byte chunk c at
+    // c ^ (r & 7)) and writes 64-byte h and l rows (SWIZZLE_64B: chunk c at
+    // c ^ ((r >> 1) & 3)); both patterns keep each warp's 16-byte accesses
+    // conflict-free.
+    const int t = threadIdx.x - 32 * R::kConv0;
+    const int r = t % kF16ConvRows;             // tile row
+    const int grp = t / kF16ConvRows;           // k-block parity this thread converts
+    const int sw128 = r & 7, sw64 = (r >> 1) & 3;
+    const float* inv = kConv == 1 ? p.inv_scale_a : p.inv_scale_b;
+    const int64_t nrows = kConv == 1 ? p.m : p.n;
+    int stage = 0, rs = 0, parity = 0;
+    uint32_t phase = 0, rphase = 0;
+    const int nw = work_count(p);
+    for (int wi = 0; wi < nw; ++wi) {
+      const Work w = work_item(p, wi);
+      const int64_t row = (int64_t)(kConv == 1 ? w.tm * BM : w.tn * BN) + r;
+      const float sc = row < nrows ? 1.f / __ldg(inv + row) : 1.f;  // exact: powers of two
+      for (int kb = w.kb0; kb < w.kb1; ++kb) {
+        if (parity == grp) {
+          // raw tile -> registers -> halves; the raw slot is released as soon as
+          // its values are consumed, before waiting for the h/l slot
+          mbar_wait(smem_u32(&rfull_bar[rs]), rphase);
+          const uint32_t raw = smem_u32(raw_ring + rs * kRawTileBytes) + r * 128;
+          float4 x[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) x[j] = lds128f(raw + ((j ^ sw128) << 4));
+          uint4 hw[4], lw[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) split8_f16(x[2 * j], x[2 * j + 1], sc, hw[j], lw[j]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&rempty_bar[rs]));
+          mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);  // MMA done with the h/l slot
+          const uint32_t hrow = smem_u32(ring + stage * S::kStageBytes) +
+                                (kConv == 1 ? 0 : 2 * S::kABytes) + r * 64;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t off = (j ^ sw64) << 4;
+            sts128(hrow + off, hw[j]);
+            sts128(hrow + kConvBytes + off, lw[j]);
           }
           fence_proxy_async_smem();  // generic-proxy smem writes -> visible to UMMA
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&conv_bar[stage]));
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
+        parity ^= 1;
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        if (++rs == kRawStages) { rs = 0; rphase ^= 1; }
       }
     }
-  } else {
-    if (kF16Conv && warp >= R::kConv0) {
-      // ===================== in-kernel FP16 split (F16S, one operand) =====================
-      // Two groups of 4 warps take alternate k-blocks, so each group's serial
-      // chain (raw wait, LDS, convert, h/l-slot wait, STS, proxy fence, arrive)
-      // has two MMA k-blocks of time. Thread r of a group owns row r of the
-      // converted tile: reads its 128-byte raw row (SWIZZLE_128B: 16-byte chunk c at
-      // c ^ (r & 7)) and writes 64-byte h and l rows (SWIZZLE_64B: chunk c at
-      // c ^ ((r >> 1) & 3)); both patterns keep each warp's 16-byte accesses
-      // conflict-free.
-      const int t = threadIdx.x - 32 * R::kConv0;
-      const int r = t % kF16ConvRows;             // tile row
-      const int grp = t / kF16ConvRows;           // k-block parity this thread converts
-      const int sw128 = r & 7, sw64 = (r >> 1) & 3;
-      const float* inv = kConv == 1 ? p.inv_scale_a : p.inv_scale_b;
-      const int64_t nrows = kConv == 1 ? p.m : p.n;
-      int stage = 0, rs = 0, parity = 0;
-      uint32_t phase = 0, rphase = 0;
-      const int nw = work_count(p);
-      for (int wi = 0; wi < nw; ++wi) {
-        const Work w = work_item(p, wi);
-        const int64_t row = (int64_t)(kConv == 1 ? w.tm * BM : w.tn * BN) + r;
-        const float sc = row < nrows ? 1.f / __ldg(inv + row) : 1.f;  // exact: powers of two
-        for (int kb = w.kb0; kb < w.kb1; ++kb) {
-          if (parity == grp) {
-            // raw tile -> registers -> halves; the raw slot is released as soon as
-            // its values are consumed, before waiting for the h/l slot
-            mbar_wait(smem_u32(&rfull_bar[rs]), rphase);
-            const uint32_t raw = smem_u32(raw_ring + rs * kRawTileBytes) + r * 128;
-            float4 x[8];
-  #pragma unroll
-            for (int j = 0; j < 8; ++j) x[j] = lds128f(raw + ((j ^ sw128) << 4));
-            uint4 hw[4], lw[4];
-  #pragma unroll
-            for (int j = 0; j < 4; ++j) split8_f16(x[2 * j], x[2 * j + 1], sc, hw[j], lw[j]);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&rempty_bar[rs]));
-            mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);  // MMA done with the h/l slot
-            const uint32_t hrow = smem_u32(ring + stage * S::kStageBytes) +
-                                  (kConv == 1 ? 0 : 2 * S::kABytes) + r * 64;
-  #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const uint32_t off = (j ^ sw64) << 4;
-              sts128(hrow + off, hw[j]);
-              sts128(hrow + kConvBytes + off, lw[j]);
-            }
-            fence_proxy_async_smem();  // generic-proxy smem writes -> visible to UMMA
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&conv_bar[stage]));
-          }
-          parity ^= 1;
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
-          if (++rs == kRawStages) { rs = 0; rphase ^= 1; }
+  } else if (warp >= kEpiWarp0) {
+    // ===================== epilogue: FP32 promotion + store =====================
+    // The tensor core's accumulator truncates (measured bias ~ -0.5 ulp per MMA
+    // accumulation), so each TMEM accumulation covers only p.chunk_kb k-blocks; the
+    // chunk is then added into round-to-nearest FP32 register sums here.
+    const int e = warp - kEpiWarp0;
+    const int q = warp % 4;             // TMEM lane quarter this warp may access
+    const int h = e / 4;                // column slice
+    uint8_t* stg = epi + e * S::kStagingBytes;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const int nw = work_count(p);
+    for (int wi = 0; wi < nw; ++wi) {
+      const Work w = work_item(p, wi);
+      const int tm = w.tm, tn = w.tn, split = w.split, kb1 = w.kb1;
+      const int64_t row = (int64_t)tm * BM + q * 32 + lane;
+      const int64_t col0 = (int64_t)tn * BN + h * kColsPerWarp;
+      float sum[kColsPerWarp];
+#pragma unroll
+      for (int j = 0; j < kColsPerWarp; ++j) sum[j] = 0.f;
+      for (int kc = w.kb0, kce; kc < kb1; kc = kce) {
+        kce = min(kb1, kc + p.chunk_kb);
+        // (the chunk's column scales load while the MMAs of the chunk finish)
+        ChunkScales<kColsPerWarp> cs{};
+        if (kChunkB && !kFS) cs = load_chunk_scales<kColsPerWarp>(p.inv_scale_b, kc / kScaleKb, p.n, col0, lane);
+        mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
+        // fused split: this chunk's scales were written by other CTAs during
+        // this grid, before the chunk's operands could be loaded: read them
+        // once the chunk's MMAs are done, from L2 (no stale L1 lines)
+        float sa_c = 1.f;
+        if (kFS) {
+          cs = load_chunk_scales<kColsPerWarp, true>(p.inv_scale_b, kc / kScaleKb, p.n, col0, lane);
+          if (row < p.m) sa_c = __ldcg(p.inv_scale_a + (int64_t)(kc / kScaleKb) * p.m + row);
         }
-      }
-    } else {
-      // ===================== epilogue: FP32 promotion + store =====================
-      // The tensor core's accumulator truncates (measured bias ~ -0.5 ulp per MMA
-      // accumulation), so each TMEM accumulation covers only p.chunk_kb k-blocks; the
-      // chunk is then added into round-to-nearest FP32 register sums here.
-      const int e = warp - kEpiWarp0;
-      const int q = warp % 4;             // TMEM lane quarter this warp may access
-      const int h = e / 4;                // column slice
-      uint8_t* stg = epi + e * S::kStagingBytes;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      const int nw = work_count(p);
-      for (int wi = 0; wi < nw; ++wi) {
-        const Work w = work_item(p, wi);
-        const int tm = w.tm, tn = w.tn, split = w.split, kb1 = w.kb1;
-        const int64_t row = (int64_t)tm * BM + q * 32 + lane;
-        const int64_t col0 = (int64_t)tn * BN + h * kColsPerWarp;
-        float sum[kColsPerWarp];
-  #pragma unroll
-        for (int j = 0; j < kColsPerWarp; ++j) sum[j] = 0.f;
-        for (int kc = w.kb0, kce; kc < kb1; kc = kce) {
-          kce = min(kb1, kc + p.chunk_kb);
-          // (the chunk's column scales load while the MMAs of the chunk finish)
-          ChunkScales<kColsPerWarp> cs{};
-          if (kChunkB && !kFS) cs = load_chunk_scales<kColsPerWarp>(p.inv_scale_b, kc / kScaleKb, p.n, col0, lane);
-          mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
-          // fused split: this chunk's scales were written by other CTAs during
-          // this grid, before the chunk's operands could be loaded: read them
-          // once the chunk's MMAs are done, from L2 (no stale L1 lines)
-          float sa_c = 1.f;
-          if (kFS) {
-            cs = load_chunk_scales<kColsPerWarp, true>(p.inv_scale_b, kc / kScaleKb, p.n, col0, lane);
-            if (row < p.m) sa_c = __ldcg(p.inv_scale_a + (int64_t)(kc / kScaleKb) * p.m + row);
-          }
-          if (e == 0 && lane == 0) trace_mark(p, wi == 0 && kc == w.kb0 ? 6 : 7);
-          tc_fence_after();
-          const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + h * kColsPerWarp;
-  #pragma unroll
-          for (int c = 0; c < kColsPerWarp / 16; ++c) {
-            uint32_t r[16];
-            tmem_ld_32x32b_x16(taddr + c * 16, r);
-            tmem_ld_wait();
-            if (kChunkA) {
-              // fused split: this chunk's row scale of A and column scales of B
-  #pragma unroll
-              for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * sa_c);
-              add_chunk_scaled(sum + c * 16, r, cs, c);
-            } else if (kChunkB) {
-              // MN-major F16S B: this promotion chunk's exact column scales
-              add_chunk_scaled(sum + c * 16, r, cs, c);
-            } else {
-  #pragma unroll
-              for (int j = 0; j < 16; ++j) sum[c * 16 + j] += __uint_as_float(r[j]);
-            }
-          }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[acc]));
-          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        }
-        // KindF16S: undo the exact power-of-two operand scales while storing,
-        // C = (acc * 1/s_a[row]) * 1/s_b[col] (MN-major B: applied per chunk
-        // above; fused split: both, per chunk)
-        const float sa = (Kind::kScaled && !kChunkA && row < p.m) ? __ldg(p.inv_scale_a + row) : 1.f;
-        // Store: 32 rows x kColsPerWarp through a 32x16 staging tile (64B swizzle).
-  #pragma unroll
+        if (e == 0 && lane == 0) trace_mark(p, wi == 0 && kc == w.kb0 ? 6 : 7);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + h * kColsPerWarp;
+#pragma unroll
         for (int c = 0; c < kColsPerWarp / 16; ++c) {
-          if (lane == 0) tma_store_wait_read<0>();
-          __syncwarp();
-  #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int pj = j ^ ((lane >> 1) & 3);
-            float4 v = make_float4(sum[c * 16 + 4 * j], sum[c * 16 + 4 * j + 1],
-                                   sum[c * 16 + 4 * j + 2], sum[c * 16 + 4 * j + 3]);
-            if (kChunkA) {
-              // (scales applied per chunk)
-            } else if (Kind::kScaled && kChunkB) {
-              v.x *= sa; v.y *= sa; v.z *= sa; v.w *= sa;
-            } else if (Kind::kScaled) {
-              // the scale vector has n entries (n % 4 == 0): whole float4s are in range
-              const int64_t cj = col0 + c * 16 + 4 * j;
-              const float4 sb = cj < p.n ? __ldg(reinterpret_cast<const float4*>(p.inv_scale_b + cj))
-                                         : make_float4(0.f, 0.f, 0.f, 0.f);
-              v.x = (v.x * sa) * sb.x;
-              v.y = (v.y * sa) * sb.y;
-              v.z = (v.z * sa) * sb.z;
-              v.w = (v.w * sa) * sb.w;
-            }
-            *reinterpret_cast<float4*>(stg + lane * 64 + pj * 16) = v;
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_3d(&map_c, smem_u32(stg), tn * BN + h * kColsPerWarp + c * 16,
-                         tm * BM + q * 32, split);
-            tma_store_commit();
+          uint32_t r[16];
+          tmem_ld_32x32b_x16(taddr + c * 16, r);
+          tmem_ld_wait();
+          if (kChunkA) {
+            // fused split: this chunk's row scale of A and column scales of B
+#pragma unroll
+            for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * sa_c);
+            add_chunk_scaled(sum + c * 16, r, cs, c);
+          } else if (kChunkB) {
+            // MN-major F16S B: this promotion chunk's exact column scales
+            add_chunk_scaled(sum + c * 16, r, cs, c);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) sum[c * 16 + j] += __uint_as_float(r[j]);
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[acc]));
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
-      if (e == 0 && lane == 0) trace_mark(p, 8);
-      if (lane == 0) tma_store_wait_all();
-      if (e == 0 && lane == 0) trace_mark(p, 9);
+      // KindF16S: undo the exact power-of-two operand scales while storing,
+      // C = (acc * 1/s_a[row]) * 1/s_b[col] (MN-major B: applied per chunk
+      // above; fused split: both, per chunk)
+      const float sa = (Kind::kScaled && !kChunkA && row < p.m) ? __ldg(p.inv_scale_a + row) : 1.f;
+      // Store: 32 rows x kColsPerWarp through a 32x16 staging tile (64B swizzle).
+#pragma unroll
+      for (int c = 0; c < kColsPerWarp / 16; ++c) {
+        if (lane == 0) tma_store_wait_read<0>();
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int pj = j ^ ((lane >> 1) & 3);
+          float4 v = make_float4(sum[c * 16 + 4 * j], sum[c * 16 + 4 * j + 1],
+                                 sum[c * 16 + 4 * j + 2], sum[c * 16 + 4 * j + 3]);
+          if (kChunkA) {
+            // (scales applied per chunk)
+          } else if (Kind::kScaled && kChunkB) {
+            v.x *= sa; v.y *= sa; v.z *= sa; v.w *= sa;
+          } else if (Kind::kScaled) {
+            // the scale vector has n entries (n % 4 == 0): whole float4s are in range
+            const int64_t cj = col0 + c * 16 + 4 * j;
+            const float4 sb = cj < p.n ? __ldg(reinterpret_cast<const float4*>(p.inv_scale_b + cj))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+            v.x = (v.x * sa) * sb.x;
+            v.y = (v.y * sa) * sb.y;
+            v.z = (v.z * sa) * sb.z;
+            v.w = (v.w * sa) * sb.w;
+          }
+          *reinterpret_cast<float4*>(stg + lane * 64 + pj * 16) = v;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&map_c, smem_u32(stg), tn * BN + h * kColsPerWarp + c * 16,
+                       tm * BM + q * 32, split);
+          tma_store_commit();
+        }
+      }
     }
+    if (e == 0 && lane == 0) trace_mark(p, 8);
+    if (lane == 0) tma_store_wait_all();
+    if (e == 0 && lane == 0) trace_mark(p, 9);
   }
 
   __syncwarp();  // reconverge the role branches: bar.sync is warp-aligned
@@ -1808,6 +1804,15 @@ static int choose_splits(int tiles, int kblocks, int64_t m, int64_t n, int sms,
     }
   }
   if (time_out) *time_out = best_t;
+  static const int cap = [] {  // MTNN_SPLITK_MAX: cap the factor (A/B runs)
+    const char* e = getenv("MTNN_SPLITK_MAX");
+    return e ? std::max(1, atoi(e)) : 0;
+  }();
+  if (cap > 0 && best > cap) {
+    int s = cap;
+    while (s > 1 && (kblocks + (kblocks + s - 1) / s - 1) / ((kblocks + s - 1) / s) != s) --s;
+    best = s;
+  }
   return best;
 }
 
