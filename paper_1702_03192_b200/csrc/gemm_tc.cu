@@ -61,6 +61,16 @@ constexpr int BM = 128;          // UMMA M (one CTA, 128 TMEM lanes)
 constexpr int kStages = 4;
 constexpr int kEpiWarp0 = 4;      // warps 0..3: TMA, MMA, TMEM alloc, spare
 constexpr int kEpiWarps = 16;     // 4 TMEM lane quarters x 4 column quarters
+// Epilogue tail: 1 = the tile's output scales are loaded while its last chunk
+// is still in the tensor core (the store loop then waits on no L2 load: the
+// exposed tail of a tile drops ~0.8-1.2 us, 1024^3 45.0 -> 43.7 us per call);
+// 0 = load them in the store loop (A/B builds: -DMTNN_TAIL=0). Staging the
+// last tile in the idle operand ring so its stores issue back to back measured
+// slower and was dropped.
+#ifndef MTNN_TAIL
+#define MTNN_TAIL 1
+#endif
+constexpr int kTail = MTNN_TAIL;
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
 // Warp roles. F16S in-kernel conversion (kConv != 0, BN = 128): 8 epilogue
 // warps (4 lane quarters x 2 column halves) and 8 converter warps (two groups
@@ -852,11 +862,19 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
       float sum[kColsPerWarp];
 #pragma unroll
       for (int j = 0; j < kColsPerWarp; ++j) sum[j] = 0.f;
+      float sa_pre = 1.f;  // (kTail >= 1: the tile's output scales, preloaded)
+      ChunkScales<kColsPerWarp> csb{};
       for (int kc = w.kb0, kce; kc < kb1; kc = kce) {
         kce = min(kb1, kc + p.chunk_kb);
         // (the chunk's column scales load while the MMAs of the chunk finish)
         ChunkScales<kColsPerWarp> cs{};
         if (kChunkB && !kFS) cs = load_chunk_scales<kColsPerWarp>(p.inv_scale_b, kc / kScaleKb, p.n, col0, lane);
+        if (kTail >= 1 && Kind::kScaled && !kChunkA && kce >= kb1) {
+          // the output scales load while the tile's last chunk is still in the
+          // tensor core (the store loop below would otherwise wait on L2 for them)
+          if (row < p.m) sa_pre = __ldg(p.inv_scale_a + row);
+          if (!kChunkB) csb = load_chunk_scales<kColsPerWarp>(p.inv_scale_b, 0, p.n, col0, lane);
+        }
         mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
         // fused split: this chunk's scales were written by other CTAs during
         // this grid, before the chunk's operands could be loaded: read them
@@ -895,7 +913,9 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
       // KindF16S: undo the exact power-of-two operand scales while storing,
       // C = (acc * 1/s_a[row]) * 1/s_b[col] (MN-major B: applied per chunk
       // above; fused split: both, per chunk)
-      const float sa = (Kind::kScaled && !kChunkA && row < p.m) ? __ldg(p.inv_scale_a + row) : 1.f;
+      if (e == 0 && lane == 0 && wi == nw - 1) trace_mark(p, 13);
+      const float sa = kTail >= 1 ? sa_pre
+                                  : (Kind::kScaled && !kChunkA && row < p.m) ? __ldg(p.inv_scale_a + row) : 1.f;
       // Store: 32 rows x kColsPerWarp through a 32x16 staging tile (64B swizzle).
 #pragma unroll
       for (int c = 0; c < kColsPerWarp / 16; ++c) {
@@ -910,6 +930,14 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
             // (scales applied per chunk)
           } else if (Kind::kScaled && kChunkB) {
             v.x *= sa; v.y *= sa; v.z *= sa; v.w *= sa;
+          } else if (kTail >= 1 && Kind::kScaled) {
+            // column c*16 + 4j + t of the warp's slice: lane (that % 32) of csb
+            const int cc = c * 16 + 4 * j;
+            const float src = csb.v[cc / 32];
+            v.x = (v.x * sa) * __shfl_sync(0xffffffffu, src, (cc + 0) % 32);
+            v.y = (v.y * sa) * __shfl_sync(0xffffffffu, src, (cc + 1) % 32);
+            v.z = (v.z * sa) * __shfl_sync(0xffffffffu, src, (cc + 2) % 32);
+            v.w = (v.w * sa) * __shfl_sync(0xffffffffu, src, (cc + 3) % 32);
           } else if (Kind::kScaled) {
             // the scale vector has n entries (n % 4 == 0): whole float4s are in range
             const int64_t cj = col0 + c * 16 + 4 * j;
@@ -929,6 +957,7 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
                        tm * BM + q * 32, split);
           tma_store_commit();
         }
+        if (c == 0 && e == 0 && lane == 0 && wi == nw - 1) trace_mark(p, 14);
       }
     }
     if (e == 0 && lane == 0) trace_mark(p, 8);
