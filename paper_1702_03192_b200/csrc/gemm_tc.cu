@@ -1439,10 +1439,18 @@ gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
       float sum[kColsPerWarp];
 #pragma unroll
       for (int j = 0; j < kColsPerWarp; ++j) sum[j] = 0.f;
+      float sa_pre = 1.f;  // (kTail >= 1: the tile's output scales, preloaded)
+      ChunkScales<kColsPerWarp> csb{};
       for (int kc = kb0; kc < kb1; kc += p.chunk_kb) {
         // (the chunk's column scales load while the MMAs of the chunk finish)
         ChunkScales<kColsPerWarp> cs{};
         if (kChunkB) cs = load_chunk_scales<kColsPerWarp>(p.inv_scale_b, kc / kScaleKb, p.n, col0, lane);
+        if (kTail >= 1 && Kind::kScaled && kc + p.chunk_kb >= kb1) {
+          // the output scales load while the tile's last chunk is still in the
+          // tensor core (as in gemm_tc3x_kernel)
+          if (row < p.m) sa_pre = __ldg(p.inv_scale_a + row);
+          if (!kChunkB) csb = load_chunk_scales<kColsPerWarp>(p.inv_scale_b, 0, p.n, col0, lane);
+        }
         mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + h * kColsPerWarp;
@@ -1463,7 +1471,7 @@ gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
         if (lane == 0) mbar_arrive_cta(smem_u32(&tempty_bar[acc]), 0);  // the leader's
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
-      const float sa = (Kind::kScaled && row < p.m) ? __ldg(p.inv_scale_a + row) : 1.f;
+      const float sa = kTail >= 1 ? sa_pre : (Kind::kScaled && row < p.m) ? __ldg(p.inv_scale_a + row) : 1.f;
 #pragma unroll
       for (int c = 0; c < kColsPerWarp / 16; ++c) {
         if (lane == 0) tma_store_wait_read<0>();
@@ -1475,6 +1483,13 @@ gemm_tc3x_pair_kernel(const __grid_constant__ CUtensorMap map_ahi,
                                  sum[c * 16 + 4 * j + 2], sum[c * 16 + 4 * j + 3]);
           if (Kind::kScaled && kChunkB) {
             v.x *= sa; v.y *= sa; v.z *= sa; v.w *= sa;
+          } else if (kTail >= 1 && Kind::kScaled) {
+            const int cc = c * 16 + 4 * j;
+            const float src = csb.v[cc / 32];
+            v.x = (v.x * sa) * __shfl_sync(0xffffffffu, src, (cc + 0) % 32);
+            v.y = (v.y * sa) * __shfl_sync(0xffffffffu, src, (cc + 1) % 32);
+            v.z = (v.z * sa) * __shfl_sync(0xffffffffu, src, (cc + 2) % 32);
+            v.w = (v.w * sa) * __shfl_sync(0xffffffffu, src, (cc + 3) % 32);
           } else if (Kind::kScaled) {
             const int64_t cj = col0 + c * 16 + 4 * j;
             const float4 sb = cj < p.n ? __ldg(reinterpret_cast<const float4*>(p.inv_scale_b + cj))
