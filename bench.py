@@ -702,9 +702,10 @@ def main():
             if events is not None:
                 # hold the stream at a gate until the whole call is enqueued, so
                 # the event window holds device work only: a host stall while
-                # enqueueing (first-use allocation, GIL, page fault) would
-                # otherwise sit inside the open window as GPU idle time
-                # (tools/probes/probe_outliers.py)
+                # enqueueing (GIL, page fault) would otherwise sit inside the
+                # open window as GPU idle time (tools/probes/probe_outliers.py).
+                # The warm-up steps have loaded every kernel and grown the pools
+                # (a lazy module load behind a held gate would synchronise).
                 gate_seq[0] += 1
                 _lib.check(L.mtnn_gate(gate_ptr, gate_seq[0], stream))
                 s = torch.cuda.Event(enable_timing=True)

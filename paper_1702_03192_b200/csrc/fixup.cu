@@ -219,29 +219,33 @@ __global__ void __launch_bounds__(kFixThreads, 2) fixup_kernel(const FixupDev p)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(16) unsigned char fix_smem[];
   __shared__ unsigned s_na, s_nb;
-  // The counters are final before this grid can start: the split kernels that
+  // The lists are final before this grid can start: the split kernels that
   // append to them completed before the GEMM passed its griddepcontrol.wait,
-  // and the GEMM triggers its dependents only after that wait. Reading them
-  // here overlaps the load with the GEMM's tail.
+  // and the GEMM triggers its dependents only after that wait. So reading the
+  // counters, releasing them and loading and sorting the entries all happen
+  // before this grid's own dependency wait, overlapped with the GEMM's tail;
+  // only the work on C waits for the GEMM. Every path still executes the wait
+  // before it exits (the next kernel's wait covers only this grid).
   // (A fused-split GEMM appends entries itself: read them after its completion.)
   const bool late = p.a_chunked || p.b_chunked;
-  if (threadIdx.x == 0 && !late) {
-    s_na = p.fa.ctr ? *reinterpret_cast<volatile unsigned*>(&p.fa.ctr->count) : 0u;
-    s_nb = p.fb.ctr ? *reinterpret_cast<volatile unsigned*>(&p.fb.ctr->count) : 0u;
-  }
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (threadIdx.x == 0 && late) {
+  auto dep_wait = [] { asm volatile("griddepcontrol.wait;" ::: "memory"); };
+  if (late) dep_wait();
+  if (threadIdx.x == 0) {
     s_na = p.fa.ctr ? *reinterpret_cast<volatile unsigned*>(&p.fa.ctr->count) : 0u;
     s_nb = p.fb.ctr ? *reinterpret_cast<volatile unsigned*>(&p.fb.ctr->count) : 0u;
   }
   __syncthreads();
   const unsigned na = s_na, nb = s_nb;
-  if (na + nb == 0) return;  // the usual case: nothing listed, counters already zero
+  if (na + nb == 0) {  // the usual case: nothing listed, counters already zero
+    if (!late) dep_wait();
+    return;
+  }
   if (threadIdx.x == 0) {
     release(p.fa, na, p.reset_a != 0);
     release(p.fb, nb, p.reset_b != 0);
   }
   if (na > p.fa.cap || nb > p.fb.cap) {
+    if (!late) dep_wait();
     // a list overflowed: recompute every output with FFMA chains of kFixChunk k,
     // each chain added to the output in memory by the thread that owns it (the
     // rounding error grows with ~k/kFixChunk + kFixChunk terms instead of k:
@@ -267,6 +271,7 @@ __global__ void __launch_bounds__(kFixThreads, 2) fixup_kernel(const FixupDev p)
   const int64_t cm = (p.m + kFixThreads - 1) / kFixThreads;
   const unsigned npa = na ? pow2_at_least(na) : 0, npb = nb ? pow2_at_least(nb) : 0;
   if (npa + npb > (unsigned)p.smem_entries) {
+    if (!late) dep_wait();
     // too many entries to sort on chip (operands of ~2^32 elements): float
     // atomics, entries meeting in one output add in arrival order
     const int64_t items_a = (int64_t)na * cn;
@@ -307,6 +312,7 @@ __global__ void __launch_bounds__(kFixThreads, 2) fixup_kernel(const FixupDev p)
   float* vb = va + npa;
   if (na) load_sorted(p.fa.e, na, npa, ka, va);
   if (nb) load_sorted(p.fb.e, nb, npb, kb, vb);
+  if (!late) dep_wait();  // C (the GEMM's output) from here on
   const bool bounded = p.rep == (int)FixRep::F16S && p.inv_a != nullptr && p.inv_b != nullptr;
   constexpr float kRowMax = 16384.f;      // max |x| of a row <= 2^14 / s
   constexpr float kNegligible = 0x1p-26f;  // of |C|: below a quarter ulp

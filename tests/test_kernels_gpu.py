@@ -246,7 +246,8 @@ class TestPipelinedHostPath:
     """Large numpy calls run the chunked H2D / compute / D2H pipeline inside the
     C-ABI (mtnn_*_host); results must match the device path and the oracle."""
 
-    @pytest.mark.parametrize("shape", [(3000, 2048, 4096), (4096, 1000, 2048), (257, 8192, 4096)])
+    @pytest.mark.parametrize("shape", [(3000, 2048, 4096), (4096, 1000, 2048), (257, 8192, 4096),
+                                       (2304, 16384, 1024)])  # (A-first prefix of the blocked pipeline)
     def test_pipelined_matches(self, rng, shape):
         import torch
 
@@ -849,3 +850,64 @@ class TestDeviceValidation:
         a = torch.zeros(8, 8, device="cuda")
         with pytest.raises(TypeError):
             gemm_nt(a, np.zeros((8, 8), np.float32))
+
+
+def test_stream_gate_holds_until_released():
+    """mtnn_gate (bench.py's window gate) holds the stream until the host writes
+    the value into the pinned flag; a pageable flag is rejected."""
+    import ctypes
+    import time
+
+    import torch
+
+    from paper_1702_03192_b200 import _lib
+
+    flag = torch.zeros(1, dtype=torch.int32).pin_memory()
+    s = torch.cuda.current_stream()
+    # (allocate and load the kernel first: a first-use allocation or a lazy
+    # module load behind a held gate synchronises, returning only once the
+    # gate's 1 s bound expires — bench.py gates only after its warm-up steps)
+    x = torch.ones(4, device="cuda")
+    y = torch.empty_like(x)
+    torch.mul(x, 2, out=y)
+    torch.cuda.synchronize()
+    _lib.check(_lib.lib.mtnn_gate(flag.data_ptr(), 1, s.cuda_stream))
+    done = torch.cuda.Event()
+    torch.mul(x, 2, out=y)
+    done.record()
+    time.sleep(0.05)
+    assert not done.query()  # held at the gate
+    flag.numpy()[0] = 1
+    done.synchronize()
+    assert torch.equal(y.cpu(), torch.full((4,), 2.0))
+    pageable = (ctypes.c_int32 * 1)()
+    with pytest.raises(ValueError, match="pinned"):
+        _lib.check(_lib.lib.mtnn_gate(ctypes.addressof(pageable), 1, s.cuda_stream))
+
+
+def test_gated_window_excludes_host_stalls():
+    """bench.py's timing method: a window opened behind the gate and released
+    after the call is enqueued holds device time only, even if the host stalls
+    20 ms while enqueueing."""
+    import time
+
+    import torch
+
+    from paper_1702_03192_b200 import _lib, device
+
+    a = torch.rand(512, 512, device="cuda")
+    b = torch.rand(512, 512, device="cuda")
+    device.gemm_nt(a, b)  # load kernels, grow pools
+    flag = torch.zeros(1, dtype=torch.int32).pin_memory()
+    s = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    _lib.check(_lib.lib.mtnn_gate(flag.data_ptr(), 1, s.cuda_stream))
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    time.sleep(0.02)  # a host stall inside the window
+    device.gemm_nt(a, b)
+    t1.record()
+    flag.numpy()[0] = 1
+    torch.cuda.synchronize()
+    assert t0.elapsed_time(t1) < 5.0  # ms: the GEMM, not the 20 ms stall
+

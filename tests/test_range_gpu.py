@@ -106,6 +106,7 @@ def test_adversarial_every_variant_and_path(case, shape):
 
 
 @pytest.mark.parametrize("shape", [(2048, 1024, 2048),   # blocked host pipeline (k <= 4096)
+                                   (2048, 8192, 2048),   # blocked, all of A first (wide C)
                                    (1024, 512, 8192)])   # B-first row-chunk pipeline
 @pytest.mark.parametrize("case", ["outlier_masked", "b_column_1e9_masked", "a_subnormal"])
 def test_adversarial_host_pipelines(case, shape):
