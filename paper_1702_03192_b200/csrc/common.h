@@ -72,6 +72,10 @@ int launch_transpose(const float* in, float* out, int64_t rows, int64_t cols,
 // SIMT NT for outputs with a side <= 16 (k % 4 == 0, 16-byte aligned operands).
 // ENOTSUP otherwise.
 bool skinny_eligible(const float* A, const float* B, int64_t m, int64_t n, int64_t k);
+// NN with a tiny inner dimension (k <= 16): output-bound outer-product kernel.
+bool nn_smallk_eligible(const float* BT, const float* C, int64_t m, int64_t n, int64_t k);
+int launch_gemm_nn_smallk(const float* A, const float* BT, float* C, int64_t m, int64_t n, int64_t k,
+                          cudaStream_t s);
 int launch_gemm_skinny(const float* A, const float* B, float* C, int64_t m, int64_t n, int64_t k,
                        cudaStream_t s);
 int launch_gemm_ffma(const float* A, const float* B, float* C, int64_t m, int64_t n,

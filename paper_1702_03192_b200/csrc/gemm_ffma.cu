@@ -129,6 +129,170 @@ gemm_skinny_kernel(const float* __restrict__ big, const float* __restrict__ smal
   }
 }
 
+
+// Staged skinny NT (round 2): the same products, restructured for memory-level
+// parallelism. A CTA (16 warps, up to 4 per SM) owns a block of long rows and pulls
+// all of them into shared memory with one bulk copy per row as its first act,
+// so the whole long operand is in flight across the chip at once (the 1 TB/s of
+// the kernel above was latency: 1.16 waves of CTAs, a few 16-byte loads in
+// flight per lane). Warps split k into kwarps slices (lane l of slice w owns the
+// float4 columns w*32 + l, + kwarps*32, ...) and the remaining warps take
+// further row groups; each lane holds its short-operand columns in registers —
+// loaded once when its columns fit one step (kOneStep) — and the R x SMAX
+// partial sums fold across the warp (butterfly) and the slices (shared memory)
+// in a fixed order, per batch of groups x R rows.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+constexpr int kStagedWarps = 16;
+
+template <int SMAX, bool kOneStep>
+__global__ void __launch_bounds__(kStagedWarps * 32, 1)
+gemm_skinny_staged_kernel(const float* __restrict__ big, const float* __restrict__ small,
+                          float* __restrict__ C, int64_t L, int s, int64_t k, bool small_is_b,
+                          int kwarps, int nb) {
+  constexpr int R = 32 / SMAX;
+  extern __shared__ __align__(128) float4 rows4[];  // [rows of this CTA][k / 4]
+  __shared__ float red[kStagedWarps][32];
+  __shared__ __align__(8) unsigned long long bar;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int groups = kStagedWarps / kwarps;
+  const int slice = warp % kwarps, grp = warp / kwarps;
+  const int64_t k4 = k / 4;
+  const int rows_per_cta = nb * groups * R;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int nr = (int)min((int64_t)rows_per_cta, L - r0);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_enter();
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar)),
+                 "r"((uint32_t)(nr * k * 4))
+                 : "memory");
+    for (int r = 0; r < nr; ++r)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_addr(rows4 + (int64_t)r * k4)),
+          "l"(big + (r0 + r) * k), "r"((uint32_t)(k * 4)), "r"(smem_addr(&bar))
+          : "memory");
+  }
+  const float4* small4 = reinterpret_cast<const float4*>(small);
+  const int step = kwarps * 32;
+  const int T = (int)((k4 + step - 1) / step);
+  float4 bv[SMAX];
+  if (kOneStep) {  // this lane's short-operand columns, for every batch
+    const int64_t q = (int64_t)slice * 32 + lane;
+#pragma unroll
+    for (int j = 0; j < SMAX; ++j)
+      bv[j] = (q < k4 && j < s) ? __ldg(small4 + (int64_t)j * k4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_addr(&bar))
+        : "memory");
+  for (int b = 0; b < nb; ++b) {
+    float acc[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+    for (int t = 0; t < T; ++t) {
+      const int64_t q = (int64_t)slice * 32 + lane + (int64_t)t * step;
+      const bool valid = q < k4;
+      if (!kOneStep) {
+#pragma unroll
+        for (int j = 0; j < SMAX; ++j)
+          bv[j] = (valid && j < s) ? __ldg(small4 + (int64_t)j * k4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int rl = (b * groups + grp) * R + r;
+        const float4 a = (valid && rl < nr) ? rows4[(int64_t)rl * k4 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < SMAX; ++j) {
+          float& c = acc[r * SMAX + j];  // (slots past R x SMAX stay 0)
+          c = fmaf(a.w, bv[j].w, fmaf(a.z, bv[j].z, fmaf(a.y, bv[j].y, fmaf(a.x, bv[j].x, c))));
+        }
+      }
+    }
+    butterfly32(acc, lane);
+    red[warp][lane] = acc[0];
+    __syncthreads();
+    if (threadIdx.x < groups * 32) {
+      const int g2 = threadIdx.x / 32, val = threadIdx.x % 32;
+      const int r = val / SMAX, j = val % SMAX;
+      const int rl = (b * groups + g2) * R + r;
+      if (r < R && j < s && rl < nr) {
+        float sum = 0.f;
+        for (int w = 0; w < kwarps; ++w) sum += red[g2 * kwarps + w][val];
+        const int64_t row = r0 + rl;
+        C[small_is_b ? row * s + j : (int64_t)j * L + row] = sum;
+      }
+    }
+    __syncthreads();  // red is reused by the next batch
+  }
+}
+
+// NN with a tiny inner dimension (k <= 16; the FCN's 1024 x 4096 x 10 backward
+// product): C = A B^T is an outer-product sum bound by writing C. A thread owns
+// 4 adjacent columns and kNnRows rows: its k float4s of B^T (L2) are loaded
+// once, the CTA's rows of A (k floats each) are staged in shared memory, and
+// each output float4 is one fixed-order FFMA chain over k, stored with STG.128
+// (64 threads write 1 KiB of a row contiguously).
+constexpr int kNnSmallK = 16, kNnRows = 8;
+
+template <int K>
+__global__ void __launch_bounds__(256)
+gemm_nn_smallk_kernel(const float* __restrict__ A, const float* __restrict__ BT,
+                      float* __restrict__ C, int64_t m, int64_t n, int k) {
+  // exactly K terms (one instantiation per k: no predicated-off iterations —
+  // these products are instruction-bound, not memory-bound); A rows padded to
+  // 16 floats so a row's k values come in with 16-byte shared loads
+  constexpr int KMAX = K;
+  __shared__ __align__(16) float As[4 * kNnRows][16];
+  pdl_enter();
+  const int tx = threadIdx.x % 64, ty = threadIdx.x / 64;  // 64 column groups x 4 row groups
+  const int64_t c0 = ((int64_t)blockIdx.x * 64 + tx) * 4;
+  const int64_t rbase = (int64_t)blockIdx.y * (4 * kNnRows);
+  for (int i = threadIdx.x; i < 4 * kNnRows * 16; i += 256) {
+    const int rr = i / 16, p = i % 16;
+    As[rr][p] = (p < k && rbase + rr < m) ? __ldg(A + (rbase + rr) * k + p) : 0.f;
+  }
+  float4 bv[KMAX];
+#pragma unroll
+  for (int p = 0; p < KMAX; ++p)
+    bv[p] = c0 < n ? __ldg(reinterpret_cast<const float4*>(BT + (int64_t)p * n + c0))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncthreads();
+  if (c0 >= n) return;
+#pragma unroll
+  for (int r = 0; r < kNnRows; ++r) {
+    const int rr = ty * kNnRows + r;
+    const int64_t row = rbase + rr;
+    if (row >= m) break;
+    float av[16];
+#pragma unroll
+    for (int p4 = 0; p4 < (KMAX + 3) / 4; ++p4) {
+      const float4 t = *reinterpret_cast<const float4*>(&As[rr][4 * p4]);
+      av[4 * p4] = t.x; av[4 * p4 + 1] = t.y; av[4 * p4 + 2] = t.z; av[4 * p4 + 3] = t.w;
+    }
+    float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int p = 0; p < KMAX; ++p) {
+      c.x = fmaf(av[p], bv[p].x, c.x);
+      c.y = fmaf(av[p], bv[p].y, c.y);
+      c.z = fmaf(av[p], bv[p].z, c.z);
+      c.w = fmaf(av[p], bv[p].w, c.w);
+    }
+    *reinterpret_cast<float4*>(C + row * n + c0) = c;
+  }
+}
 }  // namespace
 
 // Deterministic split-K reduction: C[i] = sum_s part[s][i], s ascending.
@@ -195,6 +359,112 @@ int launch_gemm_ffma(const float* A, const float* B, float* C, int64_t m, int64_
   return MTNN_OK;
 }
 
+
+// Staged skinny NT when the CTA's long rows fit shared memory (<= 200 KiB for
+// at least one batch) and the grid still covers most SMs; the register kernel
+// above otherwise (MTNN_SKINNY_STAGED=0 forces it).
+static bool skinny_staged_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MTNN_SKINNY_STAGED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+constexpr int kSkinnySmemMax = 200 * 1024;
+
+template <int SMAX>
+static int launch_skinny_staged(const float* big, const float* sml, float* C, int64_t L, int s,
+                                int64_t k, bool small_is_b, int kwarps, int nb, int64_t grid,
+                                size_t smem, cudaStream_t st) {
+  const int64_t k4 = k / 4;
+  if (k4 <= (int64_t)kwarps * 32) {
+    auto kern = gemm_skinny_staged_kernel<SMAX, true>;
+    MTNN_TRY(set_max_dynamic_smem((const void*)kern, kSkinnySmemMax));  // (set once: the cap)
+    return launch_chained(kern, dim3((unsigned)grid), dim3(kStagedWarps * 32), smem, st, big, sml,
+                          C, L, s, k, small_is_b, kwarps, nb);
+  }
+  auto kern = gemm_skinny_staged_kernel<SMAX, false>;
+  MTNN_TRY(set_max_dynamic_smem((const void*)kern, kSkinnySmemMax));
+  return launch_chained(kern, dim3((unsigned)grid), dim3(kStagedWarps * 32), smem, st, big, sml, C,
+                        L, s, k, small_is_b, kwarps, nb);
+}
+
+static int try_skinny_staged(const float* big, const float* sml, float* C, int64_t L, int sm_rows,
+                             int64_t k, bool small_is_b, int smax, const DeviceInfo* di,
+                             cudaStream_t st, bool* done) {
+  *done = false;
+  if (!skinny_staged_enabled()) return MTNN_OK;
+  const int64_t k4 = k / 4;
+  int kwarps = 1;
+  while (kwarps < kStagedWarps && (int64_t)kwarps * 32 < k4) kwarps *= 2;
+  const int groups = kStagedWarps / kwarps, R = 32 / smax;
+  const int64_t target = (L + di->sm_count - 1) / di->sm_count;
+  int nb = (int)std::max<int64_t>(1, (target + groups * R - 1) / (groups * R));
+  const size_t kSmemMax = kSkinnySmemMax;
+  while (nb > 1 && (size_t)nb * groups * R * k * 4 > kSmemMax) --nb;
+  const size_t smem = (size_t)nb * groups * R * k * 4;
+  if (smem > kSmemMax || kSkinnySmemMax > di->max_smem_optin - 8 * 1024) return MTNN_OK;
+  // (only where one k-step covers k: there the short operand stays in
+  // registers for every row and the kernel measured faster — 10 x 4096 x 1024:
+  // 12.5-13.0 vs 15.1 us under ncu; with more steps it re-reads the short
+  // operand from L2 per batch and is no faster than the register kernel)
+  if (k4 > (int64_t)kwarps * 32) return MTNN_OK;
+  const int64_t rows = (int64_t)nb * groups * R;
+  const int64_t grid = (L + rows - 1) / rows;
+  if (grid > 8 * (int64_t)di->sm_count) return MTNN_OK;  // (long row sets: the register kernel)
+  int rc;
+  switch (smax) {
+    case 4: rc = launch_skinny_staged<4>(big, sml, C, L, sm_rows, k, small_is_b, kwarps, nb, grid, smem, st); break;
+    case 8: rc = launch_skinny_staged<8>(big, sml, C, L, sm_rows, k, small_is_b, kwarps, nb, grid, smem, st); break;
+    case 10: rc = launch_skinny_staged<10>(big, sml, C, L, sm_rows, k, small_is_b, kwarps, nb, grid, smem, st); break;
+    case 12: rc = launch_skinny_staged<12>(big, sml, C, L, sm_rows, k, small_is_b, kwarps, nb, grid, smem, st); break;
+    default: rc = launch_skinny_staged<16>(big, sml, C, L, sm_rows, k, small_is_b, kwarps, nb, grid, smem, st); break;
+  }
+  MTNN_TRY(rc);
+  MTNN_CUDA_TRY(cudaGetLastError());
+  *done = true;
+  return MTNN_OK;
+}
+
+bool nn_smallk_eligible(const float* BT, const float* C, int64_t m, int64_t n, int64_t k) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  return k >= 1 && k <= kNnSmallK && m >= 1 && n >= 4 && n % 4 == 0 && al16(BT) && al16(C) &&
+         (n / 4 + 63) / 64 <= 0x7fffffff && (m + 4 * kNnRows - 1) / (4 * kNnRows) <= 65535;
+}
+
+int launch_gemm_nn_smallk(const float* A, const float* BT, float* C, int64_t m, int64_t n, int64_t k,
+                          cudaStream_t s) {
+  if (!nn_smallk_eligible(BT, C, m, n, k))
+    return fail(MTNN_ENOTSUP, "small-k NN: shape (%lld, %lld, %lld) not eligible", (long long)m,
+                (long long)n, (long long)k);
+  KernelTimer timer(MTNN_KCLASS_GEMM_FFMA, 2.0 * (double)m * (double)n * (double)k, s);
+  const dim3 grid((unsigned)((n / 4 + 63) / 64), (unsigned)((m + 4 * kNnRows - 1) / (4 * kNnRows)));
+  int rc = MTNN_OK;
+  auto go = [&](auto kern) { return launch_chained(kern, grid, dim3(256), 0, s, A, BT, C, m, n, (int)k); };
+  switch (k) {
+    case 1: rc = go(gemm_nn_smallk_kernel<1>); break;
+    case 2: rc = go(gemm_nn_smallk_kernel<2>); break;
+    case 3: rc = go(gemm_nn_smallk_kernel<3>); break;
+    case 4: rc = go(gemm_nn_smallk_kernel<4>); break;
+    case 5: rc = go(gemm_nn_smallk_kernel<5>); break;
+    case 6: rc = go(gemm_nn_smallk_kernel<6>); break;
+    case 7: rc = go(gemm_nn_smallk_kernel<7>); break;
+    case 8: rc = go(gemm_nn_smallk_kernel<8>); break;
+    case 9: rc = go(gemm_nn_smallk_kernel<9>); break;
+    case 10: rc = go(gemm_nn_smallk_kernel<10>); break;
+    case 11: rc = go(gemm_nn_smallk_kernel<11>); break;
+    case 12: rc = go(gemm_nn_smallk_kernel<12>); break;
+    case 13: rc = go(gemm_nn_smallk_kernel<13>); break;
+    case 14: rc = go(gemm_nn_smallk_kernel<14>); break;
+    case 15: rc = go(gemm_nn_smallk_kernel<15>); break;
+    default: rc = go(gemm_nn_smallk_kernel<16>); break;
+  }
+  MTNN_TRY(rc);
+  MTNN_CUDA_TRY(cudaGetLastError());
+  return MTNN_OK;
+}
+
 bool skinny_eligible(const float* A, const float* B, int64_t m, int64_t n, int64_t k) {
   const int64_t sm = std::min(m, n);
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
@@ -223,6 +493,9 @@ int launch_gemm_skinny(const float* A, const float* B, float* C, int64_t m, int6
   KernelTimer timer(MTNN_KCLASS_GEMM_FFMA, 2.0 * (double)m * (double)n * (double)k, s);
   const float* big = small_is_b ? A : B;
   const float* sml = small_is_b ? B : A;
+  bool staged = false;
+  MTNN_TRY(try_skinny_staged(big, sml, C, L, sm_rows, k, small_is_b, smax, di, s, &staged));
+  if (staged) return MTNN_OK;
   const unsigned g = (unsigned)blocks;
   switch (smax) {
     case 4: MTNN_TRY(launch_chained(gemm_skinny_kernel<4>, dim3(g), dim3(256), 0, s, big, sml, C, L, sm_rows, k, small_is_b, W)); break;

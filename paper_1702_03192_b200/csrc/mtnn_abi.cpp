@@ -165,6 +165,8 @@ static int gemm_dispatch(const float* A, const float* B, float* C, int64_t m, in
   }
   if (variant == MTNN_VARIANT_AUTO && b_is_nk && skinny_auto() && skinny_eligible(A, B, m, n, k))
     return launch_gemm_skinny(A, B, C, m, n, k, s);  // output side <= 16: GEMV-class SIMT
+  if (variant == MTNN_VARIANT_AUTO && !b_is_nk && skinny_auto() && nn_smallk_eligible(B, C, m, n, k))
+    return launch_gemm_nn_smallk(A, B, C, m, n, k, s);  // k <= 16: outer-product sum, C-write bound
   if (variant == MTNN_VARIANT_AUTO) variant = auto_variant(A, B, C, m, n, k, b_is_nk);
   if (variant == MTNN_VARIANT_TC3XF16S)
     return launch_gemm_tc(A, B, C, m, n, k, b_is_nk, TcKind::F16S, s);

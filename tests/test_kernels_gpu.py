@@ -911,3 +911,35 @@ def test_gated_window_excludes_host_stalls():
     torch.cuda.synchronize()
     assert t0.elapsed_time(t1) < 5.0  # ms: the GEMM, not the 20 ms stall
 
+
+class TestGemvClassKernels:
+    """GEMV-class products on the SIMT kernels: the staged skinny NT (output side
+    <= 16: the long operand's rows bulk-copied into shared memory, the short
+    operand in registers) and the small-k NN (k <= 16: outer-product sum bound by
+    writing C) — against float64, through the dispatcher's auto variant, on
+    both skinny orientations and one- and multi-step k."""
+
+    @pytest.mark.parametrize("shape", [(1024, 10, 4096), (10, 4096, 1024), (2000, 3, 2048),
+                                       (7, 1500, 16384), (4096, 16, 512), (333, 1, 1028),
+                                       (1, 5000, 64)])
+    def test_skinny_nt(self, rng, shape):
+        m, n, k = shape
+        a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+        want = a.astype(np.float64) @ b.astype(np.float64).T
+        got = gemm_nt(a, b)
+        assert rel_frobenius(got, want) < FP32_GATE
+        assert np.array_equal(got, gemm_nt(a, b))  # fixed summation order
+
+    @pytest.mark.parametrize("shape", [(1024, 4096, 10), (33, 100, 16), (5, 8, 1), (300, 1028, 7),
+                                       (4097, 260, 4), (64, 4096, 13)])
+    def test_smallk_nn_and_tnn(self, rng, shape):
+        m, n, k = shape
+        a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+        want = a.astype(np.float64) @ b.astype(np.float64).T
+        got = gemm_nn(a, np.ascontiguousarray(b.T))
+        assert rel_frobenius(got, want) < FP32_GATE
+        assert rel_frobenius(gemm_tnn(a, b), want) < FP32_GATE
+        # k = 1: every output is one product, exact
+        if k == 1:
+            assert np.array_equal(got, (a @ b.T).astype(np.float32))
+
