@@ -133,11 +133,6 @@ int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* w
  *   each CTA loading half of B); 2 forces it whenever structurally possible
  *   (tests), 0 keeps the single-CTA 128x256 tiles. Bit-identical results at the
  *   same split-K.
- * "fused_split": 0 (default; env MTNN_FUSED_SPLIT): 1/2 split tc3xf16s NT
- *   operands inside the GEMM (per-(256-k chunk, row) scales, chunk 0 by a
- *   pre-pass, later chunks by two warps of every GEMM CTA ahead of its TMA
- *   producer). Correct, but 2.5-4x slower on the B200 (the GEMM's own TMA
- *   traffic saturates the SMs' L1TEX path; profiles/fused_split_r02.md).
  * "host_pipeline_blocked": 1 (default; env MTNN_PIPE_BLOCKED=0 turns it off):
  *   host-buffer NT calls on the tc3xf16s path with n >= 1024, k <= 4096 stream B in row
  *   blocks against A's first row block so C leaves while B arrives; 0 = copy B

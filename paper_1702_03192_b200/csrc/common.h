@@ -120,9 +120,6 @@ void set_f16s_inkernel_max_short(int64_t v);
 // Run-time knob (mtnn_config_set "tc_pair"): 256 x 256 CTA-pair tiles for large NT.
 int tc_pair_mode();  // 0 off, 1 large problems (default), 2 always when possible
 void set_tc_pair_mode(int v);
-// Run-time knob (mtnn_config_set "fused_split"): operand split overlapped with the NT GEMM.
-int fused_split_mode();  // 0 off, 1 measured-good shapes, 2 whenever eligible
-void set_fused_split_mode(int v);
 // mtnn_profile_trace: phase timestamps of the single-CTA tensor-core kernel.
 int set_gemm_trace(void* buf, int64_t ctas);
 // ldc: C row stride in elements (-1 = n); a larger one pads each C row.
@@ -145,11 +142,6 @@ int launch_split_rows_f16_pair(const float* x0, void* hi0, void* lo0, float* inv
                                float* inv1, int64_t rows1, const FixList& fix1, int64_t k,
                                cudaStream_t s);
 // 1/s per row (s = split_rows_f16's power-of-two row scale), reading x only.
-namespace seg { struct Pair; }
-// Fused split pre-pass (split_seg.cuh): chunks [c0, c1) of both K-major
-// operands with per-(row, chunk) scales; zeroes the GEMM's chunk counters.
-int launch_split_chunks_f16(const seg::Pair& pr, int c0, int c1, unsigned* cnt, int nchunks,
-                            cudaStream_t s);
 int launch_rowmax_f16(const float* x, float* inv_scale, int64_t rows, int64_t k,
                       const FixList& fix, cudaStream_t s);
 // Rows of an MN-major (k x n) F16S operand that share one column scale: the
@@ -213,7 +205,6 @@ struct FixupArgs {
   FixList fa, fb;
   int32_t a_row0 = 0, b_row0 = 0;
   bool reset_a = true, reset_b = true;
-  bool a_chunked = false, b_chunked = false;  // per-(256-k chunk, row) scales (fused split)
 };
 int launch_fixup(const FixupArgs& args, cudaStream_t s);
 // How the tensor-core kind represents an operand element (the fix-up recomputes it).

@@ -112,7 +112,6 @@ struct FixupDev {
   int32_t a_row0, b_row0;
   int reset_a, reset_b;
   int smem_entries;
-  int a_chunked, b_chunked;  // K-major A / B with per-(256-k chunk, row) scales (fused split)
 };
 
 constexpr int kFixThreads = 256;
@@ -123,9 +122,10 @@ constexpr int64_t kFixChunk = 256;  // k per FFMA chain in the overflow recomput
 constexpr int kFixSmemEntries = 8192;
 constexpr size_t kFixSmemBytes = (size_t)kFixSmemEntries * 12;
 
-// 1/s of A at (row i, k index kcol): per row, or per (chunk, row) (fused split)
+// 1/s of A at (row i, k index kcol): one scale per row of A
 __device__ __forceinline__ float inv_a_at(const FixupDev& p, int64_t i, int64_t kcol) {
-  return p.a_chunked ? p.inv_a[(kcol / kScaleChunkK) * p.m + i] : p.inv_a[i];
+  (void)kcol;
+  return p.inv_a[i];
 }
 __device__ __forceinline__ float rep_a(const FixupDev& p, int64_t i, int64_t kcol, float a) {
   if (p.rep == (int)FixRep::F16S) return f16s_represented(a, inv_a_at(p, i, kcol));
@@ -202,11 +202,10 @@ __device__ __forceinline__ uint32_t key_row(unsigned long long k) { return (uint
 __device__ __forceinline__ uint32_t key_col(unsigned long long k) { return (uint32_t)k; }
 
 // 1/s of B at (row j of B, k index kcol): per row for K-major B (NT), per
-// (kScaleChunkK chunk, column) for MN-major B^T (NN; split_f16.cu) and for a
-// fused-split K-major B (split_seg.cuh)
+// (kScaleChunkK chunk, column) for MN-major B^T (NN; split_f16.cu)
 template <bool B_NK>
 __device__ __forceinline__ float inv_b_at(const FixupDev& p, int64_t j, int64_t kcol) {
-  return (B_NK && !p.b_chunked) ? p.inv_b[j] : p.inv_b[(kcol / kScaleChunkK) * p.n + j];
+  return B_NK ? p.inv_b[j] : p.inv_b[(kcol / kScaleChunkK) * p.n + j];
 }
 
 template <bool B_NK>
@@ -226,10 +225,7 @@ __global__ void __launch_bounds__(kFixThreads, 2) fixup_kernel(const FixupDev p)
   // before this grid's own dependency wait, overlapped with the GEMM's tail;
   // only the work on C waits for the GEMM. Every path still executes the wait
   // before it exits (the next kernel's wait covers only this grid).
-  // (A fused-split GEMM appends entries itself: read them after its completion.)
-  const bool late = p.a_chunked || p.b_chunked;
   auto dep_wait = [] { asm volatile("griddepcontrol.wait;" ::: "memory"); };
-  if (late) dep_wait();
   if (threadIdx.x == 0) {
     s_na = p.fa.ctr ? *reinterpret_cast<volatile unsigned*>(&p.fa.ctr->count) : 0u;
     s_nb = p.fb.ctr ? *reinterpret_cast<volatile unsigned*>(&p.fb.ctr->count) : 0u;
@@ -237,7 +233,7 @@ __global__ void __launch_bounds__(kFixThreads, 2) fixup_kernel(const FixupDev p)
   __syncthreads();
   const unsigned na = s_na, nb = s_nb;
   if (na + nb == 0) {  // the usual case: nothing listed, counters already zero
-    if (!late) dep_wait();
+    dep_wait();
     return;
   }
   if (threadIdx.x == 0) {
@@ -245,7 +241,7 @@ __global__ void __launch_bounds__(kFixThreads, 2) fixup_kernel(const FixupDev p)
     release(p.fb, nb, p.reset_b != 0);
   }
   if (na > p.fa.cap || nb > p.fb.cap) {
-    if (!late) dep_wait();
+    dep_wait();
     // a list overflowed: recompute every output with FFMA chains of kFixChunk k,
     // each chain added to the output in memory by the thread that owns it (the
     // rounding error grows with ~k/kFixChunk + kFixChunk terms instead of k:
@@ -271,7 +267,7 @@ __global__ void __launch_bounds__(kFixThreads, 2) fixup_kernel(const FixupDev p)
   const int64_t cm = (p.m + kFixThreads - 1) / kFixThreads;
   const unsigned npa = na ? pow2_at_least(na) : 0, npb = nb ? pow2_at_least(nb) : 0;
   if (npa + npb > (unsigned)p.smem_entries) {
-    if (!late) dep_wait();
+    dep_wait();
     // too many entries to sort on chip (operands of ~2^32 elements): float
     // atomics, entries meeting in one output add in arrival order
     const int64_t items_a = (int64_t)na * cn;
@@ -312,7 +308,7 @@ __global__ void __launch_bounds__(kFixThreads, 2) fixup_kernel(const FixupDev p)
   float* vb = va + npa;
   if (na) load_sorted(p.fa.e, na, npa, ka, va);
   if (nb) load_sorted(p.fb.e, nb, npb, kb, vb);
-  if (!late) dep_wait();  // C (the GEMM's output) from here on
+  dep_wait();  // C (the GEMM's output) from here on
   const bool bounded = p.rep == (int)FixRep::F16S && p.inv_a != nullptr && p.inv_b != nullptr;
   constexpr float kRowMax = 16384.f;      // max |x| of a row <= 2^14 / s
   constexpr float kNegligible = 0x1p-26f;  // of |C|: below a quarter ulp
@@ -409,8 +405,6 @@ static int make_dev(const FixupArgs& a, FixupDev* out) {
   p.reset_a = a.reset_a ? 1 : 0;
   p.reset_b = a.reset_b ? 1 : 0;
   p.smem_entries = kFixSmemEntries;
-  p.a_chunked = a.a_chunked ? 1 : 0;
-  p.b_chunked = a.b_chunked ? 1 : 0;
   if (p.rep == (int)FixRep::F16S && p.inv_a == nullptr && a.fb.ctr != nullptr)
     return fail(MTNN_EINVAL, "fix-up: F16S B entries need A's row scales");
   return MTNN_OK;

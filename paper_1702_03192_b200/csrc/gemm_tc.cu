@@ -48,7 +48,6 @@
 
 #include "common.h"
 #include "workspace.h"
-#include "split_seg.cuh"
 
 namespace mtnn {
 
@@ -120,22 +119,19 @@ struct KindF16S {  // per-row power-of-2 scaled fp16 hi/lo (split_f16.cu)
 // their own deeper ring (kRawStages) so more DRAM bytes are in flight per SM
 // than the 3-stage h/l ring alone would allow — the converted operand streams
 // from DRAM, the other one from L2.
-// kSegSlots: fused split (kConv == 3) — 1 KiB slots of raw (row, chunk)
-// segments the splitter warps stage with bulk copies; the h/l ring then has
-// 3 stages.
-template <int BN, int kRawBytes = 0, int kEpi = kEpiWarps, int kSegSlots = 0>
+template <int BN, int kRawBytes = 0, int kEpi = kEpiWarps>
 struct Smem {
   static constexpr int kABytes = BM * 64;                // 8 KiB (64-byte k-block rows)
   static constexpr int kBBytes = BN * 64;                // 16 KiB at BN=256
-  static constexpr int kStages = (kRawBytes || kSegSlots) ? 3 : 4;  // h/l ring
+  static constexpr int kStages = kRawBytes ? 3 : 4;      // h/l ring
   static constexpr int kRawStages = kRawBytes ? 7 : 0;   // raw fp32 ring
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
   static constexpr int kStagingBytes = 32 * 16 * 4;      // one 32x16 fp32 tile
   static constexpr int kRingBytes = kStages * kStageBytes;
   static constexpr int kRawOff = kRingBytes;             // 1024-aligned
-  static constexpr int kRawRingBytes = kRawStages * kRawBytes + kSegSlots * 1024;
+  static constexpr int kRawRingBytes = kRawStages * kRawBytes;
   static constexpr int kEpiBytes = kEpi * kStagingBytes;
-  static constexpr int kBarBytes = kSegSlots ? 512 : 256;
+  static constexpr int kBarBytes = 256;
   static constexpr int kTotal = 1024 + kRingBytes + kRawRingBytes + kEpiBytes + kBarBytes;
 };
 
@@ -325,13 +321,6 @@ struct Params {
   const float* inv_scale_a;  // KindF16S: 1/s per row of A (m) and of B (n)
   const float* inv_scale_b;
   unsigned long long* trace;    // mtnn_profile_trace: [CTA][kTracePoints] globaltimer ns
-  // Fused split (kConv == 3): both K-major operands carry per-(256-k chunk,
-  // row) scales (inv_scale_a/b = fs.op[0/1].inv, [chunk][rows]); chunks
-  // [0, fs_c0) come split from the pre-pass, the rest are split here by warps
-  // 2-3 of every CTA, each CTA's two warps bumping fs_cnt[chunk] when done.
-  seg::Pair fs;
-  unsigned* fs_cnt;
-  int fs_c0, fs_nchunks;
 };
 constexpr int kTracePoints = 16;
 
@@ -387,14 +376,6 @@ __device__ __forceinline__ void trace_mark(const Params& p, int point) {
 #endif
 }
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
-  return v;
-}
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
 // FP16 hi/lo of 8 consecutive k-values of one row with the row's exact
 // power-of-two scale s — the same operations as split_f16.cu's split2, so the
 // halves (and every C bit) equal the pre-split path's.
@@ -424,14 +405,14 @@ template <int kCols>
 struct ChunkScales {
   float v[kCols / 32];
 };
-template <int kCols, bool kCoherent = false>
+template <int kCols>
 __device__ __forceinline__ ChunkScales<kCols> load_chunk_scales(const float* inv_b, int chunk,
                                                                 int64_t n, int64_t col0, int lane) {
   const float* sc = inv_b + (int64_t)chunk * n + col0;
   ChunkScales<kCols> c;
 #pragma unroll
   for (int i = 0; i < kCols / 32; ++i)
-    c.v[i] = col0 + 32 * i + lane < n ? (kCoherent ? __ldcg(sc + 32 * i + lane) : __ldg(sc + 32 * i + lane)) : 0.f;
+    c.v[i] = col0 + 32 * i + lane < n ? __ldg(sc + 32 * i + lane) : 0.f;
   return c;
 }
 // Adds 16 TMEM columns (the c16-th group of the warp's) of one chunk into the
@@ -467,19 +448,15 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
                      const __grid_constant__ CUtensorMap map_blo,
                      const __grid_constant__ CUtensorMap map_c, const Params p) {
   constexpr bool kF16Conv = (kConv == 1 || kConv == 2) && Kind::kScaled;
-  constexpr bool kFS = kConv == 3;  // fused split (F16S, K-major A and B)
-  static_assert(!kFS || (Kind::kScaled && !B_MN), "fused split: F16S NT only");
   static_assert(!kF16Conv || (kConv == 1 ? BM : BN) == kF16ConvRows,
                 "F16S in-kernel conversion needs a 128-row converted tile");
   static_assert(!(kF16Conv && kConv == 2 && B_MN), "in-kernel F16S split of B needs K-major B (NT)");
   using R = Roles<kF16Conv>;
-  constexpr int kSegPerWarp = 24;  // fused split: staged segments in flight per splitter warp
-  using S = Smem<BN, kF16Conv ? kF16ConvRows * 128 : 0, R::kEpi, kFS ? 2 * kSegPerWarp : 0>;
+  using S = Smem<BN, kF16Conv ? kF16ConvRows * 128 : 0, R::kEpi>;
   constexpr int kColsPerWarp = BN / (R::kEpi / 4);  // each epilogue warp: a column slice
   // MN-major F16S B carries one scale per (kScaleChunkK rows, column): applied
   // per promotion chunk (the host keeps chunks and k-splits aligned to it)
-  constexpr bool kChunkB = (B_MN && Kind::kScaled) || kFS;
-  constexpr bool kChunkA = kFS;  // per-chunk row scales of A (fused split)
+  constexpr bool kChunkB = B_MN && Kind::kScaled;
   constexpr int kScaleKb = kScaleChunkK / Kind::BK;
   static_assert(kColsPerWarp % 32 == 0, "chunk scales: 32-column groups per epilogue warp");
   extern __shared__ uint8_t smem_raw[];
@@ -487,8 +464,7 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int kStages = S::kStages;
   constexpr int kRawStages = S::kRawStages;
-  constexpr int kSegBars = kFS ? 2 * kSegPerWarp : 0;
-  static_assert(3 * kStages + 4 + 2 * kRawStages + kSegBars <= S::kBarBytes / 8 - 1, "barrier space");
+  static_assert(3 * kStages + 4 + 2 * kRawStages <= S::kBarBytes / 8 - 1, "barrier space");
   uint8_t* ring = smem;
   uint8_t* raw_ring = smem + S::kRawOff;
   uint8_t* epi = smem + S::kRingBytes + S::kRawRingBytes;
@@ -500,8 +476,7 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
   uint64_t* conv_bar = bars + 2 * kStages + 4;     // [kStages] (kConv != 0)
   uint64_t* rfull_bar = bars + 3 * kStages + 4;    // [kRawStages] (F16S conversion)
   uint64_t* rempty_bar = rfull_bar + kRawStages;   // [kRawStages]
-  uint64_t* seg_bar = rempty_bar + kRawStages;     // [kSegBars] (fused split)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(seg_bar + kSegBars);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty_bar + kRawStages);
   // TMA bytes per h/l stage: F16S conversion loads only the other operand's
   // halves (the raw tile arrives on its own ring); TF32 conversion skips the
   // converted lo slot.
@@ -536,7 +511,6 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
       mbar_init(smem_u32(&rfull_bar[s]), 1);
       mbar_init(smem_u32(&rempty_bar[s]), R::kConvWarps / 2);
     }
-    for (int s = 0; s < kSegBars; ++s) mbar_init(smem_u32(&seg_bar[s]), 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -565,15 +539,6 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
         const int tm = w.tm, tn = w.tn;
         if (wi == 0) trace_mark(p, 12);
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
-          if (kFS && (kb == w.kb0 || kb % kScaleKb == 0) && kb / kScaleKb >= p.fs_c0) {
-            // chunk split inside this grid: wait until all of its splitter warps
-            // posted it, then order the TMA reads after their generic writes
-            const unsigned* cnt = p.fs_cnt + kb / kScaleKb;
-            const unsigned want = 2u * gridDim.x;
-            while (ld_acquire_u32(cnt) < want) __nanosleep(64);
-            fence_proxy_async_global();
-            trace_mark(p, 15);
-          }
           mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
           const uint32_t fb = smem_u32(&full_bar[stage]);
           mbar_expect_tx(fb, kExpectBytes);
@@ -626,7 +591,7 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
         for (int kb = kc; kb < kce; ++kb) {
           // TF32 conversion waits full_bar itself, so conv_bar implies it; the F16S
           // converters do not (the raw tile has its own ring)
-          if (kConv == 0 || kF16Conv || kFS) mbar_wait(smem_u32(&full_bar[stage]), phase);
+          if (kConv == 0 || kF16Conv) mbar_wait(smem_u32(&full_bar[stage]), phase);
           if (kConv == 1 || kConv == 2) mbar_wait(smem_u32(&conv_bar[stage]), phase);
           if (wi == 0 && kb == w.kb0 && lane == 0) trace_mark(p, 4);
           tc_fence_after();
@@ -684,80 +649,6 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
           if (kConv == 1) tma_load_2d(dst, &map_ahi, fb, kb * Kind::BK, tm * BM);
           else tma_load_2d(dst, &map_bhi, fb, kb * Kind::BK, tn * BN);
           if (++rs == kRawStages) { rs = 0; rphase ^= 1; }
-        }
-      }
-    }
-  } else if (kFS && (warp == 2 || warp == 3)) {
-    // ===================== fused split: chunks fs_c0.. of A and B =====================
-    // Global splitter warp g of 2G takes rows g, g + 2G, ... of the m + n
-    // rows, chunk by chunk in k order (the chunks the MMAs need first are
-    // posted first). Its segments stream through its own ring of 1 KiB smem
-    // slots by bulk copies issued kSegPerWarp ahead (24 KiB in flight per
-    // warp); after its share of a chunk the warp bumps fs_cnt[chunk].
-    const int sw = warp - 2;
-    uint8_t* slots = raw_ring + sw * kSegPerWarp * 1024;
-    uint64_t* sbar = seg_bar + sw * kSegPerWarp;
-    const int64_t nw2 = 2LL * gridDim.x;
-    const int64_t g = 2LL * blockIdx.x + sw;
-    const int64_t rows0 = p.fs.op[0].rows, rows = rows0 + p.fs.op[1].rows;
-    const int64_t per_chunk = g < rows ? (rows - 1 - g) / nw2 + 1 : 0;
-    const int64_t nseg = per_chunk * (p.fs_nchunks - p.fs_c0);
-    const int64_t k = p.fs.k;
-    // issue cursor (chunk ci, the warp's ji-th row of it), slot si
-    int ci = p.fs_c0, si = 0;
-    int64_t ji = 0;
-    auto issue = [&]() {  // lane 0
-      const int64_t v = g + ji * nw2;
-      const bool b = v >= rows0;
-      const int64_t r = b ? v - rows0 : v;
-      const int len = (int)min((int64_t)kScaleChunkK, k - (int64_t)ci * kScaleChunkK);
-      const float* src = (b ? p.fs.op[1].x : p.fs.op[0].x) + r * k + (int64_t)ci * kScaleChunkK;
-      const uint32_t bar = smem_u32(&sbar[si]);
-      mbar_expect_tx(bar, (uint32_t)len * 4);
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_u32(slots + si * 1024)),
-          "l"(src), "r"(len * 4), "r"(bar)
-          : "memory");
-      if (++ji == per_chunk) { ji = 0; ++ci; }
-      if (++si == kSegPerWarp) si = 0;
-    };
-    if (per_chunk == 0) {
-      if (lane == 0)
-        for (int c = p.fs_c0; c < p.fs_nchunks; ++c) atomicAdd(p.fs_cnt + c, 1u);
-    } else {
-      int64_t issued = min(nseg, (int64_t)kSegPerWarp);
-      if (lane == 0)
-        for (int64_t i = 0; i < issued; ++i) issue();
-      int c = p.fs_c0, slot = 0;
-      uint32_t parity = 0;
-      int64_t j = 0;
-      const int len_full = kScaleChunkK;
-      for (int64_t i = 0; i < nseg; ++i) {
-        mbar_wait(smem_u32(&sbar[slot]), parity);
-        const int64_t v = g + j * nw2;
-        const int o = v >= rows0 ? 1 : 0;
-        const int64_t r = o ? v - rows0 : v;
-        const int len = (c + 1) * kScaleChunkK <= k ? len_full : (int)(k - (int64_t)c * kScaleChunkK);
-        seg::split_staged_segment(reinterpret_cast<const float*>(slots + slot * 1024), len,
-                                  seg::sel(p.fs, o), r, k, c, lane);
-        __syncwarp();  // every lane is done with the slot
-        if (issued < nseg) {
-          if (lane == 0) {
-            fence_proxy_async_smem();  // generic reads of the slot before the async refill
-            issue();
-          }
-          ++issued;
-        }
-        if (++slot == kSegPerWarp) { slot = 0; parity ^= 1; }
-        if (++j == per_chunk) {  // this warp's share of chunk c is written
-          __threadfence();
-          fence_proxy_async_global();
-          __syncwarp();
-          if (lane == 0) atomicAdd(p.fs_cnt + c, 1u);
-          if (sw == 0 && lane == 0) trace_mark(p, c == p.fs_c0 ? 13 : 14);
-          j = 0;
-          ++c;
         }
       }
     }
@@ -868,23 +759,14 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
         kce = min(kb1, kc + p.chunk_kb);
         // (the chunk's column scales load while the MMAs of the chunk finish)
         ChunkScales<kColsPerWarp> cs{};
-        if (kChunkB && !kFS) cs = load_chunk_scales<kColsPerWarp>(p.inv_scale_b, kc / kScaleKb, p.n, col0, lane);
-        if (kTail >= 1 && Kind::kScaled && !kChunkA && kce >= kb1) {
+        if (kChunkB) cs = load_chunk_scales<kColsPerWarp>(p.inv_scale_b, kc / kScaleKb, p.n, col0, lane);
+        if (kTail >= 1 && Kind::kScaled && kce >= kb1) {
           // the output scales load while the tile's last chunk is still in the
           // tensor core (the store loop below would otherwise wait on L2 for them)
           if (row < p.m) sa_pre = __ldg(p.inv_scale_a + row);
           if (!kChunkB) csb = load_chunk_scales<kColsPerWarp>(p.inv_scale_b, 0, p.n, col0, lane);
         }
         mbar_wait(smem_u32(&tfull_bar[acc]), acc_phase);
-        // fused split: this chunk's scales were written by other CTAs during
-        // this grid, before the chunk's operands could be loaded: read them
-        // once the chunk's MMAs are done, from L2 (no stale L1 lines)
-        float sa_c = 1.f;
-        if (kFS) {
-          cs = load_chunk_scales<kColsPerWarp, true>(p.inv_scale_b, kc / kScaleKb, p.n, col0, lane);
-          if (row < p.m) sa_c = __ldcg(p.inv_scale_a + (int64_t)(kc / kScaleKb) * p.m + row);
-        }
-        if (e == 0 && lane == 0) trace_mark(p, wi == 0 && kc == w.kb0 ? 6 : 7);
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + h * kColsPerWarp;
 #pragma unroll
@@ -892,12 +774,7 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
           uint32_t r[16];
           tmem_ld_32x32b_x16(taddr + c * 16, r);
           tmem_ld_wait();
-          if (kChunkA) {
-            // fused split: this chunk's row scale of A and column scales of B
-#pragma unroll
-            for (int j = 0; j < 16; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * sa_c);
-            add_chunk_scaled(sum + c * 16, r, cs, c);
-          } else if (kChunkB) {
+          if (kChunkB) {
             // MN-major F16S B: this promotion chunk's exact column scales
             add_chunk_scaled(sum + c * 16, r, cs, c);
           } else {
@@ -911,11 +788,10 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
       // KindF16S: undo the exact power-of-two operand scales while storing,
-      // C = (acc * 1/s_a[row]) * 1/s_b[col] (MN-major B: applied per chunk
-      // above; fused split: both, per chunk)
+      // C = (acc * 1/s_a[row]) * 1/s_b[col] (MN-major B: applied per chunk above)
       if (e == 0 && lane == 0 && wi == nw - 1) trace_mark(p, 13);
       const float sa = kTail >= 1 ? sa_pre
-                                  : (Kind::kScaled && !kChunkA && row < p.m) ? __ldg(p.inv_scale_a + row) : 1.f;
+                                  : (Kind::kScaled && row < p.m) ? __ldg(p.inv_scale_a + row) : 1.f;
       // Store: 32 rows x kColsPerWarp through a 32x16 staging tile (64B swizzle).
 #pragma unroll
       for (int c = 0; c < kColsPerWarp / 16; ++c) {
@@ -926,9 +802,7 @@ gemm_tc3x_kernel(const __grid_constant__ CUtensorMap map_ahi,
           const int pj = j ^ ((lane >> 1) & 3);
           float4 v = make_float4(sum[c * 16 + 4 * j], sum[c * 16 + 4 * j + 1],
                                  sum[c * 16 + 4 * j + 2], sum[c * 16 + 4 * j + 3]);
-          if (kChunkA) {
-            // (scales applied per chunk)
-          } else if (Kind::kScaled && kChunkB) {
+          if (Kind::kScaled && kChunkB) {
             v.x *= sa; v.y *= sa; v.z *= sa; v.w *= sa;
           } else if (kTail >= 1 && Kind::kScaled) {
             // column c*16 + 4j + t of the warp's slice: lane (that % 32) of csb
@@ -1088,7 +962,7 @@ static int launch_impl(const void* ahi, const void* alo, const void* bhi,
                        const void* blo, float* out, const Params& p, int grid,
                        cudaStream_t s) {
   constexpr bool kF16Conv = (kConv == 1 || kConv == 2) && Kind::kScaled;
-  using S = Smem<BN, kF16Conv ? kF16ConvRows * 128 : 0, Roles<kF16Conv>::kEpi, kConv == 3 ? 48 : 0>;
+  using S = Smem<BN, kF16Conv ? kF16ConvRows * 128 : 0, Roles<kF16Conv>::kEpi>;
   constexpr int kNumThreads = Roles<kF16Conv>::kThreads;
   CUtensorMap mah, mal, mbh, mbl, mc;
   const uint64_t eb = Kind::kElemBytes;
@@ -1604,10 +1478,9 @@ static int chunk_kblocks(TcKind) {
 // promotion chunk and every k-split must then lie inside one scale chunk —
 // chunk_kb divides the scale chunk's k-blocks and k-splits start on its
 // boundaries (kblocks_per_split rounded up to a multiple of it).
-static void align_scale_chunks(tc::Params& p, TcKind kind, bool b_is_nk, int splits,
-                               bool chunked = false) {
+static void align_scale_chunks(tc::Params& p, TcKind kind, bool b_is_nk, int splits) {
   p.kblocks_per_split = (p.total_kblocks + splits - 1) / splits;
-  if (kind == TcKind::F16S && (!b_is_nk || chunked)) {
+  if (kind == TcKind::F16S && !b_is_nk) {
     constexpr int sk = kScaleChunkK / tc::KindF16S::BK;
     if (sk % p.chunk_kb != 0) p.chunk_kb = sk;
     p.kblocks_per_split = (p.kblocks_per_split + sk - 1) / sk * sk;
@@ -1969,17 +1842,9 @@ static int tc_run_pair(const TcOperand& a, const TcOperand& b, float* C, int64_t
   return MTNN_OK;
 }
 
-// Fused split (conv == 3): the pre-pass splits chunks [0, c0); the GEMM the rest.
-struct FsArgs {
-  seg::Pair pr;
-  unsigned* cnt;
-  int c0, nchunks;
-};
-
 template <int BN>
 static int tc_run_bn(const TcOperand& a, const TcOperand& b, float* C, int64_t m, int64_t n,
-                     int64_t k, int64_t ldc, bool b_is_nk, TcKind kind, int conv, cudaStream_t s,
-                     const FsArgs* fs = nullptr) {
+                     int64_t k, int64_t ldc, bool b_is_nk, TcKind kind, int conv, cudaStream_t s) {
   const DeviceInfo* di = nullptr;
   MTNN_TRY(device_info(&di));
   using S = tc::Smem<BN>;
@@ -1997,20 +1862,11 @@ static int tc_run_bn(const TcOperand& a, const TcOperand& b, float* C, int64_t m
   p.total_kblocks = (int)((k + bk - 1) / bk);
   const int tiles = p.tiles_m * p.tiles_n;
   int splits = choose_splits(tiles, p.total_kblocks, m, n, di->sm_count);
-  align_scale_chunks(p, kind, b_is_nk, splits, fs != nullptr);
+  align_scale_chunks(p, kind, b_is_nk, splits);
   splits = (p.total_kblocks + p.kblocks_per_split - 1) / p.kblocks_per_split;
   p.splits = splits;
   p.units = tiles * splits;
   const int grid = std::min(p.units, di->sm_count);
-  if (fs) {
-    p.fs = fs->pr;
-    p.fs_cnt = fs->cnt;
-    p.fs_c0 = fs->c0;
-    p.fs_nchunks = fs->nchunks;
-    if (conv != 3 || kind != TcKind::F16S || !b_is_nk)
-      return fail(MTNN_EINVAL, "fused split: F16S NT with conv 3 only");
-  }
-
   if (g_trace.load() && grid <= g_trace_ctas.load()) p.trace = g_trace.load();
   float* out = C;
   ScratchBuffer part;
@@ -2022,9 +1878,6 @@ static int tc_run_bn(const TcOperand& a, const TcOperand& b, float* C, int64_t m
   if (kind == TcKind::F16S && conv == 0)
     rc = b_is_nk ? tc::launch_impl<BN, false, tc::KindF16S>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s)
                  : tc::launch_impl<BN, true, tc::KindF16S>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s);
-  else if (conv == 3)
-    rc = fs ? tc::launch_impl<BN, false, tc::KindF16S, 3>(a.hi, a.lo, b.hi, b.lo, out, p, grid, s)
-            : fail(MTNN_EINVAL, "fused split needs its pre-pass state");
   else if (conv != 0 && kind == TcKind::F16S) {
     if constexpr (BN == tc::kF16ConvRows) {
       if (conv == 1)
@@ -2148,90 +2001,6 @@ int gemm_nt_allgather(const float* A, const float* B, float* C_local, float* con
   return MTNN_OK;
 }
 
-// Fused split switch: mtnn_config_set("fused_split", v) / MTNN_FUSED_SPLIT:
-// 0 off (default), 1 / 2 whenever eligible. Correct (tests/test_kernels_gpu.py
-// TestFusedSplit) but measured 2.5-4x SLOWER than split-then-GEMM on the B200
-// (1024x4096x4096: 326 vs 109 us per call): the GEMM's own operand TMA (64-byte
-// box rows: ~770 row requests per k-block) keeps the SM's L1TEX/TMA path
-// 87-94% busy (ncu), so the splitter warps' traffic starves — the bulk-copy
-// stream alone reaches ~0.8 TB/s chip-wide, ~0.3 TB/s once the halves are
-// stored, against the ~2.6 TB/s needed to stay ahead of the MMAs
-// (profiles/fused_split_r02.md).
-static std::atomic<int> g_fused_split{-1};
-int fused_split_mode() {
-  int v = g_fused_split.load(std::memory_order_relaxed);
-  if (v < 0) {
-    const char* e = getenv("MTNN_FUSED_SPLIT");
-    v = e ? std::min(2, std::max(0, atoi(e))) : 0;
-    g_fused_split.store(v, std::memory_order_relaxed);
-  }
-  return v;
-}
-void set_fused_split_mode(int v) { g_fused_split.store(v, std::memory_order_relaxed); }
-
-// tc3xf16s NT whose operand split overlaps the GEMM (split_seg.cuh): per-(256-k
-// chunk, row) scales, chunk 0 from a pre-pass (which also zeroes the chunk
-// counters), later chunks split by two warps of every GEMM CTA ahead of its
-// TMA producer, then the residual fix-up with the chunked scales.
-static bool fused_split_wanted(int64_t m, int64_t n, int64_t k, int conv) {
-  const int mode = fused_split_mode();
-  if (mode == 0 || conv != 0 || k <= kScaleChunkK || n <= 128) return false;
-  // single-CTA 256-wide tiles only (CTA pairs keep the pre-split path)
-  const bool pair = tc_pair_mode() == 2 ||
-                    (tc_pair_mode() == 1 && ((m + 255) / 256) * ((n + 255) / 256) >= pair_min_tiles());
-  if (pair && m > 128) return false;
-  return true;
-}
-
-static int gemm_nt_fused(const float* A, const float* B, float* C, int64_t m, int64_t n, int64_t k,
-                         cudaStream_t s) {
-  const int nchunks = (int)((k + kScaleChunkK - 1) / kScaleChunkK);
-  // chunks split by the pre-pass (MTNN_FS_PREPASS, default 1; A/B diagnostics)
-  static const int prepass = [] {
-    const char* e = getenv("MTNN_FS_PREPASS");
-    return e ? std::max(1, atoi(e)) : 1;
-  }();
-  const int c0 = std::min(nchunks, prepass);
-  const bool track = fixup_enabled();
-  ScratchBuffer wa, wb;
-  FixHandle fa, fb;
-  seg::Pair pr{};
-  pr.k = k;
-  uint8_t* extra_a = nullptr;
-  auto layout = [&](const float* X, int64_t rows, ScratchBuffer& ws, FixHandle* fh, seg::Operand* o,
-                    size_t extra, uint8_t** extra_ptr) -> int {
-    const size_t oh = align256((size_t)rows * k * 2);
-    const size_t osc = align256((size_t)nchunks * rows * 4);
-    const unsigned cap = track ? fix_capacity(rows * k) : 0;
-    MTNN_TRY(ws.alloc(2 * oh + osc + extra + (track ? fix_entry_bytes(cap) : 0), s));
-    uint8_t* base = static_cast<uint8_t*>(ws.ptr);
-    o->x = X;
-    o->h = reinterpret_cast<__half*>(base);
-    o->l = reinterpret_cast<__half*>(base + oh);
-    o->inv = reinterpret_cast<float*>(base + 2 * oh);
-    o->rows = rows;
-    o->fix = FixList{};
-    if (extra_ptr) *extra_ptr = base + 2 * oh + osc;
-    if (track) {
-      MTNN_TRY(fix_attach(fh, base + 2 * oh + osc + extra, cap, 0, s));
-      o->fix = fh->list;
-    }
-    return MTNN_OK;
-  };
-  MTNN_TRY(layout(A, m, wa, &fa, &pr.op[0], align256((size_t)nchunks * sizeof(unsigned)), &extra_a));
-  MTNN_TRY(layout(B, n, wb, &fb, &pr.op[1], 0, nullptr));
-  unsigned* cnt = reinterpret_cast<unsigned*>(extra_a);
-  MTNN_TRY(launch_split_chunks_f16(pr, 0, c0, cnt, nchunks, s));
-  TcOperand a{pr.op[0].h, pr.op[0].l, pr.op[0].inv, pr.op[0].fix};
-  TcOperand b{pr.op[1].h, pr.op[1].l, pr.op[1].inv, pr.op[1].fix};
-  const FsArgs fsa{pr, cnt, c0, nchunks};
-  float* dsts[1] = {C};
-  FixupArgs f = tc_fix_args(A, a, B, b, dsts, 1, m, n, k, n, true, TcKind::F16S);
-  f.a_chunked = f.b_chunked = true;
-  MTNN_TRY(tc_run_bn<256>(a, b, C, m, n, k, n, true, TcKind::F16S, 3, s, &fsa));
-  return tc_fixup_finish(f, fa, fb, s);
-}
-
 int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t n,
                    int64_t k, bool b_is_nk, TcKind kind, cudaStream_t s) {
   const char* name = kind == TcKind::F16S ? "tc3xf16s" : "tc3xtf32";
@@ -2242,9 +2011,6 @@ int launch_gemm_tc(const float* A, const float* B, float* C, int64_t m, int64_t 
   FixHandle fa, fb;
   TcOperand a{}, b{};
   const int conv = tc_inkernel_operand(m, n, b_is_nk, kind);
-  if (kind == TcKind::F16S && b_is_nk && tc_eligible(A, B, C, m, n, k, b_is_nk, kind) &&
-      fused_split_wanted(m, n, k, conv))
-    return gemm_nt_fused(A, B, C, m, n, k, s);
   MTNN_TRY(tc_prepare_pair(A, m, B, n, k, !b_is_nk, kind, conv, wa, wb, &fa, &fb, &a, &b, s));
   if (tc_eligible(A, B, C, m, n, k, b_is_nk, kind)) {
     float* dsts[1] = {C};

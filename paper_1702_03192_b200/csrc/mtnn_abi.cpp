@@ -748,11 +748,6 @@ int mtnn_config_set(const char* key, int64_t value) {
     set_tc_pair_mode((int)value);
     return MTNN_OK;
   }
-  if (strcmp(key, "fused_split") == 0) {
-    if (value < 0 || value > 2) return fail(MTNN_EINVAL, "fused_split must be 0, 1 or 2");
-    set_fused_split_mode((int)value);
-    return MTNN_OK;
-  }
   if (strcmp(key, "host_pipeline_blocked") == 0) {
     if (value != 0 && value != 1) return fail(MTNN_EINVAL, "host_pipeline_blocked must be 0 or 1");
     g_pipe_blocked.store((int)value, std::memory_order_relaxed);
@@ -774,10 +769,6 @@ int mtnn_config_get(const char* key, int64_t* value) {
   }
   if (strcmp(key, "tc_pair") == 0) {
     *value = tc_pair_mode();
-    return MTNN_OK;
-  }
-  if (strcmp(key, "fused_split") == 0) {
-    *value = fused_split_mode();
     return MTNN_OK;
   }
   if (strcmp(key, "host_pipeline_blocked") == 0) {

@@ -32,7 +32,6 @@
 #include "common.h"
 #include "fix.h"
 #include "pdl.h"
-#include "split_seg.cuh"
 
 namespace mtnn {
 namespace {
@@ -631,22 +630,6 @@ split_cols_chunk_kernel(const float* __restrict__ x, __half* __restrict__ hi,
 }
 
 
-// Fused split, pre-pass: chunks [c0, c1) of every row of both operands (a warp
-// per 4 (row, chunk) segments, all loads in flight first), and the GEMM's
-// per-chunk ready counters zeroed (gemm_tc.cu kConv == 3 splits the rest).
-__global__ void __launch_bounds__(256)
-split_chunks_f16_kernel(const seg::Pair pr, int c0, int c1, unsigned* cnt, int nchunks) {
-  pdl_wait();
-  pdl_trigger();
-  if (blockIdx.x == 0)
-    for (int i = threadIdx.x; i < nchunks; i += blockDim.x) cnt[i] = 0u;
-  const int lane = threadIdx.x % 32;
-  const int64_t rows = pr.op[0].rows + pr.op[1].rows;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
-  const int64_t w0 = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  for (int c = c0; c < c1; ++c)
-    for (int64_t v = w0; v < rows; v += 4 * warps) seg::split_segments<4>(pr, c, v, warps, rows, lane);
-}
 }  // namespace
 
 // Splits (hi != nullptr) or row-scales (hi == nullptr) the rows of up to two
@@ -730,20 +713,6 @@ int launch_split_cols_f16(const float* x, void* hi, void* lo, float* inv_scale, 
   MTNN_TRY(launch_chained(split_cols_chunk_kernel, dim3((unsigned)blocks), dim3(8 * kColRowLanes),
                           0, s, x, static_cast<__half*>(hi), static_cast<__half*>(lo), inv_scale,
                           k, n, fl, rj));
-  MTNN_CUDA_TRY(cudaGetLastError());
-  return MTNN_OK;
-}
-
-int launch_split_chunks_f16(const seg::Pair& pr, int c0, int c1, unsigned* cnt, int nchunks,
-                            cudaStream_t s) {
-  const DeviceInfo* di = nullptr;
-  MTNN_TRY(device_info(&di));
-  const int64_t rows = pr.op[0].rows + pr.op[1].rows;
-  const int64_t segs = rows * std::max(0, c1 - c0);
-  KernelTimer timer(MTNN_KCLASS_SPLIT, 8.0 * (double)rows * std::min<double>((double)pr.k, (double)(c1 - c0) * kScaleChunkK), s);
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((segs + 31) / 32, (int64_t)di->sm_count * 8));
-  MTNN_TRY(launch_chained(split_chunks_f16_kernel, dim3((unsigned)blocks), dim3(256), 0, s, pr, c0, c1,
-                          cnt, nchunks));
   MTNN_CUDA_TRY(cudaGetLastError());
   return MTNN_OK;
 }

@@ -124,16 +124,7 @@ def test_config_knobs_roundtrip_and_reject_unknown():
         _lib.config_set(key, old)
     with pytest.raises(ValueError, match="unknown config key"):
         _lib.config_set("no_such_knob", 1)
-    for key in ("fused_split",):
-        old = _lib.config_get(key)
-        try:
-            for v in (0, 2, 1):
-                _lib.config_set(key, v)
-                assert _lib.config_get(key) == v
-            with pytest.raises(ValueError, match="0, 1 or 2"):
-                _lib.config_set(key, 3)
-        finally:
-            _lib.config_set(key, old)
+
 
 
 def test_ipc_and_allgather_fail_cleanly_without_a_gpu():

@@ -457,85 +457,6 @@ class TestCtaPairTiles:
             _lib.config_set("tc_pair", old)
 
 
-class TestFusedSplit:
-    """tc3xf16s NT with the operand split overlapped with the GEMM (knob
-    fused_split = 2 forces it): per-(256-k chunk, row) scales, chunk 0 split by a
-    pre-pass, later chunks by two warps of every GEMM CTA ahead of its TMA
-    producer. Same FP32 gate; the per-chunk scales change the rounding of the
-    halves only within the representation error (<= 2e-6 of the pre-split path)."""
-
-    @pytest.mark.parametrize("shape", [(1024, 4096, 4096), (1024, 4096, 784), (300, 520, 1000),
-                                       (2048, 2048, 1024), (4096, 512, 2056), (129, 4096, 264)])
-    def test_fused_matches_presplit(self, rng, shape):
-        import torch
-
-        from paper_1702_03192_b200 import _lib
-
-        m, n, k = shape
-        a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
-        ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
-        want = oracle.oracle_nt_blas(a, b)
-        old = _lib.config_get("fused_split")
-        try:
-            _lib.config_set("fused_split", 0)
-            pre = gemm_nt(ta, tb, variant="tc3xf16s").cpu().numpy()
-            _lib.config_set("fused_split", 2)
-            got = gemm_nt(ta, tb, variant="tc3xf16s").cpu().numpy()
-            got2 = gemm_nt(ta, tb, variant="tc3xf16s").cpu().numpy()
-        finally:
-            _lib.config_set("fused_split", old)
-        assert np.array_equal(got, got2)
-        assert rel_frobenius(got, want) < FP32_GATE
-        assert rel_frobenius(got, pre) < 2e-6
-
-    @pytest.mark.parametrize("case", ["outlier_col", "row_magnitudes", "chunk_magnitudes", "nonfinite"])
-    def test_fused_range_and_nonfinite(self, rng, case):
-        """Residual fix-up with the chunked scales (an outlier column 10^8 x the
-        rest with a zero partner; rows and 256-k chunks of very different
-        magnitude), and NaN/Inf propagation."""
-        import torch
-
-        from paper_1702_03192_b200 import _lib
-
-        m, n, k = 512, 1024, 1536
-        a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
-        if case == "outlier_col":
-            a *= 1e-7
-            a[:, 3], b[:, 3] = 10.0, 0.0
-            b[:, 700] *= 1e9
-            a[:, 700] = 0.0
-        elif case == "row_magnitudes":
-            a *= np.float32(10.0) ** rng.integers(-20, 20, size=(m, 1)).astype(np.float32)
-            b *= np.float32(10.0) ** rng.integers(-15, 15, size=(n, 1)).astype(np.float32)
-        elif case == "chunk_magnitudes":
-            for c in range(0, k, 256):
-                a[:, c:c + 256] *= np.float32(10.0 ** ((c // 256) * 3 - 8))
-            b[:, 1000] = 1e6
-            b[:, 1001:1003] = 1e-12
-        else:
-            a[5, 300] = np.nan
-            b[9, 900] = np.inf
-        ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
-        old = _lib.config_get("fused_split")
-        try:
-            _lib.config_set("fused_split", 2)
-            got = gemm_nt(ta, tb, variant="tc3xf16s").cpu().numpy()
-        finally:
-            _lib.config_set("fused_split", old)
-        if case == "nonfinite":
-            assert np.all(np.isnan(got[5]))
-            assert np.all(~np.isfinite(got[:, 9]))
-            ok_r = np.ones(m, bool); ok_r[5] = False
-            ok_c = np.ones(n, bool); ok_c[9] = False
-            want = oracle.oracle_nt_blas(a[ok_r], b[ok_c])
-            assert rel_frobenius(got[np.ix_(ok_r, ok_c)], want) < FP32_GATE
-            return
-        want = a.astype(np.float64) @ b.astype(np.float64).T
-        assert rel_frobenius(got, want) < FP32_GATE
-        rows = np.linalg.norm(got - want, axis=1) / np.maximum(np.linalg.norm(want, axis=1), 1e-300)
-        assert rows.max() < 1e-4
-
-
 class TestEdgeCases:
     """Edge cases across the kernel families: degenerate and ragged dimensions,
     unaligned (offset) device views that TMA cannot take, non-finite inputs on

@@ -10,9 +10,8 @@ L = _lib.lib
 dev = torch.device("cuda:0"); s = torch.cuda.current_stream().cuda_stream
 _lib.config_set("tc_pair", 0)
 import os
-_lib.config_set("fused_split", int(os.environ.get("FS", "0")))
 NAMES = ["entry", "prologue", "pdl_wait", "tma0", "stage0", "mma_last", "chunk0", "chunk_last",
-         "stores_issued", "stores_done", "exit", "tma_last", "producer_w0", "last_promoted", "first_store_issued", "chunk_wait_last"]
+         "stores_issued", "stores_done", "exit", "tma_last", "producer_w0", "last_promoted", "first_store_issued"]
 A = torch.rand(4096 * 16384, device=dev); B = torch.rand(4096 * 16384, device=dev); C = torch.empty(4096 * 4096, device=dev)
 tr = torch.zeros(148 * 16, dtype=torch.int64, device=dev)
 shapes = [(1024, 4096, k) for k in (512, 4096)] + [(2048, 2048, 1024), (4096, 4096, 4096), (256, 4096, 4096)]

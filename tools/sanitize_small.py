@@ -30,15 +30,10 @@ for (m, n, k) in [(384, 4096, 512), (384, 208, 1032), (384, 1072, 4104), (256, 3
 for (m, n, k) in [(1024, 10, 4096), (10, 4096, 1024), (300, 3, 64), (5, 7, 4)]:
     a = rng.uniform(-1, 1, (m, k)).astype(np.float32); b = rng.uniform(-1, 1, (n, k)).astype(np.float32)
     assert oracle.rel_frobenius(gemm_nt(a, b), oracle.oracle_nt_blas(a, b)) < 1e-5
-# round 2: residual fix-up entries (outlier columns), the fused split (per-chunk
-# scales, in-GEMM splitter warps, grid-wide chunk counters) on one-wave shapes
-fs_old = _lib.config_get("fused_split")
+# round 2: residual fix-up entries (outlier columns)
 for (m, n, k) in [(256, 512, 1032), (384, 1024, 2048)]:
     a = rng.uniform(-1, 1, (m, k)).astype(np.float32) * 1e-7; b = rng.uniform(-1, 1, (n, k)).astype(np.float32)
     a[:, 3], b[:, 3] = 10.0, 0.0
     want = a.astype(np.float64) @ b.astype(np.float64).T
-    for fs in (0, 2):
-        _lib.config_set("fused_split", fs)
-        assert oracle.rel_frobenius(gemm_nt(a, b, variant="tc3xf16s"), want) < 1e-5, ((m, n, k), fs)
-_lib.config_set("fused_split", fs_old)
+    assert oracle.rel_frobenius(gemm_nt(a, b, variant="tc3xf16s"), want) < 1e-5, (m, n, k)
 print("sanitize run ok")
