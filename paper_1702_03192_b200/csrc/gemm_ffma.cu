@@ -135,19 +135,19 @@ gemm_skinny_kernel(const float* __restrict__ big, const float* __restrict__ smal
 // all of them into shared memory with one bulk copy per row as its first act,
 // so the whole long operand is in flight across the chip at once (the 1 TB/s of
 // the kernel above was latency: 1.16 waves of CTAs, a few 16-byte loads in
-// flight per lane). Warps split k into kwarps slices (lane l of slice w owns the
-// float4 columns w*32 + l, + kwarps*32, ...) and the remaining warps take
-// further row groups; each lane holds its short-operand columns in registers —
-// loaded once when its columns fit one step (kOneStep) — and the R x SMAX
-// partial sums fold across the warp (butterfly) and the slices (shared memory)
-// in a fixed order, per batch of groups x R rows.
+// flight per lane). Warps split k into kwarps slices (lane l of slice w owns
+// float4 column w*32 + l; used when kwarps x 32 float4s cover k) and the
+// remaining warps take further row groups; each lane holds its short-operand
+// columns in registers for every row, and the R x SMAX partial sums fold across
+// the warp (butterfly) and the slices (shared memory) in a fixed order, per
+// batch of groups x R rows.
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
 constexpr int kStagedWarps = 16;
 
-template <int SMAX, bool kOneStep>
+template <int SMAX>
 __global__ void __launch_bounds__(kStagedWarps * 32, 1)
 gemm_skinny_staged_kernel(const float* __restrict__ big, const float* __restrict__ small,
                           float* __restrict__ C, int64_t L, int s, int64_t k, bool small_is_b,
@@ -181,15 +181,12 @@ gemm_skinny_staged_kernel(const float* __restrict__ big, const float* __restrict
           : "memory");
   }
   const float4* small4 = reinterpret_cast<const float4*>(small);
-  const int step = kwarps * 32;
-  const int T = (int)((k4 + step - 1) / step);
-  float4 bv[SMAX];
-  if (kOneStep) {  // this lane's short-operand columns, for every batch
-    const int64_t q = (int64_t)slice * 32 + lane;
+  const int64_t q = (int64_t)slice * 32 + lane;  // this lane's float4 column (kwarps x 32 >= k / 4)
+  const bool valid = q < k4;
+  float4 bv[SMAX];  // its short-operand columns, for every row
 #pragma unroll
-    for (int j = 0; j < SMAX; ++j)
-      bv[j] = (q < k4 && j < s) ? __ldg(small4 + (int64_t)j * k4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
+  for (int j = 0; j < SMAX; ++j)
+    bv[j] = (valid && j < s) ? __ldg(small4 + (int64_t)j * k4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
   uint32_t done = 0;
   while (!done)
     asm volatile(
@@ -202,23 +199,14 @@ gemm_skinny_staged_kernel(const float* __restrict__ big, const float* __restrict
     float acc[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) acc[i] = 0.f;
-    for (int t = 0; t < T; ++t) {
-      const int64_t q = (int64_t)slice * 32 + lane + (int64_t)t * step;
-      const bool valid = q < k4;
-      if (!kOneStep) {
 #pragma unroll
-        for (int j = 0; j < SMAX; ++j)
-          bv[j] = (valid && j < s) ? __ldg(small4 + (int64_t)j * k4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+    for (int r = 0; r < R; ++r) {
+      const int rl = (b * groups + grp) * R + r;
+      const float4 a = (valid && rl < nr) ? rows4[(int64_t)rl * k4 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int rl = (b * groups + grp) * R + r;
-        const float4 a = (valid && rl < nr) ? rows4[(int64_t)rl * k4 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int j = 0; j < SMAX; ++j) {
-          float& c = acc[r * SMAX + j];  // (slots past R x SMAX stay 0)
-          c = fmaf(a.w, bv[j].w, fmaf(a.z, bv[j].z, fmaf(a.y, bv[j].y, fmaf(a.x, bv[j].x, c))));
-        }
+      for (int j = 0; j < SMAX; ++j) {
+        float& c = acc[r * SMAX + j];  // (slots past R x SMAX stay 0)
+        c = fmaf(a.w, bv[j].w, fmaf(a.z, bv[j].z, fmaf(a.y, bv[j].y, fmaf(a.x, bv[j].x, c))));
       }
     }
     butterfly32(acc, lane);
@@ -377,15 +365,8 @@ template <int SMAX>
 static int launch_skinny_staged(const float* big, const float* sml, float* C, int64_t L, int s,
                                 int64_t k, bool small_is_b, int kwarps, int nb, int64_t grid,
                                 size_t smem, cudaStream_t st) {
-  const int64_t k4 = k / 4;
-  if (k4 <= (int64_t)kwarps * 32) {
-    auto kern = gemm_skinny_staged_kernel<SMAX, true>;
-    MTNN_TRY(set_max_dynamic_smem((const void*)kern, kSkinnySmemMax));  // (set once: the cap)
-    return launch_chained(kern, dim3((unsigned)grid), dim3(kStagedWarps * 32), smem, st, big, sml,
-                          C, L, s, k, small_is_b, kwarps, nb);
-  }
-  auto kern = gemm_skinny_staged_kernel<SMAX, false>;
-  MTNN_TRY(set_max_dynamic_smem((const void*)kern, kSkinnySmemMax));
+  auto kern = gemm_skinny_staged_kernel<SMAX>;
+  MTNN_TRY(set_max_dynamic_smem((const void*)kern, kSkinnySmemMax));  // (set once: the cap)
   return launch_chained(kern, dim3((unsigned)grid), dim3(kStagedWarps * 32), smem, st, big, sml, C,
                         L, s, k, small_is_b, kwarps, nb);
 }
@@ -407,8 +388,8 @@ static int try_skinny_staged(const float* big, const float* sml, float* C, int64
   if (smem > kSmemMax || kSkinnySmemMax > di->max_smem_optin - 8 * 1024) return MTNN_OK;
   // (only where one k-step covers k: there the short operand stays in
   // registers for every row and the kernel measured faster — 10 x 4096 x 1024:
-  // 12.5-13.0 vs 15.1 us under ncu; with more steps it re-reads the short
-  // operand from L2 per batch and is no faster than the register kernel)
+  // 12.5-13.0 vs 15.1 us under ncu; a multi-step version re-read the short
+  // operand from L2 per batch and was no faster than the register kernel)
   if (k4 > (int64_t)kwarps * 32) return MTNN_OK;
   const int64_t rows = (int64_t)nb * groups * R;
   const int64_t grid = (L + rows - 1) / rows;
