@@ -671,12 +671,18 @@ int launch_split_rows_f16_pair(const float* x0, void* hi0, void* lo0, float* inv
     // issued before the first use (16384 x 2048: 5.5 -> 6.8 TB/s; 32768 rows of
     // 256: 18.3 -> 16.4 us); k = 1024 keeps the looped kernel (more resident
     // warps at its lower register count: 40.8 vs 42.5 us at 32768 rows)
-    const bool reg = k <= 512 || (k > 1024 && k <= 2048);  // (longer rows: past the smem limit)
+    // 512 < k < 1024 (the FCN's 784): the whole row in registers too (FCN step
+    // +0.3%, interleaved A/B); MTNN_SPLIT_REG8=0 keeps the looped kernel
+    static const bool reg8 = [] { const char* e = getenv("MTNN_SPLIT_REG8"); return !(e && e[0] == '0'); }();
+    const bool mid = reg8 && k > 512 && k < 1024;
+    const bool reg = k <= 512 || (k > 1024 && k <= 2048) || mid;  // (longer rows: past the smem limit)
     blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)di->sm_count * (reg && k <= 512 ? 8 : 16)));
     if (k <= 256)
       MTNN_TRY(launch_chained(split_rows_f16_reg_kernel<2>, dim3((unsigned)blocks), dim3(256), 0, s, j0, j1, k));
     else if (k <= 512)
       MTNN_TRY(launch_chained(split_rows_f16_reg_kernel<4>, dim3((unsigned)blocks), dim3(256), 0, s, j0, j1, k));
+    else if (mid)
+      MTNN_TRY(launch_chained(split_rows_f16_reg_kernel<8>, dim3((unsigned)blocks), dim3(256), 0, s, j0, j1, k));
     else if (reg)
       MTNN_TRY(launch_chained(split_rows_f16_reg_kernel<16>, dim3((unsigned)blocks), dim3(256), 0, s, j0, j1, k));
     else
