@@ -227,6 +227,148 @@ gemm_skinny_staged_kernel(const float* __restrict__ big, const float* __restrict
   }
 }
 
+// Streaming skinny NT (round 2, session 4). The register kernel above re-reads
+// the short operand from L2 for every R long rows (3.3x the long operand's
+// bytes at s = 10) and keeps ~4 loads per lane in flight; the staged kernel
+// needs the CTA's rows in shared memory. Here a CTA owns a k-range of
+// kStreamQ float4 columns (warp w, lane l: column 32w + l) and a block of
+// long rows: each lane loads its short-operand columns into registers once,
+// then streams the rows — every warp load is 512 contiguous bytes of one row,
+// the next R rows' loads are in flight while the current R are multiplied —
+// and folds each R x SMAX batch across the warp by the halving butterfly. Per
+// chunk of kStreamBatches batches the 8 warps fold through shared memory (warp
+// order), then the k-ranges: the CTAs of one cluster along k (up to 8, DSMEM,
+// rank order) and, when k has more ranges than a cluster, the clusters'
+// partial outputs in a second pass (splitk_reduce, group order).
+// Grid: x = k-ranges (clusters of cs consecutive ranges), y = row blocks.
+constexpr int kStreamQ = 256;       // float4 columns per CTA k-range (1024 floats)
+constexpr int kStreamWarps = 8;
+constexpr int kStreamBatches = 8;   // butterfly batches per shared-memory fold of the warps
+constexpr int kStreamMaxBatches = 256;  // batches per CTA
+constexpr int64_t kStreamMaxBytes = 32ll << 20;  // long operand bytes it is used up to
+
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+#ifdef MTNN_TRACE
+// per-CTA globaltimer stamps (trace builds only: tools/build_variant.sh)
+__device__ unsigned long long g_skinny_trace[8192 * 8];
+__device__ __forceinline__ void skinny_mark(int pt) {
+  if (threadIdx.x != 0) return;
+  const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  if (cta >= 8192) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_skinny_trace[cta * 8 + pt] = t;
+}
+#define SKINNY_MARK(p) skinny_mark(p)
+#else
+#define SKINNY_MARK(p)
+#endif
+
+template <int SMAX>
+__global__ void __launch_bounds__(kStreamWarps * 32, 2)
+gemm_skinny_stream_kernel(const float* __restrict__ big, const float* __restrict__ small,
+                          float* __restrict__ out, int64_t L, int s, int64_t k, bool small_is_b,
+                          int64_t rows_per_cta) {
+  constexpr int R = 32 / SMAX;
+  __shared__ float red[kStreamWarps][kStreamBatches][32];
+  extern __shared__ float part[];  // [batches of this CTA][32]: its k-range's sums
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t cs, rank;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(cs));
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int64_t k4 = k / 4;
+  const int64_t q = (int64_t)blockIdx.x * kStreamQ + warp * 32 + lane;  // this lane's column
+  const bool valid = q < k4;
+  float* C = out + (int64_t)(blockIdx.x / cs) * L * s;  // this cluster's output (or partial)
+  const int64_t rbeg = (int64_t)blockIdx.y * rows_per_cta;
+  const int64_t rend = min(L, rbeg + rows_per_cta);
+  SKINNY_MARK(0);
+  pdl_enter();
+  SKINNY_MARK(1);
+  const float4* col = reinterpret_cast<const float4*>(big) + q;
+  float4 bv[SMAX];
+#pragma unroll
+  for (int j = 0; j < SMAX; ++j)
+    bv[j] = (valid && j < s) ? __ldg(reinterpret_cast<const float4*>(small) + (int64_t)j * k4 + q)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+  auto load = [&](float4* a, int64_t r) {
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      a[i] = (valid && r + i < rend) ? __ldg(col + (r + i) * k4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  // batches r (cur), r + R (nxt) and r + 2R (nx2) in flight
+  float4 cur[R], nxt[R], nx2[R];
+  load(cur, rbeg);
+  load(nxt, rbeg + R);
+  SKINNY_MARK(2);
+  for (int64_t c0 = rbeg; c0 < rend; c0 += (int64_t)kStreamBatches * R) {  // chunks
+    const int nb = (int)min((int64_t)kStreamBatches, (rend - c0 + R - 1) / R);
+    for (int b = 0; b < nb; ++b) {
+      const int64_t r = c0 + (int64_t)b * R;
+      load(nx2, r + 2 * R);  // (across chunk ends)
+      float acc[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int j = 0; j < SMAX; ++j) {
+          float& t = acc[i * SMAX + j];
+          t = fmaf(cur[i].w, bv[j].w, fmaf(cur[i].z, bv[j].z, fmaf(cur[i].y, bv[j].y, fmaf(cur[i].x, bv[j].x, t))));
+        }
+      butterfly32(acc, lane);  // lane l: value l of the batch (row l / SMAX, short row l % SMAX)
+      red[warp][b][lane] = acc[0];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        cur[i] = nxt[i];
+        nxt[i] = nx2[i];
+      }
+    }
+    SKINNY_MARK(3);
+    __syncthreads();
+    const int b0 = (int)((c0 - rbeg) / R);
+    for (int i = threadIdx.x; i < nb * 32; i += kStreamWarps * 32) {
+      float v = 0.f;
+#pragma unroll
+      for (int w = 0; w < kStreamWarps; ++w) v += red[w][i / 32][i % 32];
+      part[b0 * 32 + i] = v;
+    }
+    __syncthreads();  // red is reused by the next chunk
+  }
+  if (cs > 1) cluster_barrier();  // every CTA's part[] is posted
+  SKINNY_MARK(5);
+  // CTA `rank` finishes items i = rank, rank + cs, ...: the cluster's k-range
+  // partial sums in rank order (DSMEM)
+  const int nbt = (int)((rend - rbeg + R - 1) / R);
+  for (int i = threadIdx.x * (int)cs + (int)rank; i < nbt * 32; i += kStreamWarps * 32 * (int)cs) {
+    const int l = i % 32, ri = l / SMAX, j = l % SMAX;
+    const int64_t row = rbeg + (int64_t)(i / 32) * R + ri;
+    if (ri >= R || j >= s || row >= rend) continue;
+    float v = part[i];
+    if (cs > 1) {
+      v = 0.f;
+      const uint32_t la = smem_addr(part + i);
+      for (uint32_t cc = 0; cc < cs; ++cc) {
+        float x;
+        asm volatile(
+            "{\n\t.reg .u32 ra;\n\tmapa.shared::cluster.u32 ra, %1, %2;\n\t"
+            "ld.shared::cluster.f32 %0, [ra];\n\t}"
+            : "=f"(x)
+            : "r"(la), "r"(cc)
+            : "memory");
+        v += x;
+      }
+    }
+    C[small_is_b ? row * s + j : (int64_t)j * L + row] = v;
+  }
+  SKINNY_MARK(6);
+  if (cs > 1) cluster_barrier();  // peers are done reading this CTA's part[]
+  SKINNY_MARK(7);
+}
+
 // NN with a tiny inner dimension (k <= 16; the FCN's 1024 x 4096 x 10 backward
 // product): C = A B^T is an outer-product sum bound by writing C. A thread owns
 // 4 adjacent columns and kNnRows rows: its k float4s of B^T (L2) are loaded
@@ -408,6 +550,88 @@ static int try_skinny_staged(const float* big, const float* sml, float* C, int64
   return MTNN_OK;
 }
 
+// Streaming skinny NT (MTNN_SKINNY_STREAM=0 disables it).
+static bool skinny_stream_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MTNN_SKINNY_STREAM");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <int SMAX>
+static int launch_skinny_stream(const float* big, const float* sml, float* C, int64_t L, int s,
+                                int64_t k, bool small_is_b, const DeviceInfo* di, cudaStream_t st) {
+  constexpr int R = 32 / SMAX;
+  auto kern = gemm_skinny_stream_kernel<SMAX>;
+  const int64_t nranges = (k / 4 + kStreamQ - 1) / kStreamQ;
+  const unsigned cs = (unsigned)std::min<int64_t>(8, nranges);
+  const int64_t groups = (nranges + cs - 1) / cs;
+  // rows per CTA: two CTAs per SM over the whole grid, in whole batches
+  // (capped so the CTA's folded sums, 128 B per batch, stay <= 32 KiB)
+  const int64_t want = 2 * (int64_t)di->sm_count;
+  int64_t rows = (L * nranges + want - 1) / want;
+  rows = std::min<int64_t>(rows, (int64_t)kStreamMaxBatches * R);
+  rows = std::max<int64_t>(R, (rows + R - 1) / R * R);
+  int64_t nrb = (L + rows - 1) / rows;
+  if (nrb > 65535)
+    return fail(MTNN_ENOTSUP, "streaming skinny: %lld long rows exceed the grid", (long long)L);
+  const size_t smem = (size_t)(rows / R) * 32 * sizeof(float);
+  float* out = C;
+  ScratchBuffer part;
+  if (groups > 1) {
+    MTNN_TRY(part.alloc((size_t)groups * L * s * sizeof(float), st));
+    out = static_cast<float*>(part.ptr);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(groups * cs), (unsigned)nrb);
+  cfg.blockDim = dim3(kStreamWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = chain_enabled() ? 2 : 1;
+  MTNN_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, big, sml, out, L, s, k, small_is_b, rows));
+  MTNN_CUDA_TRY(cudaGetLastError());
+  if (groups > 1) MTNN_TRY(launch_splitk_reduce(out, C, L * s, (int)groups, st));
+  return MTNN_OK;
+}
+
+static int try_skinny_stream(const float* big, const float* sml, float* C, int64_t L, int sm_rows,
+                             int64_t k, bool small_is_b, int smax, const DeviceInfo* di,
+                             cudaStream_t st, bool* done) {
+  *done = false;
+  // (measured faster only for the 10-or-fewer short rows of a one-wave long
+  // operand — the FCN's 10-class products: 1024 x 10 x 4096 13.5 vs 16.4 us,
+  // 10 x 4096 x 1024 12.3 vs 14.3 us; for longer streams its one k-step per
+  // butterfly makes it instruction-bound and the register kernel wins)
+  if (!skinny_stream_enabled() || smax > 10 || L * k * 4 > kStreamMaxBytes) return MTNN_OK;
+  int rc;
+  switch (smax) {
+    case 4: rc = launch_skinny_stream<4>(big, sml, C, L, sm_rows, k, small_is_b, di, st); break;
+    case 8: rc = launch_skinny_stream<8>(big, sml, C, L, sm_rows, k, small_is_b, di, st); break;
+    case 10: rc = launch_skinny_stream<10>(big, sml, C, L, sm_rows, k, small_is_b, di, st); break;
+    case 12: rc = launch_skinny_stream<12>(big, sml, C, L, sm_rows, k, small_is_b, di, st); break;
+    default: rc = launch_skinny_stream<16>(big, sml, C, L, sm_rows, k, small_is_b, di, st); break;
+  }
+  MTNN_TRY(rc);
+  *done = true;
+  return MTNN_OK;
+}
+
+#ifdef MTNN_TRACE
+extern "C" int mtnn_skinny_trace(void* host, int64_t n) {
+  MTNN_CUDA_TRY(cudaMemcpyFromSymbol(host, g_skinny_trace, (size_t)std::min<int64_t>(n, 8192 * 8) * 8));
+  return MTNN_OK;
+}
+#endif
+
 bool nn_smallk_eligible(const float* BT, const float* C, int64_t m, int64_t n, int64_t k) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   return k >= 1 && k <= kNnSmallK && m >= 1 && n >= 4 && n % 4 == 0 && al16(BT) && al16(C) &&
@@ -475,6 +699,8 @@ int launch_gemm_skinny(const float* A, const float* B, float* C, int64_t m, int6
   const float* big = small_is_b ? A : B;
   const float* sml = small_is_b ? B : A;
   bool staged = false;
+  MTNN_TRY(try_skinny_stream(big, sml, C, L, sm_rows, k, small_is_b, smax, di, s, &staged));
+  if (staged) return MTNN_OK;
   MTNN_TRY(try_skinny_staged(big, sml, C, L, sm_rows, k, small_is_b, smax, di, s, &staged));
   if (staged) return MTNN_OK;
   const unsigned g = (unsigned)blocks;

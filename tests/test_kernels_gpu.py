@@ -851,6 +851,21 @@ class TestGemvClassKernels:
         assert rel_frobenius(got, want) < FP32_GATE
         assert np.array_equal(got, gemm_nt(a, b))  # fixed summation order
 
+    # streaming skinny NT (<= 10 short rows, long operand <= 32 MB): one k-range
+    # (no cluster), clusters of 2 / 4 / 8 CTAs along k, more ranges than a
+    # cluster (second-pass fold), ragged k-ranges and row blocks, both
+    # orientations, short sides 1..10
+    @pytest.mark.parametrize("shape", [(4096, 10, 1024), (10, 4096, 1024), (1024, 10, 4096),
+                                       (2000, 7, 2052), (3, 777, 8192), (256, 10, 16384),
+                                       (100, 9, 9000), (1, 1, 4), (4099, 2, 1000), (5, 64, 20000)])
+    def test_streaming_skinny_nt(self, rng, shape):
+        m, n, k = shape
+        a, b = random_matrix(rng, m, k), random_matrix(rng, n, k)
+        want = a.astype(np.float64) @ b.astype(np.float64).T
+        got = gemm_nt(a, b)
+        assert rel_frobenius(got, want) < FP32_GATE
+        assert np.array_equal(got, gemm_nt(a, b))  # fixed fold order
+
     @pytest.mark.parametrize("shape", [(1024, 4096, 10), (33, 100, 16), (5, 8, 1), (300, 1028, 7),
                                        (4097, 260, 4), (64, 4096, 13)])
     def test_smallk_nn_and_tnn(self, rng, shape):

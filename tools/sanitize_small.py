@@ -36,4 +36,8 @@ for (m, n, k) in [(256, 512, 1032), (384, 1024, 2048)]:
     a[:, 3], b[:, 3] = 10.0, 0.0
     want = a.astype(np.float64) @ b.astype(np.float64).T
     assert oracle.rel_frobenius(gemm_nt(a, b, variant="tc3xf16s"), want) < 1e-5, (m, n, k)
+# session 4: streaming skinny NT (clusters along k, second-pass fold, ragged)
+for (m, n, k) in [(300, 10, 1024), (10, 300, 4100), (256, 10, 16384), (1, 1, 4), (77, 3, 2052)]:
+    a = rng.uniform(-1, 1, (m, k)).astype(np.float32); b = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    assert oracle.rel_frobenius(gemm_nt(a, b), oracle.oracle_nt_blas(a, b)) < 1e-5, (m, n, k)
 print("sanitize run ok")
