@@ -287,6 +287,45 @@ struct EventSet {
   }
 };
 
+// MTNN_PIPE_TRACE=1: the blocked host pipeline prints each copy / compute span
+// (CUDA events, ms from the call's start) to stderr — a timeline for tuning.
+struct PipeTrace {
+  bool on = false;
+  cudaEvent_t base = nullptr;
+  struct Span { const char* what; int64_t a, b; cudaEvent_t s, e; };
+  std::vector<Span> spans;
+  void start(cudaStream_t st) {
+    static const bool env = [] { const char* e = getenv("MTNN_PIPE_TRACE"); return e && e[0] == '1'; }();
+    on = env;
+    if (!on) return;
+    cudaEventCreate(&base);
+    cudaEventRecord(base, st);
+  }
+  cudaEvent_t mark(cudaStream_t st) {
+    if (!on) return nullptr;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    return e;
+  }
+  void add(const char* what, int64_t a, int64_t b, cudaEvent_t s, cudaEvent_t e) {
+    if (on) spans.push_back({what, a, b, s, e});
+  }
+  ~PipeTrace() {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    for (auto& x : spans) {
+      float t0 = 0, t1 = 0;
+      cudaEventElapsedTime(&t0, base, x.s);
+      cudaEventElapsedTime(&t1, base, x.e);
+      fprintf(stderr, "pipe %-6s %6lld %6lld %9.3f %9.3f\n", x.what, (long long)x.a, (long long)x.b, t0, t1);
+      cudaEventDestroy(x.s);
+      cudaEventDestroy(x.e);
+    }
+    cudaEventDestroy(base);
+  }
+};
+
 // Pipeline knobs: minimum problem bytes (A+B+C) to pipeline, and the target
 // bytes of A+C per chunk (MTNN_PIPE_MIN_MB / MTNN_PIPE_CHUNK_MB override).
 static double env_mb(const char* name, double dflt) {
@@ -331,6 +370,7 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
   PipeStreams* ps = nullptr;
   MTNN_TRY(pipe_streams(&ps));
   EventSet evs;
+  PipeTrace tr;
   ScratchBuffer da, db, dc, wa, wb;
   struct Drain {
     PipeStreams* p;
@@ -423,6 +463,7 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
   };
   cudaEvent_t ev;
   MTNN_TRY(evs.make(&ev));
+  tr.start(ps->in);
   MTNN_CUDA_TRY(cudaEventRecord(ev, ps->in));  // allocations above are ordered on `in`
   MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->comp, ev, 0));
   MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->out, ev, 0));
@@ -431,8 +472,10 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
     const int64_t r0 = is_a ? abeg[q] : q * nb;
     const int64_t rows = is_a ? abeg[q + 1] - r0 : std::min(nb, n - r0);
     float* dst = (is_a ? dap : dbp) + r0 * k;
+    cudaEvent_t t0 = tr.mark(ps->in);
     MTNN_CUDA_TRY(cudaMemcpyAsync(dst, (is_a ? A : B) + r0 * k, (size_t)(rows * k) * 4,
                                   cudaMemcpyHostToDevice, ps->in));
+    tr.add(is_a ? "h2d_a" : "h2d_b", r0, rows, t0, tr.mark(ps->in));
     cudaEvent_t e;
     MTNN_TRY(evs.make(&e));
     MTNN_CUDA_TRY(cudaEventRecord(e, ps->in));
@@ -441,10 +484,13 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
     const bool halves = is_a || conv != 2;
     FixList fl = (is_a ? fha : fhb).list;  // this block's rows start at global row r0
     fl.row0 = (int32_t)r0;
-    return launch_split_rows_f16_pair(dst, halves ? const_cast<void*>(o.hi) : nullptr,
-                                      const_cast<void*>(o.lo), const_cast<float*>(o.inv_scale),
-                                      rows, fl, nullptr, nullptr, nullptr, nullptr, 0, FixList{},
-                                      k, ps->comp);
+    cudaEvent_t s0 = tr.mark(ps->comp);
+    const int rc = launch_split_rows_f16_pair(dst, halves ? const_cast<void*>(o.hi) : nullptr,
+                                              const_cast<void*>(o.lo), const_cast<float*>(o.inv_scale),
+                                              rows, fl, nullptr, nullptr, nullptr, nullptr, 0,
+                                              FixList{}, k, ps->comp);
+    tr.add("split", r0, rows, s0, tr.mark(ps->comp));
+    return rc;
   };
   // GEMM + residual fix-up of C rows i0.. (mi) x B rows j0.. (nj), rows of ldc;
   // the last fix-up resets both lists
@@ -479,13 +525,17 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
     const int64_t i0 = abeg[i], j0 = j * nb;
     const int64_t mi = abeg[i + 1] - i0, nj = std::min(nb, n - j0);
     float* cij = dcp + i0 * n + mi * j0;  // rows i0.. of C, block j: mi x nj contiguous
+    cudaEvent_t g0 = tr.mark(ps->comp);
     MTNN_TRY(run_fixed(a_rows(i0), b_rows(j0), i0, mi, j0, nj, cij, nj));
+    tr.add("gemm", i0, j0, g0, tr.mark(ps->comp));
     cudaEvent_t e;
     MTNN_TRY(evs.make(&e));
     MTNN_CUDA_TRY(cudaEventRecord(e, ps->comp));
     MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->out, e, 0));
+    cudaEvent_t d0 = tr.mark(ps->out);
     MTNN_CUDA_TRY(cudaMemcpy2DAsync(C + i0 * n + j0, (size_t)n * 4, cij, (size_t)nj * 4,
                                     (size_t)nj * 4, (size_t)mi, cudaMemcpyDeviceToHost, ps->out));
+    tr.add("d2h", i0, j0, d0, tr.mark(ps->out));
     return MTNN_OK;
   };
   MTNN_TRY(bring(true, 0));
@@ -497,12 +547,16 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
     MTNN_TRY(bring(true, i));
     const int64_t i0 = abeg[i], mi = abeg[i + 1] - i0;
     float* ci = dcp + i0 * n;
+    cudaEvent_t g0 = tr.mark(ps->comp);
     MTNN_TRY(run_fixed(a_rows(i0), b_rows(0), i0, mi, 0, n, ci, n));
+    tr.add("gemm", i0, -1, g0, tr.mark(ps->comp));
     MTNN_TRY(evs.make(&ev));
     MTNN_CUDA_TRY(cudaEventRecord(ev, ps->comp));
     MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->out, ev, 0));
+    cudaEvent_t d0 = tr.mark(ps->out);
     MTNN_CUDA_TRY(cudaMemcpyAsync(C + i0 * n, ci, (size_t)(mi * n) * 4, cudaMemcpyDeviceToHost,
                                   ps->out));
+    tr.add("d2h", i0, -1, d0, tr.mark(ps->out));
   }
   cudaError_t e1 = cudaStreamSynchronize(ps->out);
   cudaError_t e2 = cudaStreamSynchronize(ps->comp);
