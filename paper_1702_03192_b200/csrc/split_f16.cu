@@ -669,12 +669,14 @@ int launch_split_rows_f16_pair(const float* x0, void* hi0, void* lo0, float* inv
     int64_t blocks = (rows + 7) / 8;
     // rows of <= 512 and 1024 < k <= 2048: whole row in registers, every load
     // issued before the first use (16384 x 2048: 5.5 -> 6.8 TB/s; 32768 rows of
-    // 256: 18.3 -> 16.4 us); k = 1024 keeps the looped kernel (more resident
-    // warps at its lower register count: 40.8 vs 42.5 us at 32768 rows)
-    // 512 < k < 1024 (the FCN's 784): the whole row in registers too (FCN step
-    // +0.3%, interleaved A/B); MTNN_SPLIT_REG8=0 keeps the looped kernel
+    // 256: 18.3 -> 16.4 us). 512 < k < 1024 (the FCN's 784): the whole row in
+    // registers too (FCN step +0.3%, interleaved A/B; MTNN_SPLIT_REG8=0 keeps the
+    // looped kernel), and k = 1024 (split time of NT calls: 16384^2 x 1024 47.1 ->
+    // 41.0 us, 2048 x 8192 x 1024 20.5 -> 16.4, 4096 x 784 x 1024 14.4 -> 12.3;
+    // MTNN_SPLIT_REG1024=0 keeps the looped kernel there)
     static const bool reg8 = [] { const char* e = getenv("MTNN_SPLIT_REG8"); return !(e && e[0] == '0'); }();
-    const bool mid = reg8 && k > 512 && k < 1024;
+    static const bool reg1024 = [] { const char* e = getenv("MTNN_SPLIT_REG1024"); return !(e && e[0] == '0'); }();
+    const bool mid = reg8 && k > 512 && (k < 1024 || (k == 1024 && reg1024));
     const bool reg = k <= 512 || (k > 1024 && k <= 2048) || mid;  // (longer rows: past the smem limit)
     blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)di->sm_count * (reg && k <= 512 ? 8 : 16)));
     if (k <= 256)
