@@ -1,6 +1,7 @@
 """Extract the roofline-relevant counters from `ncu --set full` reports into
 profiles/ncu_summary.json (+ a readable .md). Usage:
     python tools/ncu_summary.py OUT_PREFIX name=report.ncu-rep:m,n,k[:op] ...
+(shape prefixes: s = operand split rows,cols pairs; g = GEMV-class m,n,k in GB/s)
 """
 import csv
 import io
@@ -54,8 +55,13 @@ def main(prefix, specs):
         r = read(rep, parts[1] if len(parts) > 1 else None)
         r["traffic_bytes"] = r.get("dram_read", 0) + r.get("dram_write", 0)
         split = parts[0].startswith("s")
-        dims = [int(x) for x in parts[0].lstrip("s").split(",")]
-        if split:
+        gemv = parts[0].startswith("g")  # GEMV-class product: HBM-bound, report GB/s
+        dims = [int(x) for x in parts[0].lstrip("sg").split(",")]
+        if gemv:
+            m, n, k = dims
+            r["algorithmic_bytes"] = 4 * (m * k + n * k + m * n)
+            r["achieved"] = f"{r['algorithmic_bytes'] / r['duration'] / 1e9:.0f} GB/s"
+        elif split:
             # operand split: read x (4 B), write h + l (2 B + 2 B) per element
             r["algorithmic_bytes"] = 8 * sum(dims[i] * dims[i + 1] for i in range(0, len(dims), 2))
             r["achieved"] = f"{r['algorithmic_bytes'] / r['duration'] / 1e9:.0f} GB/s"
