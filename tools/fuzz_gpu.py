@@ -13,6 +13,7 @@ bad = 0
 longk = [4104, 6000, 8192, 8200, 12000, 16384, 16392, 20000]
 import os
 big = os.environ.get("FUZZ_BIG") == "1"
+skinny = os.environ.get("FUZZ_SKINNY") == "1"  # GEMV-class: one output side 1..16
 for it in range(N):
     m, n, k = (int(rng.choice(picks)) if rng.random() < 0.7 else int(rng.integers(1, 4200)) for _ in range(3))
     if it % 4 == 3:  # long-k branches of the row / column splits (register, cluster, band, smem)
@@ -21,6 +22,11 @@ for it in range(N):
         dims = [int(rng.choice([4096, 6000, 8192, 10000, 16384])), int(rng.choice(picks)),
                 int(rng.choice([256, 1000, 2048, 4104]))]
         m, n, k = (dims[0], dims[1], dims[2]) if rng.random() < 0.5 else (dims[1], dims[0], dims[2])
+    if skinny and it % 2 == 0:  # register / staged / streaming skinny kernels, clusters along k
+        sm = int(rng.integers(1, 17))
+        lg = int(rng.choice([1, 33, 300, 1024, 4096, 9000]))
+        k = int(rng.choice([4, 64, 1028, 2052, 4096, 8192, 16384, 20000])) if rng.random() < 0.8 else int(rng.integers(1, 9000))
+        m, n = (sm, lg) if rng.random() < 0.5 else (lg, sm)
     knobs = {"tc_pair": int(rng.integers(0, 3)), "f16s_inkernel_max_short": int(rng.choice([0, 256, 1 << 20])),
              "host_pipeline_blocked": int(rng.integers(0, 2))}
     for kk, vv in knobs.items():
