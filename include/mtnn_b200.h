@@ -137,6 +137,10 @@ int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* w
  *   host-buffer NT calls on the tc3xf16s path with n >= 1024, k <= 4096 stream B in row
  *   blocks against A's first row block so C leaves while B arrives; 0 = copy B
  *   first, then pipeline A/C row chunks.
+ * "host_pipeline_zc": 0 (default; env MTNN_PIPE_ZC=1 turns it on): in that
+ *   blocked pipeline, C blocks leave by SM stores into the host C when it is
+ *   pinned and device-mapped, instead of 2-D copy-engine copies (A/B: faster
+ *   on the widest outputs, slower on others; net -0.6% over the sweep's cases).
  * "fixup": 1 (default; env MTNN_FIXUP=0 turns it off): the split tensor-core
  *   paths list every operand element their two-piece representation misses by
  *   more than 2^-19 (tc3xf16s: entries far below their row's max; tc3xtf32:

@@ -67,6 +67,8 @@ struct KernelTimer {
 };
 
 // Kernel launchers (implemented in the .cu files). All asynchronous on `s`.
+int launch_store_rows(const float* src, float* dst, int64_t rows, int64_t width, int64_t pitch,
+                      cudaStream_t s);
 int launch_transpose(const float* in, float* out, int64_t rows, int64_t cols,
                      cudaStream_t s);
 // SIMT NT for outputs with a side <= 16 (k % 4 == 0, 16-byte aligned operands).

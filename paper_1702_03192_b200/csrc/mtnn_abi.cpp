@@ -365,6 +365,19 @@ static bool blocked_pipeline_enabled() {
 // earlier in theory, measured slower on the B200: more, smaller GEMMs.) Each
 // operand block is split once; kernels and operand halves are the device path's
 // (only split-K order may differ).
+// MTNN_PIPE_ZC / mtnn_config_set("host_pipeline_zc", v): the blocked
+// pipeline's 2-D C blocks leave by SM stores into the mapped host buffer.
+static std::atomic<int> g_pipe_zc{-1};
+static bool pipe_zc_enabled() {
+  int v = g_pipe_zc.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = getenv("MTNN_PIPE_ZC");
+    v = (e && e[0] == '1') ? 1 : 0;
+    g_pipe_zc.store(v, std::memory_order_relaxed);
+  }
+  return v != 0;
+}
+
 static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_t m, int64_t n,
                                 int64_t k, int conv) {
   PipeStreams* ps = nullptr;
@@ -520,6 +533,15 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
     if (f.reset_a) fha.consumed = fhb.consumed = true;
     return MTNN_OK;
   };
+  // C blocks leave by SM stores into the (pinned, device-mapped) host C when
+  // host_pipeline_zc is on, by 2-D copy-engine copies otherwise
+  bool zc_c = false;
+  if (pipe_zc_enabled()) {
+    cudaPointerAttributes at{};
+    zc_c = cudaPointerGetAttributes(&at, C) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+           at.devicePointer == static_cast<void*>(C) && n % 4 == 0;
+    (void)cudaGetLastError();
+  }
   // multiply C block (i, j) and send it out
   auto block = [&](int64_t i, int64_t j) {
     const int64_t i0 = abeg[i], j0 = j * nb;
@@ -533,8 +555,11 @@ static int host_gemm_nt_blocked(const float* A, const float* B, float* C, int64_
     MTNN_CUDA_TRY(cudaEventRecord(e, ps->comp));
     MTNN_CUDA_TRY(cudaStreamWaitEvent(ps->out, e, 0));
     cudaEvent_t d0 = tr.mark(ps->out);
-    MTNN_CUDA_TRY(cudaMemcpy2DAsync(C + i0 * n + j0, (size_t)n * 4, cij, (size_t)nj * 4,
-                                    (size_t)nj * 4, (size_t)mi, cudaMemcpyDeviceToHost, ps->out));
+    if (zc_c)
+      MTNN_TRY(launch_store_rows(cij, C + i0 * n + j0, mi, nj, n, ps->out));
+    else
+      MTNN_CUDA_TRY(cudaMemcpy2DAsync(C + i0 * n + j0, (size_t)n * 4, cij, (size_t)nj * 4,
+                                      (size_t)nj * 4, (size_t)mi, cudaMemcpyDeviceToHost, ps->out));
     tr.add("d2h", i0, j0, d0, tr.mark(ps->out));
     return MTNN_OK;
   };
@@ -807,6 +832,11 @@ int mtnn_config_set(const char* key, int64_t value) {
     g_pipe_blocked.store((int)value, std::memory_order_relaxed);
     return MTNN_OK;
   }
+  if (strcmp(key, "host_pipeline_zc") == 0) {
+    if (value != 0 && value != 1) return fail(MTNN_EINVAL, "host_pipeline_zc must be 0 or 1");
+    g_pipe_zc.store((int)value, std::memory_order_relaxed);
+    return MTNN_OK;
+  }
   if (strcmp(key, "fixup") == 0) {
     if (value != 0 && value != 1) return fail(MTNN_EINVAL, "fixup must be 0 or 1");
     set_fixup_enabled(value != 0);
@@ -827,6 +857,10 @@ int mtnn_config_get(const char* key, int64_t* value) {
   }
   if (strcmp(key, "host_pipeline_blocked") == 0) {
     *value = blocked_pipeline_enabled() ? 1 : 0;
+    return MTNN_OK;
+  }
+  if (strcmp(key, "host_pipeline_zc") == 0) {
+    *value = pipe_zc_enabled() ? 1 : 0;
     return MTNN_OK;
   }
   if (strcmp(key, "fixup") == 0) {

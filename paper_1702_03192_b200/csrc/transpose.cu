@@ -199,3 +199,31 @@ int launch_transpose(const float* in, float* out, int64_t rows, int64_t cols,
 }
 
 }  // namespace mtnn
+
+namespace mtnn {
+namespace {
+// rows x width floats from a dense device block to host-mapped pinned memory
+// rows `pitch` floats apart: SM-driven PCIe writes (A/B against the copy
+// engine's 2-D D2H in the blocked host pipeline, MTNN_PIPE_ZC=1)
+__global__ void __launch_bounds__(256) store_rows_kernel(const float4* __restrict__ src, float4* dst,
+                                                         int64_t rows, int64_t w4, int64_t p4) {
+  const int64_t n4 = rows * w4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const int64_t r = i / w4, c = i - r * w4;
+    dst[r * p4 + c] = __ldcs(src + i);
+  }
+}
+}  // namespace
+
+int launch_store_rows(const float* src, float* dst, int64_t rows, int64_t width, int64_t pitch,
+                      cudaStream_t s) {
+  if (rows <= 0 || width <= 0) return MTNN_OK;
+  if (width % 4 || pitch % 4 || (reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(dst) & 15))
+    return fail(MTNN_EINVAL, "store_rows: 16-byte rows required");
+  store_rows_kernel<<<64, 256, 0, s>>>(reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), rows,
+                                       width / 4, pitch / 4);
+  MTNN_CUDA_TRY(cudaGetLastError());
+  return MTNN_OK;
+}
+}  // namespace mtnn

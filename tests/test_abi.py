@@ -124,6 +124,15 @@ def test_config_knobs_roundtrip_and_reject_unknown():
         _lib.config_set(key, old)
     with pytest.raises(ValueError, match="unknown config key"):
         _lib.config_set("no_such_knob", 1)
+    old = _lib.config_get("host_pipeline_zc")
+    try:
+        for v in (1, 0):
+            _lib.config_set("host_pipeline_zc", v)
+            assert _lib.config_get("host_pipeline_zc") == v
+        with pytest.raises(ValueError):
+            _lib.config_set("host_pipeline_zc", 2)
+    finally:
+        _lib.config_set("host_pipeline_zc", old)
 
 
 

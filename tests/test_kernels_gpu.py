@@ -264,6 +264,34 @@ class TestPipelinedHostPath:
         assert rel_frobenius(gemm_nt(a, b), dev) < 1e-6
 
 
+    @pytest.mark.parametrize("shape", [(2304, 16384, 1024), (1024, 4096, 4096)])
+    def test_blocked_pipeline_sm_stores_match_copies(self, rng, shape):
+        """host_pipeline_zc: the blocked pipeline's C blocks written by SM stores
+        into the pinned (device-mapped) host C — the same bits as the copy-engine
+        2-D copies."""
+        import torch
+
+        from paper_1702_03192_b200 import _lib
+
+        m, n, k = shape
+        ha = torch.from_numpy(random_matrix(rng, m, k)).pin_memory()
+        hb = torch.from_numpy(random_matrix(rng, n, k)).pin_memory()
+        outs = []
+        old = _lib.config_get("host_pipeline_zc")
+        try:
+            for v in (0, 1):
+                _lib.config_set("host_pipeline_zc", v)
+                hc = torch.full((m, n), float("nan")).pin_memory()
+                _lib.check(_lib.lib.mtnn_gemm_nt_host(ha.data_ptr(), hb.data_ptr(), hc.data_ptr(), m, n, k, 0))
+                outs.append(hc.numpy().copy())
+        finally:
+            _lib.config_set("host_pipeline_zc", old)
+        assert np.array_equal(outs[0], outs[1])
+        rows = np.sort(rng.choice(m, 32, replace=False))
+        want = oracle.oracle_nt_rows(ha.numpy(), hb.numpy(), rows, np.arange(n))
+        assert rel_frobenius(outs[1][rows], want) < FP32_GATE
+
+
 def test_tf32_inkernel_split_opt_in(tmp_path):
     """MTNN_TF32_INKERNEL=1: the TF32 kernel computes the larger operand's lo half
     in shared memory; results stay within the FP32 gate (fresh process: the
