@@ -3,7 +3,12 @@ PCIe floor max(H2D / 55.5, D2H / 54.2, (H2D + D2H) / 93 GB/s)."""
 import ctypes, sys, time, torch
 sys.path.insert(0, ".")
 from paper_1702_03192_b200 import _lib
+import os
 L = _lib.lib
+if os.environ.get("ZC"):
+    _lib.config_set("host_pipeline_zc", int(os.environ["ZC"]))
+if os.environ.get("BLOCKED"):
+    _lib.config_set("host_pipeline_blocked", int(os.environ["BLOCKED"]))
 widths = [784, 4096, 4096, 4096, 10]
 layers = list(zip(widths[:-1], widths[1:]))
 calls = [("nt", 1024, dout, din) for din, dout in layers]
