@@ -5,7 +5,7 @@ L = _lib.lib
 dev = torch.device("cuda:0"); s = torch.cuda.current_stream().cuda_stream
 flush = torch.ones(64 * 2**20, device=dev)
 B = torch.rand(16384 * 16384, device=dev); C = torch.empty(16384 * 16384, device=dev)
-for (r, c) in [(4097, 1023), (12345, 6789), (8191, 8193), (1000, 1000), (3000, 5000), (16384, 16384), (8192, 8192), (4096, 4096), (1001, 16385), (16384, 128), (128, 16384), (16384, 256), (65536, 64), (64, 65536)]:
+for (r, c) in [(4097, 1023), (12345, 6789), (8191, 8193), (1000, 1000), (3000, 5000), (16384, 16384), (8192, 8192), (4096, 4096), (1001, 16385), (16384, 128), (128, 16384), (16384, 256), (65536, 64), (64, 65536), (262144, 64), (64, 262144), (131072, 128), (524288, 32)]:
     ev = []
     for rep in range(6):
         flush.sum(); torch.cuda._sleep(100000)
