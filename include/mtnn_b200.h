@@ -140,7 +140,9 @@ int mtnn_profile_read(int kclass, double* total_ms, int64_t* launches, double* w
  * "host_pipeline_zc": 0 (default; env MTNN_PIPE_ZC=1 turns it on): in that
  *   blocked pipeline, C blocks leave by SM stores into the host C when it is
  *   pinned and device-mapped, instead of 2-D copy-engine copies (A/B: faster
- *   on the widest outputs, slower on others; net -0.6% over the sweep's cases).
+ *   on the widest outputs, slower on others; net -0.6% over the sweep's cases;
+ *   the store kernel needs SMs, so it can wait behind long GEMMs: with the
+ *   pipeline forced to k = 16384 one case took 128 ms instead of 45).
  * "fixup": 1 (default; env MTNN_FIXUP=0 turns it off): the split tensor-core
  *   paths list every operand element their two-piece representation misses by
  *   more than 2^-19 (tc3xf16s: entries far below their row's max; tc3xtf32:
